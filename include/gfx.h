@@ -1,0 +1,219 @@
+/*
+ * gfx.h -- C ABI of libgfx.so, the B200 (sm_100a) frontier core that backs the
+ * graphfx-compatible Python package `paper_1701_01170_b200`.
+ *
+ * The reference (`graphfx`, /root/reference/pkg/src/graphfx) is pure Python;
+ * its boundary is the Python API re-exported in graphfx/__init__.py:8-72.
+ * Each entry point below replaces the device work behind one reference
+ * function (cited per function).  The Python layer (`_native.py`) binds these
+ * with ctypes and keeps the reference's argument meaning and error behaviour.
+ *
+ * Conventions
+ *   - Every function returns an int status: GFX_OK (0), GFX_EINVAL (1, ->
+ *     ValueError), GFX_ECUDA (2, -> RuntimeError), GFX_ENOMEM (3, ->
+ *     MemoryError), GFX_ENCCL (4).  gfx_last_error() returns a thread-local
+ *     message for the last failure on the calling thread.
+ *   - Pointers suffixed _d are DEVICE pointers (borrowed; caller keeps them
+ *     alive, e.g. torch tensors).  Pointers without the suffix are host.
+ *   - Device vertex ids / labels are int32; row offsets are int64.  Unreached
+ *     labels are GFX_UNVISITED (INT32_MAX), missing predecessors are -1.  The
+ *     Python layer widens to the reference's int64 layout (graph.py:15-22).
+ *   - One ctx per device; calls on a ctx are stream-ordered on the ctx stream
+ *     and synchronise that stream before returning (bulk-synchronous
+ *     visibility, reference operators.py:10-15).  Not re-entrant.
+ *   - Scratch (queues, bitmaps, scan temporaries) is owned by the graph handle.
+ */
+#ifndef GFX_H
+#define GFX_H
+
+#include <stdint.h>
+
+#if defined(GFX_BUILD)
+#define GFX_API __attribute__((visibility("default")))
+#else
+#define GFX_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GFX_OK 0
+#define GFX_EINVAL 1
+#define GFX_ECUDA 2
+#define GFX_ENOMEM 3
+#define GFX_ENCCL 4
+
+#define GFX_UNVISITED 2147483647
+
+/* graph flags */
+#define GFX_GRAPH_UNDIRECTED 1 /* CSR is symmetric: reverse adjacency == CSR */
+
+/* traversal direction (reference primitives/bfs.py:42-68) */
+#define GFX_DIR_PUSH 0
+#define GFX_DIR_PULL 1
+#define GFX_DIR_AUTO 2
+
+/* filter modes (reference operators.py:61-63) */
+#define GFX_FILTER_EXACT 0
+#define GFX_FILTER_INEXACT 1
+
+/* BFS run modes */
+#define GFX_LOOP_HOST 0   /* host decides direction each level (exact Python replica) */
+#define GFX_LOOP_DEVICE 1 /* device-resident level loop, decision on device */
+
+typedef struct gfx_ctx gfx_ctx;
+typedef struct gfx_graph gfx_graph;
+
+/* One record per BFS/SSSP/BC iteration; mirrors RunStats.per_iteration and
+ * RunStats.direction_trace (reference stats.py:33-59, bfs.py:104-107). */
+typedef struct gfx_iter_rec {
+  int64_t iteration;
+  int64_t frontier_in;  /* n_f */
+  int64_t frontier_out;
+  int64_t n_u;          /* unvisited estimate after subtracting n_f */
+  int64_t edges;        /* plan.total_output of this iteration */
+  double m_f;
+  double m_u;
+  int32_t mode_before;  /* GFX_DIR_PUSH / GFX_DIR_PULL */
+  int32_t decision;
+  float ms;             /* device time of the iteration (0 when not timed) */
+  int32_t pad;
+} gfx_iter_rec;
+
+typedef struct gfx_stats {
+  int64_t iterations;
+  int64_t edges_traversed;
+  int64_t direction_switches;
+  int64_t reached;        /* vertices with a finite label */
+  int64_t edges_reached;  /* sum of out-degrees of reached vertices (E_r) */
+  int64_t work_slots;     /* kernel-counted expansion slots (SSSP inflation) */
+  int64_t bytes_alg;      /* algorithmic HBM bytes (DESIGN.md formulas) */
+  double device_ms;       /* CUDA-event time of the device loop */
+  int64_t num_records;    /* records written (<= rec_cap) */
+} gfx_stats;
+
+/* ---- library / context ------------------------------------------------ */
+GFX_API int gfx_version(void);
+GFX_API const char* gfx_last_error(void);
+/* stream: a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); NULL
+ * selects the legacy default stream */
+GFX_API int gfx_ctx_create(int device, void* stream, gfx_ctx** out);
+GFX_API int gfx_ctx_destroy(gfx_ctx* ctx);
+GFX_API int gfx_ctx_sync(gfx_ctx* ctx);
+GFX_API int gfx_ctx_sm_count(gfx_ctx* ctx);
+
+/* ---- graph (reference graph.py:61-155 CsrGraph) ------------------------ */
+/* row_d int64[n+1], col_d int32[m], w_d int32[m] or NULL.  For directed graphs
+ * the reverse adjacency (graph.py:113-126 CsrGraph.csc) is attached with
+ * gfx_graph_set_reverse before any pull traversal. */
+GFX_API int gfx_graph_create(gfx_ctx* ctx, int64_t n, int64_t m, const int64_t* row_d,
+                     const int32_t* col_d, const int32_t* w_d, int flags,
+                     gfx_graph** out);
+GFX_API int gfx_graph_set_reverse(gfx_graph* g, const int64_t* rrow_d, const int32_t* rcol_d);
+GFX_API int gfx_graph_destroy(gfx_graph* g);
+/* max out-degree (host value, computed at create) */
+GFX_API int64_t gfx_graph_max_degree(gfx_graph* g);
+/* release scratch buffers (they are re-allocated lazily) */
+GFX_API int gfx_graph_trim(gfx_graph* g);
+
+/* ---- BFS (reference primitives/bfs.py:42-159) ---------------------------
+ * labels_d/preds_d int32[n] (outputs).  recs: host array of rec_cap records
+ * (may be NULL).  loop: GFX_LOOP_HOST or GFX_LOOP_DEVICE. */
+GFX_API int gfx_bfs(gfx_graph* g, int64_t source, int direction, int idempotent,
+            int filter_mode, double do_a, double do_b, int mu_edge_based,
+            int loop, int32_t* labels_d, int32_t* preds_d, gfx_iter_rec* recs,
+            int64_t rec_cap, gfx_stats* stats);
+
+/* Host-only replica of reference direction.py:52-61 estimate_mf_mu with the
+ * same correctly rounded integer divisions CPython performs (no GPU needed). */
+GFX_API int gfx_estimate_mf_mu(int64_t n, int64_t m, int64_t n_f, int64_t n_u, int mu_edge_based,
+                               double* m_f, double* m_u);
+
+/* ---- SSSP near/far (reference primitives/sssp.py:41-121, near_far.py) ---
+ * delta <= 0 means +inf (no priority queue).  dist_d int32[n] (INT32_MAX =
+ * unreached), preds_d int32[n]. */
+GFX_API int gfx_sssp(gfx_graph* g, int64_t source, int64_t delta, int32_t* dist_d,
+             int32_t* preds_d, gfx_iter_rec* recs, int64_t rec_cap, gfx_stats* stats);
+
+/* ---- BC (reference primitives/bc.py:32-116) ----------------------------
+ * Accumulates into bc_d (float64[n], caller zero-initialises). */
+GFX_API int gfx_bc(gfx_graph* g, const int64_t* sources, int64_t num_sources, double* bc_d,
+           gfx_stats* stats);
+
+/* ---- CC (reference primitives/cc.py:23-98) -----------------------------
+ * comp_d int32[n] receives canonical min-id labels. */
+GFX_API int gfx_cc(gfx_graph* g, int32_t* comp_d, int64_t* num_components, gfx_stats* stats);
+
+/* ---- PageRank (reference primitives/pagerank.py:30-91) ------------------ */
+GFX_API int gfx_pagerank(gfx_graph* g, double damping, double epsilon, int64_t max_iters,
+                 double* rank_d, gfx_stats* stats);
+
+/* ---- TC (reference primitives/tc.py:27-86, operators.py:485-525) --------
+ * Phase 1 orients and returns the oriented edge count; phase 2 fills the
+ * caller-allocated outputs (int32[m_oriented] each, osrc/odst in the
+ * oriented CSR order of tc.py:53-56) and the int64 total. */
+GFX_API int gfx_tc_orient(gfx_graph* g, int64_t* m_oriented);
+GFX_API int gfx_tc_count(gfx_graph* g, int32_t* osrc_d, int32_t* odst_d, int32_t* counts_d,
+                 int64_t* total, gfx_stats* stats);
+
+/* ---- segmented intersection (reference operators.py:485-525) ------------
+ * counts_d int32[num_pairs]; total out. */
+GFX_API int gfx_segmented_intersect(gfx_graph* g, const int32_t* u_d, const int32_t* v_d,
+                            int64_t num_pairs, int32_t* counts_d, int64_t* total);
+
+/* ---- generic advance / filter with the closed device-functor registry ---
+ * (reference operators.py:218-266, 360-384; SURVEY 8(b) functor table) */
+#define GFX_FN_NONE 0
+#define GFX_FN_BFS_CLAIM 1   /* bfs.py:118-121 */
+#define GFX_FN_BFS_IDEMP 2   /* bfs.py:113-116 */
+#define GFX_FN_SSSP_RELAX 3  /* sssp.py:95-103 */
+#define GFX_FN_TC_ORIENT 4   /* tc.py:57-59 */
+#define GFX_FN_LABEL_EQ 5    /* vertex_cond labels[v] == value */
+#define GFX_FN_LABEL_NE 6    /* vertex_cond labels[v] != value */
+
+typedef struct gfx_functor_args {
+  int32_t* labels_d;   /* int32 labels / distances */
+  int32_t* preds_d;    /* int32 preds (may be NULL) */
+  int64_t value;       /* depth / compared value */
+} gfx_functor_args;
+
+#define GFX_KIND_V2V 0
+#define GFX_KIND_V2E 1
+#define GFX_KIND_E2V 2
+#define GFX_KIND_E2E 3
+
+/* Push advance over fin_d[0..nin) (vertex or edge ids by kind).  Output ids
+ * (cond-true images) are written to fout_d (capacity fout_cap); *nout gets
+ * the count.  Returns GFX_EINVAL if the output would overflow. */
+GFX_API int gfx_advance(gfx_graph* g, const int32_t* fin_d, int64_t nin, int kind,
+                int functor_id, const gfx_functor_args* args, int32_t* fout_d,
+                int64_t fout_cap, int64_t* nout, int64_t* edges);
+/* Filter: keep items satisfying vertex functor, then (EXACT) dedup to the
+ * sorted unique set of survivors (np.unique semantics) or (INEXACT) cull. */
+GFX_API int gfx_filter(gfx_graph* g, const int32_t* fin_d, int64_t nin, int mode,
+               int functor_id, const gfx_functor_args* args, int64_t domain,
+               int32_t* fout_d, int64_t* nout);
+
+/* ---- bit-exact R-MAT + canonical CSR builder ----------------------------
+ * (reference generators.py:22-52, graph.py:158-203, graph.py:227-246)
+ * pcg_state/pcg_inc: the numpy PCG64 state of default_rng(seed) as (hi, lo)
+ * 64-bit halves.  Phase 1 writes the symmetrised, sorted, unique keys
+ * (src<<scale | dst) to keys_d (capacity 2*edge_factor*2^scale) and returns
+ * their count; phase 2 turns them into row_d int64[n+1] and col_d int32[m]. */
+GFX_API int gfx_rmat_keys(gfx_ctx* ctx, int scale, int edge_factor, const double* cum3,
+                  uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                  uint64_t inc_lo, int make_undirected, uint64_t* keys_d,
+                  int64_t* num_keys);
+GFX_API int gfx_keys_to_csr(gfx_ctx* ctx, const uint64_t* keys_d, int64_t num_keys, int scale,
+                    int64_t* row_d, int32_t* col_d);
+/* assign_random_weights(g, lo, hi, seed) for a canonical undirected CSR:
+ * per undirected pair (u<v) in sorted order, w = lo + bounded(u32 stream). */
+GFX_API int gfx_assign_weights(gfx_graph* g, int64_t lo, int64_t hi, uint64_t state_hi,
+                       uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                       int32_t* w_d);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GFX_H */

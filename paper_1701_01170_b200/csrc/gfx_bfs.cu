@@ -1,0 +1,556 @@
+// Breadth-first search on sm_100a: load-balanced push expansion, bitmap pull
+// (bottom-up) expansion, and the direction-optimising level loop.
+//
+// Reference: primitives/bfs.py:42-159 (loop), operators.py:218-266 (push
+// advance), operators.py:131-153 (compare_and_swap claim), operators.py:
+// 269-307 + direction.py:73-89 (pull step), operators.py:360-384 (exact
+// filter), load_balance.py:157-176 (LB plan), direction.py:52-70 (decision).
+//
+// Device state per traversal (HBM, graph-owned scratch):
+//   visited  uint32[words]   set-once claim bitmap (L2-resident: n/8 bytes)
+//   front[2] uint32[words]   frontier bitmaps for pull levels (double buffer)
+//   order    int32[n]        every level's frontier queue, concatenated
+//   scan     int64[n+1]      exclusive degree prefix of the current queue
+//   rowbase  int64[n]        row[F[i]] (saves a scattered re-read)
+//   part     int32[m/T+2]    tile -> first item (LB partition)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "gfx_device.cuh"
+#include "gfx_direction.cuh"
+#include "gfx_internal.cuh"
+
+namespace gfx {
+
+constexpr int kExpandBlock = 256;
+
+// ---------------------------------------------------------------------------
+// Push expansion over one LB tile of kTile output slots.
+//   Stage: warps copy each overlapping adjacency segment into shared memory
+//          with coalesced 4-byte cp.async (LDGSTS), recording the owner.
+//   Claim: each slot tests the visited bit (plain load: a stale 0 only costs
+//          an atomic), then atomicOr claims it (first claimer wins, as the
+//          reference CAS; bfs.py:118-121).  Winners write label/pred and are
+//          staged in shared memory, then appended with ONE global atomic per
+//          tile (frontier queue in shared-memory-staged buffers).
+// IDEMP: no claim atomics -- label test + plain store, duplicates allowed and
+//        culled afterwards by the filter (bfs.py:113-116, 162-166).
+// ---------------------------------------------------------------------------
+template <bool IDEMP>
+__global__ void __launch_bounds__(kExpandBlock)
+    k_bfs_expand(const int32_t* __restrict__ F, const unsigned long long* __restrict__ nf_d,
+                 const int64_t* __restrict__ scan, const int64_t* __restrict__ rowbase,
+                 const int32_t* __restrict__ part, const Counters* __restrict__ plan,
+                 const int32_t* __restrict__ col, uint32_t* __restrict__ visited,
+                 int32_t* __restrict__ labels, int32_t* __restrict__ preds, int32_t depth,
+                 int32_t* __restrict__ out, unsigned long long* __restrict__ out_len) {
+  extern __shared__ int32_t smem[];
+  int32_t* buf = smem;               // [kTile] destination ids
+  int32_t* owner = smem + kTile;     // [kTile] source ids
+  int32_t* obuf = smem + 2 * kTile;  // [kTile] winners
+  __shared__ int s_cnt;
+  __shared__ unsigned long long s_gbase;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t ntiles = (int64_t)plan->ntiles;
+  const int64_t total = (int64_t)plan->total;
+  const int64_t nf = (int64_t)*nf_d;
+  if (threadIdx.x == 0) s_cnt = 0;
+
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t s0 = t * kTile;
+    const int64_t s1 = min(s0 + (int64_t)kTile, total);
+    const int64_t i0 = part[t];
+    const int64_t i1 = (t + 1 < ntiles) ? (int64_t)part[t + 1] : nf - 1;
+
+    // ---- stage the tile's adjacency segments into shared memory
+    for (int64_t ib = i0 + (int64_t)warp * 32; ib <= i1; ib += kExpandBlock) {
+      const int64_t i = ib + lane;
+      int64_t lo = 0, len = 0, src_base = 0;
+      int32_t v = 0;
+      if (i <= i1) {
+        const int64_t sc = scan[i], sc1 = scan[i + 1];
+        lo = max(sc, s0);
+        const int64_t hi = min(sc1, s1);
+        len = hi > lo ? hi - lo : 0;
+        src_base = rowbase[i] + (lo - sc);
+        v = F[i];
+      }
+      unsigned mask = __ballot_sync(0xffffffffu, len > 0);
+      while (mask) {
+        const int k = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int64_t klo = __shfl_sync(0xffffffffu, lo, k) - s0;
+        const int64_t klen = __shfl_sync(0xffffffffu, len, k);
+        const int64_t kbase = __shfl_sync(0xffffffffu, src_base, k);
+        const int32_t kv = __shfl_sync(0xffffffffu, v, k);
+        for (int64_t j = lane; j < klen; j += 32) {
+          cp_async4(&buf[klo + j], &col[kbase + j]);
+          owner[klo + j] = kv;
+        }
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+
+    // ---- claim
+    const int nslots = (int)(s1 - s0);
+    for (int jb = 0; jb < nslots; jb += kExpandBlock * 4) {
+      int32_t d[4];
+      uint32_t wv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = jb + u * kExpandBlock + threadIdx.x;
+        d[u] = j < nslots ? buf[j] : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) wv[u] = d[u] >= 0 ? visited[d[u] >> 5] : 0xffffffffu;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = jb + u * kExpandBlock + threadIdx.x;
+        bool won = false;
+        if (d[u] >= 0 && !((wv[u] >> (d[u] & 31)) & 1u)) {
+          if (IDEMP) {
+            if (labels[d[u]] == GFX_UNVISITED) {
+              labels[d[u]] = depth;
+              preds[d[u]] = owner[j];
+              won = true;
+            }
+          } else {
+            const uint32_t bit = 1u << (d[u] & 31);
+            const uint32_t old = atomicOr(&visited[d[u] >> 5], bit);
+            if (!(old & bit)) {
+              won = true;
+              labels[d[u]] = depth;
+              preds[d[u]] = owner[j];
+            }
+          }
+        }
+        const unsigned wm = __ballot_sync(0xffffffffu, won);
+        if (wm) {
+          int base = 0;
+          if (lane == 0) base = atomicAdd(&s_cnt, __popc(wm));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (won) obuf[base + __popc(wm & ((1u << lane) - 1))] = d[u];
+        }
+      }
+    }
+    __syncthreads();
+    const int cnt = s_cnt;
+    if (cnt > 0) {
+      if (threadIdx.x == 0) s_gbase = atomicAdd(out_len, (unsigned long long)cnt);
+      __syncthreads();
+      const unsigned long long gb = s_gbase;
+      for (int j = threadIdx.x; j < cnt; j += kExpandBlock) out[gb + j] = obuf[j];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Filter over a raw (possibly duplicated) idempotent output: bitmap
+// test-and-set keeps one copy of each id (operators.py:360-384).  EXACT uses
+// atomicOr; INEXACT a plain read-modify-write, which may let a few duplicates
+// through exactly as the reference's culling contract allows
+// (operators.py:315-357).  Output capacity is bounded by the raw input.
+// ---------------------------------------------------------------------------
+template <bool EXACT>
+__global__ void __launch_bounds__(256)
+    k_bitmap_filter(const int32_t* __restrict__ in, const unsigned long long* __restrict__ n_in,
+                    uint32_t* __restrict__ seen, int32_t* __restrict__ out,
+                    unsigned long long* __restrict__ out_len) {
+  const int64_t n = (int64_t)*n_in;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    bool keep = false;
+    int32_t v = 0;
+    if (i < n) {
+      v = in[i];
+      const uint32_t bit = 1u << (v & 31);
+      if (EXACT) {
+        keep = !(atomicOr(&seen[v >> 5], bit) & bit);
+      } else {
+        const uint32_t w = seen[v >> 5];
+        keep = !(w & bit);
+        if (keep) seen[v >> 5] = w | bit;
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    unsigned long long b = 0;
+    if (lane == 0 && m) b = atomicAdd(out_len, (unsigned long long)__popc(m));
+    b = __shfl_sync(0xffffffffu, b, 0);
+    if (keep) out[b + __popc(m & ((1u << lane) - 1))] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pull (bottom-up) level.  One warp owns 32 consecutive bitmap words (1024
+// vertices); lanes are vertices.  Candidates = unvisited & in-degree > 0 (the
+// reference keeps isolated vertices in U, but they can never be reached and
+// add 0 to edges_traversed, frontier.py:97-100).  Each candidate scans its
+// in-neighbours in ascending order and stops at the first one in the current
+// frontier bitmap (the reference scans all in-edges, operators.py:269-307;
+// labels are identical, only the work differs).  The warp owns its words, so
+// visited / next-frontier words are written with plain coalesced stores.
+// counters: out_len += |new frontier|, edges += sum of in-degree(U).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+    k_bfs_pull(int64_t words, const uint32_t* __restrict__ nz_in,
+               uint32_t* __restrict__ visited, const uint32_t* __restrict__ front,
+               uint32_t* __restrict__ next, const int64_t* __restrict__ rrow,
+               const int32_t* __restrict__ rcol, int32_t* __restrict__ labels,
+               int32_t* __restrict__ preds, int32_t depth, Counters* __restrict__ ctr) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long found_cnt = 0, in_edges = 0;
+  for (int64_t grp = gw; grp * 32 < words; grp += nwarps) {
+    const int64_t w = grp * 32 + lane;
+    uint32_t vis = 0xffffffffu, cand = 0;
+    if (w < words) {
+      vis = visited[w];
+      cand = ~vis & nz_in[w];
+    }
+    uint32_t newbits_mine = 0;
+    unsigned any = __ballot_sync(0xffffffffu, cand != 0);
+    while (any) {
+      const int k = __ffs(any) - 1;
+      any &= any - 1;
+      const uint32_t c = __shfl_sync(0xffffffffu, cand, k);
+      const int64_t u = (grp * 32 + k) * 32 + lane;
+      bool found = false;
+      if ((c >> lane) & 1u) {
+        const int64_t b = rrow[u], e = rrow[u + 1];
+        in_edges += (unsigned long long)(e - b);
+        for (int64_t p = b; p < e; ++p) {
+          const int32_t s = rcol[p];
+          if ((front[s >> 5] >> (s & 31)) & 1u) {
+            found = true;
+            labels[u] = depth;
+            preds[u] = s;
+            break;
+          }
+        }
+      }
+      const unsigned fm = __ballot_sync(0xffffffffu, found);
+      if (lane == k) newbits_mine = fm;
+      found_cnt += found ? 1 : 0;
+    }
+    if (w < words) {
+      next[w] = newbits_mine;
+      if (newbits_mine) visited[w] = vis | newbits_mine;
+    }
+  }
+  found_cnt = warp_sum_u64(found_cnt);
+  in_edges = warp_sum_u64(in_edges);
+  if (lane == 0) {
+    if (found_cnt) atomicAdd(&ctr->out_len, found_cnt);
+    if (in_edges) atomicAdd(&ctr->edges, in_edges);
+  }
+}
+
+// frontier bitmap -> queue (ascending within each warp's 1024-vertex span)
+__global__ void __launch_bounds__(256)
+    k_bitmap_to_queue(int64_t words, const uint32_t* __restrict__ bm, int32_t* __restrict__ out,
+                      unsigned long long* __restrict__ out_len) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t grp = gw; grp * 32 < words; grp += nwarps) {
+    const int64_t w = grp * 32 + lane;
+    uint32_t x = w < words ? bm[w] : 0u;
+    int tot;
+    const int off = warp_excl_scan(__popc(x), lane, &tot);
+    if (tot == 0) continue;
+    unsigned long long b = 0;
+    if (lane == 0) b = atomicAdd(out_len, (unsigned long long)tot);
+    b = __shfl_sync(0xffffffffu, b, 0) + off;
+    while (x) {
+      const int k = __ffs(x) - 1;
+      x &= x - 1;
+      out[b++] = (int32_t)(w * 32 + k);
+    }
+  }
+}
+
+// queue -> frontier bitmap (bitmap pre-zeroed)
+__global__ void __launch_bounds__(256)
+    k_queue_to_bitmap(const int32_t* __restrict__ F, const unsigned long long* __restrict__ nf_d,
+                      uint32_t* __restrict__ bm) {
+  const int64_t nf = (int64_t)*nf_d;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nf;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = F[i];
+    atomicOr(&bm[v >> 5], 1u << (v & 31));
+  }
+}
+
+__global__ void k_bfs_seed(int32_t src, int32_t* labels, uint32_t* visited, int32_t* order,
+                           Counters* prev) {
+  labels[src] = 0;
+  visited[src >> 5] = 1u << (src & 31);
+  order[0] = src;
+  prev->out_len = 1;
+}
+
+// reached vertices and E_r = sum of out-degrees of reached vertices (the
+// paper's TEPS numerator)
+__global__ void __launch_bounds__(256)
+    k_reached_stats(const int32_t* __restrict__ labels, const int64_t* __restrict__ row,
+                    int64_t n, Counters* __restrict__ ctr) {
+  unsigned long long cnt = 0, deg = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    if (labels[v] != GFX_UNVISITED) {
+      ++cnt;
+      deg += (unsigned long long)(row[v + 1] - row[v]);
+    }
+  }
+  cnt = warp_sum_u64(cnt);
+  deg = warp_sum_u64(deg);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&ctr->aux0, cnt);
+    atomicAdd(&ctr->aux1, deg);
+  }
+}
+
+int reached_stats(gfx_graph* g, const int32_t* labels, int64_t* reached, int64_t* edges) {
+  gfx_ctx* ctx = g->ctx;
+  Counters* c = g->counters + 2;
+  GFX_CK(cudaMemsetAsync(c, 0, sizeof(Counters), ctx->stream));
+  k_reached_stats<<<grid_for(g->n, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(labels, g->row,
+                                                                                   g->n, c);
+  GFX_CK(cudaGetLastError());
+  auto* pin = static_cast<Counters*>(ctx->pinned);
+  GFX_CK(cudaMemcpyAsync(pin, c, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+  GFX_CK(cudaStreamSynchronize(ctx->stream));
+  *reached = (int64_t)pin->aux0;
+  *edges = (int64_t)pin->aux1;
+  return GFX_OK;
+}
+
+struct BfsBuffers {
+  uint32_t *visited, *front0, *front1;
+  int32_t *order, *part, *raw;
+  int64_t *scan, *rowbase;
+};
+
+static int bfs_buffers(gfx_graph* g, bool idemp, BfsBuffers* b) {
+  const int64_t n = g->n, W = g->words;
+  GFX_TRY(scratch_t(g, "bfs_visited", W, &b->visited));
+  GFX_TRY(scratch_t(g, "bfs_front0", W, &b->front0));
+  GFX_TRY(scratch_t(g, "bfs_front1", W, &b->front1));
+  GFX_TRY(scratch_t(g, "q_order", n + 1, &b->order));
+  GFX_TRY(scratch_t(g, "q_scan", n + 2, &b->scan));
+  GFX_TRY(scratch_t(g, "q_rowbase", n + 1, &b->rowbase));
+  GFX_TRY(scratch_t(g, "q_part", g->m / kTile + 4, &b->part));
+  b->raw = nullptr;
+  if (idemp) GFX_TRY(scratch_t(g, "q_raw", g->m + 1, &b->raw));
+  return GFX_OK;
+}
+
+static int expand_smem() { return 3 * kTile * (int)sizeof(int32_t); }
+
+// one push level over the queue at F (size in prev->out_len); winners are
+// appended at out; cur counters receive out_len / total.
+static int push_level(gfx_graph* g, const BfsBuffers& B, const int32_t* F,
+                      const Counters* prev_d, int64_t nf_host, Counters* cur_d, int32_t depth,
+                      bool idemp, bool exact, int32_t* labels, int32_t* preds, int32_t* out) {
+  gfx_ctx* ctx = g->ctx;
+  const unsigned long long* nf_d = &prev_d->out_len;
+  GFX_TRY(launch_degree_scan(g, F, nf_d, nf_host, g->row, B.scan, B.rowbase, B.part, cur_d));
+  const int grid = ctx->sm_count * 4;
+  if (!idemp) {
+    k_bfs_expand<false><<<grid, kExpandBlock, expand_smem(), ctx->stream>>>(
+        F, nf_d, B.scan, B.rowbase, B.part, cur_d, g->col, B.visited, labels, preds, depth, out,
+        &cur_d->out_len);
+  } else {
+    // raw output (duplicates allowed) counted in aux1, then filtered into out
+    k_bfs_expand<true><<<grid, kExpandBlock, expand_smem(), ctx->stream>>>(
+        F, nf_d, B.scan, B.rowbase, B.part, cur_d, g->col, B.visited, labels, preds, depth, B.raw,
+        &cur_d->aux1);
+    if (exact)
+      k_bitmap_filter<true><<<grid, 256, 0, ctx->stream>>>(B.raw, &cur_d->aux1, B.visited, out,
+                                                          &cur_d->out_len);
+    else
+      k_bitmap_filter<false><<<grid, 256, 0, ctx->stream>>>(B.raw, &cur_d->aux1, B.visited, out,
+                                                           &cur_d->out_len);
+  }
+  GFX_CK(cudaGetLastError());
+  return GFX_OK;
+}
+
+static bool g_expand_attr_set = false;
+
+static int set_expand_attrs() {
+  if (g_expand_attr_set) return GFX_OK;
+  GFX_CK(cudaFuncSetAttribute(k_bfs_expand<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              expand_smem()));
+  GFX_CK(cudaFuncSetAttribute(k_bfs_expand<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              expand_smem()));
+  g_expand_attr_set = true;
+  return GFX_OK;
+}
+
+int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool exact,
+                  double do_a, double do_b, int mu_edge, int32_t* labels, int32_t* preds,
+                  gfx_iter_rec* recs, int64_t rec_cap, gfx_stats* st) {
+  gfx_ctx* ctx = g->ctx;
+  const int64_t n = g->n, m = g->m, W = g->words;
+  const bool directed = !(g->flags & GFX_GRAPH_UNDIRECTED);
+  if (direction != GFX_DIR_PUSH) {
+    GFX_REQUIRE(g->rrow != nullptr,
+                "pull traversal on a directed graph needs the reverse adjacency "
+                "(gfx_graph_set_reverse)");
+  }
+  GFX_TRY(set_expand_attrs());
+  BfsBuffers B;
+  GFX_TRY(bfs_buffers(g, idemp, &B));
+  const uint32_t* nz_in = nullptr;
+  {
+    void* p = nullptr;
+    GFX_TRY(scratch(g, directed ? "nz_in" : "nz_out", W * 4, &p));
+    nz_in = static_cast<const uint32_t*>(p);
+  }
+  Counters* C = g->counters;  // C[0], C[1]: per-level double buffer
+  auto* pin = static_cast<Counters*>(ctx->pinned);
+
+  GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  GFX_TRY(fill_i32(ctx, labels, GFX_UNVISITED, n));
+  GFX_CK(cudaMemsetAsync(preds, 0xFF, n * sizeof(int32_t), ctx->stream));
+  GFX_CK(cudaMemsetAsync(B.visited, 0, W * 4, ctx->stream));
+  GFX_CK(cudaMemsetAsync(C, 0, 2 * sizeof(Counters), ctx->stream));
+  k_bfs_seed<<<1, 1, 0, ctx->stream>>>((int32_t)source, labels, B.visited, B.order, &C[1]);
+  GFX_CK(cudaGetLastError());
+
+  int64_t nf = 1, n_u = n, q_off = 0, q_end = 1;
+  int mode_state = GFX_DIR_PUSH;
+  bool queue_form = true;  // current frontier lives at order[q_off .. q_off+nf)
+  uint32_t* fcur = B.front0;
+  uint32_t* fnext = B.front1;
+  int64_t depth = 0, edges_total = 0, switches = 0, nrec = 0;
+
+  while (nf > 0) {
+    ++depth;
+    Counters* prev = &C[(depth + 1) & 1];
+    Counters* cur = &C[depth & 1];
+    GFX_CK(cudaMemsetAsync(cur, 0, sizeof(Counters), ctx->stream));
+    n_u -= nf;
+    DirEstimate est = estimate_mf_mu(n, m, nf, n_u, mu_edge);
+    int mode;
+    if (direction == GFX_DIR_AUTO)
+      mode = decide_direction(mode_state, est, do_a, do_b);
+    else if (direction == GFX_DIR_PULL)
+      mode = depth > 1 ? GFX_DIR_PULL : GFX_DIR_PUSH;
+    else
+      mode = GFX_DIR_PUSH;
+    if (mode != mode_state) ++switches;
+
+    int64_t level_edges = 0, nout = 0;
+    if (mode == GFX_DIR_PUSH) {
+      if (!queue_form) {
+        // previous level produced a bitmap: materialise the queue
+        GFX_CK(cudaMemsetAsync(&prev->aux2, 0, 8, ctx->stream));
+        k_bitmap_to_queue<<<grid_for(W * 32, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(
+            W, fcur, B.order + q_end, &prev->aux2);
+        q_off = q_end;
+        q_end += nf;
+        queue_form = true;
+      }
+      GFX_TRY(push_level(g, B, B.order + q_off, prev, nf, cur, (int32_t)depth, idemp, exact,
+                         labels, preds, B.order + q_end));
+      GFX_CK(cudaMemcpyAsync(pin, cur, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+      GFX_CK(cudaStreamSynchronize(ctx->stream));
+      level_edges = (int64_t)pin->total;
+      nout = (int64_t)pin->out_len;
+      q_off = q_end;
+      q_end += nout;
+    } else {
+      if (queue_form) {
+        GFX_CK(cudaMemsetAsync(fcur, 0, W * 4, ctx->stream));
+        k_queue_to_bitmap<<<grid_for(nf, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(
+            B.order + q_off, &prev->out_len, fcur);
+        GFX_CK(cudaGetLastError());
+      }
+      k_bfs_pull<<<ctx->sm_count * 8, 256, 0, ctx->stream>>>(
+          W, nz_in, B.visited, fcur, fnext, g->rrow, g->rcol, labels, preds, (int32_t)depth, cur);
+      GFX_CK(cudaGetLastError());
+      GFX_CK(cudaMemcpyAsync(pin, cur, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+      GFX_CK(cudaStreamSynchronize(ctx->stream));
+      level_edges = (int64_t)pin->edges;
+      nout = (int64_t)pin->out_len;
+      std::swap(fcur, fnext);
+      queue_form = false;
+    }
+    if (recs && nrec < rec_cap) {
+      gfx_iter_rec& r = recs[nrec];
+      r.iteration = depth;
+      r.frontier_in = nf;
+      r.frontier_out = nout;
+      r.n_u = n_u;
+      r.edges = level_edges;
+      r.m_f = est.m_f;
+      r.m_u = est.m_u;
+      r.mode_before = mode_state;
+      r.decision = mode;
+      r.ms = 0.f;
+      ++nrec;
+    }
+    edges_total += level_edges;
+    mode_state = mode;
+    nf = nout;
+  }
+  GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  GFX_CK(cudaEventSynchronize(ctx->ev1));
+  float ms = 0.f;
+  GFX_CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  if (st) {
+    st->iterations = depth;
+    st->edges_traversed = edges_total;
+    st->direction_switches = switches;
+    st->device_ms = ms;
+    st->num_records = nrec;
+    GFX_TRY(reached_stats(g, labels, &st->reached, &st->edges_reached));
+  }
+  return GFX_OK;
+}
+
+}  // namespace gfx
+
+using namespace gfx;
+
+extern "C" int gfx_bfs(gfx_graph* g, int64_t source, int direction, int idempotent,
+                       int filter_mode, double do_a, double do_b, int mu_edge_based, int loop,
+                       int32_t* labels_d, int32_t* preds_d, gfx_iter_rec* recs, int64_t rec_cap,
+                       gfx_stats* stats) {
+  GFX_REQUIRE(g, "gfx_bfs: null graph");
+  GFX_REQUIRE(source >= 0 && source < g->n, "source %lld out of range", (long long)source);
+  GFX_REQUIRE(direction == GFX_DIR_PUSH || direction == GFX_DIR_PULL || direction == GFX_DIR_AUTO,
+              "unknown direction %d", direction);
+  GFX_REQUIRE(labels_d && preds_d, "gfx_bfs: null output");
+  if (direction == GFX_DIR_AUTO)
+    GFX_REQUIRE(do_a > 0 && do_b > 0, "do_a and do_b must be positive");
+  GFX_CK(cudaSetDevice(g->ctx->device));
+  (void)loop;
+  // INEXACT may leave duplicates (reference operators.py:315-357); the order
+  // queue is sized for unique frontiers, so both modes use the exact
+  // test-and-set cull, which satisfies the inexact contract as well.
+  (void)filter_mode;
+  return bfs_host_loop(g, source, direction, idempotent != 0, true, do_a, do_b, mu_edge_based,
+                       labels_d, preds_d, recs, rec_cap, stats);
+}
+
+extern "C" int gfx_estimate_mf_mu(int64_t n, int64_t m, int64_t n_f, int64_t n_u, int mu_edge,
+                                  double* m_f, double* m_u) {
+  GFX_REQUIRE(n > 0 && m_f && m_u, "gfx_estimate_mf_mu: bad argument");
+  DirEstimate e = estimate_mf_mu(n, m, n_f, n_u, mu_edge);
+  *m_f = e.m_f;
+  *m_u = e.m_u;
+  return GFX_OK;
+}

@@ -1,0 +1,446 @@
+// libgfx core: errors, context, graph handle, scratch, fills, and the fused
+// degree-scan + tile partition shared by every load-balanced expansion.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "gfx_device.cuh"
+#include "gfx_internal.cuh"
+
+namespace gfx {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+int cuda_status(cudaError_t e, const char* what, const char* file, int line) {
+  set_error("CUDA error %s (%s) at %s:%d in %s", cudaGetErrorName(e), cudaGetErrorString(e),
+            file, line, what);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();  // clear sticky-free allocation error
+    return GFX_ENOMEM;
+  }
+  return GFX_ECUDA;
+}
+
+int scratch(gfx_graph* g, const char* name, size_t bytes, void** out, bool* fresh) {
+  auto& b = g->scratch[name];
+  if (fresh) *fresh = false;
+  if (b.bytes < bytes) {
+    if (fresh) *fresh = true;
+    if (b.ptr) {
+      GFX_CK(cudaStreamSynchronize(g->ctx->stream));
+      GFX_CK(cudaFree(b.ptr));
+      b.ptr = nullptr;
+      b.bytes = 0;
+    }
+    size_t want = std::max<size_t>(bytes, 256);
+    GFX_CK(cudaMalloc(&b.ptr, want));
+    b.bytes = want;
+  }
+  *out = b.ptr;
+  return GFX_OK;
+}
+
+unsigned int next_epoch(gfx_graph* g, unsigned int** counter, bool* wrapped) {
+  g->epoch = (g->epoch + 1) % kScanEpochs;
+  *wrapped = false;
+  if (g->epoch == 0) {
+    // wrapped: every per-epoch counter and tile status must be cleared
+    cudaMemsetAsync(g->tile_counters, 0, sizeof(unsigned int) * kScanEpochs, g->ctx->stream);
+    g->epoch = 1;
+    *wrapped = true;
+  }
+  *counter = g->tile_counters + g->epoch;
+  return g->epoch;
+}
+
+int read_counters(gfx_graph* g, Counters* host) {
+  auto* pin = static_cast<Counters*>(g->ctx->pinned);
+  GFX_CK(cudaMemcpyAsync(pin, g->counters, sizeof(Counters), cudaMemcpyDeviceToHost,
+                         g->ctx->stream));
+  GFX_CK(cudaStreamSynchronize(g->ctx->stream));
+  *host = *pin;
+  return GFX_OK;
+}
+
+int zero_counters(gfx_graph* g) {
+  GFX_CK(cudaMemsetAsync(g->counters, 0, sizeof(Counters), g->ctx->stream));
+  return GFX_OK;
+}
+
+template <typename T>
+__global__ void k_fill(T* __restrict__ p, T v, int64_t count) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; i < count; i += stride) p[i] = v;
+}
+
+int fill_i32(gfx_ctx* ctx, int32_t* p, int32_t v, int64_t count) {
+  if (count <= 0) return GFX_OK;
+  k_fill<int32_t><<<grid_for(count, 256, ctx->sm_count * 16), 256, 0, ctx->stream>>>(p, v, count);
+  GFX_CK(cudaGetLastError());
+  return GFX_OK;
+}
+
+int fill_f64(gfx_ctx* ctx, double* p, double v, int64_t count) {
+  if (count <= 0) return GFX_OK;
+  k_fill<double><<<grid_for(count, 256, ctx->sm_count * 16), 256, 0, ctx->stream>>>(p, v, count);
+  GFX_CK(cudaGetLastError());
+  return GFX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Fused degree scan + output-tile partition (decoupled look-back, persistent).
+//
+// Replaces reference load_balance.py:105-113 (compute_scan_offsets) and
+// load_balance.py:157-176 (plan_lb_output: ceil(total/N) chunks of N output
+// slots, each chunk's first source found by searchsorted).  Here the
+// partition falls out of the scan: the item whose slot range covers k*kTile
+// writes part[k] directly, so no search is needed.
+// Tile status word: [63:62] flag (1 aggregate, 2 inclusive prefix),
+// [61:48] epoch, [47:0] value.
+// ---------------------------------------------------------------------------
+constexpr unsigned long long kFlagAgg = 1ull << 62;
+constexpr unsigned long long kFlagPre = 2ull << 62;
+constexpr unsigned long long kValMask = (1ull << 48) - 1;
+
+__device__ __forceinline__ unsigned long long pack_status(unsigned long long flag, unsigned epoch,
+                                                          unsigned long long v) {
+  return flag | ((unsigned long long)(epoch & 0x3FFF) << 48) | (v & kValMask);
+}
+
+__global__ void __launch_bounds__(kScanBlock)
+    k_degree_scan(const int32_t* __restrict__ F, const unsigned long long* __restrict__ nf_d,
+                  const int64_t* __restrict__ row, int64_t* __restrict__ scan,
+                  int64_t* __restrict__ rowbase, int32_t* __restrict__ part,
+                  unsigned long long* status, unsigned int* tile_counter, unsigned epoch,
+                  Counters* __restrict__ ctr) {
+  const int64_t nf = (int64_t)*nf_d;
+  const int64_t ntiles = nf > 0 ? (nf + kScanTileItems - 1) / kScanTileItems : 1;
+  __shared__ unsigned s_tile;
+  __shared__ int64_t s_warp[kScanBlock / 32];
+  __shared__ int64_t s_prefix;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned ep = epoch & 0x3FFF;
+
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    if (tile >= ntiles) break;
+    const int64_t base = tile * kScanTileItems + (int64_t)threadIdx.x * kScanItems;
+
+    int64_t deg[kScanItems];
+    int64_t rb[kScanItems];
+    int64_t tsum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      int64_t i = base + k;
+      deg[k] = 0;
+      rb[k] = 0;
+      if (i < nf) {
+        int32_t v = F[i];
+        int64_t a = row[v], b = row[v + 1];
+        rb[k] = a;
+        deg[k] = b - a;
+      }
+      tsum += deg[k];
+    }
+    // block exclusive scan of per-thread sums
+    int64_t incl = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    int64_t warp_off = 0, agg = 0;
+#pragma unroll
+    for (int w = 0; w < kScanBlock / 32; ++w) {
+      int64_t x = s_warp[w];
+      if (w < warp) warp_off += x;
+      agg += x;
+    }
+    // decoupled look-back (warp 0)
+    if (warp == 0) {
+      int64_t excl = 0;
+      if (tile == 0) {
+        if (lane == 0) atomicExch(&status[0], pack_status(kFlagPre, ep, (unsigned long long)agg));
+      } else {
+        if (lane == 0) atomicExch(&status[tile], pack_status(kFlagAgg, ep, (unsigned long long)agg));
+        int64_t pred = tile - 1;
+        for (;;) {
+          int64_t idx = pred - lane;
+          unsigned long long s = 0;
+          unsigned flag = 0;
+          if (idx >= 0) {
+            do {
+              s = ld_volatile_u64(&status[idx]);
+              flag = (unsigned)(s >> 62);
+              if (((s >> 48) & 0x3FFF) != ep) flag = 0;
+            } while (flag == 0);
+          } else {
+            flag = 2;  // virtual prefix of zero before tile 0
+            s = 0;
+          }
+          unsigned pre_mask = __ballot_sync(0xffffffffu, flag == 2);
+          int64_t val = (int64_t)(s & kValMask);
+          if (pre_mask) {
+            int first = __ffs(pre_mask) - 1;
+            if (lane > first) val = 0;
+            excl += warp_sum_i64(val);
+            break;
+          }
+          excl += warp_sum_i64(val);
+          pred -= 32;
+        }
+        if (lane == 0)
+          atomicExch(&status[tile], pack_status(kFlagPre, ep, (unsigned long long)(excl + agg)));
+      }
+      if (lane == 0) s_prefix = excl;
+    }
+    __syncthreads();
+    int64_t run = s_prefix + warp_off + incl - tsum;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      int64_t i = base + k;
+      if (i < nf) {
+        scan[i] = run;
+        rowbase[i] = rb[k];
+        if (deg[k] > 0) {
+          int64_t k0 = (run + kTile - 1) / kTile;
+          int64_t k1 = (run + deg[k] - 1) / kTile;
+          for (int64_t t = k0; t <= k1; ++t) part[t] = (int32_t)i;
+        }
+      }
+      run += deg[k];
+    }
+    if (tile == ntiles - 1 && threadIdx.x == kScanBlock - 1) {
+      // the last thread of the last tile holds the grand total
+      int64_t total = run;
+      scan[nf] = total;
+      ctr->total = (unsigned long long)total;
+      ctr->ntiles = (unsigned long long)((total + kTile - 1) / kTile);
+    }
+    __syncthreads();
+  }
+}
+
+int launch_degree_scan(gfx_graph* g, const int32_t* F, const unsigned long long* nf_d,
+                       int64_t nf_max, const int64_t* row, int64_t* scan, int64_t* rowbase,
+                       int32_t* part, Counters* counters) {
+  gfx_ctx* ctx = g->ctx;
+  int64_t tiles_max = std::max<int64_t>(1, (nf_max + kScanTileItems - 1) / kScanTileItems);
+  void* sp = nullptr;
+  bool fresh = false;
+  GFX_TRY(scratch(g, "scan_status", (size_t)tiles_max * 8, &sp, &fresh));
+  auto* status = static_cast<unsigned long long*>(sp);
+  unsigned int* tc = nullptr;
+  bool wrapped = false;
+  unsigned ep = next_epoch(g, &tc, &wrapped);
+  if (fresh || wrapped) {
+    // clear the whole (possibly larger) buffer so no stale tag survives
+    GFX_CK(cudaMemsetAsync(status, 0, g->scratch["scan_status"].bytes, ctx->stream));
+  }
+  int grid = (int)std::min<int64_t>(tiles_max, (int64_t)ctx->sm_count * 4);
+  k_degree_scan<<<grid, kScanBlock, 0, ctx->stream>>>(F, nf_d, row, scan, rowbase, part, status, tc,
+                                                      ep, counters);
+  GFX_CK(cudaGetLastError());
+  return GFX_OK;
+}
+
+// graph-constant: bitmap of vertices with nonzero (in-)degree
+__global__ void k_nonzero_bitmap(const int64_t* __restrict__ row, int64_t n, int64_t words,
+                                 uint32_t* __restrict__ bm) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; i < words * 32; i += stride) {
+    bool nz = i < n && row[i + 1] > row[i];
+    unsigned b = __ballot_sync(0xffffffffu, nz);
+    if ((threadIdx.x & 31) == 0) bm[i >> 5] = b;
+  }
+}
+
+__global__ void k_max_degree(const int64_t* __restrict__ row, int64_t n,
+                             unsigned long long* __restrict__ out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long best = 0;
+  for (; i < n; i += stride) {
+    unsigned long long d = (unsigned long long)(row[i + 1] - row[i]);
+    best = d > best ? d : best;
+  }
+  for (int o = 16; o; o >>= 1) {
+    unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
+    best = y > best ? y : best;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(out, best);
+}
+
+int build_nonzero_bitmap(gfx_graph* g, const int64_t* row, const char* name) {
+  uint32_t* bm = nullptr;
+  GFX_TRY(scratch_t(g, name, (size_t)g->words, &bm));
+  int64_t threads = g->words * 32;
+  k_nonzero_bitmap<<<grid_for(threads, 256, g->ctx->sm_count * 16), 256, 0, g->ctx->stream>>>(
+      row, g->n, g->words, bm);
+  GFX_CK(cudaGetLastError());
+  return GFX_OK;
+}
+
+}  // namespace gfx
+
+using namespace gfx;
+
+extern "C" {
+
+int gfx_version(void) { return 1; }
+
+const char* gfx_last_error(void) { return g_last_error.c_str(); }
+
+int gfx_ctx_create(int device, void* stream, gfx_ctx** out) {
+  GFX_REQUIRE(out != nullptr, "gfx_ctx_create: out is NULL");
+  int ndev = 0;
+  GFX_CK(cudaGetDeviceCount(&ndev));
+  GFX_REQUIRE(device >= 0 && device < ndev, "gfx_ctx_create: device %d out of range (%d devices)",
+              device, ndev);
+  GFX_CK(cudaSetDevice(device));
+  auto* c = new gfx_ctx();
+  c->device = device;
+  // NULL selects the legacy default stream, which orders with torch's
+  // default stream (both are the context's NULL stream at driver level)
+  c->stream = static_cast<cudaStream_t>(stream);
+  GFX_CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+  GFX_CK(cudaEventCreate(&c->ev0));
+  GFX_CK(cudaEventCreate(&c->ev1));
+  GFX_CK(cudaMallocHost(&c->pinned, 4096));
+  GFX_CK(cudaStreamSynchronize(c->stream));
+  *out = c;
+  return GFX_OK;
+}
+
+int gfx_ctx_destroy(gfx_ctx* c) {
+  if (!c) return GFX_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  cudaFreeHost(c->pinned);
+  cudaEventDestroy(c->ev0);
+  cudaEventDestroy(c->ev1);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return GFX_OK;
+}
+
+int gfx_ctx_sync(gfx_ctx* c) {
+  GFX_REQUIRE(c, "null ctx");
+  GFX_CK(cudaStreamSynchronize(c->stream));
+  return GFX_OK;
+}
+
+int gfx_ctx_sm_count(gfx_ctx* c) { return c ? c->sm_count : 0; }
+
+int gfx_graph_create(gfx_ctx* ctx, int64_t n, int64_t m, const int64_t* row_d,
+                     const int32_t* col_d, const int32_t* w_d, int flags, gfx_graph** out) {
+  GFX_REQUIRE(ctx && out, "gfx_graph_create: null argument");
+  GFX_REQUIRE(n >= 0 && n < (int64_t)INT32_MAX, "gfx_graph_create: n=%lld out of int32 range",
+              (long long)n);
+  GFX_REQUIRE(m >= 0, "gfx_graph_create: m < 0");
+  GFX_REQUIRE(row_d != nullptr, "gfx_graph_create: row_offsets is NULL");
+  GFX_REQUIRE(m == 0 || col_d != nullptr, "gfx_graph_create: column_indices is NULL");
+  GFX_CK(cudaSetDevice(ctx->device));
+  auto* g = new gfx_graph();
+  g->ctx = ctx;
+  g->n = n;
+  g->m = m;
+  g->row = row_d;
+  g->col = col_d;
+  g->w = w_d;
+  g->flags = flags;
+  g->words = (n + 31) / 32;
+  if (flags & GFX_GRAPH_UNDIRECTED) {
+    g->rrow = row_d;
+    g->rcol = col_d;
+  }
+  int st = cudaMalloc(&g->counters, sizeof(Counters) * 4) == cudaSuccess ? GFX_OK : GFX_ENOMEM;
+  if (st != GFX_OK) {
+    delete g;
+    set_error("gfx_graph_create: cannot allocate counters");
+    return st;
+  }
+  cudaMemsetAsync(g->counters, 0, sizeof(Counters) * 4, ctx->stream);
+  if (cudaMalloc(&g->tile_counters, sizeof(unsigned int) * kScanEpochs) != cudaSuccess) {
+    cudaFree(g->counters);
+    delete g;
+    set_error("gfx_graph_create: cannot allocate tile counters");
+    return GFX_ENOMEM;
+  }
+  cudaMemsetAsync(g->tile_counters, 0, sizeof(unsigned int) * kScanEpochs, ctx->stream);
+  // max degree + nonzero bitmaps (graph constants)
+  auto* pin = static_cast<unsigned long long*>(ctx->pinned);
+  unsigned long long* dmax = reinterpret_cast<unsigned long long*>(g->counters) + 31;
+  cudaMemsetAsync(dmax, 0, 8, ctx->stream);
+  if (n > 0) {
+    k_max_degree<<<grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(row_d, n, dmax);
+    st = build_nonzero_bitmap(g, row_d, "nz_out");
+    if (st != GFX_OK) {
+      delete g;
+      return st;
+    }
+  }
+  cudaMemcpyAsync(pin, dmax, 8, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) {
+    delete g;
+    return cuda_status(e, "graph create", __FILE__, __LINE__);
+  }
+  g->max_deg = (int64_t)pin[0];
+  *out = g;
+  return GFX_OK;
+}
+
+int gfx_graph_set_reverse(gfx_graph* g, const int64_t* rrow_d, const int32_t* rcol_d) {
+  GFX_REQUIRE(g && rrow_d && (g->m == 0 || rcol_d), "gfx_graph_set_reverse: null argument");
+  g->rrow = rrow_d;
+  g->rcol = rcol_d;
+  if (g->n > 0) GFX_TRY(build_nonzero_bitmap(g, rrow_d, "nz_in"));
+  GFX_CK(cudaStreamSynchronize(g->ctx->stream));
+  return GFX_OK;
+}
+
+int gfx_graph_destroy(gfx_graph* g) {
+  if (!g) return GFX_OK;
+  cudaSetDevice(g->ctx->device);
+  cudaStreamSynchronize(g->ctx->stream);
+  for (auto& kv : g->scratch) cudaFree(kv.second.ptr);
+  cudaFree(g->counters);
+  cudaFree(g->tile_counters);
+  delete g;
+  return GFX_OK;
+}
+
+int64_t gfx_graph_max_degree(gfx_graph* g) { return g ? g->max_deg : -1; }
+
+int gfx_graph_trim(gfx_graph* g) {
+  GFX_REQUIRE(g, "null graph");
+  GFX_CK(cudaStreamSynchronize(g->ctx->stream));
+  for (auto it = g->scratch.begin(); it != g->scratch.end();) {
+    if (it->first.rfind("nz_", 0) == 0 || it->first.rfind("keep_", 0) == 0) {
+      ++it;
+      continue;
+    }
+    cudaFree(it->second.ptr);
+    it = g->scratch.erase(it);
+  }
+  return GFX_OK;
+}
+
+}  // extern "C"

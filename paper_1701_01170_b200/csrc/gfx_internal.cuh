@@ -1,0 +1,142 @@
+// Internal declarations shared by the libgfx translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+#include <unordered_map>
+
+#include "../../include/gfx.h"
+
+namespace gfx {
+
+// ---------------------------------------------------------------------------
+// error plumbing: thread-local message, status codes from gfx.h
+// ---------------------------------------------------------------------------
+void set_error(const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* what, const char* file, int line);
+
+#define GFX_CK(call)                                                            \
+  do {                                                                          \
+    cudaError_t _e = (call);                                                    \
+    if (_e != cudaSuccess) return ::gfx::cuda_status(_e, #call, __FILE__, __LINE__); \
+  } while (0)
+
+#define GFX_TRY(expr)            \
+  do {                           \
+    int _s = (expr);             \
+    if (_s != GFX_OK) return _s; \
+  } while (0)
+
+#define GFX_REQUIRE(cond, ...)         \
+  do {                                 \
+    if (!(cond)) {                     \
+      ::gfx::set_error(__VA_ARGS__);   \
+      return GFX_EINVAL;               \
+    }                                  \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// device-side counters block (one per graph, mirrored in pinned host memory)
+// ---------------------------------------------------------------------------
+struct Counters {
+  unsigned long long out_len;    // items appended to the output queue
+  unsigned long long edges;      // expansion slots / in-degree sums this step
+  unsigned long long total;      // scan total (expansion size)
+  unsigned long long ntiles;     // expansion tiles
+  unsigned long long aux0;       // kernel-specific
+  unsigned long long aux1;
+  unsigned long long aux2;
+  unsigned long long aux3;
+};
+
+struct gfx_buffer {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace gfx
+
+struct gfx_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int sm_count = 148;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  void* pinned = nullptr;  // 4 KB pinned host staging
+};
+
+struct gfx_graph {
+  gfx_ctx* ctx = nullptr;
+  int64_t n = 0, m = 0;
+  const int64_t* row = nullptr;
+  const int32_t* col = nullptr;
+  const int32_t* w = nullptr;
+  const int64_t* rrow = nullptr;  // reverse adjacency (== row/col if undirected)
+  const int32_t* rcol = nullptr;
+  int flags = 0;
+  int64_t max_deg = 0;
+  int64_t words = 0;              // ceil(n/32)
+  std::unordered_map<std::string, gfx::gfx_buffer> scratch;
+  gfx::Counters* counters = nullptr;  // device
+  // oriented CSR for TC
+  int64_t m_oriented = -1;
+  // decoupled look-back bookkeeping (per graph): epoch tags + per-epoch
+  // dynamic tile counters, both cleared when the epoch wraps
+  unsigned int epoch = 0;
+  unsigned int* tile_counters = nullptr;
+};
+
+namespace gfx {
+
+constexpr int kScanEpochs = 1 << 14;  // matches the 14-bit status tag
+
+// lazily allocated, graph-owned scratch buffer (never shrinks)
+int scratch(gfx_graph* g, const char* name, size_t bytes, void** out, bool* fresh = nullptr);
+template <typename T>
+inline int scratch_t(gfx_graph* g, const char* name, size_t count, T** out) {
+  return scratch(g, name, count * sizeof(T), reinterpret_cast<void**>(out));
+}
+
+// next decoupled-look-back epoch; returns the per-epoch tile counter and
+// whether the epoch wrapped (status buffers must then be cleared)
+unsigned int next_epoch(gfx_graph* g, unsigned int** counter, bool* wrapped);
+
+// read the counters block to host (stream-synchronous)
+int read_counters(gfx_graph* g, Counters* host);
+int zero_counters(gfx_graph* g);
+
+// fills
+int fill_i32(gfx_ctx* ctx, int32_t* p, int32_t v, int64_t count);
+int fill_f64(gfx_ctx* ctx, double* p, double v, int64_t count);
+
+// grid helpers
+inline int grid_for(int64_t items, int block, int cap_blocks) {
+  int64_t b = (items + block - 1) / block;
+  if (b < 1) b = 1;
+  if (b > cap_blocks) b = cap_blocks;
+  return static_cast<int>(b);
+}
+
+// the degree-scan + tile partition used by every load-balanced expansion
+// (reference load_balance.py:105-113 compute_scan_offsets and :157-176
+// plan_lb_output, fused).  Inputs: frontier ids F[0..nf) (nf read from
+// device *nf_d), CSR row offsets.  Outputs: scan[0..nf] exclusive prefix of
+// degrees, rowbase[i] = row[F[i]], part[k] = item holding slot k*kTile,
+// counters->total / ntiles.
+constexpr int kTile = 4096;          // expansion slots per tile
+constexpr int kScanBlock = 256;
+constexpr int kScanItems = 8;        // items per thread in the scan
+constexpr int kScanTileItems = kScanBlock * kScanItems;
+
+// reached count and E_r from an int32 label array (UNVISITED = INT32_MAX)
+int reached_stats(gfx_graph* g, const int32_t* labels, int64_t* reached, int64_t* edges);
+
+int launch_degree_scan(gfx_graph* g, const int32_t* F, const unsigned long long* nf_d,
+                       int64_t nf_max, const int64_t* row, int64_t* scan,
+                       int64_t* rowbase, int32_t* part, Counters* counters);
+
+}  // namespace gfx
