@@ -20,136 +20,61 @@
 
 #include "gfx_device.cuh"
 #include "gfx_direction.cuh"
+#include "gfx_expand.cuh"
 #include "gfx_internal.cuh"
 
 namespace gfx {
 
-constexpr int kExpandBlock = 256;
-
 // ---------------------------------------------------------------------------
-// Push expansion over one LB tile of kTile output slots.
-//   Stage: warps copy each overlapping adjacency segment into shared memory
-//          with coalesced 4-byte cp.async (LDGSTS), recording the owner.
-//   Claim: each slot tests the visited bit (plain load: a stale 0 only costs
-//          an atomic), then atomicOr claims it (first claimer wins, as the
-//          reference CAS; bfs.py:118-121).  Winners write label/pred and are
-//          staged in shared memory, then appended with ONE global atomic per
-//          tile (frontier queue in shared-memory-staged buffers).
-// IDEMP: no claim atomics -- label test + plain store, duplicates allowed and
-//        culled afterwards by the filter (bfs.py:113-116, 162-166).
+// BFS push functors for the LB expansion (gfx_expand.cuh).
+// Claim: test the visited bit with a plain load (a stale 0 only costs an
+// atomic), then atomicOr; the first claimer wins like the reference CAS
+// (operators.py:131-153, bfs.py:118-121) and writes label + pred.
+// Idempotent: label test + plain store, duplicates culled afterwards by the
+// bitmap filter (bfs.py:113-116, 162-166).
 // ---------------------------------------------------------------------------
-template <bool IDEMP>
-__global__ void __launch_bounds__(kExpandBlock)
-    k_bfs_expand(const int32_t* __restrict__ F, const unsigned long long* __restrict__ nf_d,
-                 const int64_t* __restrict__ scan, const int64_t* __restrict__ rowbase,
-                 const int32_t* __restrict__ part, const Counters* __restrict__ plan,
-                 const int32_t* __restrict__ col, uint32_t* __restrict__ visited,
-                 int32_t* __restrict__ labels, int32_t* __restrict__ preds, int32_t depth,
-                 int32_t* __restrict__ out, unsigned long long* __restrict__ out_len) {
-  extern __shared__ int32_t smem[];
-  int32_t* buf = smem;               // [kTile] destination ids
-  int32_t* owner = smem + kTile;     // [kTile] source ids
-  int32_t* obuf = smem + 2 * kTile;  // [kTile] winners
-  __shared__ int s_cnt;
-  __shared__ unsigned long long s_gbase;
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t ntiles = (int64_t)plan->ntiles;
-  const int64_t total = (int64_t)plan->total;
-  const int64_t nf = (int64_t)*nf_d;
-  if (threadIdx.x == 0) s_cnt = 0;
-
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t s0 = t * kTile;
-    const int64_t s1 = min(s0 + (int64_t)kTile, total);
-    const int64_t i0 = part[t];
-    const int64_t i1 = (t + 1 < ntiles) ? (int64_t)part[t + 1] : nf - 1;
-
-    // ---- stage the tile's adjacency segments into shared memory
-    for (int64_t ib = i0 + (int64_t)warp * 32; ib <= i1; ib += kExpandBlock) {
-      const int64_t i = ib + lane;
-      int64_t lo = 0, len = 0, src_base = 0;
-      int32_t v = 0;
-      if (i <= i1) {
-        const int64_t sc = scan[i], sc1 = scan[i + 1];
-        lo = max(sc, s0);
-        const int64_t hi = min(sc1, s1);
-        len = hi > lo ? hi - lo : 0;
-        src_base = rowbase[i] + (lo - sc);
-        v = F[i];
-      }
-      unsigned mask = __ballot_sync(0xffffffffu, len > 0);
-      while (mask) {
-        const int k = __ffs(mask) - 1;
-        mask &= mask - 1;
-        const int64_t klo = __shfl_sync(0xffffffffu, lo, k) - s0;
-        const int64_t klen = __shfl_sync(0xffffffffu, len, k);
-        const int64_t kbase = __shfl_sync(0xffffffffu, src_base, k);
-        const int32_t kv = __shfl_sync(0xffffffffu, v, k);
-        for (int64_t j = lane; j < klen; j += 32) {
-          cp_async4(&buf[klo + j], &col[kbase + j]);
-          owner[klo + j] = kv;
-        }
-      }
-    }
-    cp_async_wait_all();
-    __syncthreads();
-
-    // ---- claim
-    const int nslots = (int)(s1 - s0);
-    for (int jb = 0; jb < nslots; jb += kExpandBlock * 4) {
-      int32_t d[4];
-      uint32_t wv[4];
+struct BfsClaimOp {
+  static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
+  uint32_t* visited;
+  int32_t* labels;
+  int32_t* preds;
+  int32_t depth;
+  uint32_t wv[4];
+  __device__ int32_t src_value(int32_t) const { return 0; }
+  __device__ void prefetch(const int32_t d[4]) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = jb + u * kExpandBlock + threadIdx.x;
-        d[u] = j < nslots ? buf[j] : -1;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) wv[u] = d[u] >= 0 ? visited[d[u] >> 5] : 0xffffffffu;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = jb + u * kExpandBlock + threadIdx.x;
-        bool won = false;
-        if (d[u] >= 0 && !((wv[u] >> (d[u] & 31)) & 1u)) {
-          if (IDEMP) {
-            if (labels[d[u]] == GFX_UNVISITED) {
-              labels[d[u]] = depth;
-              preds[d[u]] = owner[j];
-              won = true;
-            }
-          } else {
-            const uint32_t bit = 1u << (d[u] & 31);
-            const uint32_t old = atomicOr(&visited[d[u] >> 5], bit);
-            if (!(old & bit)) {
-              won = true;
-              labels[d[u]] = depth;
-              preds[d[u]] = owner[j];
-            }
-          }
-        }
-        const unsigned wm = __ballot_sync(0xffffffffu, won);
-        if (wm) {
-          int base = 0;
-          if (lane == 0) base = atomicAdd(&s_cnt, __popc(wm));
-          base = __shfl_sync(0xffffffffu, base, 0);
-          if (won) obuf[base + __popc(wm & ((1u << lane) - 1))] = d[u];
-        }
-      }
-    }
-    __syncthreads();
-    const int cnt = s_cnt;
-    if (cnt > 0) {
-      if (threadIdx.x == 0) s_gbase = atomicAdd(out_len, (unsigned long long)cnt);
-      __syncthreads();
-      const unsigned long long gb = s_gbase;
-      for (int j = threadIdx.x; j < cnt; j += kExpandBlock) out[gb + j] = obuf[j];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) s_cnt = 0;
-    __syncthreads();
+    for (int u = 0; u < 4; ++u) wv[u] = d[u] >= 0 ? visited[d[u] >> 5] : 0xffffffffu;
   }
-}
+  __device__ bool visit(int u, int32_t d, int32_t s, int32_t, int32_t, int64_t) {
+    const uint32_t bit = 1u << (d & 31);
+    if (wv[u] & bit) return false;
+    if (atomicOr(&visited[d >> 5], bit) & bit) return false;
+    labels[d] = depth;
+    preds[d] = s;
+    return true;
+  }
+};
+
+struct BfsIdempOp {
+  static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
+  const uint32_t* visited;
+  int32_t* labels;
+  int32_t* preds;
+  int32_t depth;
+  uint32_t wv[4];
+  __device__ int32_t src_value(int32_t) const { return 0; }
+  __device__ void prefetch(const int32_t d[4]) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) wv[u] = d[u] >= 0 ? visited[d[u] >> 5] : 0xffffffffu;
+  }
+  __device__ bool visit(int u, int32_t d, int32_t s, int32_t, int32_t, int64_t) {
+    if ((wv[u] >> (d & 31)) & 1u) return false;
+    if (labels[d] != GFX_UNVISITED) return false;
+    labels[d] = depth;
+    preds[d] = s;
+    return true;
+  }
+};
 
 // ---------------------------------------------------------------------------
 // Filter over a raw (possibly duplicated) idempotent output: bitmap
@@ -355,8 +280,6 @@ static int bfs_buffers(gfx_graph* g, bool idemp, BfsBuffers* b) {
   return GFX_OK;
 }
 
-static int expand_smem() { return 3 * kTile * (int)sizeof(int32_t); }
-
 // one push level over the queue at F (size in prev->out_len); winners are
 // appended at out; cur counters receive out_len / total.
 static int push_level(gfx_graph* g, const BfsBuffers& B, const int32_t* F,
@@ -364,37 +287,23 @@ static int push_level(gfx_graph* g, const BfsBuffers& B, const int32_t* F,
                       bool idemp, bool exact, int32_t* labels, int32_t* preds, int32_t* out) {
   gfx_ctx* ctx = g->ctx;
   const unsigned long long* nf_d = &prev_d->out_len;
-  GFX_TRY(launch_degree_scan(g, F, nf_d, nf_host, g->row, B.scan, B.rowbase, B.part, cur_d));
-  const int grid = ctx->sm_count * 4;
   if (!idemp) {
-    k_bfs_expand<false><<<grid, kExpandBlock, expand_smem(), ctx->stream>>>(
-        F, nf_d, B.scan, B.rowbase, B.part, cur_d, g->col, B.visited, labels, preds, depth, out,
-        &cur_d->out_len);
-  } else {
-    // raw output (duplicates allowed) counted in aux1, then filtered into out
-    k_bfs_expand<true><<<grid, kExpandBlock, expand_smem(), ctx->stream>>>(
-        F, nf_d, B.scan, B.rowbase, B.part, cur_d, g->col, B.visited, labels, preds, depth, B.raw,
-        &cur_d->aux1);
-    if (exact)
-      k_bitmap_filter<true><<<grid, 256, 0, ctx->stream>>>(B.raw, &cur_d->aux1, B.visited, out,
-                                                          &cur_d->out_len);
-    else
-      k_bitmap_filter<false><<<grid, 256, 0, ctx->stream>>>(B.raw, &cur_d->aux1, B.visited, out,
-                                                           &cur_d->out_len);
+    BfsClaimOp op{B.visited, labels, preds, depth, {}};
+    return lb_advance(g, F, nf_d, nf_host, cur_d, B.scan, B.rowbase, B.part, op, out,
+                      &cur_d->out_len);
   }
+  // raw output (duplicates allowed) counted in aux1, then filtered into out
+  BfsIdempOp op{B.visited, labels, preds, depth, {}};
+  GFX_TRY(lb_advance(g, F, nf_d, nf_host, cur_d, B.scan, B.rowbase, B.part, op, B.raw,
+                     &cur_d->aux1));
+  const int grid = ctx->sm_count * 4;
+  if (exact)
+    k_bitmap_filter<true><<<grid, 256, 0, ctx->stream>>>(B.raw, &cur_d->aux1, B.visited, out,
+                                                        &cur_d->out_len);
+  else
+    k_bitmap_filter<false><<<grid, 256, 0, ctx->stream>>>(B.raw, &cur_d->aux1, B.visited, out,
+                                                         &cur_d->out_len);
   GFX_CK(cudaGetLastError());
-  return GFX_OK;
-}
-
-static bool g_expand_attr_set = false;
-
-static int set_expand_attrs() {
-  if (g_expand_attr_set) return GFX_OK;
-  GFX_CK(cudaFuncSetAttribute(k_bfs_expand<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              expand_smem()));
-  GFX_CK(cudaFuncSetAttribute(k_bfs_expand<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              expand_smem()));
-  g_expand_attr_set = true;
   return GFX_OK;
 }
 
@@ -409,7 +318,6 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
                 "pull traversal on a directed graph needs the reverse adjacency "
                 "(gfx_graph_set_reverse)");
   }
-  GFX_TRY(set_expand_attrs());
   BfsBuffers B;
   GFX_TRY(bfs_buffers(g, idemp, &B));
   const uint32_t* nz_in = nullptr;
@@ -426,7 +334,8 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
   GFX_CK(cudaMemsetAsync(preds, 0xFF, n * sizeof(int32_t), ctx->stream));
   GFX_CK(cudaMemsetAsync(B.visited, 0, W * 4, ctx->stream));
   GFX_CK(cudaMemsetAsync(C, 0, 2 * sizeof(Counters), ctx->stream));
-  k_bfs_seed<<<1, 1, 0, ctx->stream>>>((int32_t)source, labels, B.visited, B.order, &C[1]);
+  // level d reads its input size from C[(d-1)&1] and writes C[d&1]
+  k_bfs_seed<<<1, 1, 0, ctx->stream>>>((int32_t)source, labels, B.visited, B.order, &C[0]);
   GFX_CK(cudaGetLastError());
 
   int64_t nf = 1, n_u = n, q_off = 0, q_end = 1;
@@ -438,7 +347,7 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
 
   while (nf > 0) {
     ++depth;
-    Counters* prev = &C[(depth + 1) & 1];
+    Counters* prev = &C[(depth - 1) & 1];
     Counters* cur = &C[depth & 1];
     GFX_CK(cudaMemsetAsync(cur, 0, sizeof(Counters), ctx->stream));
     n_u -= nf;

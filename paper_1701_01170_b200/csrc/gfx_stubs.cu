@@ -12,7 +12,4 @@ int gfx_tc_count(gfx_graph*, int32_t*, int32_t*, int32_t*, int64_t*, gfx_stats*)
 int gfx_segmented_intersect(gfx_graph*, const int32_t*, const int32_t*, int64_t, int32_t*, int64_t*) NOT_YET("gfx_segmented_intersect")
 int gfx_advance(gfx_graph*, const int32_t*, int64_t, int, int, const gfx_functor_args*, int32_t*, int64_t, int64_t*, int64_t*) NOT_YET("gfx_advance")
 int gfx_filter(gfx_graph*, const int32_t*, int64_t, int, int, const gfx_functor_args*, int64_t, int32_t*, int64_t*) NOT_YET("gfx_filter")
-int gfx_rmat_keys(gfx_ctx*, int, int, const double*, uint64_t, uint64_t, uint64_t, uint64_t, int, uint64_t*, int64_t*) NOT_YET("gfx_rmat_keys")
-int gfx_keys_to_csr(gfx_ctx*, const uint64_t*, int64_t, int, int64_t*, int32_t*) NOT_YET("gfx_keys_to_csr")
-int gfx_assign_weights(gfx_graph*, int64_t, int64_t, uint64_t, uint64_t, uint64_t, uint64_t, int32_t*) NOT_YET("gfx_assign_weights")
 }
