@@ -1,0 +1,478 @@
+"""Benchmark: BFS GTEPS on R-MAT scale-24 ef16 (BASELINE.json metric) on B200.
+
+    python bench.py --gpus N --steps K --warmup W [--impl ours|reference]
+
+One step = one direction-optimised BFS from vertex 0 (reference
+primitives/bfs.py with direction="auto", do_a=1e-3, do_b=0.2) over the
+canonical undirected R-MAT scale-24 edge-factor-16 graph (seed 0), built
+bit-exactly on the GPU (csrc/gfx_rmat.cu).  ``value`` = E_r * steps * ranks /
+max-over-ranks device time, E_r = sum of degrees of reached vertices (the
+paper's TEPS numerator).
+
+Also reported on the same line: push-only BFS and SSSP (delta 32) GTEPS, the
+roofline of the dominant kernel, the end-to-end number through the public
+API with host buffers, the CPU baseline (oracle port of the reference
+algorithm on this host) and GPU clocks sampled during the run.
+
+--impl reference times the reference's own CPU algorithm (the numpy port in
+oracle/graphfx_port.py, the reference being pure Python) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--scale", type=int, default=24)
+    ap.add_argument("--edge-factor", type=int, default=16)
+    ap.add_argument("--source", type=int, default=0)
+    ap.add_argument("--direction", default="auto", choices=["auto", "push", "pull"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip push-only / SSSP lines")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing (one process per GPU)
+# ---------------------------------------------------------------------------
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+
+    def init(self, backend):
+        if self.world > 1:
+            import torch.distributed as dist
+
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group(backend=backend)
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            if self.pg.get_backend() == "nccl":
+                import torch
+
+                self.pg.barrier(device_ids=[self.local])
+                torch.cuda.synchronize()
+            else:
+                self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+
+        dev = torch.device("cuda", self.local) if self.pg.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+
+        dev = torch.device("cuda", self.local) if self.pg.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.pg.all_reduce(t)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the run (B200_PROFILING.md clocks line)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        samples = []
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                samples.append((float(parts[0]), float(parts[1]), float(parts[2]), parts[3:7]))
+            except ValueError:
+                continue
+        if not samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        loaded = [s for s in samples if s[2] > 0] or samples
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in loaded for i, v in enumerate(s[3])
+                          if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(s[0] for s in loaded),
+                "sm_max_mhz": max(s[1] for s in samples), "reasons": reasons,
+                "samples": len(samples), "samples_under_load": len([s for s in samples if s[2] > 0])}
+
+
+def measured_peak_gbs() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, dist: Dist):
+    import numpy as np
+    import torch
+
+    torch.cuda.set_device(dist.local)
+    dist.init("nccl")
+    import paper_1701_01170_b200 as gfx
+    from paper_1701_01170_b200 import _native
+    from paper_1701_01170_b200.generators import rmat_device_graph
+    from paper_1701_01170_b200.primitives.bfs import bfs_device
+
+    t_build = time.perf_counter()
+    dg = rmat_device_graph(args.scale, args.edge_factor, 0)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t_build
+    ctx = dg.ctx
+    n = dg.num_vertices
+    labels = torch.empty(n, dtype=torch.int32, device="cuda")
+    preds = torch.empty(n, dtype=torch.int32, device="cuda")
+
+    def step(direction):
+        return bfs_device(dg, args.source, direction=direction, labels=labels, preds=preds)[2]
+
+    sampler = ClockSampler(dist.local) if dist.rank == 0 or True else None
+    sampler.start()
+    for _ in range(max(args.warmup, 3)):
+        st = step(args.direction)
+    e_r = st.edges_reached
+    # timed region: K steps back to back (inputs -- the 2.2 GB CSR -- exceed L2;
+    # every BFS re-initialises its labels/bitmaps, so nothing carries over)
+    dist.barrier()
+    torch.cuda.synchronize()
+    l0 = _native.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        step(args.direction)
+    ev1.record()
+    torch.cuda.synchronize()
+    launches = _native.launch_count() - l0
+    dist.barrier()
+    local_ms = ev0.elapsed_time(ev1)
+    t_ms = dist.max(local_ms)
+    # a sustained window so the clock sampler sees the GPU under load
+    t_end = time.perf_counter() + 1.5
+    while time.perf_counter() < t_end:
+        step(args.direction)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+
+    total_edges = dist.sum(float(e_r) * args.steps)
+    value = total_edges / (t_ms * 1e-3) / 1e9
+    ms_per_step = t_ms / args.steps
+
+    # ---- roofline of the dominant kernel (per-level events, separate run)
+    ctx.set_timing(True)
+    prof = step(args.direction)
+    ctx.set_timing(False)
+    peak, peak_kind = measured_peak_gbs()
+    lv = max(prof.device_levels, key=lambda x: x["ms"])
+    achieved = lv["bytes_alg"] / (lv["ms"] * 1e-3) / 1e9
+    kernel = "k_bfs_pull" if lv["mode"] == "pull" else "k_degree_scan+k_lb_expand<BfsClaimOp>"
+    whole = prof.bytes_alg / (ms_per_step * 1e-3) / 1e9
+    roofline = {
+        "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+        "frac": round(achieved / peak, 4), "traffic": None,
+        "kernel": kernel, "level": lv["iteration"], "level_ms": round(lv["ms"], 4),
+        "bytes_alg_per_launch": lv["bytes_alg"], "peak_source": peak_kind,
+        "whole_bfs": {"bytes_alg": prof.bytes_alg, "achieved_gbs": round(whole, 1),
+                      "frac": round(whole / peak, 4)},
+        "levels": [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in d.items()}
+                   for d in prof.device_levels],
+    }
+
+    out = {
+        "metric": "BFS GTEPS on R-MAT scale-24 ef16 (direction-optimized, source 0)",
+        "value": round(value, 2), "unit": "GTEPS", "n_gpus": dist.world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": f"bfs_do_rmat_s{args.scale}_ef{args.edge_factor}_src{args.source}",
+                   "scale": args.scale, "edge_factor": args.edge_factor, "seed": 0,
+                   "source": args.source, "direction": args.direction, "do_a": 1e-3,
+                   "do_b": 0.2, "n": n, "m": dg.num_edges, "E_r": e_r,
+                   "reached": st.reached, "parallelism": f"replicas{dist.world}" if dist.world > 1 else "1gpu",
+                   "l2": "inputs larger than L2 (CSR 2.2 GB vs 126 MB L2); per-BFS state re-initialised each step",
+                   "graph_build_s": round(build_s, 3)},
+        "roofline": roofline, "gpu_launches": int(launches), "clocks": clocks,
+    }
+
+    # ---- extras: push-only BFS and SSSP on the same graph
+    if not args.no_extras:
+        out["extras"] = extras(args, dg, labels, preds, dist, peak)
+
+    # ---- end to end through the public API with host buffers
+    if not args.no_e2e:
+        out["e2e"] = e2e(args, dg, dist, e_r)
+
+    # ---- CPU baseline (oracle port of the reference algorithm), rank 0, N=1
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args, dg, e_r)
+    if dist.rank == 0:
+        print(json.dumps(out), flush=True)
+    dist.close()
+
+
+def extras(args, dg, labels, preds, dist, peak):
+    import torch
+
+    from paper_1701_01170_b200.primitives.bfs import bfs_device
+
+    res = {}
+    # push-only BFS
+    for _ in range(2):
+        st = bfs_device(dg, args.source, direction="push", labels=labels, preds=preds)[2]
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k = max(3, args.steps // 2)
+    ev0.record()
+    for _ in range(k):
+        bfs_device(dg, args.source, direction="push", labels=labels, preds=preds)
+    ev1.record()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / k
+    res["bfs_push"] = {"gteps": round(st.edges_reached / (ms * 1e-3) / 1e9, 2),
+                       "ms": round(ms, 4), "bytes_alg": st.bytes_alg,
+                       "frac_of_hbm": round(st.bytes_alg / (ms * 1e-3) / 1e9 / peak, 4)}
+    try:
+        from paper_1701_01170_b200.primitives.sssp import sssp_device
+    except ImportError:
+        return res
+    try:
+        from paper_1701_01170_b200.generators import rmat_device_graph
+
+        dgw = rmat_device_graph(args.scale, args.edge_factor, 0, weights=(1, 64), weight_seed=0)
+        for delta in (32, None):
+            for _ in range(2):
+                st = sssp_device(dgw, args.source, delta=delta)[2]
+            ev0.record()
+            for _ in range(k):
+                sssp_device(dgw, args.source, delta=delta)
+            ev1.record()
+            torch.cuda.synchronize()
+            ms = ev0.elapsed_time(ev1) / k
+            res[f"sssp_delta{delta or 'default'}"] = {
+                "gteps": round(st.edges_reached / (ms * 1e-3) / 1e9, 2), "ms": round(ms, 4),
+                "relaxed_slots": st.work_slots, "work_inflation": round(st.work_slots / max(st.edges_reached, 1), 3),
+                "bytes_alg": st.bytes_alg,
+                "frac_of_hbm": round(st.bytes_alg / (ms * 1e-3) / 1e9 / peak, 4)}
+        del dgw
+    except Exception as exc:  # report, do not hide
+        res["sssp_error"] = repr(exc)
+    return res
+
+
+def e2e(args, dg, dist, e_r):
+    """Public-API BFS with host buffers: each step uploads the CSR from pinned
+    host memory through the C ABI (gfx_graph_create over fresh device
+    buffers), runs the BFS and reads the reference-layout int64 labels and
+    preds back to the host."""
+    import numpy as np
+    import torch
+
+    from paper_1701_01170_b200 import _native
+    from paper_1701_01170_b200._results import labels_to_host, preds_to_host
+    from paper_1701_01170_b200.graph import DeviceGraph
+    from paper_1701_01170_b200.primitives.bfs import bfs_device
+
+    row_h = dg.row.cpu().pin_memory()
+    col_h = dg.col.cpu().pin_memory()
+    n, m = dg.num_vertices, dg.num_edges
+    row_d = torch.empty_like(dg.row)
+    col_d = torch.empty_like(dg.col)
+    labels = torch.empty(n, dtype=torch.int32, device="cuda")
+    preds = torch.empty(n, dtype=torch.int32, device="cuda")
+
+    def one():
+        row_d.copy_(row_h, non_blocking=True)
+        col_d.copy_(col_h, non_blocking=True)
+        g = DeviceGraph.from_tensors(row_d, col_d, None, undirected=True)
+        _, _, st = bfs_device(g, args.source, direction=args.direction, labels=labels, preds=preds)
+        lab = labels_to_host(labels)
+        prd = preds_to_host(preds)
+        return st, lab, prd
+
+    one()
+    dist.barrier()
+    torch.cuda.synchronize()
+    k = max(2, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(k):
+        st, lab, prd = one()
+    torch.cuda.synchronize()
+    dt = dist.max((time.perf_counter() - t0) / k)
+    total = dist.sum(float(e_r))
+    h2d = row_h.numel() * 8 + col_h.numel() * 4
+    d2h = n * 8 * 2
+    resident = None
+    # resident-graph variant (graph cached on device, per-query copies only)
+    t0 = time.perf_counter()
+    for _ in range(k):
+        bfs_device(dg, args.source, direction=args.direction, labels=labels, preds=preds)
+        labels_to_host(labels)
+        preds_to_host(preds)
+    torch.cuda.synchronize()
+    dt_res = dist.max((time.perf_counter() - t0) / k)
+    resident = {"value": round(total / dt_res / 1e9, 3), "unit": "GTEPS",
+                "h2d_bytes_per_step": 8, "d2h_bytes_per_step": d2h,
+                "ms_per_step": round(dt_res * 1e3, 3)}
+    return {"value": round(total / dt / 1e9, 3), "unit": "GTEPS", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": round(dt * 1e3, 3), "steps": k,
+            "what": "upload CSR from pinned host + BFS + int64 labels/preds to host, per step",
+            "graph_resident": resident}
+
+
+def _host_graph(dg):
+    import numpy as np
+
+    row = dg.row.cpu().numpy().astype(np.int64)
+    col = dg.col.cpu().numpy().astype(np.int64)
+    return row, col
+
+
+def cpu_baseline(args, dg, e_r):
+    """One DO-BFS of the oracle port (numpy restatement of reference
+    bfs.py) on this host, same graph, same source."""
+    from oracle import graphfx_port as port
+
+    row, col = _host_graph(dg)
+    t0 = time.perf_counter()
+    labels, _, _, _ = port.bfs(row, col, args.source, direction=args.direction,
+                               rev=(row, col, None))
+    dt = time.perf_counter() - t0
+    return {"value": round(e_r / dt / 1e9, 6), "unit": "GTEPS", "cores": 1, "kind": "port",
+            "sample": f"one {args.direction} BFS from vertex {args.source} on the full "
+                      f"s{args.scale} graph ({dt:.1f} s), oracle/graphfx_port.py (numpy, 1 thread)",
+            "seconds": round(dt, 3), "host_cpus": os.cpu_count()}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference's CPU algorithm (oracle port) on host cores
+# ---------------------------------------------------------------------------
+def run_reference(args, dist: Dist):
+    if dist.world > 1 and dist.rank != 0:
+        return
+    import torch
+
+    from oracle import graphfx_port as port
+    from paper_1701_01170_b200.generators import rmat_device_graph
+
+    # input generation only (untimed, reference bench.py:1-7): the bit-exact
+    # GPU builder, downloaded to the reference's int64 host layout
+    torch.cuda.set_device(dist.local)
+    dg = rmat_device_graph(args.scale, args.edge_factor, 0)
+    row, col = _host_graph(dg)
+    del dg
+    torch.cuda.empty_cache()
+    import numpy as np
+
+    deg = np.diff(row)
+
+    def one():
+        labels, _, _, _ = port.bfs(row, col, args.source, direction=args.direction,
+                                   rev=(row, col, None))
+        return labels
+
+    for _ in range(args.warmup):
+        labels = one()
+    e_r = int(deg[labels != port.UNVISITED].sum())
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one()
+    dt = (time.perf_counter() - t0) / args.steps
+    v = e_r / dt / 1e9
+    out = {"metric": "BFS GTEPS on R-MAT scale-24 ef16 (direction-optimized, source 0)",
+           "value": round(v, 6), "unit": "GTEPS", "n_gpus": dist.world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+           "impl": "reference",
+           "config": {"workload": f"bfs_do_rmat_s{args.scale}_ef{args.edge_factor}_src{args.source}",
+                      "scale": args.scale, "edge_factor": args.edge_factor, "source": args.source,
+                      "direction": args.direction, "E_r": e_r},
+           "cpu_baseline": {"value": round(v, 6), "unit": "GTEPS", "cores": 1, "kind": "port",
+                            "sample": "full DO-BFS per step, oracle/graphfx_port.py (numpy "
+                                      "restatement of reference bfs.py), 1 thread"},
+           "e2e": {"value": round(v, 6), "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse_args()
+    dist = Dist()
+    if args.impl == "reference":
+        run_reference(args, dist)
+    else:
+        run_ours(args, dist)
+
+
+if __name__ == "__main__":
+    main()

@@ -77,8 +77,11 @@ typedef struct gfx_iter_rec {
   double m_u;
   int32_t mode_before;  /* GFX_DIR_PUSH / GFX_DIR_PULL */
   int32_t decision;
-  float ms;             /* device time of the iteration (0 when not timed) */
+  float ms;             /* device time of the iteration (0 unless timing is on) */
   int32_t pad;
+  int64_t candidates;   /* pull: |U| with in-degree > 0 */
+  int64_t work;         /* push: expansion slots; pull: early-exit probes S(U) */
+  int64_t bytes_alg;    /* algorithmic HBM bytes of the iteration */
 } gfx_iter_rec;
 
 typedef struct gfx_stats {
@@ -95,6 +98,10 @@ typedef struct gfx_stats {
 
 /* ---- library / context ------------------------------------------------ */
 GFX_API int gfx_version(void);
+/* number of kernels libgfx has launched in this process (monotonic) */
+GFX_API int64_t gfx_launch_count(void);
+/* per-iteration CUDA-event timing of the level loops (records' ms field) */
+GFX_API int gfx_ctx_set_timing(gfx_ctx* ctx, int enabled);
 GFX_API const char* gfx_last_error(void);
 /* stream: a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); NULL
  * selects the legacy default stream */

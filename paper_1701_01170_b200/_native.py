@@ -31,6 +31,7 @@ class IterRec(Structure):
         ("iteration", c_int64), ("frontier_in", c_int64), ("frontier_out", c_int64),
         ("n_u", c_int64), ("edges", c_int64), ("m_f", c_double), ("m_u", c_double),
         ("mode_before", c_int32), ("decision", c_int32), ("ms", c_float), ("pad", c_int32),
+        ("candidates", c_int64), ("work", c_int64), ("bytes_alg", c_int64),
     ]
 
 
@@ -50,6 +51,8 @@ class FunctorArgs(Structure):
 # name -> (restype, argtypes); every function listed here is declared in gfx.h
 _SIGS = {
     "gfx_version": (c_int, []),
+    "gfx_launch_count": (c_int64, []),
+    "gfx_ctx_set_timing": (c_int, [c_void_p, c_int]),
     "gfx_last_error": (c_char_p, []),
     "gfx_ctx_create": (c_int, [c_int, c_void_p, POINTER(c_void_p)]),
     "gfx_ctx_destroy": (c_int, [c_void_p]),
@@ -167,6 +170,13 @@ class Context:
 
     def sync(self) -> None:
         call("gfx_ctx_sync", self.handle)
+
+    def set_timing(self, enabled: bool) -> None:
+        call("gfx_ctx_set_timing", self.handle, int(bool(enabled)))
+
+
+def launch_count() -> int:
+    return int(load_library().gfx_launch_count())
 
 
 def ptr(t) -> c_void_p:

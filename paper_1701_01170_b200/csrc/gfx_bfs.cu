@@ -123,7 +123,8 @@ __global__ void __launch_bounds__(256)
 // frontier bitmap (the reference scans all in-edges, operators.py:269-307;
 // labels are identical, only the work differs).  The warp owns its words, so
 // visited / next-frontier words are written with plain coalesced stores.
-// counters: out_len += |new frontier|, edges += sum of in-degree(U).
+// counters: out_len += |new frontier|, edges += sum of in-degree(U),
+//           aux0 += early-exit probes S(U), aux1 += |U| (in-degree > 0).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256)
     k_bfs_pull(int64_t words, const uint32_t* __restrict__ nz_in,
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(256)
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  unsigned long long found_cnt = 0, in_edges = 0;
+  unsigned long long found_cnt = 0, in_edges = 0, probes = 0, cands = 0;
   for (int64_t grp = gw; grp * 32 < words; grp += nwarps) {
     const int64_t w = grp * 32 + lane;
     uint32_t vis = 0xffffffffu, cand = 0;
@@ -153,7 +154,9 @@ __global__ void __launch_bounds__(256)
       if ((c >> lane) & 1u) {
         const int64_t b = rrow[u], e = rrow[u + 1];
         in_edges += (unsigned long long)(e - b);
-        for (int64_t p = b; p < e; ++p) {
+        ++cands;
+        int64_t p = b;
+        for (; p < e; ++p) {
           const int32_t s = rcol[p];
           if ((front[s >> 5] >> (s & 31)) & 1u) {
             found = true;
@@ -162,6 +165,7 @@ __global__ void __launch_bounds__(256)
             break;
           }
         }
+        probes += (unsigned long long)(found ? p - b + 1 : e - b);
       }
       const unsigned fm = __ballot_sync(0xffffffffu, found);
       if (lane == k) newbits_mine = fm;
@@ -174,9 +178,13 @@ __global__ void __launch_bounds__(256)
   }
   found_cnt = warp_sum_u64(found_cnt);
   in_edges = warp_sum_u64(in_edges);
+  probes = warp_sum_u64(probes);
+  cands = warp_sum_u64(cands);
   if (lane == 0) {
     if (found_cnt) atomicAdd(&ctr->out_len, found_cnt);
     if (in_edges) atomicAdd(&ctr->edges, in_edges);
+    if (probes) atomicAdd(&ctr->aux0, probes);
+    if (cands) atomicAdd(&ctr->aux1, cands);
   }
 }
 
@@ -249,7 +257,7 @@ int reached_stats(gfx_graph* g, const int32_t* labels, int64_t* reached, int64_t
   gfx_ctx* ctx = g->ctx;
   Counters* c = g->counters + 2;
   GFX_CK(cudaMemsetAsync(c, 0, sizeof(Counters), ctx->stream));
-  k_reached_stats<<<grid_for(g->n, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(labels, g->row,
+  GFX_LAUNCH(k_reached_stats, grid_for(g->n, 256, ctx->sm_count * 8), 256, 0, ctx->stream, labels, g->row,
                                                                                    g->n, c);
   GFX_CK(cudaGetLastError());
   auto* pin = static_cast<Counters*>(ctx->pinned);
@@ -298,10 +306,10 @@ static int push_level(gfx_graph* g, const BfsBuffers& B, const int32_t* F,
                      &cur_d->aux1));
   const int grid = ctx->sm_count * 4;
   if (exact)
-    k_bitmap_filter<true><<<grid, 256, 0, ctx->stream>>>(B.raw, &cur_d->aux1, B.visited, out,
+    GFX_LAUNCH((k_bitmap_filter<true>), grid, 256, 0, ctx->stream, B.raw, &cur_d->aux1, B.visited, out,
                                                         &cur_d->out_len);
   else
-    k_bitmap_filter<false><<<grid, 256, 0, ctx->stream>>>(B.raw, &cur_d->aux1, B.visited, out,
+    GFX_LAUNCH((k_bitmap_filter<false>), grid, 256, 0, ctx->stream, B.raw, &cur_d->aux1, B.visited, out,
                                                          &cur_d->out_len);
   GFX_CK(cudaGetLastError());
   return GFX_OK;
@@ -335,7 +343,7 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
   GFX_CK(cudaMemsetAsync(B.visited, 0, W * 4, ctx->stream));
   GFX_CK(cudaMemsetAsync(C, 0, 2 * sizeof(Counters), ctx->stream));
   // level d reads its input size from C[(d-1)&1] and writes C[d&1]
-  k_bfs_seed<<<1, 1, 0, ctx->stream>>>((int32_t)source, labels, B.visited, B.order, &C[0]);
+  GFX_LAUNCH(k_bfs_seed, 1, 1, 0, ctx->stream, (int32_t)source, labels, B.visited, B.order, &C[0]);
   GFX_CK(cudaGetLastError());
 
   int64_t nf = 1, n_u = n, q_off = 0, q_end = 1;
@@ -343,7 +351,7 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
   bool queue_form = true;  // current frontier lives at order[q_off .. q_off+nf)
   uint32_t* fcur = B.front0;
   uint32_t* fnext = B.front1;
-  int64_t depth = 0, edges_total = 0, switches = 0, nrec = 0;
+  int64_t depth = 0, edges_total = 0, switches = 0, nrec = 0, bytes_total = 0, work_total = 0;
 
   while (nf > 0) {
     ++depth;
@@ -361,12 +369,13 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
       mode = GFX_DIR_PUSH;
     if (mode != mode_state) ++switches;
 
-    int64_t level_edges = 0, nout = 0;
+    int64_t level_edges = 0, nout = 0, work = 0, cands = 0, bytes = 0;
+    if (ctx->timing) GFX_CK(cudaEventRecord(ctx->lev0, ctx->stream));
     if (mode == GFX_DIR_PUSH) {
       if (!queue_form) {
         // previous level produced a bitmap: materialise the queue
         GFX_CK(cudaMemsetAsync(&prev->aux2, 0, 8, ctx->stream));
-        k_bitmap_to_queue<<<grid_for(W * 32, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(
+        GFX_LAUNCH(k_bitmap_to_queue, grid_for(W * 32, 256, ctx->sm_count * 8), 256, 0, ctx->stream, 
             W, fcur, B.order + q_end, &prev->aux2);
         q_off = q_end;
         q_end += nf;
@@ -374,26 +383,37 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
       }
       GFX_TRY(push_level(g, B, B.order + q_off, prev, nf, cur, (int32_t)depth, idemp, exact,
                          labels, preds, B.order + q_end));
+      if (ctx->timing) GFX_CK(cudaEventRecord(ctx->lev1, ctx->stream));
       GFX_CK(cudaMemcpyAsync(pin, cur, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
       GFX_CK(cudaStreamSynchronize(ctx->stream));
       level_edges = (int64_t)pin->total;
       nout = (int64_t)pin->out_len;
+      work = level_edges;
+      // push: frontier id + row pair per item, one col id per slot, label +
+      // queue write per discovered vertex
+      bytes = 20 * nf + 4 * level_edges + 8 * nout;
       q_off = q_end;
       q_end += nout;
     } else {
       if (queue_form) {
         GFX_CK(cudaMemsetAsync(fcur, 0, W * 4, ctx->stream));
-        k_queue_to_bitmap<<<grid_for(nf, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(
+        GFX_LAUNCH(k_queue_to_bitmap, grid_for(nf, 256, ctx->sm_count * 8), 256, 0, ctx->stream, 
             B.order + q_off, &prev->out_len, fcur);
         GFX_CK(cudaGetLastError());
       }
-      k_bfs_pull<<<ctx->sm_count * 8, 256, 0, ctx->stream>>>(
+      GFX_LAUNCH(k_bfs_pull, ctx->sm_count * 8, 256, 0, ctx->stream, 
           W, nz_in, B.visited, fcur, fnext, g->rrow, g->rcol, labels, preds, (int32_t)depth, cur);
       GFX_CK(cudaGetLastError());
+      if (ctx->timing) GFX_CK(cudaEventRecord(ctx->lev1, ctx->stream));
       GFX_CK(cudaMemcpyAsync(pin, cur, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
       GFX_CK(cudaStreamSynchronize(ctx->stream));
       level_edges = (int64_t)pin->edges;
       nout = (int64_t)pin->out_len;
+      work = (int64_t)pin->aux0;
+      cands = (int64_t)pin->aux1;
+      // pull: id + row per candidate, one col id per early-exit probe, label
+      // + frontier write per discovered vertex
+      bytes = 12 * cands + 4 * work + 8 * nout;
       std::swap(fcur, fnext);
       queue_form = false;
     }
@@ -409,9 +429,15 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
       r.mode_before = mode_state;
       r.decision = mode;
       r.ms = 0.f;
+      if (ctx->timing) GFX_CK(cudaEventElapsedTime(&r.ms, ctx->lev0, ctx->lev1));
+      r.candidates = cands;
+      r.work = work;
+      r.bytes_alg = bytes;
       ++nrec;
     }
     edges_total += level_edges;
+    bytes_total += bytes;
+    work_total += work;
     mode_state = mode;
     nf = nout;
   }
@@ -425,6 +451,8 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
     st->direction_switches = switches;
     st->device_ms = ms;
     st->num_records = nrec;
+    st->bytes_alg = bytes_total;
+    st->work_slots = work_total;
     GFX_TRY(reached_stats(g, labels, &st->reached, &st->edges_reached));
   }
   return GFX_OK;

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 
 #include "gfx_device.cuh"
@@ -11,6 +12,9 @@
 namespace gfx {
 
 static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   char buf[1024];
@@ -86,14 +90,14 @@ __global__ void k_fill(T* __restrict__ p, T v, int64_t count) {
 
 int fill_i32(gfx_ctx* ctx, int32_t* p, int32_t v, int64_t count) {
   if (count <= 0) return GFX_OK;
-  k_fill<int32_t><<<grid_for(count, 256, ctx->sm_count * 16), 256, 0, ctx->stream>>>(p, v, count);
+  GFX_LAUNCH((k_fill<int32_t>), grid_for(count, 256, ctx->sm_count * 16), 256, 0, ctx->stream, p, v, count);
   GFX_CK(cudaGetLastError());
   return GFX_OK;
 }
 
 int fill_f64(gfx_ctx* ctx, double* p, double v, int64_t count) {
   if (count <= 0) return GFX_OK;
-  k_fill<double><<<grid_for(count, 256, ctx->sm_count * 16), 256, 0, ctx->stream>>>(p, v, count);
+  GFX_LAUNCH((k_fill<double>), grid_for(count, 256, ctx->sm_count * 16), 256, 0, ctx->stream, p, v, count);
   GFX_CK(cudaGetLastError());
   return GFX_OK;
 }
@@ -253,7 +257,7 @@ int launch_degree_scan(gfx_graph* g, const int32_t* F, const unsigned long long*
     GFX_CK(cudaMemsetAsync(status, 0, g->scratch["scan_status"].bytes, ctx->stream));
   }
   int grid = (int)std::min<int64_t>(tiles_max, (int64_t)ctx->sm_count * 4);
-  k_degree_scan<<<grid, kScanBlock, 0, ctx->stream>>>(F, nf_d, row, scan, rowbase, part, status, tc,
+  GFX_LAUNCH(k_degree_scan, grid, kScanBlock, 0, ctx->stream, F, nf_d, row, scan, rowbase, part, status, tc,
                                                       ep, counters);
   GFX_CK(cudaGetLastError());
   return GFX_OK;
@@ -291,7 +295,7 @@ int build_nonzero_bitmap(gfx_graph* g, const int64_t* row, const char* name) {
   uint32_t* bm = nullptr;
   GFX_TRY(scratch_t(g, name, (size_t)g->words, &bm));
   int64_t threads = g->words * 32;
-  k_nonzero_bitmap<<<grid_for(threads, 256, g->ctx->sm_count * 16), 256, 0, g->ctx->stream>>>(
+  GFX_LAUNCH(k_nonzero_bitmap, grid_for(threads, 256, g->ctx->sm_count * 16), 256, 0, g->ctx->stream, 
       row, g->n, g->words, bm);
   GFX_CK(cudaGetLastError());
   return GFX_OK;
@@ -304,6 +308,14 @@ using namespace gfx;
 extern "C" {
 
 int gfx_version(void) { return 1; }
+
+int64_t gfx_launch_count(void) { return (int64_t)g_launches.load(); }
+
+int gfx_ctx_set_timing(gfx_ctx* c, int enabled) {
+  GFX_REQUIRE(c, "null ctx");
+  c->timing = enabled != 0;
+  return GFX_OK;
+}
 
 const char* gfx_last_error(void) { return g_last_error.c_str(); }
 
@@ -322,6 +334,8 @@ int gfx_ctx_create(int device, void* stream, gfx_ctx** out) {
   GFX_CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
   GFX_CK(cudaEventCreate(&c->ev0));
   GFX_CK(cudaEventCreate(&c->ev1));
+  GFX_CK(cudaEventCreate(&c->lev0));
+  GFX_CK(cudaEventCreate(&c->lev1));
   GFX_CK(cudaMallocHost(&c->pinned, 4096));
   GFX_CK(cudaStreamSynchronize(c->stream));
   *out = c;
@@ -335,6 +349,8 @@ int gfx_ctx_destroy(gfx_ctx* c) {
   cudaFreeHost(c->pinned);
   cudaEventDestroy(c->ev0);
   cudaEventDestroy(c->ev1);
+  cudaEventDestroy(c->lev0);
+  cudaEventDestroy(c->lev1);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
   return GFX_OK;
@@ -389,7 +405,7 @@ int gfx_graph_create(gfx_ctx* ctx, int64_t n, int64_t m, const int64_t* row_d,
   unsigned long long* dmax = reinterpret_cast<unsigned long long*>(g->counters) + 31;
   cudaMemsetAsync(dmax, 0, 8, ctx->stream);
   if (n > 0) {
-    k_max_degree<<<grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream>>>(row_d, n, dmax);
+    GFX_LAUNCH(k_max_degree, grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream, row_d, n, dmax);
     st = build_nonzero_bitmap(g, row_d, "nz_out");
     if (st != GFX_OK) {
       delete g;

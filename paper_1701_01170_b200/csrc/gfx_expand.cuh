@@ -177,7 +177,7 @@ int lb_advance(gfx_graph* g, const int32_t* F, const unsigned long long* nf_d, i
   GFX_TRY(launch_degree_scan(g, F, nf_d, nf_max, g->row, scan, rowbase, part, plan_ctr));
   GFX_TRY(set_expand_smem<Op>());
   const int grid = ctx->sm_count * expand_ctas_per_sm<Op>();
-  k_lb_expand<Op><<<grid, kExpandBlock, expand_smem_bytes<Op>(), ctx->stream>>>(
+  GFX_LAUNCH((k_lb_expand<Op>), grid, kExpandBlock, expand_smem_bytes<Op>(), ctx->stream, 
       F, nf_d, scan, rowbase, part, plan_ctr, g->col, g->w, op, out, out_len);
   GFX_CK(cudaGetLastError());
   return GFX_OK;

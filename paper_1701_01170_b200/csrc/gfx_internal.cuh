@@ -25,6 +25,14 @@ int cuda_status(cudaError_t e, const char* what, const char* file, int line);
     if (_e != cudaSuccess) return ::gfx::cuda_status(_e, #call, __FILE__, __LINE__); \
   } while (0)
 
+// every kernel launch goes through GFX_LAUNCH so gfx_launch_count() is exact
+void count_launch();
+#define GFX_LAUNCH(K, G, B, S, ST, ...)       \
+  do {                                        \
+    K<<<(G), (B), (S), (ST)>>>(__VA_ARGS__);  \
+    ::gfx::count_launch();                    \
+  } while (0)
+
 #define GFX_TRY(expr)            \
   do {                           \
     int _s = (expr);             \
@@ -67,6 +75,8 @@ struct gfx_ctx {
   int sm_count = 148;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   void* pinned = nullptr;  // 4 KB pinned host staging
+  bool timing = false;     // per-iteration events
+  cudaEvent_t lev0 = nullptr, lev1 = nullptr;
 };
 
 struct gfx_graph {

@@ -218,7 +218,7 @@ extern "C" int gfx_rmat_keys(gfx_ctx* ctx, int scale, int edge_factor, const dou
   const Jump jm = jump_params(m - kRmatEPT, inc);
   const uint64_t threads = (m + kRmatEPT - 1) / kRmatEPT;
   const int grid = grid_for((int64_t)threads, 256, ctx->sm_count * 32);
-  k_rmat_keys<<<grid, 256, 0, ctx->stream>>>(
+  GFX_LAUNCH(k_rmat_keys, grid, 256, 0, ctx->stream, 
       scale, m, state_hi, state_lo, inc_hi, inc_lo, (uint64_t)(jm.a >> 64), (uint64_t)jm.a,
       (uint64_t)(jm.c >> 64), (uint64_t)jm.c, cum3[0], cum3[1], cum3[2], make_undirected, keys_d);
   GFX_CK(cudaGetLastError());
@@ -270,9 +270,9 @@ extern "C" int gfx_keys_to_csr(gfx_ctx* ctx, const uint64_t* keys_d, int64_t num
   GFX_REQUIRE(ctx && keys_d && row_d && (num_keys == 0 || col_d), "gfx_keys_to_csr: null argument");
   GFX_CK(cudaSetDevice(ctx->device));
   const int64_t n = 1ll << scale;
-  k_csr_cols<<<grid_for(num_keys, 256, ctx->sm_count * 32), 256, 0, ctx->stream>>>(
+  GFX_LAUNCH(k_csr_cols, grid_for(num_keys, 256, ctx->sm_count * 32), 256, 0, ctx->stream, 
       keys_d, num_keys, scale, col_d);
-  k_csr_rows<<<grid_for(n + 1, 256, ctx->sm_count * 32), 256, 0, ctx->stream>>>(
+  GFX_LAUNCH(k_csr_rows, grid_for(n + 1, 256, ctx->sm_count * 32), 256, 0, ctx->stream, 
       keys_d, num_keys, scale, n, row_d);
   GFX_CK(cudaGetLastError());
   GFX_CK(cudaStreamSynchronize(ctx->stream));
@@ -300,7 +300,7 @@ extern "C" int gfx_assign_weights(gfx_graph* g, int64_t lo, int64_t hi, uint64_t
   int64_t* base = nullptr;
   GFX_TRY(scratch_t(g, "w_base", n + 1, &base));
   const int grid = grid_for(n, 256, ctx->sm_count * 16);
-  k_upper_counts<<<grid, 256, 0, ctx->stream>>>(g->row, g->col, n, cnt);
+  GFX_LAUNCH(k_upper_counts, grid, 256, 0, ctx->stream, g->row, g->col, n, cnt);
   size_t tb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, base, n, ctx->stream);
   void* tmp = nullptr;
@@ -309,9 +309,9 @@ extern "C" int gfx_assign_weights(gfx_graph* g, int64_t lo, int64_t hi, uint64_t
   if (range1 == 1) {
     GFX_TRY(fill_i32(ctx, w_d, (int32_t)lo, g->m));
   } else {
-    k_upper_weights<<<grid, 256, 0, ctx->stream>>>(g->row, g->col, n, base, state_hi, state_lo,
+    GFX_LAUNCH(k_upper_weights, grid, 256, 0, ctx->stream, g->row, g->col, n, base, state_hi, state_lo,
                                                    inc_hi, inc_lo, lo, range1, w_d);
-    k_lower_weights<<<grid, 256, 0, ctx->stream>>>(g->row, g->col, n, w_d);
+    GFX_LAUNCH(k_lower_weights, grid, 256, 0, ctx->stream, g->row, g->col, n, w_d);
   }
   GFX_CK(cudaGetLastError());
   GFX_CK(cudaStreamSynchronize(ctx->stream));

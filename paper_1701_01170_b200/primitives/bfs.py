@@ -42,6 +42,11 @@ def stats_from_records(primitive, recs, st, count_trace=True) -> RunStats:
                 "m_u": float(r.m_u), "decision": _NAMES[r.decision]})
         stats.record_iteration(int(r.iteration), int(r.frontier_in), int(r.frontier_out),
                                _NAMES.get(r.decision, "push"), float(r.ms))
+        stats.device_levels.append({
+            "iteration": int(r.iteration), "mode": _NAMES.get(r.decision, "push"),
+            "ms": float(r.ms), "bytes_alg": int(r.bytes_alg), "work": int(r.work),
+            "candidates": int(r.candidates), "frontier_in": int(r.frontier_in),
+            "frontier_out": int(r.frontier_out), "edges": int(r.edges)})
     stats.iterations = int(st.iterations)
     stats.edges_traversed = int(st.edges_traversed)
     stats.direction_switches = int(st.direction_switches)
@@ -49,6 +54,7 @@ def stats_from_records(primitive, recs, st, count_trace=True) -> RunStats:
     stats.edges_reached = int(st.edges_reached)
     stats.work_slots = int(st.work_slots)
     stats.device_ms = float(st.device_ms)
+    stats.bytes_alg = int(st.bytes_alg)
     return stats
 
 
