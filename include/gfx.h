@@ -138,9 +138,9 @@ GFX_API int gfx_estimate_mf_mu(int64_t n, int64_t m, int64_t n_f, int64_t n_u, i
                                double* m_f, double* m_u);
 
 /* ---- SSSP near/far (reference primitives/sssp.py:41-121, near_far.py) ---
- * delta <= 0 means +inf (no priority queue).  dist_d int32[n] (INT32_MAX =
- * unreached), preds_d int32[n]. */
-GFX_API int gfx_sssp(gfx_graph* g, int64_t source, int64_t delta, int32_t* dist_d,
+ * delta: bucket width (<= 0 or +inf: no priority queue).  dist_d int32[n]
+ * (INT32_MAX = unreached), preds_d int32[n]. */
+GFX_API int gfx_sssp(gfx_graph* g, int64_t source, double delta, int32_t* dist_d,
              int32_t* preds_d, gfx_iter_rec* recs, int64_t rec_cap, gfx_stats* stats);
 
 /* ---- BC (reference primitives/bc.py:32-116) ----------------------------

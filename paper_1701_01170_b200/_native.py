@@ -68,7 +68,7 @@ _SIGS = {
                         c_int, c_void_p, c_void_p, POINTER(IterRec), c_int64, POINTER(Stats)]),
     "gfx_estimate_mf_mu": (c_int, [c_int64, c_int64, c_int64, c_int64, c_int,
                                    POINTER(c_double), POINTER(c_double)]),
-    "gfx_sssp": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, POINTER(IterRec),
+    "gfx_sssp": (c_int, [c_void_p, c_int64, c_double, c_void_p, c_void_p, POINTER(IterRec),
                          c_int64, POINTER(Stats)]),
     "gfx_bc": (c_int, [c_void_p, POINTER(c_int64), c_int64, c_void_p, POINTER(Stats)]),
     "gfx_cc": (c_int, [c_void_p, c_void_p, POINTER(c_int64), POINTER(Stats)]),

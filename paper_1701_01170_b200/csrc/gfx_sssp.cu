@@ -1,0 +1,289 @@
+// Single-source shortest paths with near/far bucketing on sm_100a.
+//
+// Reference: primitives/sssp.py:41-121 (loop, relax = atomic_min,
+// set_pred + stamp, exact filter on the stamp) and near_far.py:20-85
+// (two-slice pile: near = key < threshold, far keeps its enqueue key; when
+// near drains, threshold += delta, stale far entries -- live key != enqueue
+// key -- are dropped and the rest re-split).
+//
+// Device state:
+//   dp     uint64[n]  (dist << 32 | pred): one 64-bit atomicMin settles the
+//                     distance and a valid predecessor together, so preds are
+//                     always consistent with the final distances
+//   stamp  int32[n]   iteration id of the last enqueue (dedup: each improved
+//                     vertex is enqueued once per iteration, sssp.py:112-115)
+//   near[2] int32[n]  near queues (double buffer)
+//   touched int32[n]  vertices improved this iteration
+//   far / far_key     far pile with enqueue keys, capacity 2n (compacted when
+//                     it would overflow: after dropping stale entries each
+//                     vertex appears at most once)
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "gfx_device.cuh"
+#include "gfx_expand.cuh"
+#include "gfx_internal.cuh"
+
+namespace gfx {
+
+struct SsspRelaxOp {
+  static constexpr bool kWeights = true, kSrcVal = true, kEmitEdge = false;
+  unsigned long long* dp;
+  int32_t* stamp;
+  int32_t it;
+  unsigned long long cur[4];
+  __device__ int32_t src_value(int32_t v) const { return (int32_t)(dp[v] >> 32); }
+  __device__ void prefetch(const int32_t d[4]) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) cur[u] = d[u] >= 0 ? dp[d[u]] : 0ull;
+  }
+  // atomic_min relax (operators.py:111-124): emit d once per iteration when
+  // its distance strictly improved
+  __device__ bool visit(int u, int32_t d, int32_t s, int32_t w, int32_t sdist, int64_t) {
+    const unsigned long long nd = (unsigned long long)(uint32_t)sdist + (uint32_t)w;
+    if (nd >= (cur[u] >> 32)) return false;
+    const unsigned long long key = (nd << 32) | (uint32_t)s;
+    const unsigned long long old = atomicMin(&dp[d], key);
+    if ((old >> 32) <= nd) return false;
+    return atomicExch(&stamp[d], it) != it;
+  }
+};
+
+__global__ void k_sssp_seed(unsigned long long* dp, int32_t src, int32_t* near) {
+  dp[src] = 0xFFFFFFFFull;  // dist 0, pred -1
+  near[0] = src;
+}
+
+// split the improved vertices against the threshold (near_far.py:40-57)
+__global__ void __launch_bounds__(256)
+    k_sssp_split(const int32_t* __restrict__ touched, const unsigned long long* __restrict__ n_d,
+                 const unsigned long long* __restrict__ dp, double threshold,
+                 int32_t* __restrict__ near, unsigned long long* __restrict__ near_len,
+                 int32_t* __restrict__ far, int32_t* __restrict__ far_key,
+                 unsigned long long* __restrict__ far_len) {
+  const int64_t n = (int64_t)*n_d;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    int32_t v = 0;
+    int32_t key = 0;
+    bool valid = i < n, is_near = false;
+    if (valid) {
+      v = touched[i];
+      key = (int32_t)(dp[v] >> 32);
+      is_near = (double)key < threshold;
+    }
+    const unsigned nm = __ballot_sync(0xffffffffu, valid && is_near);
+    const unsigned fm = __ballot_sync(0xffffffffu, valid && !is_near);
+    unsigned long long nb = 0, fb = 0;
+    if (lane == 0) {
+      if (nm) nb = atomicAdd(near_len, (unsigned long long)__popc(nm));
+      if (fm) fb = atomicAdd(far_len, (unsigned long long)__popc(fm));
+    }
+    nb = __shfl_sync(0xffffffffu, nb, 0);
+    fb = __shfl_sync(0xffffffffu, fb, 0);
+    const unsigned below = (1u << lane) - 1;
+    if (valid && is_near) near[nb + __popc(nm & below)] = v;
+    if (valid && !is_near) {
+      const unsigned long long p = fb + __popc(fm & below);
+      far[p] = v;
+      far_key[p] = key;
+    }
+  }
+}
+
+// advance_bucket (near_far.py:68-85): drop stale far entries, split the rest
+// against the new threshold.  With split == false only the stale drop runs
+// (capacity compaction; everything fresh stays far).
+__global__ void __launch_bounds__(256)
+    k_sssp_refar(const int32_t* __restrict__ far, const int32_t* __restrict__ far_key, int64_t n,
+                 const unsigned long long* __restrict__ dp, double threshold, int split,
+                 int32_t* __restrict__ near, unsigned long long* __restrict__ near_len,
+                 int32_t* __restrict__ far2, int32_t* __restrict__ far2_key,
+                 unsigned long long* __restrict__ far2_len) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    bool to_near = false, to_far = false;
+    int32_t v = 0, key = 0;
+    if (i < n) {
+      v = far[i];
+      key = far_key[i];
+      const bool fresh = (int32_t)(dp[v] >> 32) == key;
+      if (fresh) {
+        if (split && (double)key < threshold) to_near = true; else to_far = true;
+      }
+    }
+    const unsigned nm = __ballot_sync(0xffffffffu, to_near);
+    const unsigned fm = __ballot_sync(0xffffffffu, to_far);
+    unsigned long long nb = 0, fb = 0;
+    if (lane == 0) {
+      if (nm) nb = atomicAdd(near_len, (unsigned long long)__popc(nm));
+      if (fm) fb = atomicAdd(far2_len, (unsigned long long)__popc(fm));
+    }
+    nb = __shfl_sync(0xffffffffu, nb, 0);
+    fb = __shfl_sync(0xffffffffu, fb, 0);
+    const unsigned below = (1u << lane) - 1;
+    if (to_near) near[nb + __popc(nm & below)] = v;
+    if (to_far) {
+      const unsigned long long p = fb + __popc(fm & below);
+      far2[p] = v;
+      far2_key[p] = key;
+    }
+  }
+}
+
+__global__ void k_sssp_unpack(const unsigned long long* __restrict__ dp, int64_t n,
+                              int32_t* __restrict__ dist, int32_t* __restrict__ preds) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long x = dp[v];
+    const uint32_t d = (uint32_t)(x >> 32);
+    dist[v] = d == 0xFFFFFFFFu ? GFX_UNVISITED : (int32_t)d;
+    preds[v] = (int32_t)(uint32_t)x;
+  }
+}
+
+int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t* preds,
+             gfx_iter_rec* recs, int64_t rec_cap, gfx_stats* st) {
+  gfx_ctx* ctx = g->ctx;
+  const int64_t n = g->n;
+  unsigned long long* dp;
+  int32_t *stamp, *nearA, *nearB, *touched, *far, *fkey, *far2, *fkey2, *part;
+  int64_t *scan, *rowbase;
+  GFX_TRY(scratch_t(g, "sssp_dp", n, &dp));
+  GFX_TRY(scratch_t(g, "sssp_stamp", n, &stamp));
+  GFX_TRY(scratch_t(g, "q_order", n + 1, &nearA));
+  GFX_TRY(scratch_t(g, "sssp_nearB", n + 1, &nearB));
+  GFX_TRY(scratch_t(g, "sssp_touched", n + 1, &touched));
+  GFX_TRY(scratch_t(g, "sssp_far", 2 * n + 64, &far));
+  GFX_TRY(scratch_t(g, "sssp_fkey", 2 * n + 64, &fkey));
+  GFX_TRY(scratch_t(g, "sssp_far2", 2 * n + 64, &far2));
+  GFX_TRY(scratch_t(g, "sssp_fkey2", 2 * n + 64, &fkey2));
+  GFX_TRY(scratch_t(g, "q_scan", n + 2, &scan));
+  GFX_TRY(scratch_t(g, "q_rowbase", n + 1, &rowbase));
+  GFX_TRY(scratch_t(g, "q_part", g->m / kTile + 4, &part));
+
+  Counters* C = g->counters;  // C[0]/C[1]: near sizes, C[2]: relax plan, C[3]: far
+  auto* pin = static_cast<Counters*>(ctx->pinned);
+  const int grid = ctx->sm_count * 8;
+
+  GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  GFX_CK(cudaMemsetAsync(dp, 0xFF, n * sizeof(unsigned long long), ctx->stream));
+  GFX_CK(cudaMemsetAsync(stamp, 0, n * sizeof(int32_t), ctx->stream));
+  GFX_CK(cudaMemsetAsync(C, 0, 4 * sizeof(Counters), ctx->stream));
+  GFX_LAUNCH(k_sssp_seed, 1, 1, 0, ctx->stream, dp, (int32_t)source, nearA);
+  // near count lives in C[cur].out_len
+  int curq = 0;
+  unsigned long long one = 1;
+  GFX_CK(cudaMemcpyAsync(&C[0].out_len, &one, 8, cudaMemcpyHostToDevice, ctx->stream));
+
+  int64_t nnear = 1, nfar = 0, it = 0, slots_total = 0, bytes_total = 0, nrec = 0;
+  double threshold = delta;
+  int32_t* nearq[2] = {nearA, nearB};
+  while (nnear > 0 || nfar > 0) {
+    if (nnear == 0) {
+      // advance_bucket: threshold += delta, drop stale, re-split
+      threshold += delta;
+      Counters* nxt = &C[curq];
+      GFX_CK(cudaMemsetAsync(nxt, 0, sizeof(Counters), ctx->stream));
+      GFX_CK(cudaMemsetAsync(&C[3].aux1, 0, 8, ctx->stream));
+      GFX_LAUNCH(k_sssp_refar, grid_for(nfar, 256, grid), 256, 0, ctx->stream, far, fkey, nfar,
+                 dp, threshold, 1, nearq[curq], &nxt->out_len, far2, fkey2, &C[3].aux1);
+      GFX_CK(cudaMemcpyAsync(pin, C, 4 * sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+      GFX_CK(cudaStreamSynchronize(ctx->stream));
+      bytes_total += 8 * nfar;
+      nnear = (int64_t)pin[curq].out_len;
+      nfar = (int64_t)pin[3].aux1;
+      std::swap(far, far2);
+      std::swap(fkey, fkey2);
+      GFX_CK(cudaMemcpyAsync(&C[3].aux0, &pin[3].aux1, 8, cudaMemcpyHostToDevice, ctx->stream));
+      continue;
+    }
+    ++it;
+    float ms = 0.f;
+    if (ctx->timing) GFX_CK(cudaEventRecord(ctx->lev0, ctx->stream));
+    Counters* cur = &C[curq];
+    Counters* nxt = &C[curq ^ 1];
+    GFX_CK(cudaMemsetAsync(&C[2], 0, sizeof(Counters), ctx->stream));
+    GFX_CK(cudaMemsetAsync(nxt, 0, sizeof(Counters), ctx->stream));
+    SsspRelaxOp op{dp, stamp, (int32_t)it, {}};
+    GFX_TRY(lb_advance(g, nearq[curq], &cur->out_len, nnear, &C[2], scan, rowbase, part, op,
+                       touched, &C[2].out_len));
+    GFX_LAUNCH(k_sssp_split, grid_for(n, 256, grid), 256, 0, ctx->stream, touched, &C[2].out_len,
+               dp, threshold, nearq[curq ^ 1], &nxt->out_len, far, fkey, &C[3].aux0);
+    GFX_CK(cudaGetLastError());
+    if (ctx->timing) GFX_CK(cudaEventRecord(ctx->lev1, ctx->stream));
+    GFX_CK(cudaMemcpyAsync(pin, C, 4 * sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+    GFX_CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->timing) GFX_CK(cudaEventElapsedTime(&ms, ctx->lev0, ctx->lev1));
+    const int64_t slots = (int64_t)pin[2].total;
+    const int64_t ntouched = (int64_t)pin[2].out_len;
+    const int64_t nnext = (int64_t)pin[curq ^ 1].out_len;
+    const int64_t bytes = 20 * nnear + 8 * slots + 8 * ntouched;
+    slots_total += slots;
+    bytes_total += bytes;
+    nfar = (int64_t)pin[3].aux0;
+    if (recs && nrec < rec_cap) {
+      gfx_iter_rec& r = recs[nrec++];
+      r = gfx_iter_rec{};
+      r.iteration = it;
+      r.frontier_in = nnear;
+      r.frontier_out = ntouched;
+      r.edges = slots;
+      r.work = slots;
+      r.bytes_alg = bytes;
+      r.ms = ms;
+      r.n_u = nfar;
+    }
+    nnear = nnext;
+    curq ^= 1;
+    if (nfar > n) {
+      // capacity guard: drop stale far entries (each vertex then appears once)
+      GFX_CK(cudaMemsetAsync(&C[3].aux1, 0, 8, ctx->stream));
+      GFX_LAUNCH(k_sssp_refar, grid_for(nfar, 256, grid), 256, 0, ctx->stream, far, fkey, nfar,
+                 dp, threshold, 0, nearq[curq], &C[2].aux2, far2, fkey2, &C[3].aux1);
+      GFX_CK(cudaMemcpyAsync(pin, C, 4 * sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+      GFX_CK(cudaStreamSynchronize(ctx->stream));
+      nfar = (int64_t)pin[3].aux1;
+      std::swap(far, far2);
+      std::swap(fkey, fkey2);
+      GFX_CK(cudaMemcpyAsync(&C[3].aux0, &pin[3].aux1, 8, cudaMemcpyHostToDevice, ctx->stream));
+    }
+  }
+  GFX_LAUNCH(k_sssp_unpack, grid_for(n, 256, grid), 256, 0, ctx->stream, dp, n, dist, preds);
+  GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  GFX_CK(cudaEventSynchronize(ctx->ev1));
+  float ms = 0.f;
+  GFX_CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  if (st) {
+    *st = gfx_stats{};
+    st->iterations = it;
+    st->edges_traversed = slots_total;
+    st->work_slots = slots_total;
+    st->bytes_alg = bytes_total;
+    st->device_ms = ms;
+    st->num_records = nrec;
+    GFX_TRY(reached_stats(g, dist, &st->reached, &st->edges_reached));
+  }
+  return GFX_OK;
+}
+
+}  // namespace gfx
+
+using namespace gfx;
+
+extern "C" int gfx_sssp(gfx_graph* g, int64_t source, double delta, int32_t* dist_d,
+                        int32_t* preds_d, gfx_iter_rec* recs, int64_t rec_cap, gfx_stats* stats) {
+  GFX_REQUIRE(g, "gfx_sssp: null graph");
+  GFX_REQUIRE(source >= 0 && source < g->n, "source %lld out of range", (long long)source);
+  GFX_REQUIRE(g->w != nullptr,
+              "sssp requires edge weights (assign_random_weights or a weighted file)");
+  GFX_REQUIRE(dist_d && preds_d, "gfx_sssp: null output");
+  GFX_CK(cudaSetDevice(g->ctx->device));
+  const double d = (delta > 0 && !std::isnan(delta)) ? delta : INFINITY;
+  return sssp_run(g, source, d, dist_d, preds_d, recs, rec_cap, stats);
+}

@@ -3,7 +3,6 @@
 using namespace gfx;
 #define NOT_YET(name) { set_error(name ": not implemented yet"); return GFX_EINVAL; }
 extern "C" {
-int gfx_sssp(gfx_graph*, int64_t, int64_t, int32_t*, int32_t*, gfx_iter_rec*, int64_t, gfx_stats*) NOT_YET("gfx_sssp")
 int gfx_bc(gfx_graph*, const int64_t*, int64_t, double*, gfx_stats*) NOT_YET("gfx_bc")
 int gfx_cc(gfx_graph*, int32_t*, int64_t*, gfx_stats*) NOT_YET("gfx_cc")
 int gfx_pagerank(gfx_graph*, double, double, int64_t, double*, gfx_stats*) NOT_YET("gfx_pagerank")

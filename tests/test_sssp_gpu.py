@@ -1,0 +1,74 @@
+"""SSSP on the GPU vs reference goldens, Dijkstra and property checks."""
+import numpy as np
+import pytest
+
+from _checks import valid_sssp_preds
+from conftest import host_graph, rmat_golden, sha
+
+pytestmark = pytest.mark.gpu
+
+
+def test_kat_sssp(kat):
+    import paper_1701_01170_b200 as gfx
+
+    for d in kat:
+        g = host_graph(d, weighted=True)
+        src = d["source"]
+        for kw in ({}, {"delta": 1}, {"delta": 7}, {"delta": 1000}, {"use_priority_queue": False}):
+            r = gfx.sssp(g, src, **kw)
+            assert np.array_equal(r.labels, d["sssp"]), (d["name"], kw)
+            assert valid_sssp_preds(g.row_offsets, g.column_indices, g.edge_weights, r.labels,
+                                    r.preds, src), (d["name"], kw)
+
+
+def test_reference_kats():
+    """reference test_primitives.py:73-114."""
+    import paper_1701_01170_b200 as gfx
+
+    g = gfx.coo_to_csr(gfx.CooGraph(3, np.array([0, 1]), np.array([1, 2])), make_undirected=True)
+    w = np.zeros(g.num_edges, dtype=np.int64)
+    s, d = g.edge_sources(), g.column_indices
+    w[np.minimum(s, d) == 0] = 5
+    w[np.minimum(s, d) == 1] = 7
+    g.edge_weights = w
+    assert gfx.sssp(g, 0).labels.tolist() == [0, 5, 12]
+    g2 = gfx.assign_random_weights(
+        gfx.coo_to_csr(gfx.CooGraph(4, np.array([1, 2]), np.array([2, 3])), make_undirected=True),
+        1, 9, seed=0)
+    r = gfx.sssp(g2, 0)
+    assert r.labels[0] == 0 and np.all(r.labels[1:] == gfx.UNVISITED)
+    star = gfx.coo_to_csr(gfx.CooGraph(5, np.array([0, 0, 0, 0]), np.array([1, 2, 3, 4])),
+                          make_undirected=True)
+    with pytest.raises(ValueError):
+        gfx.sssp(star, 0)
+    unit = gfx.assign_random_weights(star, 1, 1, seed=0)
+    assert np.array_equal(gfx.sssp(unit, 0).labels, gfx.bfs(unit, 0).labels)
+    with pytest.raises(ValueError):
+        gfx.sssp(unit, 9)
+
+
+@pytest.mark.parametrize("delta", [32, None])
+def test_s16_golden(delta):
+    import paper_1701_01170_b200 as gfx
+
+    rec, arrays = rmat_golden(16)
+    g = gfx.CsrGraph(rec["n"], arrays["row"], arrays["col"].astype(np.int64),
+                     arrays["w"].astype(np.int64), undirected=True)
+    r = gfx.sssp(g, 0, delta=delta)
+    key = "sssp_d32" if delta == 32 else "sssp_default"
+    assert sha(r.labels) == rec[key + "_sha"]
+    assert valid_sssp_preds(g.row_offsets, g.column_indices, g.edge_weights, r.labels, r.preds, 0)
+
+
+@pytest.mark.parametrize("scale", [20, 22])
+def test_device_graph_golden(scale):
+    """C2 config: SSSP on R-MAT s22 + weights 1..64 (GPU-built, bit-exact input)."""
+    from paper_1701_01170_b200._results import labels_to_host
+    from paper_1701_01170_b200.generators import rmat_device_graph
+    from paper_1701_01170_b200.primitives.sssp import sssp_device
+
+    rec, _ = rmat_golden(scale)
+    dg = rmat_device_graph(scale, 16, 0, weights=(1, 64), weight_seed=0)
+    for delta, key in ((32, "sssp_d32"), (None, "sssp_default")):
+        dist, preds, st = sssp_device(dg, 0, delta=delta)
+        assert sha(labels_to_host(dist)) == rec[key + "_sha"], (scale, delta)
