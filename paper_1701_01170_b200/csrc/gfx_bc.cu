@@ -1,0 +1,166 @@
+// Betweenness centrality (Brandes) with deterministic pull-gathers.
+//
+// Reference: primitives/bc.py:32-116.  Forward: level-synchronous BFS with a
+// CAS claim, and per level sigma[d] += sigma[s] over every edge landing on
+// the new level (np.add.at).  Backward: deepest level first, delta[s] +=
+// sigma[s]/sigma[d] * (1 + delta[d]) over edges s -> d with d one level
+// deeper; delta[source] = 0; bc += delta.
+//
+// Device: the forward BFS is the push LB expansion (gfx_bfs.cu) keeping every
+// level's frontier; sigma and delta are then gathered level by level with no
+// fp64 atomics: sigma[v] = sum of sigma over in-neighbours one level up,
+// delta[v] = sum over out-neighbours one level down, each term computed as
+// (sigma[v] / sigma[w]) * (1 + delta[w]) with round-to-nearest intrinsics (no
+// FMA contraction).  Light rows (<= 32) are summed sequentially in ascending
+// neighbour order -- the reference's slot order -- so their values are
+// bit-identical; heavier rows use a warp reduction (rel <= 1e-5, north_star).
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "gfx_device.cuh"
+#include "gfx_internal.cuh"
+
+namespace gfx {
+
+struct SigmaTerm {
+  const int32_t* labels;
+  const double* sigma;
+  int32_t want;  // level of contributing neighbours
+  __device__ double term(int32_t, int32_t u) const {
+    return labels[u] == want ? sigma[u] : 0.0;
+  }
+};
+
+struct DeltaTerm {
+  const int32_t* labels;
+  const double* sigma;
+  const double* delta;
+  int32_t want;
+  __device__ double term(int32_t v, int32_t w) const {
+    if (labels[w] != want) return 0.0;
+    return __dmul_rn(__ddiv_rn(sigma[v], sigma[w]), __dadd_rn(1.0, delta[w]));
+  }
+};
+
+// out[v] = sum_{u in adj(v)} T.term(v, u) for v in items[0..cnt)
+template <class T>
+__global__ void __launch_bounds__(256)
+    k_level_gather(const int32_t* __restrict__ items, int64_t cnt, const int64_t* __restrict__ rows,
+                   const int32_t* __restrict__ cols, T term, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t grp = gw; grp * 32 < cnt; grp += nw) {
+    const int64_t i = grp * 32 + lane;
+    int32_t v = 0;
+    int64_t b = 0, e = 0;
+    if (i < cnt) {
+      v = items[i];
+      b = rows[v];
+      e = rows[v + 1];
+    }
+    const bool heavy = (e - b) > 32;
+    double acc = 0.0;
+    if (i < cnt && !heavy)
+      for (int64_t p = b; p < e; ++p) {
+        const double t = term.term(v, cols[p]);
+        if (t != 0.0) acc = __dadd_rn(acc, t);
+      }
+    unsigned hm = __ballot_sync(0xffffffffu, heavy);
+    while (hm) {
+      const int k = __ffs(hm) - 1;
+      hm &= hm - 1;
+      const int32_t kv = __shfl_sync(0xffffffffu, v, k);
+      const int64_t kb = __shfl_sync(0xffffffffu, b, k), ke = __shfl_sync(0xffffffffu, e, k);
+      double part = 0.0;
+      for (int64_t p = kb + lane; p < ke; p += 32) part = __dadd_rn(part, term.term(kv, cols[p]));
+      part = warp_sum_f64(part);
+      if (lane == k) acc = part;
+    }
+    if (i < cnt) out[v] = acc;
+  }
+}
+
+__global__ void k_bc_seed(double* sigma, int32_t src) { sigma[src] = 1.0; }
+
+__global__ void k_bc_accumulate(const int32_t* __restrict__ items, int64_t cnt,
+                                const double* __restrict__ delta, int32_t src,
+                                double* __restrict__ bc) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = items[i];
+    if (v != src) bc[v] = __dadd_rn(bc[v], delta[v]);
+  }
+}
+
+}  // namespace gfx
+
+using namespace gfx;
+
+extern "C" int gfx_bc(gfx_graph* g, const int64_t* sources, int64_t num_sources, double* bc_d,
+                      gfx_stats* stats) {
+  GFX_REQUIRE(g && bc_d && (num_sources == 0 || sources), "gfx_bc: null argument");
+  for (int64_t i = 0; i < num_sources; ++i)
+    GFX_REQUIRE(sources[i] >= 0 && sources[i] < g->n, "source %lld out of range",
+                (long long)sources[i]);
+  GFX_REQUIRE(g->rrow != nullptr, "bc on a directed graph needs the reverse adjacency");
+  gfx_ctx* ctx = g->ctx;
+  GFX_CK(cudaSetDevice(ctx->device));
+  const int64_t n = g->n;
+  int32_t *labels, *preds;
+  double *sigma, *delta;
+  GFX_TRY(scratch_t(g, "bc_labels", n + 1, &labels));
+  GFX_TRY(scratch_t(g, "bc_preds", n + 1, &preds));
+  GFX_TRY(scratch_t(g, "bc_sigma", n + 1, &sigma));
+  GFX_TRY(scratch_t(g, "bc_delta", n + 1, &delta));
+  const int grid = ctx->sm_count * 8;
+  int64_t iterations = 0, edges = 0;
+  std::vector<int64_t> off;
+  GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  for (int64_t si = 0; si < num_sources; ++si) {
+    const int32_t src = (int32_t)sources[si];
+    int32_t* order = nullptr;
+    GFX_TRY(bfs_push_levels(g, src, labels, preds, &off, &order));
+    const int64_t L = (int64_t)off.size() - 1;  // levels 0..L-1 (last is empty)
+    // forward: sigma level by level (bc.py:87-92)
+    GFX_CK(cudaMemsetAsync(sigma, 0, n * sizeof(double), ctx->stream));
+    GFX_LAUNCH(k_bc_seed, 1, 1, 0, ctx->stream, sigma, src);
+    for (int64_t d = 1; d < L; ++d) {
+      const int64_t cnt = off[d + 1] - off[d];
+      if (cnt <= 0) continue;
+      SigmaTerm t{labels, sigma, (int32_t)(d - 1)};
+      GFX_LAUNCH((k_level_gather<SigmaTerm>), grid_for(cnt * 32, 256, grid), 256, 0, ctx->stream,
+                 order + off[d], cnt, g->rrow, g->rcol, t, sigma);
+    }
+    // backward: delta deepest level first (bc.py:98-116)
+    GFX_CK(cudaMemsetAsync(delta, 0, n * sizeof(double), ctx->stream));
+    for (int64_t d = L - 2; d >= 0; --d) {
+      const int64_t cnt = off[d + 1] - off[d];
+      if (cnt <= 0) continue;
+      DeltaTerm t{labels, sigma, delta, (int32_t)(d + 1)};
+      GFX_LAUNCH((k_level_gather<DeltaTerm>), grid_for(cnt * 32, 256, grid), 256, 0, ctx->stream,
+                 order + off[d], cnt, g->row, g->col, t, delta);
+    }
+    const int64_t reached = off[L];
+    GFX_LAUNCH(k_bc_accumulate, grid_for(reached, 256, grid), 256, 0, ctx->stream, order, reached,
+               delta, src, bc_d);
+    GFX_CK(cudaGetLastError());
+    iterations += L - 1;
+    int64_t er = 0, rc = 0;
+    GFX_TRY(reached_stats(g, labels, &rc, &er));
+    edges += er;
+  }
+  GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  GFX_CK(cudaEventSynchronize(ctx->ev1));
+  float ms = 0.f;
+  GFX_CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  if (stats) {
+    *stats = gfx_stats{};
+    stats->iterations = iterations;
+    stats->edges_traversed = edges;  // forward plans only (bc.py:67-68)
+    stats->edges_reached = edges;
+    stats->device_ms = ms;
+  }
+  return GFX_OK;
+}

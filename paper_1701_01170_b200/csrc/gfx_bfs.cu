@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <vector>
 
 #include "gfx_device.cuh"
 #include "gfx_direction.cuh"
@@ -126,6 +127,8 @@ __global__ void __launch_bounds__(256)
 // counters: out_len += |new frontier|, edges += sum of in-degree(U),
 //           aux0 += early-exit probes S(U), aux1 += |U| (in-degree > 0).
 // ---------------------------------------------------------------------------
+constexpr int kPullBatch = 4;  // bitmap words (vertices per lane) in flight
+
 __global__ void __launch_bounds__(256)
     k_bfs_pull(int64_t words, const uint32_t* __restrict__ nz_in,
                uint32_t* __restrict__ visited, const uint32_t* __restrict__ front,
@@ -144,32 +147,63 @@ __global__ void __launch_bounds__(256)
       cand = ~vis & nz_in[w];
     }
     uint32_t newbits_mine = 0;
-    unsigned any = __ballot_sync(0xffffffffu, cand != 0);
-    while (any) {
-      const int k = __ffs(any) - 1;
-      any &= any - 1;
-      const uint32_t c = __shfl_sync(0xffffffffu, cand, k);
-      const int64_t u = (grp * 32 + k) * 32 + lane;
-      bool found = false;
-      if ((c >> lane) & 1u) {
-        const int64_t b = rrow[u], e = rrow[u + 1];
-        in_edges += (unsigned long long)(e - b);
-        ++cands;
-        int64_t p = b;
-        for (; p < e; ++p) {
-          const int32_t s = rcol[p];
-          if ((front[s >> 5] >> (s & 31)) & 1u) {
-            found = true;
+    // words of this group that hold candidates, processed kPullBatch at a time
+    unsigned todo = __ballot_sync(0xffffffffu, cand != 0);
+    while (todo) {
+      int kw[kPullBatch];
+      uint32_t c[kPullBatch];
+#pragma unroll
+      for (int q = 0; q < kPullBatch; ++q) {
+        kw[q] = todo ? __ffs(todo) - 1 : -1;
+        if (todo) todo &= todo - 1;
+        c[q] = __shfl_sync(0xffffffffu, cand, kw[q] < 0 ? 0 : kw[q]);
+        if (kw[q] < 0) c[q] = 0;
+      }
+      // phase 1: row pairs of every candidate lane (independent loads)
+      int64_t b[kPullBatch], e[kPullBatch];
+#pragma unroll
+      for (int q = 0; q < kPullBatch; ++q) {
+        b[q] = e[q] = 0;
+        if ((c[q] >> lane) & 1u) {
+          const int64_t u = (grp * 32 + kw[q]) * 32 + lane;
+          b[q] = rrow[u];
+          e[q] = rrow[u + 1];
+        }
+      }
+      // phase 2: first in-neighbour of each candidate
+      int32_t s0[kPullBatch];
+#pragma unroll
+      for (int q = 0; q < kPullBatch; ++q) s0[q] = (e[q] > b[q]) ? ld_stream_i32(rcol + b[q]) : -1;
+      // phase 3: frontier test, then the (rare) sequential tail scan
+#pragma unroll
+      for (int q = 0; q < kPullBatch; ++q) {
+        bool found = false;
+        int32_t par = -1;
+        if (e[q] > b[q]) {
+          ++cands;
+          in_edges += (unsigned long long)(e[q] - b[q]);
+          int64_t p = b[q];
+          int32_t s = s0[q];
+          for (;;) {
+            if ((front[s >> 5] >> (s & 31)) & 1u) {
+              found = true;
+              par = s;
+              break;
+            }
+            if (++p >= e[q]) break;
+            s = rcol[p];
+          }
+          probes += (unsigned long long)(found ? p - b[q] + 1 : e[q] - b[q]);
+          if (found) {
+            const int64_t u = (grp * 32 + kw[q]) * 32 + lane;
             labels[u] = depth;
-            preds[u] = s;
-            break;
+            preds[u] = par;
           }
         }
-        probes += (unsigned long long)(found ? p - b + 1 : e - b);
+        const unsigned fm = __ballot_sync(0xffffffffu, found);
+        if (kw[q] >= 0 && lane == kw[q]) newbits_mine = fm;
+        found_cnt += found ? 1 : 0;
       }
-      const unsigned fm = __ballot_sync(0xffffffffu, found);
-      if (lane == k) newbits_mine = fm;
-      found_cnt += found ? 1 : 0;
     }
     if (w < words) {
       next[w] = newbits_mine;
@@ -312,6 +346,41 @@ static int push_level(gfx_graph* g, const BfsBuffers& B, const int32_t* F,
     GFX_LAUNCH((k_bitmap_filter<false>), grid, 256, 0, ctx->stream, B.raw, &cur_d->aux1, B.visited, out,
                                                          &cur_d->out_len);
   GFX_CK(cudaGetLastError());
+  return GFX_OK;
+}
+
+// push-only level-synchronous BFS that keeps every level's frontier in the
+// order array: level d occupies order[off[d], off[d+1]) (used by BC, which
+// replays the levels like reference bc.py:73-116)
+int bfs_push_levels(gfx_graph* g, int64_t source, int32_t* labels, int32_t* preds,
+                    std::vector<int64_t>* off, int32_t** order_out) {
+  gfx_ctx* ctx = g->ctx;
+  const int64_t n = g->n;
+  BfsBuffers B;
+  GFX_TRY(bfs_buffers(g, false, &B));
+  Counters* C = g->counters;
+  auto* pin = static_cast<Counters*>(ctx->pinned);
+  GFX_TRY(fill_i32(ctx, labels, GFX_UNVISITED, n));
+  GFX_CK(cudaMemsetAsync(preds, 0xFF, n * sizeof(int32_t), ctx->stream));
+  GFX_CK(cudaMemsetAsync(B.visited, 0, g->words * 4, ctx->stream));
+  GFX_CK(cudaMemsetAsync(C, 0, 2 * sizeof(Counters), ctx->stream));
+  GFX_LAUNCH(k_bfs_seed, 1, 1, 0, ctx->stream, (int32_t)source, labels, B.visited, B.order, &C[0]);
+  off->assign(1, 0);
+  int64_t nf = 1, q_off = 0, depth = 0;
+  while (nf > 0) {
+    ++depth;
+    off->push_back(q_off + nf);
+    Counters* prev = &C[(depth - 1) & 1];
+    Counters* cur = &C[depth & 1];
+    GFX_CK(cudaMemsetAsync(cur, 0, sizeof(Counters), ctx->stream));
+    GFX_TRY(push_level(g, B, B.order + q_off, prev, nf, cur, (int32_t)depth, false, true, labels,
+                       preds, B.order + q_off + nf));
+    GFX_CK(cudaMemcpyAsync(pin, cur, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+    GFX_CK(cudaStreamSynchronize(ctx->stream));
+    q_off += nf;
+    nf = (int64_t)pin->out_len;
+  }
+  *order_out = B.order;
   return GFX_OK;
 }
 

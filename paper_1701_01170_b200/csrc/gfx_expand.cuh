@@ -5,23 +5,25 @@
 // OUTPUT slots of the frontier's expansion (tiles come from the fused degree
 // scan, so hubs are split across many CTAs and every CTA does the same work).
 //
-//   stage : warps copy every adjacency segment overlapping the tile into
-//           shared memory with coalesced 4-byte cp.async (LDGSTS), plus the
-//           owning source id (and weights / a per-source value when the
-//           functor needs them);
-//   visit : each thread walks slots j, j+B, ... of the tile and calls the
-//           functor; it returns whether the slot's output id is emitted;
+// Per tile (in passes of <= kPassItems frontier items):
+//   items : each thread loads one item's (scan, delta = row[v] - scan, v)
+//           into shared memory and drops a marker at the item's first slot;
+//   owner : a CTA-wide inclusive max-scan over the markers gives every slot
+//           its owning item (load-balancing search without binary search);
+//   visit : thread t handles slots t, t+B, ... (consecutive lanes read
+//           consecutive column ids: coalesced), 4 slots in flight per thread,
+//           col id = col[delta[item] + slot]; the functor decides emission;
 //   emit  : emitted ids are staged in shared memory and appended with ONE
 //           global atomicAdd per tile, then written coalesced.
 //
-// Functor interface (see gfx_bfs.cu / gfx_sssp.cu / gfx_operators.cu):
-//   static constexpr bool kWeights;    stage w[e]
-//   static constexpr bool kSrcVal;     stage src_value(v) per slot
+// Functor interface (gfx_bfs.cu / gfx_sssp.cu / gfx_operators.cu):
+//   static constexpr bool kWeights;    load w[e]
+//   static constexpr bool kSrcVal;     per-item src_value(v)
 //   static constexpr bool kEmitEdge;   emit edge ids instead of dst ids
 //   __device__ int32_t src_value(int32_t v) const;
-//   __device__ void prefetch(const int32_t d[4]);   // issue loads for 4 slots
+//   __device__ void prefetch(const int32_t d[4]);
 //   __device__ bool visit(int u, int32_t dst, int32_t src, int32_t w,
-//                         int32_t sval, int64_t edge);  // u = slot of prefetch
+//                         int32_t sval, int64_t edge);   // u = prefetch slot
 #pragma once
 
 #include "gfx_device.cuh"
@@ -30,11 +32,19 @@
 namespace gfx {
 
 constexpr int kExpandBlock = 256;
+constexpr int kPassItems = 1024;
+constexpr int kSlotsPerThread = kTile / kExpandBlock;  // 16
 
-template <class Op>
-constexpr int expand_smem_bytes() {
-  return kTile * 4 * (3 + (Op::kWeights ? 1 : 0) + (Op::kSrcVal ? 1 : 0) + (Op::kEmitEdge ? 1 : 0));
-}
+struct ExpandSmem {
+  int64_t delta[kPassItems];   // row[v] - scan[i]: col index = delta + global slot
+  int32_t src[kPassItems];     // frontier id
+  int32_t sval[kPassItems];    // functor per-source value
+  int16_t owner[kTile];        // slot -> item (relative to the pass)
+  int32_t obuf[kTile];         // emitted ids
+  int32_t warp_max[kExpandBlock / 32];
+  int cnt;
+  unsigned long long gbase;
+};
 
 template <class Op>
 __global__ void __launch_bounds__(kExpandBlock)
@@ -43,25 +53,13 @@ __global__ void __launch_bounds__(kExpandBlock)
                 const int32_t* __restrict__ part, const Counters* __restrict__ plan,
                 const int32_t* __restrict__ col, const int32_t* __restrict__ wgt, Op op,
                 int32_t* __restrict__ out, unsigned long long* __restrict__ out_len) {
-  extern __shared__ int32_t smem[];
-  int32_t* buf = smem;               // [kTile] destination ids
-  int32_t* owner = smem + kTile;     // [kTile] source ids
-  int32_t* obuf = smem + 2 * kTile;  // [kTile] emitted ids
-  int32_t* extra = smem + 3 * kTile;
-  int32_t* wbuf = Op::kWeights ? extra : nullptr;
-  if (Op::kWeights) extra += kTile;
-  int32_t* sval = Op::kSrcVal ? extra : nullptr;
-  if (Op::kSrcVal) extra += kTile;
-  int32_t* ebuf = Op::kEmitEdge ? extra : nullptr;  // low 32 bits of edge ids (E kinds)
-  __shared__ int s_cnt;
-  __shared__ unsigned long long s_gbase;
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ExpandSmem& S = *reinterpret_cast<ExpandSmem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t ntiles = (int64_t)plan->ntiles;
   const int64_t total = (int64_t)plan->total;
   const int64_t nf = (int64_t)*nf_d;
-  if (threadIdx.x == 0) s_cnt = 0;
-  __syncthreads();
+  if (tid == 0) S.cnt = 0;
   Op o = op;  // mutable copy: functors keep per-thread prefetch registers
 
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -70,84 +68,112 @@ __global__ void __launch_bounds__(kExpandBlock)
     const int64_t i0 = part[t];
     const int64_t i1 = (t + 1 < ntiles) ? (int64_t)part[t + 1] : nf - 1;
 
-    // ---- stage
-    for (int64_t ib = i0 + (int64_t)warp * 32; ib <= i1; ib += kExpandBlock) {
-      const int64_t i = ib + lane;
-      int64_t lo = 0, len = 0, src_base = 0;
-      int32_t v = 0, sv = 0;
-      if (i <= i1) {
-        const int64_t sc = scan[i], sc1 = scan[i + 1];
-        lo = max(sc, s0);
-        const int64_t hi = min(sc1, s1);
-        len = hi > lo ? hi - lo : 0;
-        src_base = rowbase[i] + (lo - sc);
-        v = F[i];
-        if (Op::kSrcVal && len > 0) sv = o.src_value(v);
-      }
-      unsigned mask = __ballot_sync(0xffffffffu, len > 0);
-      while (mask) {
-        const int k = __ffs(mask) - 1;
-        mask &= mask - 1;
-        const int klo = (int)(__shfl_sync(0xffffffffu, lo, k) - s0);
-        const int klen = (int)__shfl_sync(0xffffffffu, len, k);
-        const int64_t kbase = __shfl_sync(0xffffffffu, src_base, k);
-        const int32_t kv = __shfl_sync(0xffffffffu, v, k);
-        const int32_t ksv = Op::kSrcVal ? __shfl_sync(0xffffffffu, sv, k) : 0;
-        for (int j = lane; j < klen; j += 32) {
-          cp_async4(&buf[klo + j], &col[kbase + j]);
-          if (Op::kWeights) cp_async4(&wbuf[klo + j], &wgt[kbase + j]);
-          owner[klo + j] = kv;
-          if (Op::kSrcVal) sval[klo + j] = ksv;
-          if (Op::kEmitEdge) ebuf[klo + j] = (int32_t)(kbase + j);
-        }
-      }
-    }
-    cp_async_wait_all();
-    __syncthreads();
-
-    // ---- visit (4 slots in flight per thread)
-    const int nslots = (int)(s1 - s0);
-    for (int jb = 0; jb < nslots; jb += kExpandBlock * 4) {
-      int32_t d[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = jb + u * kExpandBlock + threadIdx.x;
-        d[u] = j < nslots ? buf[j] : -1;
-      }
-      o.prefetch(d);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = jb + u * kExpandBlock + threadIdx.x;
-        bool emit = false;
-        int32_t outv = 0;
-        if (d[u] >= 0) {
-          const int32_t w = Op::kWeights ? wbuf[j] : 1;
-          const int32_t sv = Op::kSrcVal ? sval[j] : 0;
-          const int64_t edge = Op::kEmitEdge ? (int64_t)(uint32_t)ebuf[j] : 0;
-          emit = o.visit(u, d[u], owner[j], w, sv, edge);
-          outv = Op::kEmitEdge ? ebuf[j] : d[u];
-        }
-        const unsigned wm = __ballot_sync(0xffffffffu, emit);
-        if (wm) {
-          int base = 0;
-          if (lane == 0) base = atomicAdd(&s_cnt, __popc(wm));
-          base = __shfl_sync(0xffffffffu, base, 0);
-          if (emit) obuf[base + __popc(wm & ((1u << lane) - 1))] = outv;
-        }
-      }
-    }
-    __syncthreads();
-    const int cnt = s_cnt;
-    if (cnt > 0) {
-      if (threadIdx.x == 0) s_gbase = atomicAdd(out_len, (unsigned long long)cnt);
+    for (int64_t pa = i0; pa <= i1; pa += kPassItems) {
+      const int64_t pb = min(pa + kPassItems - 1, i1);
+      // slot range of this pass, clipped to the tile
+      const int64_t sl = max(scan[pa], s0);
+      const int64_t sh = min(scan[pb + 1], s1);
+      const int nsl = (int)max(sh - sl, (int64_t)0);
+      __syncthreads();  // previous pass / tile fully consumed
+      for (int j = tid; j < nsl; j += kExpandBlock) S.owner[j] = -1;
       __syncthreads();
-      const unsigned long long gb = s_gbase;
-      for (int j = threadIdx.x; j < cnt; j += kExpandBlock) out[gb + j] = obuf[j];
+      for (int64_t i = pa + tid; i <= pb; i += kExpandBlock) {
+        const int r = (int)(i - pa);
+        const int64_t sc = scan[i], sc1 = scan[i + 1];
+        const int32_t v = F[i];
+        S.delta[r] = rowbase[i] - sc;
+        S.src[r] = v;
+        const int64_t lo = max(sc, sl), hi = min(sc1, sh);
+        if (hi > lo) {
+          S.owner[lo - sl] = (int16_t)r;
+          if (Op::kSrcVal) S.sval[r] = o.src_value(v);
+        }
+      }
+      __syncthreads();
+      // inclusive max-scan of owner[0..nsl): kSlotsPerThread consecutive per thread
+      {
+        int16_t loc[kSlotsPerThread];
+        const int base = tid * kSlotsPerThread;
+        int run = -1;
+#pragma unroll
+        for (int k = 0; k < kSlotsPerThread; ++k) {
+          const int j = base + k;
+          const int x = j < nsl ? S.owner[j] : -1;
+          run = x > run ? x : run;
+          loc[k] = (int16_t)run;
+        }
+        int incl = run;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= off) incl = y > incl ? y : incl;
+        }
+        if (lane == 31) S.warp_max[warp] = incl;
+        int excl = __shfl_up_sync(0xffffffffu, incl, 1);
+        if (lane == 0) excl = -1;
+        __syncthreads();
+        int wpre = -1;
+        for (int w = 0; w < warp; ++w) wpre = S.warp_max[w] > wpre ? S.warp_max[w] : wpre;
+        const int pre = wpre > excl ? wpre : excl;
+#pragma unroll
+        for (int k = 0; k < kSlotsPerThread; ++k) {
+          const int j = base + k;
+          if (j < nsl) S.owner[j] = (int16_t)(loc[k] > pre ? loc[k] : pre);
+        }
+      }
+      __syncthreads();
+
+      // ---- visit: 4 slots in flight per thread
+      for (int jb = 0; jb < nsl; jb += kExpandBlock * 4) {
+        int32_t d[4], it[4], w[4];
+        int64_t e[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = jb + u * kExpandBlock + tid;
+          it[u] = j < nsl ? S.owner[j] : -1;
+          e[u] = it[u] >= 0 ? S.delta[it[u]] + sl + j : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          d[u] = it[u] >= 0 ? ld_stream_i32(col + e[u]) : -1;
+          if (Op::kWeights) w[u] = it[u] >= 0 ? ld_stream_i32(wgt + e[u]) : 0;
+        }
+        o.prefetch(d);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          bool emit = false;
+          if (d[u] >= 0) {
+            const int32_t sv = Op::kSrcVal ? S.sval[it[u]] : 0;
+            emit = o.visit(u, d[u], S.src[it[u]], Op::kWeights ? w[u] : 1, sv, e[u]);
+          }
+          const unsigned wm = __ballot_sync(0xffffffffu, emit);
+          if (wm) {
+            int b = 0;
+            if (lane == 0) b = atomicAdd(&S.cnt, __popc(wm));
+            b = __shfl_sync(0xffffffffu, b, 0);
+            if (emit)
+              S.obuf[b + __popc(wm & ((1u << lane) - 1))] =
+                  Op::kEmitEdge ? (int32_t)e[u] : d[u];
+          }
+        }
+      }
     }
     __syncthreads();
-    if (threadIdx.x == 0) s_cnt = 0;
-    __syncthreads();
+    const int cnt = S.cnt;
+    if (cnt > 0) {
+      if (tid == 0) S.gbase = atomicAdd(out_len, (unsigned long long)cnt);
+      __syncthreads();
+      const unsigned long long gb = S.gbase;
+      for (int j = tid; j < cnt; j += kExpandBlock) out[gb + j] = S.obuf[j];
+      __syncthreads();
+      if (tid == 0) S.cnt = 0;
+    }
   }
+}
+
+template <class Op>
+constexpr int expand_smem_bytes() {
+  return (int)sizeof(ExpandSmem);
 }
 
 template <class Op>
@@ -160,7 +186,7 @@ int set_expand_smem() {
   return GFX_OK;
 }
 
-// CTAs per SM that fit the functor's shared-memory footprint
+// CTAs per SM that fit the shared-memory footprint
 template <class Op>
 inline int expand_ctas_per_sm() {
   const int per = expand_smem_bytes<Op>() + 1024;
@@ -177,8 +203,8 @@ int lb_advance(gfx_graph* g, const int32_t* F, const unsigned long long* nf_d, i
   GFX_TRY(launch_degree_scan(g, F, nf_d, nf_max, g->row, scan, rowbase, part, plan_ctr));
   GFX_TRY(set_expand_smem<Op>());
   const int grid = ctx->sm_count * expand_ctas_per_sm<Op>();
-  GFX_LAUNCH((k_lb_expand<Op>), grid, kExpandBlock, expand_smem_bytes<Op>(), ctx->stream, 
-      F, nf_d, scan, rowbase, part, plan_ctr, g->col, g->w, op, out, out_len);
+  GFX_LAUNCH((k_lb_expand<Op>), grid, kExpandBlock, expand_smem_bytes<Op>(), ctx->stream, F,
+             nf_d, scan, rowbase, part, plan_ctr, g->col, g->w, op, out, out_len);
   GFX_CK(cudaGetLastError());
   return GFX_OK;
 }

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <string>
 #include <unordered_map>
+#include <vector>
 
 #include "../../include/gfx.h"
 
@@ -144,6 +145,12 @@ constexpr int kScanTileItems = kScanBlock * kScanItems;
 
 // reached count and E_r from an int32 label array (UNVISITED = INT32_MAX)
 int reached_stats(gfx_graph* g, const int32_t* labels, int64_t* reached, int64_t* edges);
+
+// push-only BFS keeping each level's frontier: order[off[d], off[d+1])
+int bfs_push_levels(gfx_graph* g, int64_t source, int32_t* labels, int32_t* preds,
+                    std::vector<int64_t>* off, int32_t** order_out);
+// identity frontier 0..n-1 (graph-constant scratch)
+int iota_frontier(gfx_graph* g, int32_t** out);
 
 int launch_degree_scan(gfx_graph* g, const int32_t* F, const unsigned long long* nf_d,
                        int64_t nf_max, const int64_t* row, int64_t* scan,

@@ -1,0 +1,194 @@
+// PageRank as a deterministic pull-gather SpMV on sm_100a.
+//
+// Reference: primitives/pagerank.py:30-91.  Each round: dangling mass of the
+// active frontier, rank_next = (1-d)/n + d*dangling/n everywhere, then every
+// active s scatters d*rank[s]/outdeg[s] to its out-neighbours (np.add.at),
+// then the frontier keeps vertices with |rank_next - rank| >= epsilon.
+//
+// Here the scatter becomes a gather over in-neighbours (no fp64 atomics, so
+// runs are reproducible): contrib[u] = d*rank[u]/outdeg[u] for active u (0
+// otherwise), rank_next[v] = base + sum contrib[u] in ascending u.  Vertices
+// with in-degree <= 32 are summed sequentially by one thread in exactly the
+// reference's slot order (bit-identical terms and order); heavier rows are
+// reduced by a whole warp (tolerance: L1 <= 1e-6, north_star).
+#include <cuda_runtime.h>
+
+#include "gfx_device.cuh"
+#include "gfx_internal.cuh"
+
+namespace gfx {
+
+constexpr int kPrBlock = 256;
+
+// contrib + per-block dangling partial sums (deterministic order)
+__global__ void __launch_bounds__(kPrBlock)
+    k_pr_contrib(const int64_t* __restrict__ row, int64_t n, const double* __restrict__ rank,
+                 const uint8_t* __restrict__ active, double damping, double* __restrict__ contrib,
+                 double* __restrict__ partials, unsigned long long* __restrict__ edges) {
+  __shared__ double s_warp[kPrBlock / 32];
+  double dang = 0.0;
+  unsigned long long work = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t deg = row[v + 1] - row[v];
+    double c = 0.0;
+    if (active[v]) {
+      work += (unsigned long long)deg;
+      if (deg == 0) dang = __dadd_rn(dang, rank[v]);
+      else c = __ddiv_rn(__dmul_rn(damping, rank[v]), (double)deg);
+    }
+    contrib[v] = c;
+  }
+  dang = warp_sum_f64(dang);
+  work = warp_sum_u64(work);
+  if ((threadIdx.x & 31) == 0) {
+    s_warp[threadIdx.x >> 5] = dang;
+    if (work) atomicAdd(edges, work);  // plan.total_output of the round
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kPrBlock / 32; ++w) t = __dadd_rn(t, s_warp[w]);
+    partials[blockIdx.x] = t;
+  }
+}
+
+// base = (1-d)/n + d*dangling/n (reference pagerank.py:68-69, same operation order)
+__global__ void k_pr_base(const double* __restrict__ partials, int nparts, int64_t n,
+                          double damping, double* __restrict__ base) {
+  __shared__ double s[256];
+  double t = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) t = __dadd_rn(t, partials[i]);
+  s[threadIdx.x] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double dm = 0.0;
+    for (int i = 0; i < (int)blockDim.x; ++i) dm = __dadd_rn(dm, s[i]);
+    const double nn = (double)n;
+    *base = __dadd_rn(__ddiv_rn(__dadd_rn(1.0, -damping), nn), __ddiv_rn(__dmul_rn(damping, dm), nn));
+  }
+}
+
+// warp per 32 consecutive vertices: light rows sequential per lane, heavy
+// rows (in-degree > 32) cooperative across the warp
+__global__ void __launch_bounds__(kPrBlock)
+    k_pr_gather(const int64_t* __restrict__ rrow, const int32_t* __restrict__ rcol, int64_t n,
+                const double* __restrict__ contrib, const double* __restrict__ base_p,
+                double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const double base = *base_p;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t grp = gw; grp * 32 < n; grp += nw) {
+    const int64_t v = grp * 32 + lane;
+    int64_t b = 0, e = 0;
+    if (v < n) {
+      b = rrow[v];
+      e = rrow[v + 1];
+    }
+    const bool heavy = (e - b) > 32;
+    double s = base;
+    if (v < n && !heavy) {
+      for (int64_t p = b; p < e; ++p) s = __dadd_rn(s, contrib[rcol[p]]);
+    }
+    unsigned hm = __ballot_sync(0xffffffffu, heavy);
+    while (hm) {
+      const int k = __ffs(hm) - 1;
+      hm &= hm - 1;
+      const int64_t kb = __shfl_sync(0xffffffffu, b, k), ke = __shfl_sync(0xffffffffu, e, k);
+      double part = 0.0;
+      for (int64_t p = kb + lane; p < ke; p += 32) part = __dadd_rn(part, contrib[rcol[p]]);
+      part = warp_sum_f64(part);
+      if (lane == k) s = __dadd_rn(base, part);
+    }
+    if (v < n) out[v] = s;
+  }
+}
+
+// frontier filter |rank_next - rank| >= eps (pagerank.py:81-85); counts actives
+__global__ void __launch_bounds__(kPrBlock)
+    k_pr_moved(const double* __restrict__ nxt, const double* __restrict__ cur, int64_t n,
+               double eps, uint8_t* __restrict__ active, unsigned long long* __restrict__ cnt) {
+  unsigned long long c = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    if (active[v]) {
+      const bool keep = fabs(__dadd_rn(nxt[v], -cur[v])) >= eps;
+      if (!keep) active[v] = 0;
+      c += keep;
+    }
+  }
+  c = warp_sum_u64(c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, c);
+}
+
+}  // namespace gfx
+
+using namespace gfx;
+
+extern "C" int gfx_pagerank(gfx_graph* g, double damping, double epsilon, int64_t max_iters,
+                            double* rank_d, gfx_stats* stats) {
+  GFX_REQUIRE(g && rank_d, "gfx_pagerank: null argument");
+  GFX_REQUIRE(damping > 0.0 && damping < 1.0, "damping must be in (0, 1)");
+  GFX_REQUIRE(epsilon >= 0.0, "epsilon must be >= 0");
+  GFX_REQUIRE(g->rrow != nullptr, "pagerank on a directed graph needs the reverse adjacency");
+  gfx_ctx* ctx = g->ctx;
+  GFX_CK(cudaSetDevice(ctx->device));
+  const int64_t n = g->n;
+  if (n == 0) return GFX_OK;
+  double *nxt, *contrib, *partials, *base;
+  uint8_t* active;
+  GFX_TRY(scratch_t(g, "pr_next", n, &nxt));
+  GFX_TRY(scratch_t(g, "pr_contrib", n, &contrib));
+  GFX_TRY(scratch_t(g, "pr_active", n, &active));
+  const int cgrid = grid_for(n, kPrBlock, ctx->sm_count * 8);
+  GFX_TRY(scratch_t(g, "pr_partials", cgrid + 1, &partials));
+  GFX_TRY(scratch_t(g, "pr_base", 1, &base));
+  Counters* C = g->counters + 2;
+  auto* pin = static_cast<Counters*>(ctx->pinned);
+
+  GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  GFX_TRY(fill_f64(ctx, rank_d, 1.0 / (double)n, n));
+  GFX_CK(cudaMemsetAsync(active, 1, n, ctx->stream));
+  GFX_CK(cudaMemsetAsync(C, 0, sizeof(Counters), ctx->stream));
+  double* cur = rank_d;
+  double* nx = nxt;
+  int64_t it = 0, nactive = n;
+  const int ggrid = grid_for((n + 31) / 32 * 32, kPrBlock, ctx->sm_count * 16);
+  while (nactive > 0 && it < max_iters) {
+    ++it;
+    GFX_LAUNCH(k_pr_contrib, cgrid, kPrBlock, 0, ctx->stream, g->row, n, cur, active, damping,
+               contrib, partials, &C->edges);
+    GFX_LAUNCH(k_pr_base, 1, 256, 0, ctx->stream, partials, cgrid, n, damping, base);
+    GFX_LAUNCH(k_pr_gather, ggrid, kPrBlock, 0, ctx->stream, g->rrow, g->rcol, n, contrib, base,
+               nx);
+    if (epsilon > 0.0) {
+      GFX_CK(cudaMemsetAsync(&C->out_len, 0, 8, ctx->stream));
+      GFX_LAUNCH(k_pr_moved, cgrid, kPrBlock, 0, ctx->stream, nx, cur, n, epsilon, active,
+                 &C->out_len);
+      GFX_CK(cudaMemcpyAsync(pin, C, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+      GFX_CK(cudaStreamSynchronize(ctx->stream));
+      nactive = (int64_t)pin->out_len;
+    }
+    std::swap(cur, nx);
+  }
+  GFX_CK(cudaGetLastError());
+  if (cur != rank_d)
+    GFX_CK(cudaMemcpyAsync(rank_d, cur, n * sizeof(double), cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+  GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  GFX_CK(cudaEventSynchronize(ctx->ev1));
+  float ms = 0.f;
+  GFX_CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  GFX_CK(cudaMemcpyAsync(pin, C, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+  GFX_CK(cudaStreamSynchronize(ctx->stream));
+  if (stats) {
+    *stats = gfx_stats{};
+    stats->iterations = it;
+    stats->edges_traversed = (int64_t)pin->edges;
+    stats->device_ms = ms;
+    // per round: col (4m) + row, contrib write/read, rank read/write (40n)
+    stats->bytes_alg = it * (4 * g->m + 40 * n);
+  }
+  return GFX_OK;
+}

@@ -1,0 +1,260 @@
+// Triangle counting: degree orientation + sorted-list intersection.
+//
+// Reference: primitives/tc.py:27-86 keeps slot s -> d iff deg[s] > deg[d] or
+// (deg[s] == deg[d] and s < d) (tc.py:57-59), rebuilds a canonical oriented
+// CSR with coo_to_csr (tc.py:53-56), then counts |N+(u) ∩ N+(v)| for every
+// oriented edge in that CSR order (segmented_intersect, operators.py:485-525).
+//
+// Device: orientation keeps each row's surviving slots in order, so the
+// compacted rows ARE the canonical oriented CSR (sorted by (src, dst)).
+// Intersections: one thread merges both lists when they are short; longer
+// pairs go to a list handled warp-cooperatively (each lane binary-searches
+// elements of the shorter list in the longer one).  Counts are exact int32.
+#include <cub/device/device_scan.cuh>
+#include <cuda_runtime.h>
+
+#include "gfx_device.cuh"
+#include "gfx_internal.cuh"
+
+namespace gfx {
+
+__device__ __forceinline__ bool keep_slot(const int64_t* row, int64_t ds, int32_t s, int32_t d) {
+  const int64_t dd = row[d + 1] - row[d];
+  return ds > dd || (ds == dd && s < d);
+}
+
+// pass 0: count kept slots per row; pass 1: write them (ordered compaction)
+template <bool WRITE>
+__global__ void __launch_bounds__(256)
+    k_tc_orient(const int64_t* __restrict__ row, const int32_t* __restrict__ col, int64_t n,
+                int64_t* __restrict__ ocnt, const int64_t* __restrict__ orow,
+                int32_t* __restrict__ ocol, int32_t* __restrict__ osrc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t grp = gw; grp * 32 < n; grp += nw) {
+    const int64_t v = grp * 32 + lane;
+    int64_t b = 0, e = 0;
+    if (v < n) {
+      b = row[v];
+      e = row[v + 1];
+    }
+    const bool heavy = (e - b) > 32;
+    if (v < n && !heavy) {
+      int64_t k = WRITE ? orow[v] : 0;
+      for (int64_t p = b; p < e; ++p) {
+        const int32_t d = col[p];
+        if (keep_slot(row, e - b, (int32_t)v, d)) {
+          if (WRITE) {
+            ocol[k] = d;
+            osrc[k] = (int32_t)v;
+          }
+          ++k;
+        }
+      }
+      if (!WRITE) ocnt[v] = k;
+    }
+    unsigned hm = __ballot_sync(0xffffffffu, heavy);
+    while (hm) {
+      const int k = __ffs(hm) - 1;
+      hm &= hm - 1;
+      const int64_t kv = grp * 32 + k;
+      const int64_t kb = __shfl_sync(0xffffffffu, b, k), ke = __shfl_sync(0xffffffffu, e, k);
+      int64_t pos = WRITE ? orow[kv] : 0;
+      for (int64_t p0 = kb; p0 < ke; p0 += 32) {
+        const int64_t p = p0 + lane;
+        int32_t d = 0;
+        bool keep = false;
+        if (p < ke) {
+          d = col[p];
+          keep = keep_slot(row, ke - kb, (int32_t)kv, d);
+        }
+        const unsigned km = __ballot_sync(0xffffffffu, keep);
+        if (WRITE && keep) {
+          const int64_t at = pos + __popc(km & ((1u << lane) - 1));
+          ocol[at] = d;
+          osrc[at] = (int32_t)kv;
+        }
+        pos += __popc(km);
+      }
+      if (!WRITE && lane == 0) ocnt[kv] = pos;
+    }
+  }
+}
+
+// short lists: one thread merges; long: queued for the warp kernel
+__global__ void __launch_bounds__(256)
+    k_tc_small(const int32_t* __restrict__ us, const int32_t* __restrict__ vs, int64_t npairs,
+               const int64_t* __restrict__ rows, const int32_t* __restrict__ cols,
+               int32_t* __restrict__ counts, int32_t* __restrict__ heavy,
+               unsigned long long* __restrict__ nheavy, unsigned long long* __restrict__ total) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long sum = 0;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < npairs;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    bool big = false;
+    if (i < npairs) {
+      const int32_t u = us[i], v = vs[i];
+      int64_t a = rows[u], ae = rows[u + 1], b = rows[v], be = rows[v + 1];
+      if (ae - a + be - b > 64) {
+        big = true;
+      } else {
+        int c = 0;
+        while (a < ae && b < be) {
+          const int32_t x = cols[a], y = cols[b];
+          c += (x == y);
+          a += (x <= y);
+          b += (y <= x);
+        }
+        counts[i] = c;
+        sum += (unsigned long long)c;
+      }
+    }
+    const unsigned hm = __ballot_sync(0xffffffffu, big);
+    if (hm) {
+      unsigned long long at = 0;
+      if (lane == 0) at = atomicAdd(nheavy, (unsigned long long)__popc(hm));
+      at = __shfl_sync(0xffffffffu, at, 0);
+      if (big) heavy[at + __popc(hm & ((1u << lane) - 1))] = (int32_t)i;
+    }
+  }
+  sum = warp_sum_u64(sum);
+  if (lane == 0 && sum) atomicAdd(total, sum);
+}
+
+__global__ void __launch_bounds__(256)
+    k_tc_heavy(const int32_t* __restrict__ us, const int32_t* __restrict__ vs,
+               const int32_t* __restrict__ heavy, const unsigned long long* __restrict__ nheavy_d,
+               const int64_t* __restrict__ rows, const int32_t* __restrict__ cols,
+               int32_t* __restrict__ counts, unsigned long long* __restrict__ total) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nheavy = (int64_t)*nheavy_d;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long sum = 0;
+  for (int64_t h = gw; h < nheavy; h += nw) {
+    const int32_t i = heavy[h];
+    const int32_t u = us[i], v = vs[i];
+    int64_t a = rows[u], ae = rows[u + 1], b = rows[v], be = rows[v + 1];
+    if (ae - a > be - b) {  // a = shorter list
+      int64_t t = a; a = b; b = t;
+      t = ae; ae = be; be = t;
+    }
+    int c = 0;
+    for (int64_t p = a + lane; p < ae; p += 32) {
+      const int32_t x = cols[p];
+      int64_t lo = b, hi = be;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (cols[mid] < x) lo = mid + 1; else hi = mid;
+      }
+      c += (lo < be && cols[lo] == x);
+    }
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) {
+      counts[i] = c;
+      sum += (unsigned long long)c;
+    }
+  }
+  if (lane == 0 && sum) atomicAdd(total, sum);
+}
+
+int intersect_pairs(gfx_graph* g, const int32_t* us, const int32_t* vs, int64_t npairs,
+                    const int64_t* rows, const int32_t* cols, int32_t* counts, int64_t* total) {
+  gfx_ctx* ctx = g->ctx;
+  int32_t* heavy = nullptr;
+  GFX_TRY(scratch_t(g, "tc_heavy", npairs + 1, &heavy));
+  Counters* C = g->counters + 3;
+  GFX_CK(cudaMemsetAsync(C, 0, sizeof(Counters), ctx->stream));
+  const int grid = ctx->sm_count * 8;
+  GFX_LAUNCH(k_tc_small, grid_for(npairs, 256, grid), 256, 0, ctx->stream, us, vs, npairs, rows,
+             cols, counts, heavy, &C->aux0, &C->total);
+  GFX_LAUNCH(k_tc_heavy, grid, 256, 0, ctx->stream, us, vs, heavy, &C->aux0, rows, cols, counts,
+             &C->total);
+  GFX_CK(cudaGetLastError());
+  auto* pin = static_cast<Counters*>(ctx->pinned);
+  GFX_CK(cudaMemcpyAsync(pin, C, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+  GFX_CK(cudaStreamSynchronize(ctx->stream));
+  *total = (int64_t)pin->total;
+  return GFX_OK;
+}
+
+}  // namespace gfx
+
+using namespace gfx;
+
+extern "C" int gfx_tc_orient(gfx_graph* g, int64_t* m_oriented) {
+  GFX_REQUIRE(g && m_oriented, "gfx_tc_orient: null argument");
+  GFX_REQUIRE(g->flags & GFX_GRAPH_UNDIRECTED, "tc expects a canonical undirected graph");
+  gfx_ctx* ctx = g->ctx;
+  GFX_CK(cudaSetDevice(ctx->device));
+  const int64_t n = g->n;
+  int64_t *ocnt, *orow;
+  int32_t *ocol, *osrc;
+  GFX_TRY(scratch_t(g, "tc_ocnt", n + 1, &ocnt));
+  GFX_TRY(scratch_t(g, "tc_orow", n + 1, &orow));
+  const int grid = grid_for(n, 256, ctx->sm_count * 16);
+  GFX_LAUNCH((k_tc_orient<false>), grid, 256, 0, ctx->stream, g->row, g->col, n, ocnt, nullptr,
+             nullptr, nullptr);
+  GFX_CK(cudaMemsetAsync(ocnt + n, 0, 8, ctx->stream));
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, ocnt, orow, n + 1, ctx->stream);
+  void* tmp = nullptr;
+  GFX_TRY(scratch(g, "tc_scan_tmp", tb, &tmp));
+  cub::DeviceScan::ExclusiveSum(tmp, tb, ocnt, orow, n + 1, ctx->stream);
+  int64_t mo = 0;
+  GFX_CK(cudaMemcpyAsync(&mo, orow + n, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  GFX_CK(cudaStreamSynchronize(ctx->stream));
+  GFX_TRY(scratch_t(g, "tc_ocol", mo + 1, &ocol));
+  GFX_TRY(scratch_t(g, "tc_osrc", mo + 1, &osrc));
+  GFX_LAUNCH((k_tc_orient<true>), grid, 256, 0, ctx->stream, g->row, g->col, n, nullptr, orow,
+             ocol, osrc);
+  GFX_CK(cudaGetLastError());
+  GFX_CK(cudaStreamSynchronize(ctx->stream));
+  g->m_oriented = mo;
+  *m_oriented = mo;
+  return GFX_OK;
+}
+
+extern "C" int gfx_tc_count(gfx_graph* g, int32_t* osrc_d, int32_t* odst_d, int32_t* counts_d,
+                            int64_t* total, gfx_stats* stats) {
+  GFX_REQUIRE(g && total, "gfx_tc_count: null argument");
+  GFX_REQUIRE(g->m_oriented >= 0, "gfx_tc_count: call gfx_tc_orient first");
+  gfx_ctx* ctx = g->ctx;
+  GFX_CK(cudaSetDevice(ctx->device));
+  const int64_t mo = g->m_oriented;
+  int64_t* orow = static_cast<int64_t*>(g->scratch["tc_orow"].ptr);
+  int32_t* ocol = static_cast<int32_t*>(g->scratch["tc_ocol"].ptr);
+  int32_t* osrc = static_cast<int32_t*>(g->scratch["tc_osrc"].ptr);
+  int32_t* counts = counts_d;
+  if (!counts) GFX_TRY(scratch_t(g, "tc_counts", mo + 1, &counts));
+  GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  GFX_TRY(intersect_pairs(g, osrc, ocol, mo, orow, ocol, counts, total));
+  GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  if (osrc_d)
+    GFX_CK(cudaMemcpyAsync(osrc_d, osrc, mo * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (odst_d)
+    GFX_CK(cudaMemcpyAsync(odst_d, ocol, mo * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  GFX_CK(cudaStreamSynchronize(ctx->stream));
+  float ms = 0.f;
+  GFX_CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  if (stats) {
+    *stats = gfx_stats{};
+    stats->iterations = 1;
+    stats->device_ms = ms;
+  }
+  return GFX_OK;
+}
+
+extern "C" int gfx_segmented_intersect(gfx_graph* g, const int32_t* u_d, const int32_t* v_d,
+                                       int64_t num_pairs, int32_t* counts_d, int64_t* total) {
+  GFX_REQUIRE(g && total && (num_pairs == 0 || (u_d && v_d && counts_d)),
+              "gfx_segmented_intersect: null argument");
+  GFX_CK(cudaSetDevice(g->ctx->device));
+  if (num_pairs == 0) {
+    *total = 0;
+    return GFX_OK;
+  }
+  return intersect_pairs(g, u_d, v_d, num_pairs, g->row, g->col, counts_d, total);
+}
