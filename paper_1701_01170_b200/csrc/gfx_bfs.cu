@@ -125,7 +125,9 @@ __global__ void __launch_bounds__(256)
 // labels are identical, only the work differs).  The warp owns its words, so
 // visited / next-frontier words are written with plain coalesced stores.
 // counters: out_len += |new frontier|, edges += sum of in-degree(U),
-//           aux0 += early-exit probes S(U), aux1 += |U| (in-degree > 0).
+//           aux0 += early-exit probes S(U), aux1 += |U| (in-degree > 0),
+//           aux2 += sum of out-degrees of the new frontier (E_r bookkeeping;
+//           row == NULL on undirected graphs, where in- and out-degree agree).
 // ---------------------------------------------------------------------------
 constexpr int kPullBatch = 4;  // bitmap words (vertices per lane) in flight
 
@@ -133,12 +135,13 @@ __global__ void __launch_bounds__(256)
     k_bfs_pull(int64_t words, const uint32_t* __restrict__ nz_in,
                uint32_t* __restrict__ visited, const uint32_t* __restrict__ front,
                uint32_t* __restrict__ next, const int64_t* __restrict__ rrow,
-               const int32_t* __restrict__ rcol, int32_t* __restrict__ labels,
-               int32_t* __restrict__ preds, int32_t depth, Counters* __restrict__ ctr) {
+               const int32_t* __restrict__ rcol, const int64_t* __restrict__ row,
+               int32_t* __restrict__ labels, int32_t* __restrict__ preds, int32_t depth,
+               Counters* __restrict__ ctr) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  unsigned long long found_cnt = 0, in_edges = 0, probes = 0, cands = 0;
+  unsigned long long found_cnt = 0, in_edges = 0, probes = 0, cands = 0, found_deg = 0;
   for (int64_t grp = gw; grp * 32 < words; grp += nwarps) {
     const int64_t w = grp * 32 + lane;
     uint32_t vis = 0xffffffffu, cand = 0;
@@ -198,6 +201,8 @@ __global__ void __launch_bounds__(256)
             const int64_t u = (grp * 32 + kw[q]) * 32 + lane;
             labels[u] = depth;
             preds[u] = par;
+            found_deg += row ? (unsigned long long)(row[u + 1] - row[u])
+                             : (unsigned long long)(e[q] - b[q]);
           }
         }
         const unsigned fm = __ballot_sync(0xffffffffu, found);
@@ -214,11 +219,13 @@ __global__ void __launch_bounds__(256)
   in_edges = warp_sum_u64(in_edges);
   probes = warp_sum_u64(probes);
   cands = warp_sum_u64(cands);
+  found_deg = warp_sum_u64(found_deg);
   if (lane == 0) {
     if (found_cnt) atomicAdd(&ctr->out_len, found_cnt);
     if (in_edges) atomicAdd(&ctr->edges, in_edges);
     if (probes) atomicAdd(&ctr->aux0, probes);
     if (cands) atomicAdd(&ctr->aux1, cands);
+    if (found_deg) atomicAdd(&ctr->aux2, found_deg);
   }
 }
 
@@ -246,16 +253,21 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// queue -> frontier bitmap (bitmap pre-zeroed)
+// queue -> frontier bitmap (bitmap pre-zeroed); deg_sum += sum of out-degrees
 __global__ void __launch_bounds__(256)
     k_queue_to_bitmap(const int32_t* __restrict__ F, const unsigned long long* __restrict__ nf_d,
-                      uint32_t* __restrict__ bm) {
+                      uint32_t* __restrict__ bm, const int64_t* __restrict__ row,
+                      unsigned long long* __restrict__ deg_sum) {
   const int64_t nf = (int64_t)*nf_d;
+  unsigned long long dsum = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nf;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t v = F[i];
     atomicOr(&bm[v >> 5], 1u << (v & 31));
+    dsum += (unsigned long long)(row[v + 1] - row[v]);
   }
+  dsum = warp_sum_u64(dsum);
+  if ((threadIdx.x & 31) == 0 && dsum) atomicAdd(deg_sum, dsum);
 }
 
 __global__ void k_bfs_seed(int32_t src, int32_t* labels, uint32_t* visited, int32_t* order,
@@ -421,6 +433,7 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
   uint32_t* fcur = B.front0;
   uint32_t* fnext = B.front1;
   int64_t depth = 0, edges_total = 0, switches = 0, nrec = 0, bytes_total = 0, work_total = 0;
+  int64_t e_r = 0, reached = 0, pull_found_deg = 0;
 
   while (nf > 0) {
     ++depth;
@@ -458,6 +471,7 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
       level_edges = (int64_t)pin->total;
       nout = (int64_t)pin->out_len;
       work = level_edges;
+      e_r += level_edges;  // sum of degrees of this frontier
       // push: frontier id + row pair per item, one col id per slot, label +
       // queue write per discovered vertex
       bytes = 20 * nf + 4 * level_edges + 8 * nout;
@@ -466,12 +480,13 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
     } else {
       if (queue_form) {
         GFX_CK(cudaMemsetAsync(fcur, 0, W * 4, ctx->stream));
-        GFX_LAUNCH(k_queue_to_bitmap, grid_for(nf, 256, ctx->sm_count * 8), 256, 0, ctx->stream, 
-            B.order + q_off, &prev->out_len, fcur);
+        GFX_LAUNCH(k_queue_to_bitmap, grid_for(nf, 256, ctx->sm_count * 8), 256, 0, ctx->stream,
+                   B.order + q_off, &prev->out_len, fcur, g->row, &cur->aux3);
         GFX_CK(cudaGetLastError());
       }
-      GFX_LAUNCH(k_bfs_pull, ctx->sm_count * 8, 256, 0, ctx->stream, 
-          W, nz_in, B.visited, fcur, fnext, g->rrow, g->rcol, labels, preds, (int32_t)depth, cur);
+      GFX_LAUNCH(k_bfs_pull, ctx->sm_count * 8, 256, 0, ctx->stream, W, nz_in, B.visited, fcur,
+                 fnext, g->rrow, g->rcol, directed ? g->row : nullptr, labels, preds,
+                 (int32_t)depth, cur);
       GFX_CK(cudaGetLastError());
       if (ctx->timing) GFX_CK(cudaEventRecord(ctx->lev1, ctx->stream));
       GFX_CK(cudaMemcpyAsync(pin, cur, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
@@ -480,6 +495,10 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
       nout = (int64_t)pin->out_len;
       work = (int64_t)pin->aux0;
       cands = (int64_t)pin->aux1;
+      // E_r: degree sum of this level's input frontier, from the conversion
+      // (push -> pull) or from the previous pull's found set
+      e_r += queue_form ? (int64_t)pin->aux3 : pull_found_deg;
+      pull_found_deg = (int64_t)pin->aux2;
       // pull: id + row per candidate, one col id per early-exit probe, label
       // + frontier write per discovered vertex
       bytes = 12 * cands + 4 * work + 8 * nout;
@@ -505,6 +524,7 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
       ++nrec;
     }
     edges_total += level_edges;
+    reached += nf;
     bytes_total += bytes;
     work_total += work;
     mode_state = mode;
@@ -522,7 +542,8 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
     st->num_records = nrec;
     st->bytes_alg = bytes_total;
     st->work_slots = work_total;
-    GFX_TRY(reached_stats(g, labels, &st->reached, &st->edges_reached));
+    st->reached = reached;
+    st->edges_reached = e_r;
   }
   return GFX_OK;
 }
