@@ -40,11 +40,11 @@ struct BfsClaimOp {
   int32_t* labels;
   int32_t* preds;
   int32_t depth;
-  uint32_t wv[4];
+  uint32_t wv[kVisitBatch];
   __device__ int32_t src_value(int32_t) const { return 0; }
-  __device__ void prefetch(const int32_t d[4]) {
+  __device__ void prefetch(const int32_t d[kVisitBatch]) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) wv[u] = d[u] >= 0 ? visited[d[u] >> 5] : 0xffffffffu;
+    for (int u = 0; u < kVisitBatch; ++u) wv[u] = d[u] >= 0 ? visited[d[u] >> 5] : 0xffffffffu;
   }
   __device__ bool visit(int u, int32_t d, int32_t s, int32_t, int32_t, int64_t) {
     const uint32_t bit = 1u << (d & 31);
@@ -62,11 +62,11 @@ struct BfsIdempOp {
   int32_t* labels;
   int32_t* preds;
   int32_t depth;
-  uint32_t wv[4];
+  uint32_t wv[kVisitBatch];
   __device__ int32_t src_value(int32_t) const { return 0; }
-  __device__ void prefetch(const int32_t d[4]) {
+  __device__ void prefetch(const int32_t d[kVisitBatch]) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) wv[u] = d[u] >= 0 ? visited[d[u] >> 5] : 0xffffffffu;
+    for (int u = 0; u < kVisitBatch; ++u) wv[u] = d[u] >= 0 ? visited[d[u] >> 5] : 0xffffffffu;
   }
   __device__ bool visit(int u, int32_t d, int32_t s, int32_t, int32_t, int64_t) {
     if ((wv[u] >> (d & 31)) & 1u) return false;
@@ -115,27 +115,26 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// ---------------------------------------------------------------------------
-// Pull (bottom-up) level.  One warp owns 32 consecutive bitmap words (1024
-// vertices); lanes are vertices.  Candidates = unvisited & in-degree > 0 (the
-// reference keeps isolated vertices in U, but they can never be reached and
-// add 0 to edges_traversed, frontier.py:97-100).  Each candidate scans its
-// in-neighbours in ascending order and stops at the first one in the current
-// frontier bitmap (the reference scans all in-edges, operators.py:269-307;
-// labels are identical, only the work differs).  The warp owns its words, so
-// visited / next-frontier words are written with plain coalesced stores.
-// counters: out_len += |new frontier|, edges += sum of in-degree(U),
-//           aux0 += early-exit probes S(U), aux1 += |U| (in-degree > 0),
-//           aux2 += sum of out-degrees of the new frontier (E_r bookkeeping;
-//           row == NULL on undirected graphs, where in- and out-degree agree).
-// ---------------------------------------------------------------------------
 constexpr int kPullBatch = 4;  // bitmap words (vertices per lane) in flight
 
+// Pull (bottom-up) level.  One warp owns 32 consecutive bitmap words (1024
+// vertices); lanes are vertices.  Candidates = unvisited & in-degree > 0.
+// The first probe reads head[u] -- the graph-constant copy of each vertex's
+// first in-neighbour, stored densely so the probe is a coalesced 4-byte read
+// instead of a scattered sector -- and only candidates whose first
+// in-neighbour is not in the frontier fetch their row bounds and scan on in
+// ascending order (reference pull_expand, operators.py:269-307, scans every
+// in-edge; labels are identical, only the work differs).
+// counters: out_len += |new frontier|, edges += sum of in-degree(U) (only
+//           when count_in_edges; undirected callers derive it on the host as
+//           m - E_r(visited)), aux0 += early-exit probes S(U), aux1 += |U|,
+//           aux2 += sum of out-degrees of the new frontier (E_r bookkeeping).
 __global__ void __launch_bounds__(256)
     k_bfs_pull(int64_t words, const uint32_t* __restrict__ nz_in,
                uint32_t* __restrict__ visited, const uint32_t* __restrict__ front,
-               uint32_t* __restrict__ next, const int64_t* __restrict__ rrow,
-               const int32_t* __restrict__ rcol, const int64_t* __restrict__ row,
+               uint32_t* __restrict__ next, const int32_t* __restrict__ head,
+               const int64_t* __restrict__ rrow, const int32_t* __restrict__ rcol,
+               const int64_t* __restrict__ row, int count_in_edges,
                int32_t* __restrict__ labels, int32_t* __restrict__ preds, int32_t depth,
                Counters* __restrict__ ctr) {
   const int lane = threadIdx.x & 31;
@@ -150,7 +149,6 @@ __global__ void __launch_bounds__(256)
       cand = ~vis & nz_in[w];
     }
     uint32_t newbits_mine = 0;
-    // words of this group that hold candidates, processed kPullBatch at a time
     unsigned todo = __ballot_sync(0xffffffffu, cand != 0);
     while (todo) {
       int kw[kPullBatch];
@@ -162,47 +160,50 @@ __global__ void __launch_bounds__(256)
         c[q] = __shfl_sync(0xffffffffu, cand, kw[q] < 0 ? 0 : kw[q]);
         if (kw[q] < 0) c[q] = 0;
       }
-      // phase 1: row pairs of every candidate lane (independent loads)
-      int64_t b[kPullBatch], e[kPullBatch];
+      // first probe: dense head array (coalesced across the warp)
+      int32_t h[kPullBatch];
 #pragma unroll
-      for (int q = 0; q < kPullBatch; ++q) {
-        b[q] = e[q] = 0;
-        if ((c[q] >> lane) & 1u) {
-          const int64_t u = (grp * 32 + kw[q]) * 32 + lane;
-          b[q] = rrow[u];
-          e[q] = rrow[u + 1];
-        }
-      }
-      // phase 2: first in-neighbour of each candidate
-      int32_t s0[kPullBatch];
+      for (int q = 0; q < kPullBatch; ++q)
+        h[q] = ((c[q] >> lane) & 1u) ? head[(grp * 32 + kw[q]) * 32 + lane] : -1;
+      uint32_t fw[kPullBatch];
 #pragma unroll
-      for (int q = 0; q < kPullBatch; ++q) s0[q] = (e[q] > b[q]) ? ld_stream_i32(rcol + b[q]) : -1;
-      // phase 3: frontier test, then the (rare) sequential tail scan
+      for (int q = 0; q < kPullBatch; ++q) fw[q] = h[q] >= 0 ? front[h[q] >> 5] : 0u;
 #pragma unroll
       for (int q = 0; q < kPullBatch; ++q) {
         bool found = false;
-        int32_t par = -1;
-        if (e[q] > b[q]) {
+        if (h[q] >= 0) {
+          const int64_t u = (grp * 32 + kw[q]) * 32 + lane;
           ++cands;
-          in_edges += (unsigned long long)(e[q] - b[q]);
-          int64_t p = b[q];
-          int32_t s = s0[q];
-          for (;;) {
-            if ((front[s >> 5] >> (s & 31)) & 1u) {
-              found = true;
-              par = s;
-              break;
+          int32_t par = -1;
+          int64_t b = 0, e = 0;
+          if ((fw[q] >> (h[q] & 31)) & 1u) {
+            found = true;
+            par = h[q];
+            ++probes;
+            if (count_in_edges) {
+              b = rrow[u];
+              e = rrow[u + 1];
             }
-            if (++p >= e[q]) break;
-            s = rcol[p];
+          } else {
+            // tail: continue from the second in-neighbour
+            b = rrow[u];
+            e = rrow[u + 1];
+            int64_t p = b + 1;
+            for (; p < e; ++p) {
+              const int32_t s = rcol[p];
+              if ((front[s >> 5] >> (s & 31)) & 1u) {
+                found = true;
+                par = s;
+                break;
+              }
+            }
+            probes += (unsigned long long)(found ? p - b + 1 : e - b);
           }
-          probes += (unsigned long long)(found ? p - b[q] + 1 : e[q] - b[q]);
+          in_edges += (unsigned long long)(e - b);
           if (found) {
-            const int64_t u = (grp * 32 + kw[q]) * 32 + lane;
             labels[u] = depth;
             preds[u] = par;
-            found_deg += row ? (unsigned long long)(row[u + 1] - row[u])
-                             : (unsigned long long)(e[q] - b[q]);
+            if (row) found_deg += (unsigned long long)(row[u + 1] - row[u]);
           }
         }
         const unsigned fm = __ballot_sync(0xffffffffu, found);
@@ -226,6 +227,16 @@ __global__ void __launch_bounds__(256)
     if (probes) atomicAdd(&ctr->aux0, probes);
     if (cands) atomicAdd(&ctr->aux1, cands);
     if (found_deg) atomicAdd(&ctr->aux2, found_deg);
+  }
+}
+
+// graph-constant first in-neighbour per vertex (-1 when in-degree is 0)
+__global__ void k_pull_heads(const int64_t* __restrict__ rrow, const int32_t* __restrict__ rcol,
+                             int64_t n, int32_t* __restrict__ head) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = rrow[v];
+    head[v] = rrow[v + 1] > b ? rcol[b] : -1;
   }
 }
 
@@ -410,10 +421,19 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
   BfsBuffers B;
   GFX_TRY(bfs_buffers(g, idemp, &B));
   const uint32_t* nz_in = nullptr;
+  int32_t* head = nullptr;
   {
     void* p = nullptr;
     GFX_TRY(scratch(g, directed ? "nz_in" : "nz_out", W * 4, &p));
     nz_in = static_cast<const uint32_t*>(p);
+    if (direction != GFX_DIR_PUSH) {
+      bool fresh = false;
+      GFX_TRY(scratch(g, "keep_head", (size_t)(n + 1) * 4, &p, &fresh));
+      head = static_cast<int32_t*>(p);
+      if (fresh)
+        GFX_LAUNCH(k_pull_heads, grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream,
+                   g->rrow, g->rcol, n, head);
+    }
   }
   Counters* C = g->counters;  // C[0], C[1]: per-level double buffer
   auto* pin = static_cast<Counters*>(ctx->pinned);
@@ -485,13 +505,16 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
         GFX_CK(cudaGetLastError());
       }
       GFX_LAUNCH(k_bfs_pull, ctx->sm_count * 8, 256, 0, ctx->stream, W, nz_in, B.visited, fcur,
-                 fnext, g->rrow, g->rcol, directed ? g->row : nullptr, labels, preds,
+                 fnext, head, g->rrow, g->rcol, g->row, directed ? 1 : 0, labels, preds,
                  (int32_t)depth, cur);
       GFX_CK(cudaGetLastError());
       if (ctx->timing) GFX_CK(cudaEventRecord(ctx->lev1, ctx->stream));
       GFX_CK(cudaMemcpyAsync(pin, cur, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
       GFX_CK(cudaStreamSynchronize(ctx->stream));
-      level_edges = (int64_t)pin->edges;
+      // sum of in-degrees of U: counted by the kernel on directed graphs; on
+      // undirected ones it is m minus the degrees of everything visited so far
+      level_edges = directed ? (int64_t)pin->edges
+                             : m - (e_r + (queue_form ? (int64_t)pin->aux3 : pull_found_deg));
       nout = (int64_t)pin->out_len;
       work = (int64_t)pin->aux0;
       cands = (int64_t)pin->aux1;

@@ -21,7 +21,7 @@
 //   static constexpr bool kSrcVal;     per-item src_value(v)
 //   static constexpr bool kEmitEdge;   emit edge ids instead of dst ids
 //   __device__ int32_t src_value(int32_t v) const;
-//   __device__ void prefetch(const int32_t d[4]);
+//   __device__ void prefetch(const int32_t d[kVisitBatch]);
 //   __device__ bool visit(int u, int32_t dst, int32_t src, int32_t w,
 //                         int32_t sval, int64_t edge);   // u = prefetch slot
 #pragma once
@@ -34,6 +34,7 @@ namespace gfx {
 constexpr int kExpandBlock = 256;
 constexpr int kPassItems = 1024;
 constexpr int kSlotsPerThread = kTile / kExpandBlock;  // 16
+constexpr int kVisitBatch = 8;  // slots (column loads) in flight per thread
 
 struct ExpandSmem {
   int64_t delta[kPassItems];   // row[v] - scan[i]: col index = delta + global slot
@@ -123,24 +124,24 @@ __global__ void __launch_bounds__(kExpandBlock)
       }
       __syncthreads();
 
-      // ---- visit: 4 slots in flight per thread
-      for (int jb = 0; jb < nsl; jb += kExpandBlock * 4) {
-        int32_t d[4], it[4], w[4];
-        int64_t e[4];
+      // ---- visit: kVisitBatch slots in flight per thread
+      for (int jb = 0; jb < nsl; jb += kExpandBlock * kVisitBatch) {
+        int32_t d[kVisitBatch], it[kVisitBatch], w[kVisitBatch];
+        int64_t e[kVisitBatch];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kVisitBatch; ++u) {
           const int j = jb + u * kExpandBlock + tid;
           it[u] = j < nsl ? S.owner[j] : -1;
           e[u] = it[u] >= 0 ? S.delta[it[u]] + sl + j : 0;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kVisitBatch; ++u) {
           d[u] = it[u] >= 0 ? ld_stream_i32(col + e[u]) : -1;
           if (Op::kWeights) w[u] = it[u] >= 0 ? ld_stream_i32(wgt + e[u]) : 0;
         }
         o.prefetch(d);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kVisitBatch; ++u) {
           bool emit = false;
           if (d[u] >= 0) {
             const int32_t sv = Op::kSrcVal ? S.sval[it[u]] : 0;

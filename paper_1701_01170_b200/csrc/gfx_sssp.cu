@@ -32,11 +32,11 @@ struct SsspRelaxOp {
   unsigned long long* dp;
   int32_t* stamp;
   int32_t it;
-  unsigned long long cur[4];
+  unsigned long long cur[kVisitBatch];
   __device__ int32_t src_value(int32_t v) const { return (int32_t)(dp[v] >> 32); }
-  __device__ void prefetch(const int32_t d[4]) {
+  __device__ void prefetch(const int32_t d[kVisitBatch]) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) cur[u] = d[u] >= 0 ? dp[d[u]] : 0ull;
+    for (int u = 0; u < kVisitBatch; ++u) cur[u] = d[u] >= 0 ? dp[d[u]] : 0ull;
   }
   // atomic_min relax (operators.py:111-124): emit d once per iteration when
   // its distance strictly improved
