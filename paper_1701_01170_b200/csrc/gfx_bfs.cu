@@ -13,6 +13,7 @@
 //   scan     int64[n+1]      exclusive degree prefix of the current queue
 //   rowbase  int64[n]        row[F[i]] (saves a scattered re-read)
 //   part     int32[m/T+2]    tile -> first item (LB partition)
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -23,6 +24,7 @@
 #include "gfx_direction.cuh"
 #include "gfx_expand.cuh"
 #include "gfx_internal.cuh"
+#include "gfx_scan.cuh"
 
 namespace gfx {
 
@@ -129,17 +131,14 @@ constexpr int kPullBatch = 4;  // bitmap words (vertices per lane) in flight
 //           when count_in_edges; undirected callers derive it on the host as
 //           m - E_r(visited)), aux0 += early-exit probes S(U), aux1 += |U|,
 //           aux2 += sum of out-degrees of the new frontier (E_r bookkeeping).
-__global__ void __launch_bounds__(256)
-    k_bfs_pull(int64_t words, const uint32_t* __restrict__ nz_in,
-               uint32_t* __restrict__ visited, const uint32_t* __restrict__ front,
-               uint32_t* __restrict__ next, const int32_t* __restrict__ head,
-               const int64_t* __restrict__ rrow, const int32_t* __restrict__ rcol,
-               const int64_t* __restrict__ row, int count_in_edges,
-               int32_t* __restrict__ labels, int32_t* __restrict__ preds, int32_t depth,
-               Counters* __restrict__ ctr) {
+__device__ __forceinline__ void pull_groups(
+    int64_t words, const uint32_t* __restrict__ nz_in, uint32_t* __restrict__ visited,
+    const uint32_t* __restrict__ front, uint32_t* __restrict__ next,
+    const int32_t* __restrict__ head, const int64_t* __restrict__ rrow,
+    const int32_t* __restrict__ rcol, const int64_t* __restrict__ row, int count_in_edges,
+    int32_t* __restrict__ labels, int32_t* __restrict__ preds, int32_t depth,
+    Counters* __restrict__ ctr, int64_t gw, int64_t nwarps) {
   const int lane = threadIdx.x & 31;
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned long long found_cnt = 0, in_edges = 0, probes = 0, cands = 0, found_deg = 0;
   for (int64_t grp = gw; grp * 32 < words; grp += nwarps) {
     const int64_t w = grp * 32 + lane;
@@ -230,6 +229,19 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+__global__ void __launch_bounds__(256)
+    k_bfs_pull(int64_t words, const uint32_t* __restrict__ nz_in,
+               uint32_t* __restrict__ visited, const uint32_t* __restrict__ front,
+               uint32_t* __restrict__ next, const int32_t* __restrict__ head,
+               const int64_t* __restrict__ rrow, const int32_t* __restrict__ rcol,
+               const int64_t* __restrict__ row, int count_in_edges,
+               int32_t* __restrict__ labels, int32_t* __restrict__ preds, int32_t depth,
+               Counters* __restrict__ ctr) {
+  pull_groups(words, nz_in, visited, front, next, head, rrow, rcol, row, count_in_edges, labels,
+              preds, depth, ctr, (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5,
+              ((int64_t)gridDim.x * blockDim.x) >> 5);
+}
+
 // graph-constant first in-neighbour per vertex (-1 when in-degree is 0)
 __global__ void k_pull_heads(const int64_t* __restrict__ rrow, const int32_t* __restrict__ rcol,
                              int64_t n, int32_t* __restrict__ head) {
@@ -241,12 +253,11 @@ __global__ void k_pull_heads(const int64_t* __restrict__ rrow, const int32_t* __
 }
 
 // frontier bitmap -> queue (ascending within each warp's 1024-vertex span)
-__global__ void __launch_bounds__(256)
-    k_bitmap_to_queue(int64_t words, const uint32_t* __restrict__ bm, int32_t* __restrict__ out,
-                      unsigned long long* __restrict__ out_len) {
+__device__ __forceinline__ void bitmap_to_queue(int64_t words, const uint32_t* __restrict__ bm,
+                                                int32_t* __restrict__ out,
+                                                unsigned long long* __restrict__ out_len,
+                                                int64_t gw, int64_t nwarps) {
   const int lane = threadIdx.x & 31;
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t grp = gw; grp * 32 < words; grp += nwarps) {
     const int64_t w = grp * 32 + lane;
     uint32_t x = w < words ? bm[w] : 0u;
@@ -264,21 +275,35 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// queue -> frontier bitmap (bitmap pre-zeroed); deg_sum += sum of out-degrees
 __global__ void __launch_bounds__(256)
-    k_queue_to_bitmap(const int32_t* __restrict__ F, const unsigned long long* __restrict__ nf_d,
-                      uint32_t* __restrict__ bm, const int64_t* __restrict__ row,
-                      unsigned long long* __restrict__ deg_sum) {
-  const int64_t nf = (int64_t)*nf_d;
+    k_bitmap_to_queue(int64_t words, const uint32_t* __restrict__ bm, int32_t* __restrict__ out,
+                      unsigned long long* __restrict__ out_len) {
+  bitmap_to_queue(words, bm, out, out_len, (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5,
+                  ((int64_t)gridDim.x * blockDim.x) >> 5);
+}
+
+// queue -> frontier bitmap (bitmap pre-zeroed); deg_sum += sum of out-degrees
+__device__ __forceinline__ void queue_to_bitmap(const int32_t* __restrict__ F, int64_t nf,
+                                                uint32_t* __restrict__ bm,
+                                                const int64_t* __restrict__ row,
+                                                unsigned long long* __restrict__ deg_sum,
+                                                int64_t tid0, int64_t nthreads) {
   unsigned long long dsum = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nf;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t i = tid0; i < nf; i += nthreads) {
     const int32_t v = F[i];
     atomicOr(&bm[v >> 5], 1u << (v & 31));
     dsum += (unsigned long long)(row[v + 1] - row[v]);
   }
   dsum = warp_sum_u64(dsum);
   if ((threadIdx.x & 31) == 0 && dsum) atomicAdd(deg_sum, dsum);
+}
+
+__global__ void __launch_bounds__(256)
+    k_queue_to_bitmap(const int32_t* __restrict__ F, const unsigned long long* __restrict__ nf_d,
+                      uint32_t* __restrict__ bm, const int64_t* __restrict__ row,
+                      unsigned long long* __restrict__ deg_sum) {
+  queue_to_bitmap(F, (int64_t)*nf_d, bm, row, deg_sum, blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
+                  (int64_t)gridDim.x * blockDim.x);
 }
 
 __global__ void k_bfs_seed(int32_t src, int32_t* labels, uint32_t* visited, int32_t* order,
@@ -571,6 +596,335 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
   return GFX_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Device-resident level loop: ONE cooperative launch runs the whole
+// direction-optimising BFS.  Every CTA keeps an identical copy of the loop
+// state and evaluates the reference decision (direction.py:52-70, exact
+// replica in gfx_direction.cuh) itself; phases are separated by grid-wide
+// barriers instead of kernel boundaries and host round trips.  The grid
+// barrier's gpu-scope fence also invalidates L1, so every phase reads the
+// previous phase's bitmaps fresh.
+// ---------------------------------------------------------------------------
+namespace cg = cooperative_groups;
+
+struct PBfsArgs {
+  int64_t n, m, words;
+  const int64_t* row;
+  const int32_t* col;
+  const int64_t* rrow;
+  const int32_t* rcol;
+  const int32_t* head;
+  const uint32_t* nz_in;
+  uint32_t* visited;
+  uint32_t* front[2];
+  int32_t* order;
+  int64_t* scan;
+  int64_t* rowbase;
+  int32_t* part;
+  unsigned long long* status;
+  int32_t* labels;
+  int32_t* preds;
+  Counters* C;  // 3 rotating counter blocks
+  gfx_iter_rec* recs;
+  int64_t rec_cap;
+  long long* summary;
+  int direction, mu_edge, directed;
+  double do_a, do_b;
+  int32_t source;
+  unsigned epoch_base;
+};
+
+struct PCtl {
+  long long nf, n_u, q_off, q_end, e_r, pfd, depth, reached, edges_total, bytes_total, work_total,
+      switches, nrec;
+  int mode_state, queue_form, mode, fsel;
+  double mf, mu;
+  unsigned long long t0;
+};
+
+__device__ __forceinline__ unsigned long long ld_ctr(const unsigned long long* p) {
+  return ld_volatile_u64(p);
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// kept out of line: the 128-bit division would otherwise inflate every phase's
+// register allocation
+__device__ __noinline__ void device_decide(long long n, long long m, long long nf, long long n_u,
+                                           int mu_edge, int direction, int mode_state,
+                                           long long depth, double do_a, double do_b,
+                                           double* mf, double* mu, int* mode) {
+  const DirEstimate est = estimate_mf_mu(n, m, nf, n_u, mu_edge);
+  *mf = est.m_f;
+  *mu = est.m_u;
+  if (direction == GFX_DIR_AUTO)
+    *mode = decide_direction(mode_state, est, do_a, do_b);
+  else if (direction == GFX_DIR_PULL)
+    *mode = depth > 1 ? GFX_DIR_PULL : GFX_DIR_PUSH;
+  else
+    *mode = GFX_DIR_PUSH;
+}
+
+__global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ExpandSmem& S = *reinterpret_cast<ExpandSmem*>(smem_raw);
+  __shared__ ScanSmem ss;
+  __shared__ PCtl c;
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int64_t gw = gtid >> 5, nw = nthr >> 5;
+  const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+
+  // ---- initialise outputs and state
+  for (int64_t i = gtid; i < a.n; i += nthr) {
+    a.labels[i] = GFX_UNVISITED;
+    a.preds[i] = -1;
+  }
+  for (int64_t i = gtid; i < a.words; i += nthr) a.visited[i] = 0u;
+  for (int64_t i = gtid; i < 3 * (int64_t)(sizeof(Counters) / 8); i += nthr)
+    reinterpret_cast<unsigned long long*>(a.C)[i] = 0ull;
+  if (threadIdx.x == 0) {
+    S.cnt = 0;
+    c.nf = 1;
+    c.n_u = a.n;
+    c.q_off = 0;
+    c.q_end = 1;
+    c.e_r = c.pfd = c.depth = c.reached = c.edges_total = c.bytes_total = c.work_total = 0;
+    c.switches = c.nrec = 0;
+    c.mode_state = GFX_DIR_PUSH;
+    c.queue_form = 1;
+    c.fsel = 0;
+  }
+  grid.sync();
+  if (leader) {
+    a.labels[a.source] = 0;
+    a.visited[a.source >> 5] = 1u << (a.source & 31);
+    a.order[0] = a.source;
+  }
+  grid.sync();
+
+  for (;;) {
+    if (threadIdx.x == 0) {
+      c.depth += 1;
+      c.n_u -= c.nf;
+      int mode;
+      double mf, mu;
+      device_decide(a.n, a.m, c.nf, c.n_u, a.mu_edge, a.direction, c.mode_state, c.depth, a.do_a,
+                    a.do_b, &mf, &mu, &mode);
+      c.mf = mf;
+      c.mu = mu;
+      c.mode = mode;
+      if (mode != c.mode_state) c.switches += 1;
+      c.t0 = globaltimer();
+    }
+    __syncthreads();
+    const int32_t depth = (int32_t)c.depth;
+    const int64_t nf = c.nf;
+    Counters* cur = &a.C[c.depth % 3];
+    if (blockIdx.x == 0 && threadIdx.x < (int)(sizeof(Counters) / 8))
+      reinterpret_cast<unsigned long long*>(&a.C[(c.depth + 1) % 3])[threadIdx.x] = 0ull;
+    uint32_t* fcur = a.front[c.fsel];
+    uint32_t* fnext = a.front[c.fsel ^ 1];
+    long long level_edges = 0, nout = 0, work = 0, cands = 0, bytes = 0;
+
+    if (c.mode == GFX_DIR_PUSH) {
+      if (!c.queue_form) {
+        bitmap_to_queue(a.words, fcur, a.order + c.q_end, &cur->aux2, gw, nw);
+        grid.sync();
+        if (threadIdx.x == 0) {
+          c.q_off = c.q_end;
+          c.q_end += nf;
+          c.queue_form = 1;
+        }
+        __syncthreads();
+      }
+      const int32_t* F = a.order + c.q_off;
+      const int64_t stiles = nf > 0 ? (nf + kScanTileItems - 1) / kScanTileItems : 1;
+      const unsigned ep = a.epoch_base + (unsigned)c.depth;
+      for (int64_t t = blockIdx.x; t < stiles; t += gridDim.x)
+        scan_tile(t, stiles, F, nf, a.row, a.scan, a.rowbase, a.part, a.status, ep, cur, ss);
+      grid.sync();
+      BfsClaimOp op{a.visited, a.labels, a.preds, depth, {}};
+      expand_tiles(S, op, F, nf, a.scan, a.rowbase, a.part, (int64_t)ld_ctr(&cur->ntiles),
+                   (int64_t)ld_ctr(&cur->total), a.col, nullptr, a.order + c.q_end,
+                   &cur->out_len, blockIdx.x, gridDim.x);
+      for (int64_t i = gtid; i < stiles; i += nthr) a.status[i] = 0ull;
+      grid.sync();
+      level_edges = (long long)ld_ctr(&cur->total);
+      nout = (long long)ld_ctr(&cur->out_len);
+      work = level_edges;
+      bytes = 20 * nf + 4 * level_edges + 8 * nout;
+      if (threadIdx.x == 0) {
+        c.e_r += level_edges;
+        c.q_off = c.q_end;
+        c.q_end += nout;
+      }
+    } else {
+      if (c.queue_form) {
+        for (int64_t i = gtid; i < a.words; i += nthr) fcur[i] = 0u;
+        grid.sync();
+        queue_to_bitmap(a.order + c.q_off, nf, fcur, a.row, &cur->aux3, gtid, nthr);
+        grid.sync();
+      }
+      pull_groups(a.words, a.nz_in, a.visited, fcur, fnext, a.head, a.rrow, a.rcol, a.row,
+                  a.directed, a.labels, a.preds, depth, cur, gw, nw);
+      grid.sync();
+      nout = (long long)ld_ctr(&cur->out_len);
+      work = (long long)ld_ctr(&cur->aux0);
+      cands = (long long)ld_ctr(&cur->aux1);
+      const long long fdeg = c.queue_form ? (long long)ld_ctr(&cur->aux3) : c.pfd;
+      level_edges = a.directed ? (long long)ld_ctr(&cur->edges) : a.m - (c.e_r + fdeg);
+      bytes = 12 * cands + 4 * work + 8 * nout;
+      if (threadIdx.x == 0) {
+        c.e_r += fdeg;
+        c.pfd = (long long)ld_ctr(&cur->aux2);
+        c.fsel ^= 1;
+        c.queue_form = 0;
+      }
+    }
+    if (leader && c.nrec < a.rec_cap) {
+      gfx_iter_rec r{};
+      r.iteration = c.depth;
+      r.frontier_in = nf;
+      r.frontier_out = nout;
+      r.n_u = c.n_u;
+      r.edges = level_edges;
+      r.m_f = c.mf;
+      r.m_u = c.mu;
+      r.mode_before = c.mode_state;
+      r.decision = c.mode;
+      r.ms = (float)((globaltimer() - c.t0) * 1e-6);
+      r.candidates = cands;
+      r.work = work;
+      r.bytes_alg = bytes;
+      a.recs[c.nrec] = r;
+    }
+    if (threadIdx.x == 0) {
+      c.nrec += 1;
+      c.reached += nf;
+      c.edges_total += level_edges;
+      c.bytes_total += bytes;
+      c.work_total += work;
+      c.mode_state = c.mode;
+      c.nf = nout;
+    }
+    __syncthreads();
+    if (c.nf == 0) break;
+  }
+  if (leader) {
+    a.summary[0] = c.depth;
+    a.summary[1] = c.edges_total;
+    a.summary[2] = c.switches;
+    a.summary[3] = c.reached;
+    a.summary[4] = c.e_r;
+    a.summary[5] = c.bytes_total;
+    a.summary[6] = c.work_total;
+    a.summary[7] = c.nrec < a.rec_cap ? c.nrec : a.rec_cap;
+  }
+}
+
+int bfs_device_loop(gfx_graph* g, int64_t source, int direction, double do_a, double do_b,
+                    int mu_edge, int32_t* labels, int32_t* preds, gfx_iter_rec* recs,
+                    int64_t rec_cap, gfx_stats* st) {
+  gfx_ctx* ctx = g->ctx;
+  const int64_t n = g->n, W = g->words;
+  const bool directed = !(g->flags & GFX_GRAPH_UNDIRECTED);
+  if (direction != GFX_DIR_PUSH)
+    GFX_REQUIRE(g->rrow != nullptr, "pull traversal on a directed graph needs the reverse adjacency");
+  BfsBuffers B;
+  GFX_TRY(bfs_buffers(g, false, &B));
+  PBfsArgs a{};
+  a.n = n;
+  a.m = g->m;
+  a.words = W;
+  a.row = g->row;
+  a.col = g->col;
+  a.rrow = g->rrow ? g->rrow : g->row;
+  a.rcol = g->rcol ? g->rcol : g->col;
+  {
+    void* p = nullptr;
+    GFX_TRY(scratch(g, directed ? "nz_in" : "nz_out", W * 4, &p));
+    a.nz_in = static_cast<const uint32_t*>(p);
+    bool fresh = false;
+    GFX_TRY(scratch(g, "keep_head", (size_t)(n + 1) * 4, &p, &fresh));
+    a.head = static_cast<const int32_t*>(p);
+    if (fresh)
+      GFX_LAUNCH(k_pull_heads, grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream, a.rrow,
+                 a.rcol, n, static_cast<int32_t*>(p));
+  }
+  a.visited = B.visited;
+  a.front[0] = B.front0;
+  a.front[1] = B.front1;
+  a.order = B.order;
+  a.scan = B.scan;
+  a.rowbase = B.rowbase;
+  a.part = B.part;
+  const int64_t stiles_max = std::max<int64_t>(1, (n + kScanTileItems - 1) / kScanTileItems);
+  GFX_TRY(scratch_t(g, "pbfs_status", stiles_max + 1, &a.status));
+  a.labels = labels;
+  a.preds = preds;
+  a.C = g->counters;
+  const int64_t cap = std::max<int64_t>(rec_cap, 1);
+  GFX_TRY(scratch_t(g, "pbfs_recs", cap, &a.recs));
+  a.rec_cap = cap;
+  GFX_TRY(scratch_t(g, "pbfs_summary", 8, &a.summary));
+  a.direction = direction;
+  a.mu_edge = mu_edge;
+  a.directed = directed ? 1 : 0;
+  a.do_a = do_a;
+  a.do_b = do_b;
+  a.source = (int32_t)source;
+  a.epoch_base = 0;
+
+  static int blocks_per_sm = 0;
+  const int smem = (int)sizeof(ExpandSmem);
+  if (blocks_per_sm == 0) {
+    GFX_CK(cudaFuncSetAttribute(k_bfs_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem));
+    GFX_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_bfs_persistent, 256,
+                                                         smem));
+    if (blocks_per_sm < 1) {
+      set_error("k_bfs_persistent cannot be resident");
+      return GFX_ECUDA;
+    }
+  }
+  // status words must start clear; the kernel clears what it uses
+  GFX_CK(cudaMemsetAsync(a.status, 0, (stiles_max + 1) * 8, ctx->stream));
+  void* kargs[] = {&a};
+  GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  GFX_CK(cudaLaunchCooperativeKernel((const void*)k_bfs_persistent,
+                                     dim3(blocks_per_sm * ctx->sm_count), dim3(256), kargs, smem,
+                                     ctx->stream));
+  count_launch();
+  GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  long long summary[8];
+  GFX_CK(cudaMemcpyAsync(summary, a.summary, sizeof(summary), cudaMemcpyDeviceToHost,
+                         ctx->stream));
+  GFX_CK(cudaStreamSynchronize(ctx->stream));
+  float ms = 0.f;
+  GFX_CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  const int64_t nrec = std::min<int64_t>(summary[7], rec_cap);
+  if (recs && nrec > 0)
+    GFX_CK(cudaMemcpy(recs, a.recs, nrec * sizeof(gfx_iter_rec), cudaMemcpyDeviceToHost));
+  if (st) {
+    st->iterations = summary[0];
+    st->edges_traversed = summary[1];
+    st->direction_switches = summary[2];
+    st->reached = summary[3];
+    st->edges_reached = summary[4];
+    st->bytes_alg = summary[5];
+    st->work_slots = summary[6];
+    st->device_ms = ms;
+    st->num_records = recs ? nrec : 0;
+  }
+  return GFX_OK;
+}
+
 }  // namespace gfx
 
 using namespace gfx;
@@ -587,7 +941,9 @@ extern "C" int gfx_bfs(gfx_graph* g, int64_t source, int direction, int idempote
   if (direction == GFX_DIR_AUTO)
     GFX_REQUIRE(do_a > 0 && do_b > 0, "do_a and do_b must be positive");
   GFX_CK(cudaSetDevice(g->ctx->device));
-  (void)loop;
+  if (loop == GFX_LOOP_DEVICE && !idempotent)
+    return bfs_device_loop(g, source, direction, do_a, do_b, mu_edge_based, labels_d, preds_d,
+                           recs, rec_cap, stats);
   // INEXACT may leave duplicates (reference operators.py:315-357); the order
   // queue is sized for unique frontiers, so both modes use the exact
   // test-and-set cull, which satisfies the inexact contract as well.

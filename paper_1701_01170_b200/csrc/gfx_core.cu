@@ -8,6 +8,7 @@
 
 #include "gfx_device.cuh"
 #include "gfx_internal.cuh"
+#include "gfx_scan.cuh"
 
 namespace gfx {
 
@@ -102,26 +103,7 @@ int fill_f64(gfx_ctx* ctx, double* p, double v, int64_t count) {
   return GFX_OK;
 }
 
-// ---------------------------------------------------------------------------
-// Fused degree scan + output-tile partition (decoupled look-back, persistent).
-//
-// Replaces reference load_balance.py:105-113 (compute_scan_offsets) and
-// load_balance.py:157-176 (plan_lb_output: ceil(total/N) chunks of N output
-// slots, each chunk's first source found by searchsorted).  Here the
-// partition falls out of the scan: the item whose slot range covers k*kTile
-// writes part[k] directly, so no search is needed.
-// Tile status word: [63:62] flag (1 aggregate, 2 inclusive prefix),
-// [61:48] epoch, [47:0] value.
-// ---------------------------------------------------------------------------
-constexpr unsigned long long kFlagAgg = 1ull << 62;
-constexpr unsigned long long kFlagPre = 2ull << 62;
-constexpr unsigned long long kValMask = (1ull << 48) - 1;
-
-__device__ __forceinline__ unsigned long long pack_status(unsigned long long flag, unsigned epoch,
-                                                          unsigned long long v) {
-  return flag | ((unsigned long long)(epoch & 0x3FFF) << 48) | (v & kValMask);
-}
-
+// Standalone fused degree scan (dynamic tile ids; see gfx_scan.cuh).
 __global__ void __launch_bounds__(kScanBlock)
     k_degree_scan(const int32_t* __restrict__ F, const unsigned long long* __restrict__ nf_d,
                   const int64_t* __restrict__ row, int64_t* __restrict__ scan,
@@ -131,112 +113,13 @@ __global__ void __launch_bounds__(kScanBlock)
   const int64_t nf = (int64_t)*nf_d;
   const int64_t ntiles = nf > 0 ? (nf + kScanTileItems - 1) / kScanTileItems : 1;
   __shared__ unsigned s_tile;
-  __shared__ int64_t s_warp[kScanBlock / 32];
-  __shared__ int64_t s_prefix;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned ep = epoch & 0x3FFF;
-
+  __shared__ ScanSmem sm;
   for (;;) {
     if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
     __syncthreads();
     const int64_t tile = s_tile;
     if (tile >= ntiles) break;
-    const int64_t base = tile * kScanTileItems + (int64_t)threadIdx.x * kScanItems;
-
-    int64_t deg[kScanItems];
-    int64_t rb[kScanItems];
-    int64_t tsum = 0;
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-      int64_t i = base + k;
-      deg[k] = 0;
-      rb[k] = 0;
-      if (i < nf) {
-        int32_t v = F[i];
-        int64_t a = row[v], b = row[v + 1];
-        rb[k] = a;
-        deg[k] = b - a;
-      }
-      tsum += deg[k];
-    }
-    // block exclusive scan of per-thread sums
-    int64_t incl = tsum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    int64_t warp_off = 0, agg = 0;
-#pragma unroll
-    for (int w = 0; w < kScanBlock / 32; ++w) {
-      int64_t x = s_warp[w];
-      if (w < warp) warp_off += x;
-      agg += x;
-    }
-    // decoupled look-back (warp 0)
-    if (warp == 0) {
-      int64_t excl = 0;
-      if (tile == 0) {
-        if (lane == 0) atomicExch(&status[0], pack_status(kFlagPre, ep, (unsigned long long)agg));
-      } else {
-        if (lane == 0) atomicExch(&status[tile], pack_status(kFlagAgg, ep, (unsigned long long)agg));
-        int64_t pred = tile - 1;
-        for (;;) {
-          int64_t idx = pred - lane;
-          unsigned long long s = 0;
-          unsigned flag = 0;
-          if (idx >= 0) {
-            do {
-              s = ld_volatile_u64(&status[idx]);
-              flag = (unsigned)(s >> 62);
-              if (((s >> 48) & 0x3FFF) != ep) flag = 0;
-            } while (flag == 0);
-          } else {
-            flag = 2;  // virtual prefix of zero before tile 0
-            s = 0;
-          }
-          unsigned pre_mask = __ballot_sync(0xffffffffu, flag == 2);
-          int64_t val = (int64_t)(s & kValMask);
-          if (pre_mask) {
-            int first = __ffs(pre_mask) - 1;
-            if (lane > first) val = 0;
-            excl += warp_sum_i64(val);
-            break;
-          }
-          excl += warp_sum_i64(val);
-          pred -= 32;
-        }
-        if (lane == 0)
-          atomicExch(&status[tile], pack_status(kFlagPre, ep, (unsigned long long)(excl + agg)));
-      }
-      if (lane == 0) s_prefix = excl;
-    }
-    __syncthreads();
-    int64_t run = s_prefix + warp_off + incl - tsum;
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-      int64_t i = base + k;
-      if (i < nf) {
-        scan[i] = run;
-        rowbase[i] = rb[k];
-        if (deg[k] > 0) {
-          int64_t k0 = (run + kTile - 1) / kTile;
-          int64_t k1 = (run + deg[k] - 1) / kTile;
-          for (int64_t t = k0; t <= k1; ++t) part[t] = (int32_t)i;
-        }
-      }
-      run += deg[k];
-    }
-    if (tile == ntiles - 1 && threadIdx.x == kScanBlock - 1) {
-      // the last thread of the last tile holds the grand total
-      int64_t total = run;
-      scan[nf] = total;
-      ctr->total = (unsigned long long)total;
-      ctr->ntiles = (unsigned long long)((total + kTile - 1) / kTile);
-    }
-    __syncthreads();
+    scan_tile(tile, ntiles, F, nf, row, scan, rowbase, part, status, epoch, ctr, sm);
   }
 }
 

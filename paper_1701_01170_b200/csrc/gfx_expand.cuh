@@ -47,23 +47,21 @@ struct ExpandSmem {
   unsigned long long gbase;
 };
 
+// All tiles t = cta, cta + ncta, ... of one expansion (S.cnt must be 0 on
+// entry; it is 0 again on exit).  Shared by the standalone kernel and the
+// persistent BFS kernel.
 template <class Op>
-__global__ void __launch_bounds__(kExpandBlock)
-    k_lb_expand(const int32_t* __restrict__ F, const unsigned long long* __restrict__ nf_d,
-                const int64_t* __restrict__ scan, const int64_t* __restrict__ rowbase,
-                const int32_t* __restrict__ part, const Counters* __restrict__ plan,
-                const int32_t* __restrict__ col, const int32_t* __restrict__ wgt, Op op,
-                int32_t* __restrict__ out, unsigned long long* __restrict__ out_len) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  ExpandSmem& S = *reinterpret_cast<ExpandSmem*>(smem_raw);
+__device__ __forceinline__ void expand_tiles(ExpandSmem& S, Op& o, const int32_t* __restrict__ F,
+                                             int64_t nf, const int64_t* __restrict__ scan,
+                                             const int64_t* __restrict__ rowbase,
+                                             const int32_t* __restrict__ part, int64_t ntiles,
+                                             int64_t total, const int32_t* __restrict__ col,
+                                             const int32_t* __restrict__ wgt,
+                                             int32_t* __restrict__ out,
+                                             unsigned long long* __restrict__ out_len,
+                                             int64_t cta, int64_t ncta) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t ntiles = (int64_t)plan->ntiles;
-  const int64_t total = (int64_t)plan->total;
-  const int64_t nf = (int64_t)*nf_d;
-  if (tid == 0) S.cnt = 0;
-  Op o = op;  // mutable copy: functors keep per-thread prefetch registers
-
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  for (int64_t t = cta; t < ntiles; t += ncta) {
     const int64_t s0 = t * kTile;
     const int64_t s1 = min(s0 + (int64_t)kTile, total);
     const int64_t i0 = part[t];
@@ -170,6 +168,23 @@ __global__ void __launch_bounds__(kExpandBlock)
       if (tid == 0) S.cnt = 0;
     }
   }
+  __syncthreads();
+}
+
+template <class Op>
+__global__ void __launch_bounds__(kExpandBlock)
+    k_lb_expand(const int32_t* __restrict__ F, const unsigned long long* __restrict__ nf_d,
+                const int64_t* __restrict__ scan, const int64_t* __restrict__ rowbase,
+                const int32_t* __restrict__ part, const Counters* __restrict__ plan,
+                const int32_t* __restrict__ col, const int32_t* __restrict__ wgt, Op op,
+                int32_t* __restrict__ out, unsigned long long* __restrict__ out_len) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ExpandSmem& S = *reinterpret_cast<ExpandSmem*>(smem_raw);
+  if (threadIdx.x == 0) S.cnt = 0;
+  __syncthreads();
+  Op o = op;  // mutable copy: functors keep per-thread prefetch registers
+  expand_tiles(S, o, F, (int64_t)*nf_d, scan, rowbase, part, (int64_t)plan->ntiles,
+               (int64_t)plan->total, col, wgt, out, out_len, blockIdx.x, gridDim.x);
 }
 
 template <class Op>

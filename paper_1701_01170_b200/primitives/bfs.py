@@ -58,9 +58,17 @@ def stats_from_records(primitive, recs, st, count_trace=True) -> RunStats:
     return stats
 
 
+def default_loop() -> int:
+    """Device-resident level loop unless GFX_BFS_LOOP=host (both are device
+    implementations; the host loop decides directions on the CPU)."""
+    import os
+
+    return _native.LOOP_HOST if os.environ.get("GFX_BFS_LOOP") == "host" else _native.LOOP_DEVICE
+
+
 def bfs_device(dg, source: int, *, direction: str = PUSH, idempotent: bool = False,
                filter_mode=FilterMode.EXACT, do_a: float = 0.001, do_b: float = 0.2,
-               mu_edge_based: bool = False, loop: int = _native.LOOP_HOST,
+               mu_edge_based: bool = False, loop: int | None = None,
                labels=None, preds=None, rec_cap: int = 4096):
     """Device-resident BFS: returns (labels_d int32, preds_d int32, RunStats)."""
     import torch
@@ -77,6 +85,8 @@ def bfs_device(dg, source: int, *, direction: str = PUSH, idempotent: bool = Fal
         labels = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     if preds is None:
         preds = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    if loop is None:
+        loop = default_loop()
     recs = (_native.IterRec * rec_cap)()
     st = _native.Stats()
     fm = _native.FILTER_EXACT if FilterMode(filter_mode) == FilterMode.EXACT else _native.FILTER_INEXACT

@@ -132,6 +132,8 @@ def test_rmat_golden_large(scale):
         assert sha(counts.to(torch.int64).cpu().numpy()) == rec["tc_counts_sha"]
 
 
+@pytest.mark.skipif(not __import__("os").environ.get("GFX_SLOW_TESTS"),
+                    reason="host C oracle needs minutes at s22; run with GFX_SLOW_TESTS=1")
 def test_tc_s22_vs_c_oracle():
     """TC on s22 (no reference golden: the reference needs > 30 min) against
     the C restatement of tc.py:53-76."""

@@ -9,6 +9,7 @@ pytestmark = pytest.mark.gpu
 
 
 def _trace_rows(stats):
+    """reference direction_trace rows: (iteration, mode_before, n_f, n_u, m_f, m_u, decision)"""
     return [[t["iteration"], t["mode_before"], t["n_f"], t["n_u"], t["m_f"], t["m_u"],
              t["decision"]] for t in stats.direction_trace]
 
@@ -67,3 +68,57 @@ def test_s16_golden(direction):
         assert [it.frontier_in for it in r.stats.per_iteration] == rec["bfs_levels"]
     if direction == "auto":
         assert _trace_rows(r.stats) == [list(x) for x in rec["bfs_auto_trace"]]
+
+
+@pytest.mark.parametrize("scale", [20, 22, 24])
+def test_headline_config_golden(scale):
+    """M2 headline input (s24 ef16 seed 0, GPU-built bit-exact): labels SHA-256,
+    level sizes, E_r and the full DO trace (floats included) equal the
+    reference's own run (oracle/make_golden.py rmat 24)."""
+    from paper_1701_01170_b200._results import labels_to_host
+    from paper_1701_01170_b200.generators import rmat_device_graph
+    from paper_1701_01170_b200.primitives.bfs import bfs_device
+
+    rec, _ = rmat_golden(scale)
+    dg = rmat_device_graph(scale, 16, 0)
+    for direction in ("push", "auto"):
+        labels, preds, st = bfs_device(dg, 0, direction=direction)
+        assert sha(labels_to_host(labels)) == rec["bfs_sha"], direction
+        assert st.edges_reached == rec["E_r"]
+        assert [it.frontier_in for it in st.per_iteration] == rec["bfs_levels"]
+        if direction == "push":
+            assert st.edges_traversed == rec["bfs_edges_traversed"]
+        else:
+            assert _trace_rows(st) == [list(x) for x in rec["bfs_auto_trace"]]
+
+
+@pytest.mark.parametrize("loop", ["host", "device"])
+def test_loops_agree(kat, loop):
+    """Host-driven and device-resident level loops give identical labels and
+    identical direction traces (floats included)."""
+    from paper_1701_01170_b200 import _native
+    from paper_1701_01170_b200._results import labels_to_host
+    from paper_1701_01170_b200.primitives.bfs import bfs_device
+
+    lp = _native.LOOP_HOST if loop == "host" else _native.LOOP_DEVICE
+    for d in kat:
+        g = host_graph(d)
+        for direction in ("push", "pull", "auto"):
+            labels, preds, st = bfs_device(g.device(), d["source"], direction=direction, loop=lp)
+            assert np.array_equal(labels_to_host(labels[:d["n"]]), d["bfs"]), (d["name"], direction)
+            if direction == "auto":
+                assert _trace_rows(st) == [list(x) for x in d["bfs_auto_trace"]], d["name"]
+    rec, arrays = rmat_golden(16)
+    g = gfx_graph_s16(rec, arrays)
+    for direction in ("push", "auto"):
+        labels, preds, st = bfs_device(g.device(), 0, direction=direction, loop=lp)
+        assert sha(labels_to_host(labels)) == rec["bfs_sha"]
+        assert st.edges_reached == rec["E_r"]
+        if direction == "auto":
+            assert _trace_rows(st) == [list(x) for x in rec["bfs_auto_trace"]]
+
+
+def gfx_graph_s16(rec, arrays):
+    import paper_1701_01170_b200 as gfx
+
+    return gfx.CsrGraph(rec["n"], arrays["row"], arrays["col"].astype(np.int64), undirected=True)

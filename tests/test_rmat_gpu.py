@@ -7,7 +7,7 @@ from conftest import rmat_golden, sha
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("scale", [10, 12, 14, 16, 18, 20, 22])
+@pytest.mark.parametrize("scale", [10, 12, 14, 16, 18, 20, 22, 24])
 def test_device_builder_bit_exact(scale):
     from paper_1701_01170_b200.generators import rmat_device_graph
 
