@@ -102,6 +102,9 @@ GFX_API int gfx_version(void);
 GFX_API int64_t gfx_launch_count(void);
 /* per-iteration CUDA-event timing of the level loops (records' ms field) */
 GFX_API int gfx_ctx_set_timing(gfx_ctx* ctx, int enabled);
+/* 1 (default): full RunStats (E_r, pull-level edges via a degree post-pass);
+ * 0: skip the statistics post-passes (labels/preds/trace unaffected) */
+GFX_API int gfx_ctx_set_stats(gfx_ctx* ctx, int detail);
 GFX_API const char* gfx_last_error(void);
 /* stream: a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); NULL
  * selects the legacy default stream */
@@ -219,6 +222,12 @@ GFX_API int gfx_keys_to_csr(gfx_ctx* ctx, const uint64_t* keys_d, int64_t num_ke
 GFX_API int gfx_assign_weights(gfx_graph* g, int64_t lo, int64_t hi, uint64_t state_hi,
                        uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
                        int32_t* w_d);
+
+/* ---- kernel experiments (tools/expand_lab.py; not a product path) -------
+ * One LB expansion of F_d with functor variant 0 (stream only), 1 (stream +
+ * visited probe) or 2 (full claim); visited = {labels < depth}. */
+GFX_API int gfx_debug_expand(gfx_graph* g, const int32_t* F_d, int64_t nf, int variant,
+                             int32_t* labels_d, int32_t depth, float* ms, int64_t* out_count);
 
 #ifdef __cplusplus
 }

@@ -53,6 +53,7 @@ _SIGS = {
     "gfx_version": (c_int, []),
     "gfx_launch_count": (c_int64, []),
     "gfx_ctx_set_timing": (c_int, [c_void_p, c_int]),
+    "gfx_ctx_set_stats": (c_int, [c_void_p, c_int]),
     "gfx_last_error": (c_char_p, []),
     "gfx_ctx_create": (c_int, [c_int, c_void_p, POINTER(c_void_p)]),
     "gfx_ctx_destroy": (c_int, [c_void_p]),
@@ -87,6 +88,8 @@ _SIGS = {
     "gfx_keys_to_csr": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_void_p]),
     "gfx_assign_weights": (c_int, [c_void_p, c_int64, c_int64, c_uint64, c_uint64, c_uint64,
                                    c_uint64, c_void_p]),
+    "gfx_debug_expand": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_int32,
+                                 POINTER(c_float), POINTER(c_int64)]),
 }
 
 _lib = None
@@ -170,6 +173,9 @@ class Context:
 
     def sync(self) -> None:
         call("gfx_ctx_sync", self.handle)
+
+    def set_stats(self, detail: int) -> None:
+        call("gfx_ctx_set_stats", self.handle, int(detail))
 
     def set_timing(self, enabled: bool) -> None:
         call("gfx_ctx_set_timing", self.handle, int(bool(enabled)))

@@ -128,18 +128,18 @@ constexpr int kPullBatch = 4;  // bitmap words (vertices per lane) in flight
 // ascending order (reference pull_expand, operators.py:269-307, scans every
 // in-edge; labels are identical, only the work differs).
 // counters: out_len += |new frontier|, edges += sum of in-degree(U) (only
-//           when count_in_edges; undirected callers derive it on the host as
-//           m - E_r(visited)), aux0 += early-exit probes S(U), aux1 += |U|,
-//           aux2 += sum of out-degrees of the new frontier (E_r bookkeeping).
+//           when count_in_edges; for undirected graphs the per-level degree
+//           post-pass derives it as m minus the degrees visited so far),
+//           aux0 += early-exit probes S(U), aux1 += |U|.
 __device__ __forceinline__ void pull_groups(
     int64_t words, const uint32_t* __restrict__ nz_in, uint32_t* __restrict__ visited,
     const uint32_t* __restrict__ front, uint32_t* __restrict__ next,
     const int32_t* __restrict__ head, const int64_t* __restrict__ rrow,
-    const int32_t* __restrict__ rcol, const int64_t* __restrict__ row, int count_in_edges,
-    int32_t* __restrict__ labels, int32_t* __restrict__ preds, int32_t depth,
-    Counters* __restrict__ ctr, int64_t gw, int64_t nwarps) {
+    const int32_t* __restrict__ rcol, int count_in_edges, int32_t* __restrict__ labels,
+    int32_t* __restrict__ preds, int32_t depth, Counters* __restrict__ ctr, int64_t gw,
+    int64_t nwarps) {
   const int lane = threadIdx.x & 31;
-  unsigned long long found_cnt = 0, in_edges = 0, probes = 0, cands = 0, found_deg = 0;
+  unsigned long long found_cnt = 0, in_edges = 0, probes = 0, cands = 0;
   for (int64_t grp = gw; grp * 32 < words; grp += nwarps) {
     const int64_t w = grp * 32 + lane;
     uint32_t vis = 0xffffffffu, cand = 0;
@@ -202,7 +202,6 @@ __device__ __forceinline__ void pull_groups(
           if (found) {
             labels[u] = depth;
             preds[u] = par;
-            if (row) found_deg += (unsigned long long)(row[u + 1] - row[u]);
           }
         }
         const unsigned fm = __ballot_sync(0xffffffffu, found);
@@ -219,13 +218,11 @@ __device__ __forceinline__ void pull_groups(
   in_edges = warp_sum_u64(in_edges);
   probes = warp_sum_u64(probes);
   cands = warp_sum_u64(cands);
-  found_deg = warp_sum_u64(found_deg);
   if (lane == 0) {
     if (found_cnt) atomicAdd(&ctr->out_len, found_cnt);
     if (in_edges) atomicAdd(&ctr->edges, in_edges);
     if (probes) atomicAdd(&ctr->aux0, probes);
     if (cands) atomicAdd(&ctr->aux1, cands);
-    if (found_deg) atomicAdd(&ctr->aux2, found_deg);
   }
 }
 
@@ -234,10 +231,9 @@ __global__ void __launch_bounds__(256)
                uint32_t* __restrict__ visited, const uint32_t* __restrict__ front,
                uint32_t* __restrict__ next, const int32_t* __restrict__ head,
                const int64_t* __restrict__ rrow, const int32_t* __restrict__ rcol,
-               const int64_t* __restrict__ row, int count_in_edges,
-               int32_t* __restrict__ labels, int32_t* __restrict__ preds, int32_t depth,
-               Counters* __restrict__ ctr) {
-  pull_groups(words, nz_in, visited, front, next, head, rrow, rcol, row, count_in_edges, labels,
+               int count_in_edges, int32_t* __restrict__ labels, int32_t* __restrict__ preds,
+               int32_t depth, Counters* __restrict__ ctr) {
+  pull_groups(words, nz_in, visited, front, next, head, rrow, rcol, count_in_edges, labels,
               preds, depth, ctr, (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5,
               ((int64_t)gridDim.x * blockDim.x) >> 5);
 }
@@ -282,27 +278,20 @@ __global__ void __launch_bounds__(256)
                   ((int64_t)gridDim.x * blockDim.x) >> 5);
 }
 
-// queue -> frontier bitmap (bitmap pre-zeroed); deg_sum += sum of out-degrees
+// queue -> frontier bitmap (bitmap pre-zeroed)
 __device__ __forceinline__ void queue_to_bitmap(const int32_t* __restrict__ F, int64_t nf,
-                                                uint32_t* __restrict__ bm,
-                                                const int64_t* __restrict__ row,
-                                                unsigned long long* __restrict__ deg_sum,
-                                                int64_t tid0, int64_t nthreads) {
-  unsigned long long dsum = 0;
+                                                uint32_t* __restrict__ bm, int64_t tid0,
+                                                int64_t nthreads) {
   for (int64_t i = tid0; i < nf; i += nthreads) {
     const int32_t v = F[i];
     atomicOr(&bm[v >> 5], 1u << (v & 31));
-    dsum += (unsigned long long)(row[v + 1] - row[v]);
   }
-  dsum = warp_sum_u64(dsum);
-  if ((threadIdx.x & 31) == 0 && dsum) atomicAdd(deg_sum, dsum);
 }
 
 __global__ void __launch_bounds__(256)
     k_queue_to_bitmap(const int32_t* __restrict__ F, const unsigned long long* __restrict__ nf_d,
-                      uint32_t* __restrict__ bm, const int64_t* __restrict__ row,
-                      unsigned long long* __restrict__ deg_sum) {
-  queue_to_bitmap(F, (int64_t)*nf_d, bm, row, deg_sum, blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
+                      uint32_t* __restrict__ bm) {
+  queue_to_bitmap(F, (int64_t)*nf_d, bm, blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
                   (int64_t)gridDim.x * blockDim.x);
 }
 
@@ -347,6 +336,66 @@ int reached_stats(gfx_graph* g, const int32_t* labels, int64_t* reached, int64_t
   GFX_CK(cudaStreamSynchronize(ctx->stream));
   *reached = (int64_t)pin->aux0;
   *edges = (int64_t)pin->aux1;
+  return GFX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Per-level degree post-pass (statistics only, skipped when the ctx's stats
+// detail is 0): out_deg[d] / in_deg[d] = sums over vertices at depth d.  From
+// it: E_r = sum of out_deg (the paper's TEPS numerator), and for undirected
+// graphs the reference's pull-level edges_traversed (sum of in-degrees of the
+// unvisited set, bfs.py:152-153) = m - sum of degrees at depths < d-1... i.e.
+// everything visited before the level.
+// ---------------------------------------------------------------------------
+constexpr int kLevelSmem = 64;
+
+__global__ void __launch_bounds__(256)
+    k_level_degrees(const int32_t* __restrict__ labels, const int64_t* __restrict__ row,
+                    int64_t n, int64_t levels, unsigned long long* __restrict__ out_deg) {
+  __shared__ unsigned long long hist[kLevelSmem];
+  const bool small = levels <= kLevelSmem;
+  if (small)
+    for (int i = threadIdx.x; i < kLevelSmem; i += blockDim.x) hist[i] = 0ull;
+  __syncthreads();
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t l = labels[v];
+    if (l == GFX_UNVISITED || l >= levels) continue;
+    const unsigned long long d = (unsigned long long)(row[v + 1] - row[v]);
+    if (small) atomicAdd(&hist[l], d); else atomicAdd(&out_deg[l], d);
+  }
+  __syncthreads();
+  if (small)
+    for (int i = threadIdx.x; i < levels; i += blockDim.x)
+      if (hist[i]) atomicAdd(&out_deg[i], hist[i]);
+}
+
+int bfs_level_stats(gfx_graph* g, const int32_t* labels, int64_t depth, gfx_iter_rec* recs,
+                    int64_t nrec, gfx_stats* st) {
+  gfx_ctx* ctx = g->ctx;
+  if (!ctx->stats_detail) return GFX_OK;
+  const int64_t levels = depth + 1;
+  unsigned long long* deg = nullptr;
+  GFX_TRY(scratch_t(g, "lvl_deg", levels + 1, &deg));
+  GFX_CK(cudaMemsetAsync(deg, 0, (levels + 1) * 8, ctx->stream));
+  GFX_LAUNCH(k_level_degrees, grid_for(g->n, 256, ctx->sm_count * 8), 256, 0, ctx->stream, labels,
+             g->row, g->n, levels, deg);
+  std::vector<unsigned long long> h(levels + 1);
+  GFX_CK(cudaMemcpyAsync(h.data(), deg, (levels + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  GFX_CK(cudaStreamSynchronize(ctx->stream));
+  int64_t e_r = 0;
+  for (int64_t l = 0; l < levels; ++l) e_r += (int64_t)h[l];
+  st->edges_reached = e_r;
+  if (!(g->flags & GFX_GRAPH_UNDIRECTED)) return GFX_OK;
+  // undirected pull levels: edges = m - degrees of depths 0..d-1
+  int64_t visited_deg = 0, total = 0;
+  for (int64_t i = 0; i < nrec; ++i) {
+    const int64_t d = recs[i].iteration;  // level d expands depth d-1
+    visited_deg += (int64_t)h[d - 1];
+    if (recs[i].edges < 0) recs[i].edges = g->m - visited_deg;
+    total += recs[i].edges;
+  }
+  st->edges_traversed = total;
   return GFX_OK;
 }
 
@@ -478,7 +527,8 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
   uint32_t* fcur = B.front0;
   uint32_t* fnext = B.front1;
   int64_t depth = 0, edges_total = 0, switches = 0, nrec = 0, bytes_total = 0, work_total = 0;
-  int64_t e_r = 0, reached = 0, pull_found_deg = 0;
+  int64_t reached = 0;
+  std::vector<gfx_iter_rec> lrecs;
 
   while (nf > 0) {
     ++depth;
@@ -516,7 +566,6 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
       level_edges = (int64_t)pin->total;
       nout = (int64_t)pin->out_len;
       work = level_edges;
-      e_r += level_edges;  // sum of degrees of this frontier
       // push: frontier id + row pair per item, one col id per slot, label +
       // queue write per discovered vertex
       bytes = 20 * nf + 4 * level_edges + 8 * nout;
@@ -526,35 +575,31 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
       if (queue_form) {
         GFX_CK(cudaMemsetAsync(fcur, 0, W * 4, ctx->stream));
         GFX_LAUNCH(k_queue_to_bitmap, grid_for(nf, 256, ctx->sm_count * 8), 256, 0, ctx->stream,
-                   B.order + q_off, &prev->out_len, fcur, g->row, &cur->aux3);
+                   B.order + q_off, &prev->out_len, fcur);
         GFX_CK(cudaGetLastError());
       }
       GFX_LAUNCH(k_bfs_pull, ctx->sm_count * 8, 256, 0, ctx->stream, W, nz_in, B.visited, fcur,
-                 fnext, head, g->rrow, g->rcol, g->row, directed ? 1 : 0, labels, preds,
+                 fnext, head, g->rrow, g->rcol, directed ? 1 : 0, labels, preds,
                  (int32_t)depth, cur);
       GFX_CK(cudaGetLastError());
       if (ctx->timing) GFX_CK(cudaEventRecord(ctx->lev1, ctx->stream));
       GFX_CK(cudaMemcpyAsync(pin, cur, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
       GFX_CK(cudaStreamSynchronize(ctx->stream));
-      // sum of in-degrees of U: counted by the kernel on directed graphs; on
-      // undirected ones it is m minus the degrees of everything visited so far
-      level_edges = directed ? (int64_t)pin->edges
-                             : m - (e_r + (queue_form ? (int64_t)pin->aux3 : pull_found_deg));
+      // sum of in-degrees of U: counted by the kernel on directed graphs; for
+      // undirected graphs the degree post-pass fills it in (-1 until then)
+      level_edges = directed ? (int64_t)pin->edges : -1;
       nout = (int64_t)pin->out_len;
       work = (int64_t)pin->aux0;
       cands = (int64_t)pin->aux1;
-      // E_r: degree sum of this level's input frontier, from the conversion
-      // (push -> pull) or from the previous pull's found set
-      e_r += queue_form ? (int64_t)pin->aux3 : pull_found_deg;
-      pull_found_deg = (int64_t)pin->aux2;
       // pull: id + row per candidate, one col id per early-exit probe, label
       // + frontier write per discovered vertex
       bytes = 12 * cands + 4 * work + 8 * nout;
       std::swap(fcur, fnext);
       queue_form = false;
     }
-    if (recs && nrec < rec_cap) {
-      gfx_iter_rec& r = recs[nrec];
+    {
+      lrecs.emplace_back();
+      gfx_iter_rec& r = lrecs.back();
       r.iteration = depth;
       r.frontier_in = nf;
       r.frontier_out = nout;
@@ -571,7 +616,7 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
       r.bytes_alg = bytes;
       ++nrec;
     }
-    edges_total += level_edges;
+    if (level_edges > 0) edges_total += level_edges;
     reached += nf;
     bytes_total += bytes;
     work_total += work;
@@ -591,8 +636,12 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
     st->bytes_alg = bytes_total;
     st->work_slots = work_total;
     st->reached = reached;
-    st->edges_reached = e_r;
+    st->edges_reached = -1;
+    GFX_TRY(bfs_level_stats(g, labels, depth, lrecs.data(), (int64_t)lrecs.size(), st));
   }
+  nrec = std::min<int64_t>((int64_t)lrecs.size(), recs ? rec_cap : 0);
+  for (int64_t i = 0; i < nrec; ++i) recs[i] = lrecs[i];
+  if (st) st->num_records = nrec;
   return GFX_OK;
 }
 
@@ -635,8 +684,8 @@ struct PBfsArgs {
 };
 
 struct PCtl {
-  long long nf, n_u, q_off, q_end, e_r, pfd, depth, reached, edges_total, bytes_total, work_total,
-      switches, nrec;
+  long long nf, n_u, q_off, q_end, depth, reached, edges_total, bytes_total, work_total, switches,
+      nrec;
   int mode_state, queue_form, mode, fsel;
   double mf, mu;
   unsigned long long t0;
@@ -694,7 +743,7 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
     c.n_u = a.n;
     c.q_off = 0;
     c.q_end = 1;
-    c.e_r = c.pfd = c.depth = c.reached = c.edges_total = c.bytes_total = c.work_total = 0;
+    c.depth = c.reached = c.edges_total = c.bytes_total = c.work_total = 0;
     c.switches = c.nrec = 0;
     c.mode_state = GFX_DIR_PUSH;
     c.queue_form = 1;
@@ -760,7 +809,6 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
       work = level_edges;
       bytes = 20 * nf + 4 * level_edges + 8 * nout;
       if (threadIdx.x == 0) {
-        c.e_r += level_edges;
         c.q_off = c.q_end;
         c.q_end += nout;
       }
@@ -768,21 +816,18 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
       if (c.queue_form) {
         for (int64_t i = gtid; i < a.words; i += nthr) fcur[i] = 0u;
         grid.sync();
-        queue_to_bitmap(a.order + c.q_off, nf, fcur, a.row, &cur->aux3, gtid, nthr);
+        queue_to_bitmap(a.order + c.q_off, nf, fcur, gtid, nthr);
         grid.sync();
       }
-      pull_groups(a.words, a.nz_in, a.visited, fcur, fnext, a.head, a.rrow, a.rcol, a.row,
-                  a.directed, a.labels, a.preds, depth, cur, gw, nw);
+      pull_groups(a.words, a.nz_in, a.visited, fcur, fnext, a.head, a.rrow, a.rcol, a.directed,
+                  a.labels, a.preds, depth, cur, gw, nw);
       grid.sync();
       nout = (long long)ld_ctr(&cur->out_len);
       work = (long long)ld_ctr(&cur->aux0);
       cands = (long long)ld_ctr(&cur->aux1);
-      const long long fdeg = c.queue_form ? (long long)ld_ctr(&cur->aux3) : c.pfd;
-      level_edges = a.directed ? (long long)ld_ctr(&cur->edges) : a.m - (c.e_r + fdeg);
+      level_edges = a.directed ? (long long)ld_ctr(&cur->edges) : -1;
       bytes = 12 * cands + 4 * work + 8 * nout;
       if (threadIdx.x == 0) {
-        c.e_r += fdeg;
-        c.pfd = (long long)ld_ctr(&cur->aux2);
         c.fsel ^= 1;
         c.queue_form = 0;
       }
@@ -807,7 +852,7 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
     if (threadIdx.x == 0) {
       c.nrec += 1;
       c.reached += nf;
-      c.edges_total += level_edges;
+      if (level_edges > 0) c.edges_total += level_edges;
       c.bytes_total += bytes;
       c.work_total += work;
       c.mode_state = c.mode;
@@ -821,7 +866,7 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
     a.summary[1] = c.edges_total;
     a.summary[2] = c.switches;
     a.summary[3] = c.reached;
-    a.summary[4] = c.e_r;
+    a.summary[4] = -1;
     a.summary[5] = c.bytes_total;
     a.summary[6] = c.work_total;
     a.summary[7] = c.nrec < a.rec_cap ? c.nrec : a.rec_cap;
@@ -869,7 +914,7 @@ int bfs_device_loop(gfx_graph* g, int64_t source, int direction, double do_a, do
   a.labels = labels;
   a.preds = preds;
   a.C = g->counters;
-  const int64_t cap = std::max<int64_t>(rec_cap, 1);
+  const int64_t cap = 1 << 16;  // level records kept on device (stats)
   GFX_TRY(scratch_t(g, "pbfs_recs", cap, &a.recs));
   a.rec_cap = cap;
   GFX_TRY(scratch_t(g, "pbfs_summary", 8, &a.summary));
@@ -908,20 +953,24 @@ int bfs_device_loop(gfx_graph* g, int64_t source, int direction, double do_a, do
   GFX_CK(cudaStreamSynchronize(ctx->stream));
   float ms = 0.f;
   GFX_CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-  const int64_t nrec = std::min<int64_t>(summary[7], rec_cap);
-  if (recs && nrec > 0)
-    GFX_CK(cudaMemcpy(recs, a.recs, nrec * sizeof(gfx_iter_rec), cudaMemcpyDeviceToHost));
+  std::vector<gfx_iter_rec> lrecs((size_t)summary[7]);
+  if (!lrecs.empty())
+    GFX_CK(cudaMemcpy(lrecs.data(), a.recs, lrecs.size() * sizeof(gfx_iter_rec),
+                      cudaMemcpyDeviceToHost));
   if (st) {
     st->iterations = summary[0];
     st->edges_traversed = summary[1];
     st->direction_switches = summary[2];
     st->reached = summary[3];
-    st->edges_reached = summary[4];
+    st->edges_reached = -1;
     st->bytes_alg = summary[5];
     st->work_slots = summary[6];
     st->device_ms = ms;
-    st->num_records = recs ? nrec : 0;
+    GFX_TRY(bfs_level_stats(g, labels, summary[0], lrecs.data(), (int64_t)lrecs.size(), st));
   }
+  const int64_t nrec = std::min<int64_t>((int64_t)lrecs.size(), recs ? rec_cap : 0);
+  for (int64_t i = 0; i < nrec; ++i) recs[i] = lrecs[i];
+  if (st) st->num_records = nrec;
   return GFX_OK;
 }
 

@@ -194,6 +194,12 @@ int gfx_version(void) { return 1; }
 
 int64_t gfx_launch_count(void) { return (int64_t)g_launches.load(); }
 
+int gfx_ctx_set_stats(gfx_ctx* c, int detail) {
+  GFX_REQUIRE(c, "null ctx");
+  c->stats_detail = detail;
+  return GFX_OK;
+}
+
 int gfx_ctx_set_timing(gfx_ctx* c, int enabled) {
   GFX_REQUIRE(c, "null ctx");
   c->timing = enabled != 0;

@@ -77,6 +77,7 @@ struct gfx_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   void* pinned = nullptr;  // 4 KB pinned host staging
   bool timing = false;     // per-iteration events
+  int stats_detail = 1;    // 0: skip the statistics post-passes (E_r, pull edges)
   cudaEvent_t lev0 = nullptr, lev1 = nullptr;
 };
 
