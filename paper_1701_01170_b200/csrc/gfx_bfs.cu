@@ -38,15 +38,16 @@ namespace gfx {
 // ---------------------------------------------------------------------------
 struct BfsClaimOp {
   static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
+  static constexpr int kBatch = kVisitBatch;
   uint32_t* visited;
   int32_t* labels;
   int32_t* preds;
   int32_t depth;
-  uint32_t wv[kVisitBatch];
+  uint32_t wv[kBatch];
   __device__ int32_t src_value(int32_t) const { return 0; }
-  __device__ void prefetch(const int32_t d[kVisitBatch]) {
+  __device__ void prefetch(const int32_t* d) {
 #pragma unroll
-    for (int u = 0; u < kVisitBatch; ++u) wv[u] = d[u] >= 0 ? visited[d[u] >> 5] : 0xffffffffu;
+    for (int u = 0; u < kBatch; ++u) wv[u] = d[u] >= 0 ? visited[d[u] >> 5] : 0xffffffffu;
   }
   __device__ bool visit(int u, int32_t d, int32_t s, int32_t, int32_t, int64_t) {
     const uint32_t bit = 1u << (d & 31);
@@ -60,15 +61,16 @@ struct BfsClaimOp {
 
 struct BfsIdempOp {
   static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
+  static constexpr int kBatch = kVisitBatch;
   const uint32_t* visited;
   int32_t* labels;
   int32_t* preds;
   int32_t depth;
-  uint32_t wv[kVisitBatch];
+  uint32_t wv[kBatch];
   __device__ int32_t src_value(int32_t) const { return 0; }
-  __device__ void prefetch(const int32_t d[kVisitBatch]) {
+  __device__ void prefetch(const int32_t* d) {
 #pragma unroll
-    for (int u = 0; u < kVisitBatch; ++u) wv[u] = d[u] >= 0 ? visited[d[u] >> 5] : 0xffffffffu;
+    for (int u = 0; u < kBatch; ++u) wv[u] = d[u] >= 0 ? visited[d[u] >> 5] : 0xffffffffu;
   }
   __device__ bool visit(int u, int32_t d, int32_t s, int32_t, int32_t, int64_t) {
     if ((wv[u] >> (d & 31)) & 1u) return false;
@@ -721,7 +723,7 @@ __device__ __noinline__ void device_decide(long long n, long long m, long long n
 __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  ExpandSmem& S = *reinterpret_cast<ExpandSmem*>(smem_raw);
+  WarpSmem& W = warp_smem(smem_raw);
   __shared__ ScanSmem ss;
   __shared__ PCtl c;
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -738,7 +740,6 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
   for (int64_t i = gtid; i < 3 * (int64_t)(sizeof(Counters) / 8); i += nthr)
     reinterpret_cast<unsigned long long*>(a.C)[i] = 0ull;
   if (threadIdx.x == 0) {
-    S.cnt = 0;
     c.nf = 1;
     c.n_u = a.n;
     c.q_off = 0;
@@ -799,9 +800,9 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
         scan_tile(t, stiles, F, nf, a.row, a.scan, a.rowbase, a.part, a.status, ep, cur, ss);
       grid.sync();
       BfsClaimOp op{a.visited, a.labels, a.preds, depth, {}};
-      expand_tiles(S, op, F, nf, a.scan, a.rowbase, a.part, (int64_t)ld_ctr(&cur->ntiles),
+      expand_tasks(W, op, F, nf, a.scan, a.rowbase, a.part, (int64_t)ld_ctr(&cur->ntiles),
                    (int64_t)ld_ctr(&cur->total), a.col, nullptr, a.order + c.q_end,
-                   &cur->out_len, blockIdx.x, gridDim.x);
+                   &cur->out_len, gw, nw);
       for (int64_t i = gtid; i < stiles; i += nthr) a.status[i] = 0ull;
       grid.sync();
       level_edges = (long long)ld_ctr(&cur->total);
@@ -927,7 +928,7 @@ int bfs_device_loop(gfx_graph* g, int64_t source, int direction, double do_a, do
   a.epoch_base = 0;
 
   static int blocks_per_sm = 0;
-  const int smem = (int)sizeof(ExpandSmem);
+  const int smem = expand_smem_bytes();
   if (blocks_per_sm == 0) {
     GFX_CK(cudaFuncSetAttribute(k_bfs_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem));

@@ -12,6 +12,7 @@ namespace gfx {
 // variant 0: stream the adjacency only (no functor memory traffic)
 struct StreamOp {
   static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
+  static constexpr int kBatch = kVisitBatch;
   int32_t sentinel;
   __device__ int32_t src_value(int32_t) const { return 0; }
   __device__ void prefetch(const int32_t*) {}
@@ -23,12 +24,13 @@ struct StreamOp {
 // variant 1: stream + visited-bit probe, no atomics (emits unvisited slots)
 struct ProbeOp {
   static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
+  static constexpr int kBatch = kVisitBatch;
   const uint32_t* visited;
-  uint32_t wv[kVisitBatch];
+  uint32_t wv[kBatch];
   __device__ int32_t src_value(int32_t) const { return 0; }
-  __device__ void prefetch(const int32_t d[kVisitBatch]) {
+  __device__ void prefetch(const int32_t* d) {
 #pragma unroll
-    for (int u = 0; u < kVisitBatch; ++u) wv[u] = d[u] >= 0 ? visited[d[u] >> 5] : 0xffffffffu;
+    for (int u = 0; u < kBatch; ++u) wv[u] = d[u] >= 0 ? visited[d[u] >> 5] : 0xffffffffu;
   }
   __device__ bool visit(int u, int32_t d, int32_t, int32_t, int32_t, int64_t) {
     return !((wv[u] >> (d & 31)) & 1u);
@@ -38,14 +40,15 @@ struct ProbeOp {
 // variant 2: full claim (as BfsClaimOp) on a private visited copy
 struct ClaimOp {
   static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
+  static constexpr int kBatch = kVisitBatch;
   uint32_t* visited;
   int32_t* labels;
   int32_t depth;
-  uint32_t wv[kVisitBatch];
+  uint32_t wv[kBatch];
   __device__ int32_t src_value(int32_t) const { return 0; }
-  __device__ void prefetch(const int32_t d[kVisitBatch]) {
+  __device__ void prefetch(const int32_t* d) {
 #pragma unroll
-    for (int u = 0; u < kVisitBatch; ++u) wv[u] = d[u] >= 0 ? visited[d[u] >> 5] : 0xffffffffu;
+    for (int u = 0; u < kBatch; ++u) wv[u] = d[u] >= 0 ? visited[d[u] >> 5] : 0xffffffffu;
   }
   __device__ bool visit(int u, int32_t d, int32_t, int32_t, int32_t, int64_t) {
     const uint32_t bit = 1u << (d & 31);

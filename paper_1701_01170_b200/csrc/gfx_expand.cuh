@@ -1,29 +1,34 @@
-// Load-balanced push expansion template (the device `advance`).
+// Load-balanced push expansion (the device `advance`), warp-centric.
 //
 // Reference semantics: operators.py:218-266 (advance, push) with the LB plan
-// of load_balance.py:157-176.  One CTA owns one tile of kTile consecutive
-// OUTPUT slots of the frontier's expansion (tiles come from the fused degree
-// scan, so hubs are split across many CTAs and every CTA does the same work).
+// of load_balance.py:157-176.  The fused degree scan (gfx_scan.cuh) cuts the
+// frontier's expansion into tiles of kTile = 512 consecutive OUTPUT slots and
+// records the item owning each tile's first slot, so hub vertices are split
+// across many tiles and every tile is the same amount of work.
 //
-// Per tile (in passes of <= kPassItems frontier items):
-//   items : each thread loads one item's (scan, delta = row[v] - scan, v)
-//           into shared memory and drops a marker at the item's first slot;
-//   owner : a CTA-wide inclusive max-scan over the markers gives every slot
-//           its owning item (load-balancing search without binary search);
-//   visit : thread t handles slots t, t+B, ... (consecutive lanes read
-//           consecutive column ids: coalesced), 4 slots in flight per thread,
-//           col id = col[delta[item] + slot]; the functor decides emission;
-//   emit  : emitted ids are staged in shared memory and appended with ONE
-//           global atomicAdd per tile, then written coalesced.
+// One WARP owns one tile at a time -- no CTA barriers anywhere:
+//   items : lanes load up to 32 overlapping items (scan, delta = row[v] -
+//           scan, v) into the warp's shared-memory slice and mark each
+//           item's first slot;
+//   owner : a warp-wide inclusive max-scan over the 512 markers (16 per lane
+//           + shuffles) gives every slot its owning item;
+//   visit : lane l handles slots l, l+32, ... -- consecutive lanes read
+//           consecutive column ids (coalesced) -- with Op::kBatch column
+//           loads in flight per lane before the functor runs;
+//   emit  : survivors are compacted with ballot/popc into the warp's
+//           shared-memory staging buffer and appended to the global queue
+//           with ONE atomicAdd per flush (frontier queues in shared-memory
+//           staged buffers).
 //
-// Functor interface (gfx_bfs.cu / gfx_sssp.cu / gfx_operators.cu):
+// Functor interface (gfx_bfs.cu / gfx_sssp.cu / gfx_cc.cu / gfx_operators.cu):
 //   static constexpr bool kWeights;    load w[e]
 //   static constexpr bool kSrcVal;     per-item src_value(v)
 //   static constexpr bool kEmitEdge;   emit edge ids instead of dst ids
+//   static constexpr int  kBatch;      slots in flight per lane (divides 16)
 //   __device__ int32_t src_value(int32_t v) const;
-//   __device__ void prefetch(const int32_t d[kVisitBatch]);
+//   __device__ void prefetch(const int32_t* d);       // d[kBatch]
 //   __device__ bool visit(int u, int32_t dst, int32_t src, int32_t w,
-//                         int32_t sval, int64_t edge);   // u = prefetch slot
+//                         int32_t sval, int64_t edge);  // u = prefetch slot
 #pragma once
 
 #include "gfx_device.cuh"
@@ -32,26 +37,41 @@
 namespace gfx {
 
 constexpr int kExpandBlock = 256;
-constexpr int kPassItems = 1024;
-constexpr int kSlotsPerThread = kTile / kExpandBlock;  // 16
-constexpr int kVisitBatch = 8;  // slots (column loads) in flight per thread
+constexpr int kWarpsPerBlock = kExpandBlock / 32;
+constexpr int kLaneSlots = kTile / 32;  // 16 slots per lane per tile
+constexpr int kOutCap = 640;            // per-warp staged output (flushed past kOutCap - 32*kBatch)
+constexpr int kVisitBatch = 8;          // default Op::kBatch
 
-struct ExpandSmem {
-  int64_t delta[kPassItems];   // row[v] - scan[i]: col index = delta + global slot
-  int32_t src[kPassItems];     // frontier id
-  int32_t sval[kPassItems];    // functor per-source value
-  int16_t owner[kTile];        // slot -> item (relative to the pass)
-  int32_t obuf[kTile];         // emitted ids
-  int32_t warp_max[kExpandBlock / 32];
-  int cnt;
-  unsigned long long gbase;
+struct WarpSmem {
+  int64_t delta[32];     // row[v] - scan[i]: col index = delta + global slot
+  int32_t src[32];
+  int32_t sval[32];
+  int8_t owner[kTile];   // slot -> item lane (within the 32-item chunk)
+  int32_t obuf[kOutCap];
 };
 
-// All tiles t = cta, cta + ncta, ... of one expansion (S.cnt must be 0 on
-// entry; it is 0 again on exit).  Shared by the standalone kernel and the
-// persistent BFS kernel.
+__device__ __forceinline__ WarpSmem& warp_smem(unsigned char* base) {
+  return reinterpret_cast<WarpSmem*>(base)[threadIdx.x >> 5];
+}
+
+// flush the warp's staged output (count is warp-uniform)
+__device__ __forceinline__ void warp_flush(WarpSmem& W, int& ocnt, int32_t* __restrict__ out,
+                                           unsigned long long* __restrict__ out_len) {
+  const int lane = threadIdx.x & 31;
+  if (ocnt == 0) return;
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(out_len, (unsigned long long)ocnt);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  __syncwarp();
+  for (int j = lane; j < ocnt; j += 32) out[base + j] = W.obuf[j];
+  __syncwarp();
+  ocnt = 0;
+}
+
+// All tiles t = task0, task0 + ntasks, ... of one expansion, processed by the
+// calling warp.  Shared by the standalone kernel and the persistent BFS.
 template <class Op>
-__device__ __forceinline__ void expand_tiles(ExpandSmem& S, Op& o, const int32_t* __restrict__ F,
+__device__ __forceinline__ void expand_tasks(WarpSmem& W, Op& o, const int32_t* __restrict__ F,
                                              int64_t nf, const int64_t* __restrict__ scan,
                                              const int64_t* __restrict__ rowbase,
                                              const int32_t* __restrict__ part, int64_t ntiles,
@@ -59,47 +79,53 @@ __device__ __forceinline__ void expand_tiles(ExpandSmem& S, Op& o, const int32_t
                                              const int32_t* __restrict__ wgt,
                                              int32_t* __restrict__ out,
                                              unsigned long long* __restrict__ out_len,
-                                             int64_t cta, int64_t ncta) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int64_t t = cta; t < ntiles; t += ncta) {
+                                             int64_t task0, int64_t ntasks) {
+  constexpr int B = Op::kBatch;
+  const int lane = threadIdx.x & 31;
+  int ocnt = 0;
+  for (int64_t t = task0; t < ntiles; t += ntasks) {
     const int64_t s0 = t * kTile;
     const int64_t s1 = min(s0 + (int64_t)kTile, total);
     const int64_t i0 = part[t];
     const int64_t i1 = (t + 1 < ntiles) ? (int64_t)part[t + 1] : nf - 1;
-
-    for (int64_t pa = i0; pa <= i1; pa += kPassItems) {
-      const int64_t pb = min(pa + kPassItems - 1, i1);
-      // slot range of this pass, clipped to the tile
-      const int64_t sl = max(scan[pa], s0);
-      const int64_t sh = min(scan[pb + 1], s1);
-      const int nsl = (int)max(sh - sl, (int64_t)0);
-      __syncthreads();  // previous pass / tile fully consumed
-      for (int j = tid; j < nsl; j += kExpandBlock) S.owner[j] = -1;
-      __syncthreads();
-      for (int64_t i = pa + tid; i <= pb; i += kExpandBlock) {
-        const int r = (int)(i - pa);
-        const int64_t sc = scan[i], sc1 = scan[i + 1];
-        const int32_t v = F[i];
-        S.delta[r] = rowbase[i] - sc;
-        S.src[r] = v;
-        const int64_t lo = max(sc, sl), hi = min(sc1, sh);
-        if (hi > lo) {
-          S.owner[lo - sl] = (int16_t)r;
-          if (Op::kSrcVal) S.sval[r] = o.src_value(v);
-        }
+    for (int64_t ib = i0; ib <= i1; ib += 32) {
+      const int64_t i = ib + lane;
+      const bool valid = i <= i1;
+      int64_t sc = 0, sc1 = 0;
+      if (valid) {
+        sc = scan[i];
+        sc1 = scan[i + 1];
       }
-      __syncthreads();
-      // inclusive max-scan of owner[0..nsl): kSlotsPerThread consecutive per thread
+      const int64_t lo = max(sc, s0), hi = min(sc1, s1);
+      const bool has = valid && hi > lo;
+      // chunk slot range [cl, ch) relative to s0
+      const int cl = (int)(__shfl_sync(0xffffffffu, lo, 0) - s0);
+      const unsigned vm = __ballot_sync(0xffffffffu, valid);
+      const int last = 31 - __clz(vm);
+      const int ch = (int)(__shfl_sync(0xffffffffu, hi, last) - s0);
+      if (ch <= cl) continue;
+      __syncwarp();
+      for (int j = cl + lane; j < ch; j += 32) W.owner[j] = -1;
+      __syncwarp();
+      if (has) {
+        const int32_t v = F[i];
+        W.owner[lo - s0] = (int8_t)lane;
+        W.delta[lane] = rowbase[i] - sc;
+        W.src[lane] = v;
+        if (Op::kSrcVal) W.sval[lane] = o.src_value(v);
+      }
+      __syncwarp();
+      // inclusive max-scan of owner[cl, ch): 16 consecutive entries per lane
       {
-        int16_t loc[kSlotsPerThread];
-        const int base = tid * kSlotsPerThread;
+        const int base = cl + lane * kLaneSlots;
         int run = -1;
+        int8_t loc[kLaneSlots];
 #pragma unroll
-        for (int k = 0; k < kSlotsPerThread; ++k) {
+        for (int k = 0; k < kLaneSlots; ++k) {
           const int j = base + k;
-          const int x = j < nsl ? S.owner[j] : -1;
+          const int x = j < ch ? W.owner[j] : -1;
           run = x > run ? x : run;
-          loc[k] = (int16_t)run;
+          loc[k] = (int8_t)run;
         }
         int incl = run;
 #pragma unroll
@@ -107,68 +133,54 @@ __device__ __forceinline__ void expand_tiles(ExpandSmem& S, Op& o, const int32_t
           const int y = __shfl_up_sync(0xffffffffu, incl, off);
           if (lane >= off) incl = y > incl ? y : incl;
         }
-        if (lane == 31) S.warp_max[warp] = incl;
-        int excl = __shfl_up_sync(0xffffffffu, incl, 1);
-        if (lane == 0) excl = -1;
-        __syncthreads();
-        int wpre = -1;
-        for (int w = 0; w < warp; ++w) wpre = S.warp_max[w] > wpre ? S.warp_max[w] : wpre;
-        const int pre = wpre > excl ? wpre : excl;
+        int pre = __shfl_up_sync(0xffffffffu, incl, 1);
+        if (lane == 0) pre = -1;
+        __syncwarp();
 #pragma unroll
-        for (int k = 0; k < kSlotsPerThread; ++k) {
+        for (int k = 0; k < kLaneSlots; ++k) {
           const int j = base + k;
-          if (j < nsl) S.owner[j] = (int16_t)(loc[k] > pre ? loc[k] : pre);
+          if (j < ch) W.owner[j] = (int8_t)(loc[k] > pre ? loc[k] : pre);
         }
       }
-      __syncthreads();
-
-      // ---- visit: kVisitBatch slots in flight per thread
-      for (int jb = 0; jb < nsl; jb += kExpandBlock * kVisitBatch) {
-        int32_t d[kVisitBatch], it[kVisitBatch], w[kVisitBatch];
-        int64_t e[kVisitBatch];
+      __syncwarp();
+      // visit in batches of B slots per lane
+      for (int jb = cl; jb < ch; jb += 32 * B) {
+        int32_t d[B];
+        int32_t w[Op::kWeights ? B : 1];
 #pragma unroll
-        for (int u = 0; u < kVisitBatch; ++u) {
-          const int j = jb + u * kExpandBlock + tid;
-          it[u] = j < nsl ? S.owner[j] : -1;
-          e[u] = it[u] >= 0 ? S.delta[it[u]] + sl + j : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < kVisitBatch; ++u) {
-          d[u] = it[u] >= 0 ? ld_stream_i32(col + e[u]) : -1;
-          if (Op::kWeights) w[u] = it[u] >= 0 ? ld_stream_i32(wgt + e[u]) : 0;
+        for (int k = 0; k < B; ++k) {
+          const int j = jb + k * 32 + lane;
+          d[k] = -1;
+          if (Op::kWeights) w[Op::kWeights ? k : 0] = 0;
+          if (j < ch) {
+            const int it = W.owner[j];
+            const int64_t e = W.delta[it] + s0 + j;
+            d[k] = ld_stream_i32(col + e);
+            if (Op::kWeights) w[Op::kWeights ? k : 0] = ld_stream_i32(wgt + e);
+          }
         }
         o.prefetch(d);
 #pragma unroll
-        for (int u = 0; u < kVisitBatch; ++u) {
+        for (int k = 0; k < B; ++k) {
+          const int j = jb + k * 32 + lane;
           bool emit = false;
-          if (d[u] >= 0) {
-            const int32_t sv = Op::kSrcVal ? S.sval[it[u]] : 0;
-            emit = o.visit(u, d[u], S.src[it[u]], Op::kWeights ? w[u] : 1, sv, e[u]);
+          int32_t outv = d[k];
+          if (d[k] >= 0) {
+            const int it = W.owner[j];
+            const int64_t e = Op::kEmitEdge ? W.delta[it] + s0 + j : 0;
+            emit = o.visit(k, d[k], W.src[it], Op::kWeights ? w[Op::kWeights ? k : 0] : 1,
+                           Op::kSrcVal ? W.sval[it] : 0, e);
+            if (Op::kEmitEdge) outv = (int32_t)e;
           }
-          const unsigned wm = __ballot_sync(0xffffffffu, emit);
-          if (wm) {
-            int b = 0;
-            if (lane == 0) b = atomicAdd(&S.cnt, __popc(wm));
-            b = __shfl_sync(0xffffffffu, b, 0);
-            if (emit)
-              S.obuf[b + __popc(wm & ((1u << lane) - 1))] =
-                  Op::kEmitEdge ? (int32_t)e[u] : d[u];
-          }
+          const unsigned em = __ballot_sync(0xffffffffu, emit);
+          if (emit) W.obuf[ocnt + __popc(em & ((1u << lane) - 1))] = outv;
+          ocnt += __popc(em);
         }
+        if (ocnt > kOutCap - 32 * B) warp_flush(W, ocnt, out, out_len);
       }
     }
-    __syncthreads();
-    const int cnt = S.cnt;
-    if (cnt > 0) {
-      if (tid == 0) S.gbase = atomicAdd(out_len, (unsigned long long)cnt);
-      __syncthreads();
-      const unsigned long long gb = S.gbase;
-      for (int j = tid; j < cnt; j += kExpandBlock) out[gb + j] = S.obuf[j];
-      __syncthreads();
-      if (tid == 0) S.cnt = 0;
-    }
   }
-  __syncthreads();
+  warp_flush(W, ocnt, out, out_len);
 }
 
 template <class Op>
@@ -179,35 +191,24 @@ __global__ void __launch_bounds__(kExpandBlock)
                 const int32_t* __restrict__ col, const int32_t* __restrict__ wgt, Op op,
                 int32_t* __restrict__ out, unsigned long long* __restrict__ out_len) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  ExpandSmem& S = *reinterpret_cast<ExpandSmem*>(smem_raw);
-  if (threadIdx.x == 0) S.cnt = 0;
-  __syncthreads();
+  WarpSmem& W = warp_smem(smem_raw);
   Op o = op;  // mutable copy: functors keep per-thread prefetch registers
-  expand_tiles(S, o, F, (int64_t)*nf_d, scan, rowbase, part, (int64_t)plan->ntiles,
-               (int64_t)plan->total, col, wgt, out, out_len, blockIdx.x, gridDim.x);
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  expand_tasks(W, o, F, (int64_t)*nf_d, scan, rowbase, part, (int64_t)plan->ntiles,
+               (int64_t)plan->total, col, wgt, out, out_len, gw, nw);
 }
 
-template <class Op>
-constexpr int expand_smem_bytes() {
-  return (int)sizeof(ExpandSmem);
-}
+constexpr int expand_smem_bytes() { return (int)sizeof(WarpSmem) * kWarpsPerBlock; }
 
 template <class Op>
 int set_expand_smem() {
   static bool done = false;
   if (done) return GFX_OK;
   GFX_CK(cudaFuncSetAttribute(k_lb_expand<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              expand_smem_bytes<Op>()));
+                              expand_smem_bytes()));
   done = true;
   return GFX_OK;
-}
-
-// CTAs per SM that fit the shared-memory footprint
-template <class Op>
-inline int expand_ctas_per_sm() {
-  const int per = expand_smem_bytes<Op>() + 1024;
-  int k = (227 * 1024) / per;
-  return k < 1 ? 1 : (k > 8 ? 8 : k);
 }
 
 // scan + expand over queue F (size at *nf_d), emitting into out / *out_len
@@ -218,9 +219,15 @@ int lb_advance(gfx_graph* g, const int32_t* F, const unsigned long long* nf_d, i
   gfx_ctx* ctx = g->ctx;
   GFX_TRY(launch_degree_scan(g, F, nf_d, nf_max, g->row, scan, rowbase, part, plan_ctr));
   GFX_TRY(set_expand_smem<Op>());
-  const int grid = ctx->sm_count * expand_ctas_per_sm<Op>();
-  GFX_LAUNCH((k_lb_expand<Op>), grid, kExpandBlock, expand_smem_bytes<Op>(), ctx->stream, F,
-             nf_d, scan, rowbase, part, plan_ctr, g->col, g->w, op, out, out_len);
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    GFX_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lb_expand<Op>, kExpandBlock,
+                                                         expand_smem_bytes()));
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int grid = ctx->sm_count * per_sm;
+  GFX_LAUNCH((k_lb_expand<Op>), grid, kExpandBlock, expand_smem_bytes(), ctx->stream, F, nf_d,
+             scan, rowbase, part, plan_ctr, g->col, g->w, op, out, out_len);
   GFX_CK(cudaGetLastError());
   return GFX_OK;
 }

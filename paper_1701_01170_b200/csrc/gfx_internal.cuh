@@ -139,7 +139,7 @@ inline int grid_for(int64_t items, int block, int cap_blocks) {
 // device *nf_d), CSR row offsets.  Outputs: scan[0..nf] exclusive prefix of
 // degrees, rowbase[i] = row[F[i]], part[k] = item holding slot k*kTile,
 // counters->total / ntiles.
-constexpr int kTile = 4096;          // expansion slots per tile
+constexpr int kTile = 512;           // expansion slots per (warp) tile
 constexpr int kScanBlock = 256;
 constexpr int kScanItems = 8;        // items per thread in the scan
 constexpr int kScanTileItems = kScanBlock * kScanItems;

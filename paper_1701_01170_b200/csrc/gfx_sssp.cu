@@ -29,14 +29,15 @@ namespace gfx {
 
 struct SsspRelaxOp {
   static constexpr bool kWeights = true, kSrcVal = true, kEmitEdge = false;
+  static constexpr int kBatch = 8;
   unsigned long long* dp;
   int32_t* stamp;
   int32_t it;
-  unsigned long long cur[kVisitBatch];
+  unsigned long long cur[kBatch];
   __device__ int32_t src_value(int32_t v) const { return (int32_t)(dp[v] >> 32); }
-  __device__ void prefetch(const int32_t d[kVisitBatch]) {
+  __device__ void prefetch(const int32_t* d) {
 #pragma unroll
-    for (int u = 0; u < kVisitBatch; ++u) cur[u] = d[u] >= 0 ? dp[d[u]] : 0ull;
+    for (int u = 0; u < kBatch; ++u) cur[u] = d[u] >= 0 ? dp[d[u]] : 0ull;
   }
   // atomic_min relax (operators.py:111-124): emit d once per iteration when
   // its distance strictly improved
