@@ -9,10 +9,12 @@
 
 namespace gfx {
 
-// variant 0: stream the adjacency only (no functor memory traffic)
-struct StreamOp {
+// variant 0 / 3: stream the adjacency only (no functor memory traffic),
+// 16 / 8 column loads in flight per lane
+template <int KB>
+struct StreamOpT {
   static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
-  static constexpr int kBatch = kVisitBatch;
+  static constexpr int kBatch = KB;
   int32_t sentinel;
   __device__ int32_t src_value(int32_t) const { return 0; }
   __device__ void prefetch(const int32_t*) {}
@@ -97,7 +99,10 @@ extern "C" int gfx_debug_expand(gfx_graph* g, const int32_t* F_d, int64_t nf, in
   GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
   int st = GFX_OK;
   if (variant == 0) {
-    StreamOp op{-7};
+    StreamOpT<16> op{-7};
+    st = lb_advance(g, F_d, &C[0].out_len, nf, &C[1], scan, rowbase, part, op, out, &C[1].out_len);
+  } else if (variant == 3) {
+    StreamOpT<8> op{-7};
     st = lb_advance(g, F_d, &C[0].out_len, nf, &C[1], scan, rowbase, part, op, out, &C[1].out_len);
   } else if (variant == 1) {
     ProbeOp op{vis, {}};

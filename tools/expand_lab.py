@@ -23,7 +23,7 @@ def main():
         slots = int(deg[F.long()].sum().item())
         base = labels.clone()
         base[base >= depth] = _native.UNVISITED32
-        for variant, name in ((0, "stream"), (1, "probe"), (2, "claim")):
+        for variant, name in ((0, "strm16"), (3, "strm8"), (1, "probe"), (2, "claim")):
             times = []
             for _ in range(4):
                 lab = base.clone()
