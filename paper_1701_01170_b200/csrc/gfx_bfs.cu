@@ -161,7 +161,10 @@ __device__ __forceinline__ void pull_groups(
     }
     int total;
     const int off = warp_excl_scan(__popc(cand), lane, &total);
-    if (total == 0) continue;
+    if (total == 0) {
+      if (w < words) next[w] = 0u;  // the frontier buffer is reused across levels
+      continue;
+    }
     P.newbits[lane] = 0u;
     {
       uint32_t x = cand;

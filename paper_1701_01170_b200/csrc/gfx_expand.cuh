@@ -83,18 +83,47 @@ __device__ __forceinline__ void expand_tasks(WarpSmem& W, Op& o, const int32_t* 
   constexpr int B = Op::kBatch;
   const int lane = threadIdx.x & 31;
   int ocnt = 0;
+  // software pipeline: the next tile's partition entry and first 32 items
+  // are loaded while the current tile's column loads are in flight
+  int64_t p_i0 = 0, p_i1 = -1, p_sc = 0, p_sc1 = 0, p_rb = 0;
+  int32_t p_v = 0;
+  auto prefetch_tile = [&](int64_t t) {
+    if (t >= ntiles) return;
+    p_i0 = part[t];
+    p_i1 = (t + 1 < ntiles) ? (int64_t)part[t + 1] : nf - 1;
+    const int64_t i = p_i0 + lane;
+    if (i <= p_i1) {
+      p_sc = scan[i];
+      p_sc1 = scan[i + 1];
+      p_rb = rowbase[i];
+      p_v = F[i];
+    }
+  };
+  prefetch_tile(task0);
   for (int64_t t = task0; t < ntiles; t += ntasks) {
     const int64_t s0 = t * kTile;
     const int64_t s1 = min(s0 + (int64_t)kTile, total);
-    const int64_t i0 = part[t];
-    const int64_t i1 = (t + 1 < ntiles) ? (int64_t)part[t + 1] : nf - 1;
+    const int64_t i0 = p_i0, i1 = p_i1;
+    const int64_t f_sc = p_sc, f_sc1 = p_sc1, f_rb = p_rb;
+    const int32_t f_v = p_v;
+    prefetch_tile(t + ntasks);
     for (int64_t ib = i0; ib <= i1; ib += 32) {
       const int64_t i = ib + lane;
       const bool valid = i <= i1;
-      int64_t sc = 0, sc1 = 0;
+      int64_t sc = 0, sc1 = 0, rb = 0;
+      int32_t v = 0;
       if (valid) {
-        sc = scan[i];
-        sc1 = scan[i + 1];
+        if (ib == i0) {
+          sc = f_sc;
+          sc1 = f_sc1;
+          rb = f_rb;
+          v = f_v;
+        } else {
+          sc = scan[i];
+          sc1 = scan[i + 1];
+          rb = rowbase[i];
+          v = F[i];
+        }
       }
       const int64_t lo = max(sc, s0), hi = min(sc1, s1);
       const bool has = valid && hi > lo;
@@ -108,9 +137,8 @@ __device__ __forceinline__ void expand_tasks(WarpSmem& W, Op& o, const int32_t* 
       for (int j = cl + lane; j < ch; j += 32) W.owner[j] = -1;
       __syncwarp();
       if (has) {
-        const int32_t v = F[i];
         W.owner[lo - s0] = (int8_t)lane;
-        W.delta[lane] = rowbase[i] - sc;
+        W.delta[lane] = rb - sc;
         W.src[lane] = v;
         if (Op::kSrcVal) W.sval[lane] = o.src_value(v);
       }
