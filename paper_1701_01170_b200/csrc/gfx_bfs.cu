@@ -24,6 +24,7 @@
 #include "gfx_direction.cuh"
 #include "gfx_expand.cuh"
 #include "gfx_internal.cuh"
+#include "gfx_pull.cuh"
 #include "gfx_scan.cuh"
 
 namespace gfx {
@@ -119,135 +120,6 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-constexpr int kPullBatch = 4;  // candidates per lane in flight
-
-// per-warp scratch of the pull phase (aliases the expansion's WarpSmem)
-struct PullSmem {
-  int32_t cand[1024];    // compacted candidate vertices of the warp's 32 words
-  uint32_t newbits[32];  // found bits per word of the group
-};
-static_assert(sizeof(PullSmem) <= sizeof(WarpSmem) + 1024, "pull scratch must fit the warp slice");
-constexpr int kWarpScratch = sizeof(PullSmem) > sizeof(WarpSmem) ? sizeof(PullSmem) : sizeof(WarpSmem);
-
-// Pull (bottom-up) level.  One warp owns 32 consecutive bitmap words (1024
-// vertices).  Candidates (unvisited & in-degree > 0) are first compacted
-// into the warp's shared-memory list, so every lane always works on a real
-// candidate however sparse the unvisited set is.  Each candidate's first
-// probe reads head[u] -- the graph-constant copy of its first in-neighbour,
-// stored densely -- and only misses fetch their row bounds and scan on in
-// ascending order (reference pull_expand, operators.py:269-307, scans every
-// in-edge; labels are identical, only the work differs).  Found bits are
-// gathered per word in shared memory and written with plain coalesced
-// stores (the warp owns its words).
-// counters: out_len += |new frontier|, edges += sum of in-degree(U) (only
-//           when count_in_edges; for undirected graphs the per-level degree
-//           post-pass derives it), aux0 += early-exit probes S(U),
-//           aux1 += |U| with in-degree > 0.
-__device__ __forceinline__ void pull_groups(
-    int64_t words, const uint32_t* __restrict__ nz_in, uint32_t* __restrict__ visited,
-    const uint32_t* __restrict__ front, uint32_t* __restrict__ next,
-    const int32_t* __restrict__ head, const int64_t* __restrict__ rrow,
-    const int32_t* __restrict__ rcol, int count_in_edges, int32_t* __restrict__ labels,
-    int32_t* __restrict__ preds, int32_t depth, Counters* __restrict__ ctr, int64_t gw,
-    int64_t nwarps, PullSmem& P) {
-  const int lane = threadIdx.x & 31;
-  unsigned long long found_cnt = 0, in_edges = 0, probes = 0, cands = 0;
-  for (int64_t grp = gw; grp * 32 < words; grp += nwarps) {
-    const int64_t w = grp * 32 + lane;
-    uint32_t vis = 0xffffffffu, cand = 0;
-    if (w < words) {
-      vis = visited[w];
-      cand = ~vis & nz_in[w];
-    }
-    int total;
-    const int off = warp_excl_scan(__popc(cand), lane, &total);
-    if (total == 0) {
-      if (w < words) next[w] = 0u;  // the frontier buffer is reused across levels
-      continue;
-    }
-    P.newbits[lane] = 0u;
-    {
-      uint32_t x = cand;
-      int k = off;
-      while (x) {
-        const int b = __ffs(x) - 1;
-        x &= x - 1;
-        P.cand[k++] = (int32_t)(w * 32 + b);
-      }
-    }
-    __syncwarp();
-    cands += (unsigned long long)(lane == 0 ? total : 0);
-    for (int base = 0; base < total; base += 32 * kPullBatch) {
-      int32_t u[kPullBatch], h[kPullBatch];
-      uint32_t fw[kPullBatch];
-#pragma unroll
-      for (int q = 0; q < kPullBatch; ++q) {
-        const int k = base + q * 32 + lane;
-        u[q] = k < total ? P.cand[k] : -1;
-        h[q] = u[q] >= 0 ? head[u[q]] : -1;
-      }
-#pragma unroll
-      for (int q = 0; q < kPullBatch; ++q) fw[q] = h[q] >= 0 ? front[h[q] >> 5] : 0u;
-#pragma unroll
-      for (int q = 0; q < kPullBatch; ++q) {
-        if (u[q] < 0) continue;
-        bool found = false;
-        int32_t par = -1;
-        int64_t b = 0, e = 0;
-        if ((fw[q] >> (h[q] & 31)) & 1u) {
-          found = true;
-          par = h[q];
-          ++probes;
-          if (count_in_edges) {
-            b = rrow[u[q]];
-            e = rrow[u[q] + 1];
-          }
-        } else {
-          // miss: continue from the second in-neighbour
-          b = rrow[u[q]];
-          e = rrow[u[q] + 1];
-          int64_t p = b + 1;
-          for (; p < e; ++p) {
-            const int32_t s = rcol[p];
-            if ((front[s >> 5] >> (s & 31)) & 1u) {
-              found = true;
-              par = s;
-              break;
-            }
-          }
-          probes += (unsigned long long)(found ? p - b + 1 : e - b);
-        }
-        in_edges += (unsigned long long)(e - b);
-        if (found) {
-          labels[u[q]] = depth;
-          preds[u[q]] = par;
-          atomicOr(&P.newbits[(u[q] >> 5) - grp * 32], 1u << (u[q] & 31));
-          ++found_cnt;
-        }
-      }
-    }
-    __syncwarp();
-    if (w < words) {
-      const uint32_t nb = P.newbits[lane];
-      next[w] = nb;
-      if (nb) visited[w] = vis | nb;
-    } else {
-      (void)0;
-    }
-    __syncwarp();
-  }
-  found_cnt = warp_sum_u64(found_cnt);
-  in_edges = warp_sum_u64(in_edges);
-  probes = warp_sum_u64(probes);
-  cands = warp_sum_u64(cands);
-  if (lane == 0) {
-    if (found_cnt) atomicAdd(&ctr->out_len, found_cnt);
-    if (in_edges) atomicAdd(&ctr->edges, in_edges);
-    if (probes) atomicAdd(&ctr->aux0, probes);
-    if (cands) atomicAdd(&ctr->aux1, cands);
-  }
-}
-
 __global__ void __launch_bounds__(256)
     k_bfs_pull(int64_t words, const uint32_t* __restrict__ nz_in,
                uint32_t* __restrict__ visited, const uint32_t* __restrict__ front,
@@ -256,7 +128,7 @@ __global__ void __launch_bounds__(256)
                int count_in_edges, int32_t* __restrict__ labels, int32_t* __restrict__ preds,
                int32_t depth, Counters* __restrict__ ctr) {
   __shared__ PullSmem ps[8];
-  pull_groups(words, nz_in, visited, front, next, head, rrow, rcol, count_in_edges, labels,
+  pull_groups(words, nz_in, visited, BitmapFront{front}, next, head, rrow, rcol, count_in_edges, labels,
               preds, depth, ctr, (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5,
               ((int64_t)gridDim.x * blockDim.x) >> 5, ps[threadIdx.x >> 5]);
 }
@@ -842,7 +714,7 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
         queue_to_bitmap(a.order + c.q_off, nf, fcur, gtid, nthr);
         grid.sync();
       }
-      pull_groups(a.words, a.nz_in, a.visited, fcur, fnext, a.head, a.rrow, a.rcol, a.directed,
+      pull_groups(a.words, a.nz_in, a.visited, BitmapFront{fcur}, fnext, a.head, a.rrow, a.rcol, a.directed,
                   a.labels, a.preds, depth, cur, gw, nw, PS);
       grid.sync();
       nout = (long long)ld_ctr(&cur->out_len);

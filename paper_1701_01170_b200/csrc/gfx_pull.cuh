@@ -1,0 +1,170 @@
+// Pull (bottom-up) level body shared by the single-GPU BFS (gfx_bfs.cu) and
+// the partitioned multi-GPU BFS (gfx_dist.cu).
+#pragma once
+
+#include "gfx_device.cuh"
+#include "gfx_expand.cuh"
+#include "gfx_internal.cuh"
+
+namespace gfx {
+
+// frontier = one bitmap over global ids (single GPU)
+struct BitmapFront {
+  const uint32_t* bm;
+  __device__ __forceinline__ uint32_t word(int32_t s) const { return bm[s >> 5]; }
+  __device__ __forceinline__ bool bit(uint32_t w, int32_t s) const { return (w >> (s & 31)) & 1u; }
+};
+
+constexpr int kPullBatch = 8;  // candidates per lane in flight
+
+// per-warp scratch of the pull phase (aliases the expansion's WarpSmem)
+struct PullSmem {
+  int32_t cand[1024];    // compacted candidate vertices of the warp's 32 words
+  uint32_t newbits[32];  // found bits per word of the group
+};
+static_assert(sizeof(PullSmem) <= sizeof(WarpSmem) + 1024, "pull scratch must fit the warp slice");
+constexpr int kWarpScratch = sizeof(PullSmem) > sizeof(WarpSmem) ? sizeof(PullSmem) : sizeof(WarpSmem);
+
+// Pull (bottom-up) level.  One warp owns 32 consecutive bitmap words (1024
+// vertices).  Candidates (unvisited & in-degree > 0) are first compacted
+// into the warp's shared-memory list, so every lane always works on a real
+// candidate however sparse the unvisited set is.  Each candidate's first
+// probe reads head[u] -- the graph-constant copy of its first in-neighbour,
+// stored densely -- and only misses fetch their row bounds and scan on in
+// ascending order (reference pull_expand, operators.py:269-307, scans every
+// in-edge; labels are identical, only the work differs).  Found bits are
+// gathered per word in shared memory and written with plain coalesced
+// stores (the warp owns its words).
+// counters: out_len += |new frontier|, edges += sum of in-degree(U) (only
+//           when count_in_edges; for undirected graphs the per-level degree
+//           post-pass derives it), aux0 += early-exit probes S(U),
+//           aux1 += |U| with in-degree > 0.
+// FrontT: frontier membership of an in-neighbour s (global id):
+//   uint32_t word(s) loads the bitmap word holding s; bool bit(w, s) tests it.
+template <class FrontT>
+__device__ __forceinline__ void pull_groups(
+    int64_t words, const uint32_t* __restrict__ nz_in, uint32_t* __restrict__ visited,
+    const FrontT front, uint32_t* __restrict__ next,
+    const int32_t* __restrict__ head, const int64_t* __restrict__ rrow,
+    const int32_t* __restrict__ rcol, int count_in_edges, int32_t* __restrict__ labels,
+    int32_t* __restrict__ preds, int32_t depth, Counters* __restrict__ ctr, int64_t gw,
+    int64_t nwarps, PullSmem& P) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long found_cnt = 0, in_edges = 0, probes = 0, cands = 0;
+  for (int64_t grp = gw; grp * 32 < words; grp += nwarps) {
+    const int64_t w = grp * 32 + lane;
+    uint32_t vis = 0xffffffffu, cand = 0;
+    if (w < words) {
+      vis = visited[w];
+      cand = ~vis & nz_in[w];
+    }
+    int total;
+    const int off = warp_excl_scan(__popc(cand), lane, &total);
+    if (total == 0) {
+      if (w < words) next[w] = 0u;  // the frontier buffer is reused across levels
+      continue;
+    }
+    P.newbits[lane] = 0u;
+    {
+      uint32_t x = cand;
+      int k = off;
+      while (x) {
+        const int b = __ffs(x) - 1;
+        x &= x - 1;
+        P.cand[k++] = (int32_t)(w * 32 + b);
+      }
+    }
+    __syncwarp();
+    cands += (unsigned long long)(lane == 0 ? total : 0);
+    // phase 1: first probe of every candidate from the dense head array;
+    // misses are compacted in place to the front of the list
+    int nmiss = 0;
+    for (int base = 0; base < total; base += 32 * kPullBatch) {
+      int32_t u[kPullBatch], h[kPullBatch];
+      uint32_t fw[kPullBatch];
+#pragma unroll
+      for (int q = 0; q < kPullBatch; ++q) {
+        const int k = base + q * 32 + lane;
+        u[q] = k < total ? P.cand[k] : -1;
+        h[q] = u[q] >= 0 ? head[u[q]] : -1;
+      }
+#pragma unroll
+      for (int q = 0; q < kPullBatch; ++q) fw[q] = h[q] >= 0 ? front.word(h[q]) : 0u;
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < kPullBatch; ++q) {
+        const bool hit = h[q] >= 0 && front.bit(fw[q], h[q]);
+        const bool miss = h[q] >= 0 && !hit;
+        if (hit) {
+          labels[u[q]] = depth;
+          preds[u[q]] = h[q];
+          atomicOr(&P.newbits[(u[q] >> 5) - grp * 32], 1u << (u[q] & 31));
+          ++found_cnt;
+          ++probes;
+          if (count_in_edges) in_edges += (unsigned long long)(rrow[u[q] + 1] - rrow[u[q]]);
+        }
+        const unsigned mm = __ballot_sync(0xffffffffu, miss);
+        if (miss) P.cand[nmiss + __popc(mm & ((1u << lane) - 1))] = u[q];
+        nmiss += __popc(mm);
+      }
+    }
+    __syncwarp();
+    // phase 2: misses, one per lane, scanning on from the second in-neighbour
+    // with four column loads in flight (early-exit count stays exact)
+    for (int base = 0; base < nmiss; base += 32) {
+      const int k = base + lane;
+      if (k >= nmiss) continue;
+      const int32_t uu = P.cand[k];
+      const int64_t b = rrow[uu], e = rrow[uu + 1];
+      bool found = false;
+      int32_t par = -1;
+      int64_t p = b + 1;
+      while (p < e && !found) {
+        int32_t sv[4];
+        uint32_t wv[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) sv[t] = (p + t < e) ? ld_stream_i32(rcol + p + t) : -1;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) wv[t] = sv[t] >= 0 ? front.word(sv[t]) : 0u;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          if (!found && sv[t] >= 0 && front.bit(wv[t], sv[t])) {
+            found = true;
+            par = sv[t];
+            p = p + t;
+          }
+        }
+        if (!found) p += 4;
+      }
+      probes += (unsigned long long)(found ? p - b + 1 : e - b);
+      in_edges += (unsigned long long)(e - b);
+      if (found) {
+        labels[uu] = depth;
+        preds[uu] = par;
+        atomicOr(&P.newbits[(uu >> 5) - grp * 32], 1u << (uu & 31));
+        ++found_cnt;
+      }
+    }
+    __syncwarp();
+    if (w < words) {
+      const uint32_t nb = P.newbits[lane];
+      next[w] = nb;
+      if (nb) visited[w] = vis | nb;
+    } else {
+      (void)0;
+    }
+    __syncwarp();
+  }
+  found_cnt = warp_sum_u64(found_cnt);
+  in_edges = warp_sum_u64(in_edges);
+  probes = warp_sum_u64(probes);
+  cands = warp_sum_u64(cands);
+  if (lane == 0) {
+    if (found_cnt) atomicAdd(&ctr->out_len, found_cnt);
+    if (in_edges) atomicAdd(&ctr->edges, in_edges);
+    if (probes) atomicAdd(&ctr->aux0, probes);
+    if (cands) atomicAdd(&ctr->aux1, cands);
+  }
+}
+
+}  // namespace gfx
