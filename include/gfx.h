@@ -94,6 +94,8 @@ typedef struct gfx_stats {
   int64_t bytes_alg;      /* algorithmic HBM bytes (DESIGN.md formulas) */
   double device_ms;       /* CUDA-event time of the device loop */
   int64_t num_records;    /* records written (<= rec_cap) */
+  int64_t init_ns;        /* device-resident BFS: output/state initialisation */
+  int64_t loop_ns;        /* device-resident BFS: level loop */
 } gfx_stats;
 
 /* ---- library / context ------------------------------------------------ */
@@ -222,6 +224,35 @@ GFX_API int gfx_keys_to_csr(gfx_ctx* ctx, const uint64_t* keys_d, int64_t num_ke
 GFX_API int gfx_assign_weights(gfx_graph* g, int64_t lo, int64_t hi, uint64_t state_hi,
                        uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
                        int32_t* w_d);
+
+/* ---- partitioned multi-GPU BFS (1D cyclic partition) -------
+ * Rank r of P owns vertices v = l*P + r (local id l); its local CSR holds
+ * the owned rows with GLOBAL column ids.  The host drives the levels and the
+ * collectives (allreduce of n_f, all_to_all of (dst, src) pairs for push
+ * levels, all_gather of local frontier bitmaps for pull levels) on buffers it
+ * owns and binds here; the direction decision is the reference formula on the
+ * global counts (direction.py:52-70).  Undirected graphs only. */
+typedef struct gfx_dbfs gfx_dbfs;
+GFX_API int gfx_dist_partition_sizes(gfx_graph* g, int P, int r, int64_t* n_local,
+                                     int64_t* m_local);
+GFX_API int gfx_dist_partition(gfx_graph* g, int P, int r, int64_t* lrow_d, int32_t* lcol_d);
+GFX_API int gfx_dbfs_create(gfx_ctx* ctx, int64_t n, int64_t m, int P, int r,
+                            const int64_t* lrow_d, const int32_t* lcol_d, int64_t n_local,
+                            int64_t m_local, gfx_dbfs** out);
+GFX_API int gfx_dbfs_destroy(gfx_dbfs* db);
+GFX_API int gfx_dbfs_words(gfx_dbfs* db, int64_t* words_local, int64_t* words_max);
+/* labels/preds: int32[n_local]; send/recv: uint64 pairs (dst << 32 | src);
+ * front_local: uint32[words_max]; gathered: uint32[P * words_max] */
+GFX_API int gfx_dbfs_bind(gfx_dbfs* db, int32_t* labels_d, int32_t* preds_d, void* send_d,
+                          int64_t send_cap, void* recv_d, int64_t recv_cap,
+                          uint32_t* front_local_d, uint32_t* gathered_d);
+GFX_API int gfx_dbfs_reset(gfx_dbfs* db, int64_t source, int64_t* nf_local);
+GFX_API int gfx_dbfs_push_expand(gfx_dbfs* db, int32_t depth, int64_t* send_counts,
+                                 int64_t* local_new, int64_t* edges);
+GFX_API int gfx_dbfs_push_claim(gfx_dbfs* db, int64_t nrecv, int32_t depth, int64_t* nf_local);
+GFX_API int gfx_dbfs_pull_prepare(gfx_dbfs* db);
+GFX_API int gfx_dbfs_pull(gfx_dbfs* db, int32_t depth, int64_t* nf_local, int64_t* probes,
+                          int64_t* candidates);
 
 /* ---- kernel experiments (tools/expand_lab.py; not a product path) -------
  * One LB expansion of F_d with functor variant 0 (stream only), 1 (stream +

@@ -40,7 +40,7 @@ class Stats(Structure):
         ("iterations", c_int64), ("edges_traversed", c_int64),
         ("direction_switches", c_int64), ("reached", c_int64), ("edges_reached", c_int64),
         ("work_slots", c_int64), ("bytes_alg", c_int64), ("device_ms", c_double),
-        ("num_records", c_int64),
+        ("num_records", c_int64), ("init_ns", c_int64), ("loop_ns", c_int64),
     ]
 
 
@@ -88,6 +88,22 @@ _SIGS = {
     "gfx_keys_to_csr": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_void_p]),
     "gfx_assign_weights": (c_int, [c_void_p, c_int64, c_int64, c_uint64, c_uint64, c_uint64,
                                    c_uint64, c_void_p]),
+    "gfx_dist_partition_sizes": (c_int, [c_void_p, c_int, c_int, POINTER(c_int64),
+                                         POINTER(c_int64)]),
+    "gfx_dist_partition": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p]),
+    "gfx_dbfs_create": (c_int, [c_void_p, c_int64, c_int64, c_int, c_int, c_void_p, c_void_p,
+                                c_int64, c_int64, POINTER(c_void_p)]),
+    "gfx_dbfs_destroy": (c_int, [c_void_p]),
+    "gfx_dbfs_words": (c_int, [c_void_p, POINTER(c_int64), POINTER(c_int64)]),
+    "gfx_dbfs_bind": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int64,
+                              c_void_p, c_void_p]),
+    "gfx_dbfs_reset": (c_int, [c_void_p, c_int64, POINTER(c_int64)]),
+    "gfx_dbfs_push_expand": (c_int, [c_void_p, c_int32, POINTER(c_int64), POINTER(c_int64),
+                                     POINTER(c_int64)]),
+    "gfx_dbfs_push_claim": (c_int, [c_void_p, c_int64, c_int32, POINTER(c_int64)]),
+    "gfx_dbfs_pull_prepare": (c_int, [c_void_p]),
+    "gfx_dbfs_pull": (c_int, [c_void_p, c_int32, POINTER(c_int64), POINTER(c_int64),
+                              POINTER(c_int64)]),
     "gfx_debug_expand": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_int32,
                                  POINTER(c_float), POINTER(c_int64)]),
 }

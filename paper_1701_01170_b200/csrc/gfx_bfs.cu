@@ -624,6 +624,7 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   const int64_t gw = gtid >> 5, nw = nthr >> 5;
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+  const unsigned long long t_start = leader ? globaltimer() : 0ull;
 
   // ---- initialise outputs and state
   for (int64_t i = gtid; i < a.n; i += nthr) {
@@ -651,6 +652,7 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
     a.order[0] = a.source;
   }
   grid.sync();
+  const unsigned long long t_init = leader ? globaltimer() : 0ull;
 
   for (;;) {
     if (threadIdx.x == 0) {
@@ -765,6 +767,8 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
     a.summary[5] = c.bytes_total;
     a.summary[6] = c.work_total;
     a.summary[7] = c.nrec < a.rec_cap ? c.nrec : a.rec_cap;
+    a.summary[8] = (long long)(t_init - t_start);
+    a.summary[9] = (long long)(globaltimer() - t_init);
   }
 }
 
@@ -812,7 +816,7 @@ int bfs_device_loop(gfx_graph* g, int64_t source, int direction, double do_a, do
   const int64_t cap = 1 << 16;  // level records kept on device (stats)
   GFX_TRY(scratch_t(g, "pbfs_recs", cap, &a.recs));
   a.rec_cap = cap;
-  GFX_TRY(scratch_t(g, "pbfs_summary", 8, &a.summary));
+  GFX_TRY(scratch_t(g, "pbfs_summary", 10, &a.summary));
   a.direction = direction;
   a.mu_edge = mu_edge;
   a.directed = directed ? 1 : 0;
@@ -842,7 +846,7 @@ int bfs_device_loop(gfx_graph* g, int64_t source, int direction, double do_a, do
                                      ctx->stream));
   count_launch();
   GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));
-  long long summary[8];
+  long long summary[10];
   GFX_CK(cudaMemcpyAsync(summary, a.summary, sizeof(summary), cudaMemcpyDeviceToHost,
                          ctx->stream));
   GFX_CK(cudaStreamSynchronize(ctx->stream));
@@ -861,6 +865,8 @@ int bfs_device_loop(gfx_graph* g, int64_t source, int direction, double do_a, do
     st->bytes_alg = summary[5];
     st->work_slots = summary[6];
     st->device_ms = ms;
+    st->init_ns = summary[8];
+    st->loop_ns = summary[9];
     GFX_TRY(bfs_level_stats(g, labels, summary[0], lrecs.data(), (int64_t)lrecs.size(), st));
   }
   const int64_t nrec = std::min<int64_t>((int64_t)lrecs.size(), recs ? rec_cap : 0);

@@ -55,6 +55,8 @@ def stats_from_records(primitive, recs, st, count_trace=True) -> RunStats:
     stats.work_slots = int(st.work_slots)
     stats.device_ms = float(st.device_ms)
     stats.bytes_alg = int(st.bytes_alg)
+    stats.init_ms = st.init_ns * 1e-6
+    stats.loop_ms = st.loop_ns * 1e-6
     return stats
 
 

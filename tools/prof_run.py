@@ -44,7 +44,10 @@ def main():
         st = fn()[2]
     torch.cuda.synchronize()
     torch.cuda.cudart().cudaProfilerStop()
-    print("device_ms", st.device_ms, "E_r", st.edges_reached)
+    print("device_ms", st.device_ms, "E_r", st.edges_reached, "init_ms",
+          getattr(st, "init_ms", None), "loop_ms", getattr(st, "loop_ms", None))
+    for lv in getattr(st, "device_levels", []):
+        print("  ", lv)
 
 
 if __name__ == "__main__":
