@@ -308,7 +308,7 @@ static int bfs_buffers(gfx_graph* g, bool idemp, BfsBuffers* b) {
   GFX_TRY(scratch_t(g, "q_order", n + 1, &b->order));
   GFX_TRY(scratch_t(g, "q_scan", n + 2, &b->scan));
   GFX_TRY(scratch_t(g, "q_rowbase", n + 1, &b->rowbase));
-  GFX_TRY(scratch_t(g, "q_part", g->m / kTile + 4, &b->part));
+  GFX_TRY(scratch_t(g, "q_part", part_capacity(g->m, g->n), &b->part));
   b->raw = nullptr;
   if (idemp) GFX_TRY(scratch_t(g, "q_raw", g->m + 1, &b->raw));
   return GFX_OK;

@@ -114,7 +114,7 @@ extern "C" int gfx_cc(gfx_graph* g, int32_t* comp_d, int64_t* num_components, gf
   GFX_TRY(iota_frontier(g, &iota));
   GFX_TRY(scratch_t(g, "q_scan", n + 2, &scan));
   GFX_TRY(scratch_t(g, "q_rowbase", n + 1, &rowbase));
-  GFX_TRY(scratch_t(g, "q_part", g->m / kTile + 4, &part));
+  GFX_TRY(scratch_t(g, "q_part", part_capacity(g->m, g->n), &part));
   Counters* C = g->counters;
   auto* pin = static_cast<Counters*>(ctx->pinned);
 

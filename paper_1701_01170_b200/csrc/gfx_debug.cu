@@ -87,7 +87,7 @@ extern "C" int gfx_debug_expand(gfx_graph* g, const int32_t* F_d, int64_t nf, in
   uint32_t* vis;
   GFX_TRY(scratch_t(g, "q_scan", n + 2, &scan));
   GFX_TRY(scratch_t(g, "q_rowbase", n + 1, &rowbase));
-  GFX_TRY(scratch_t(g, "q_part", g->m / kTile + 4, &part));
+  GFX_TRY(scratch_t(g, "q_part", part_capacity(g->m, g->n), &part));
   GFX_TRY(scratch_t(g, "dbg_out", g->m + 1, &out));
   GFX_TRY(scratch_t(g, "dbg_vis", g->words, &vis));
   Counters* C = g->counters;

@@ -413,7 +413,7 @@ int gfx_dbfs_push_expand(gfx_dbfs* db, int32_t depth, int64_t* send_counts, int6
   GFX_TRY(db_scratch_i32(db, "d_emit", db->n + 1, &emit));
   GFX_TRY(scratch_t(g, "q_scan", db->nl + 2, &scan));
   GFX_TRY(scratch_t(g, "q_rowbase", db->nl + 1, &rowbase));
-  GFX_TRY(scratch_t(g, "q_part", db->ml / kTile + 4, &part));
+  GFX_TRY(scratch_t(g, "q_part", part_capacity(db->ml, db->nl), &part));
   Counters* C = g->counters;
   auto* pin = static_cast<Counters*>(ctx->pinned);
   GFX_CK(cudaMemsetAsync(C, 0, 3 * sizeof(Counters), ctx->stream));

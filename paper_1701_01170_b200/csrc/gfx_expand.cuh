@@ -100,13 +100,15 @@ __device__ __forceinline__ void expand_tasks(WarpSmem& W, Op& o, const int32_t* 
     }
   };
   prefetch_tile(task0);
+  const int64_t units = total + (int64_t)kItemUnits * nf;
   for (int64_t t = task0; t < ntiles; t += ntasks) {
-    const int64_t s0 = t * kTile;
-    const int64_t s1 = min(s0 + (int64_t)kTile, total);
+    const int64_t u0 = t * kTile;
+    const int64_t u1 = min(u0 + (int64_t)kTile, units);
     const int64_t i0 = p_i0, i1 = p_i1;
     const int64_t f_sc = p_sc, f_sc1 = p_sc1, f_rb = p_rb;
     const int32_t f_v = p_v;
     prefetch_tile(t + ntasks);
+    int64_t s0 = 0;  // first slot of the tile (set by the first chunk)
     for (int64_t ib = i0; ib <= i1; ib += 32) {
       const int64_t i = ib + lane;
       const bool valid = i <= i1;
@@ -125,8 +127,13 @@ __device__ __forceinline__ void expand_tasks(WarpSmem& W, Op& o, const int32_t* 
           v = F[i];
         }
       }
-      const int64_t lo = max(sc, s0), hi = min(sc1, s1);
+      // clip the item's slots to the tile's unit range
+      const int64_t ub = sc + (int64_t)kItemUnits * i + kItemUnits;  // unit of slot sc
+      const int64_t deg = sc1 - sc;
+      const int64_t lo = sc + min(max(u0 - ub, (int64_t)0), deg);
+      const int64_t hi = sc + min(max(u1 - ub, (int64_t)0), deg);
       const bool has = valid && hi > lo;
+      if (ib == i0) s0 = __shfl_sync(0xffffffffu, lo, 0);
       // chunk slot range [cl, ch) relative to s0
       const int cl = (int)(__shfl_sync(0xffffffffu, lo, 0) - s0);
       const unsigned vm = __ballot_sync(0xffffffffu, valid);

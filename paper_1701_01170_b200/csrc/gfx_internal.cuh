@@ -139,7 +139,13 @@ inline int grid_for(int64_t items, int block, int cap_blocks) {
 // device *nf_d), CSR row offsets.  Outputs: scan[0..nf] exclusive prefix of
 // degrees, rowbase[i] = row[F[i]], part[k] = item holding slot k*kTile,
 // counters->total / ntiles.
-constexpr int kTile = 512;           // expansion slots per (warp) tile
+constexpr int kTile = 512;           // expansion units per (warp) tile
+// Each frontier item weighs kItemUnits units plus one per slot, so a tile
+// never holds more than ~32 items (merge-path style: slots + items balanced)
+constexpr int kItemUnits = 16;
+inline int64_t part_capacity(int64_t m, int64_t n) {
+  return (m + (int64_t)kItemUnits * (n + 1)) / kTile + 8;
+}
 constexpr int kScanBlock = 256;
 constexpr int kScanItems = 8;        // items per thread in the scan
 constexpr int kScanTileItems = kScanBlock * kScanItems;

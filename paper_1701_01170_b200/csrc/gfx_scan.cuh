@@ -3,8 +3,10 @@
 // Replaces reference load_balance.py:105-113 (compute_scan_offsets) and
 // load_balance.py:157-176 (plan_lb_output: ceil(total/N) chunks of N output
 // slots, each chunk's first source found by searchsorted).  Here the
-// partition falls out of the scan: the item whose slot range covers k*kTile
-// writes part[k] directly, so no search is needed.
+// partition falls out of the scan: the item whose units cover k*kTile writes
+// part[k] directly, so no search is needed.  Units: every item weighs
+// kItemUnits plus its degree (merge-path over items and slots), so a tile
+// holds at most kTile slots AND about kTile/kItemUnits items.
 // Tile status word: [63:62] flag (1 aggregate, 2 inclusive prefix),
 // [61:48] epoch tag, [47:0] value.  Used by the standalone scan kernel
 // (dynamic tile ids) and by the persistent BFS kernel (static tile ids; all
@@ -118,11 +120,12 @@ __device__ __forceinline__ void scan_tile(int64_t tile, int64_t ntiles,
     if (i < nf) {
       scan[i] = run;
       rowbase[i] = rb[k];
-      if (deg[k] > 0) {
-        const int64_t k0 = (run + kTile - 1) / kTile;
-        const int64_t k1 = (run + deg[k] - 1) / kTile;
-        for (int64_t t = k0; t <= k1; ++t) part[t] = (int32_t)i;
-      }
+      // item i occupies units [ub, ub + kItemUnits + deg) of the merged
+      // (items + slots) sequence; it owns every tile starting inside them
+      const int64_t ub = run + (int64_t)kItemUnits * i;
+      const int64_t k0 = (ub + kTile - 1) / kTile;
+      const int64_t k1 = (ub + kItemUnits + deg[k] - 1) / kTile;
+      for (int64_t t = k0; t <= k1; ++t) part[t] = (int32_t)i;
     }
     run += deg[k];
   }
@@ -130,7 +133,8 @@ __device__ __forceinline__ void scan_tile(int64_t tile, int64_t ntiles,
     // the last thread of the last tile holds the grand total
     scan[nf] = run;
     ctr->total = (unsigned long long)run;
-    ctr->ntiles = (unsigned long long)((run + kTile - 1) / kTile);
+    const int64_t units = run + (int64_t)kItemUnits * nf;
+    ctr->ntiles = (unsigned long long)((units + kTile - 1) / kTile);
   }
   __syncthreads();
 }

@@ -166,7 +166,7 @@ int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t*
   GFX_TRY(scratch_t(g, "sssp_fkey2", 2 * n + 64, &fkey2));
   GFX_TRY(scratch_t(g, "q_scan", n + 2, &scan));
   GFX_TRY(scratch_t(g, "q_rowbase", n + 1, &rowbase));
-  GFX_TRY(scratch_t(g, "q_part", g->m / kTile + 4, &part));
+  GFX_TRY(scratch_t(g, "q_part", part_capacity(g->m, g->n), &part));
 
   Counters* C = g->counters;  // C[0]/C[1]: near sizes, C[2]: relax plan, C[3]: far
   auto* pin = static_cast<Counters*>(ctx->pinned);

@@ -210,6 +210,7 @@ class DistBfsStats:
     direction_trace: list = field(default_factory=list)
     per_level: list = field(default_factory=list)
     edges_push: int = 0
+    bytes_alg: int = 0   # SURVEY 8(d) formulas summed over ranks and levels
 
 
 def bfs_partitioned(comm, n: int, m: int, source: int, direction: str = PUSH,
@@ -243,13 +244,19 @@ def bfs_partitioned(comm, n: int, m: int, source: int, direction: str = PUSH,
             outs = [e.push_expand(depth) for e in engines]
             recv = comm.exchange_pairs([o[0] for o in outs])
             local = [e.push_claim(rc, depth) for e, rc in zip(engines, recv)]
-            st.edges_push += comm.allreduce_sum([o[2] for o in outs])
+            edges = comm.allreduce_sum([o[2] for o in outs])
+            st.edges_push += edges
+            work = 20 * nf + 4 * edges
         else:
             for e in engines:
                 e.pull_prepare()
             comm.allgather_frontier()
-            local = [e.pull(depth)[0] for e in engines]
+            res = [e.pull(depth) for e in engines]
+            local = [x[0] for x in res]
+            work = 12 * comm.allreduce_sum([x[2] for x in res]) + \
+                4 * comm.allreduce_sum([x[1] for x in res])
         nout = comm.allreduce_sum(local)
+        st.bytes_alg += work + 8 * nout
         st.per_level.append({"iteration": depth, "mode": mode, "frontier_in": nf,
                              "frontier_out": nout})
         state.mode = mode
