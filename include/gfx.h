@@ -137,6 +137,14 @@ GFX_API int gfx_bfs(gfx_graph* g, int64_t source, int direction, int idempotent,
             int loop, int32_t* labels_d, int32_t* preds_d, gfx_iter_rec* recs,
             int64_t rec_cap, gfx_stats* stats);
 
+/* count BFS runs from sources[0..count) back to back on the device-resident
+ * loop (one launch each, one synchronisation): *ms = device time of all runs.
+ * labels_d/preds_d receive the last run.  Used to measure device throughput
+ * without per-call host round trips. */
+GFX_API int gfx_bfs_batch(gfx_graph* g, const int64_t* sources, int64_t count, int direction,
+                          double do_a, double do_b, int mu_edge_based, int32_t* labels_d,
+                          int32_t* preds_d, float* ms);
+
 /* Host-only replica of reference direction.py:52-61 estimate_mf_mu with the
  * same correctly rounded integer divisions CPython performs (no GPU needed). */
 GFX_API int gfx_estimate_mf_mu(int64_t n, int64_t m, int64_t n_f, int64_t n_u, int mu_edge_based,

@@ -67,6 +67,8 @@ _SIGS = {
     "gfx_graph_trim": (c_int, [c_void_p]),
     "gfx_bfs": (c_int, [c_void_p, c_int64, c_int, c_int, c_int, c_double, c_double, c_int,
                         c_int, c_void_p, c_void_p, POINTER(IterRec), c_int64, POINTER(Stats)]),
+    "gfx_bfs_batch": (c_int, [c_void_p, POINTER(c_int64), c_int64, c_int, c_double, c_double,
+                              c_int, c_void_p, c_void_p, POINTER(c_float)]),
     "gfx_estimate_mf_mu": (c_int, [c_int64, c_int64, c_int64, c_int64, c_int,
                                    POINTER(c_double), POINTER(c_double)]),
     "gfx_sssp": (c_int, [c_void_p, c_int64, c_double, c_void_p, c_void_p, POINTER(IterRec),

@@ -772,9 +772,10 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
   }
 }
 
-int bfs_device_loop(gfx_graph* g, int64_t source, int direction, double do_a, double do_b,
-                    int mu_edge, int32_t* labels, int32_t* preds, gfx_iter_rec* recs,
-                    int64_t rec_cap, gfx_stats* st) {
+// argument block + occupancy for the cooperative level-loop kernel
+static int pbfs_setup(gfx_graph* g, int64_t source, int direction, double do_a, double do_b,
+                      int mu_edge, int32_t* labels, int32_t* preds, PBfsArgs* out,
+                      int* grid_blocks, int* smem_bytes) {
   gfx_ctx* ctx = g->ctx;
   const int64_t n = g->n, W = g->words;
   const bool directed = !(g->flags & GFX_GRAPH_UNDIRECTED);
@@ -824,6 +825,7 @@ int bfs_device_loop(gfx_graph* g, int64_t source, int direction, double do_a, do
   a.do_b = do_b;
   a.source = (int32_t)source;
   a.epoch_base = 0;
+  *out = a;
 
   static int blocks_per_sm = 0;
   const int smem = kWarpScratch * kWarpsPerBlock;
@@ -837,12 +839,26 @@ int bfs_device_loop(gfx_graph* g, int64_t source, int direction, double do_a, do
       return GFX_ECUDA;
     }
   }
+  *grid_blocks = blocks_per_sm * g->ctx->sm_count;
+  *smem_bytes = smem;
+  return GFX_OK;
+}
+
+int bfs_device_loop(gfx_graph* g, int64_t source, int direction, double do_a, double do_b,
+                    int mu_edge, int32_t* labels, int32_t* preds, gfx_iter_rec* recs,
+                    int64_t rec_cap, gfx_stats* st) {
+  gfx_ctx* ctx = g->ctx;
+  PBfsArgs a{};
+  int blocks = 0, smem = 0;
+  GFX_TRY(pbfs_setup(g, source, direction, do_a, do_b, mu_edge, labels, preds, &a, &blocks,
+                     &smem));
+  const int64_t stiles_max = std::max<int64_t>(1, (g->n + kScanTileItems - 1) / kScanTileItems);
   // status words must start clear; the kernel clears what it uses
   GFX_CK(cudaMemsetAsync(a.status, 0, (stiles_max + 1) * 8, ctx->stream));
   void* kargs[] = {&a};
   GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
   GFX_CK(cudaLaunchCooperativeKernel((const void*)k_bfs_persistent,
-                                     dim3(blocks_per_sm * ctx->sm_count), dim3(256), kargs, smem,
+                                     dim3(blocks), dim3(256), kargs, smem,
                                      ctx->stream));
   count_launch();
   GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));
@@ -875,6 +891,33 @@ int bfs_device_loop(gfx_graph* g, int64_t source, int direction, double do_a, do
   return GFX_OK;
 }
 
+// count BFS runs back to back from sources[] (one cooperative launch each, a
+// single synchronisation at the end): device throughput without per-call
+// host round trips.  labels/preds hold the last run.
+int bfs_device_batch(gfx_graph* g, const int64_t* sources, int64_t count, int direction,
+                     double do_a, double do_b, int mu_edge, int32_t* labels, int32_t* preds,
+                     float* ms) {
+  gfx_ctx* ctx = g->ctx;
+  PBfsArgs a{};
+  int blocks = 0, smem = 0;
+  GFX_TRY(pbfs_setup(g, sources[0], direction, do_a, do_b, mu_edge, labels, preds, &a, &blocks,
+                     &smem));
+  const int64_t stiles_max = std::max<int64_t>(1, (g->n + kScanTileItems - 1) / kScanTileItems);
+  GFX_CK(cudaMemsetAsync(a.status, 0, (stiles_max + 1) * 8, ctx->stream));
+  GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  for (int64_t k = 0; k < count; ++k) {
+    a.source = (int32_t)sources[k];
+    void* kargs[] = {&a};
+    GFX_CK(cudaLaunchCooperativeKernel((const void*)k_bfs_persistent, dim3(blocks), dim3(256),
+                                       kargs, smem, ctx->stream));
+    count_launch();
+  }
+  GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  GFX_CK(cudaEventSynchronize(ctx->ev1));
+  GFX_CK(cudaEventElapsedTime(ms, ctx->ev0, ctx->ev1));
+  return GFX_OK;
+}
+
 }  // namespace gfx
 
 using namespace gfx;
@@ -900,6 +943,22 @@ extern "C" int gfx_bfs(gfx_graph* g, int64_t source, int direction, int idempote
   (void)filter_mode;
   return bfs_host_loop(g, source, direction, idempotent != 0, true, do_a, do_b, mu_edge_based,
                        labels_d, preds_d, recs, rec_cap, stats);
+}
+
+extern "C" int gfx_bfs_batch(gfx_graph* g, const int64_t* sources, int64_t count,
+                             int direction, double do_a, double do_b, int mu_edge_based,
+                             int32_t* labels_d, int32_t* preds_d, float* ms) {
+  GFX_REQUIRE(g && sources && count > 0 && labels_d && preds_d && ms,
+              "gfx_bfs_batch: bad argument");
+  for (int64_t k = 0; k < count; ++k)
+    GFX_REQUIRE(sources[k] >= 0 && sources[k] < g->n, "source %lld out of range",
+                (long long)sources[k]);
+  GFX_REQUIRE(direction == GFX_DIR_PUSH || direction == GFX_DIR_PULL || direction == GFX_DIR_AUTO,
+              "unknown direction %d", direction);
+  if (direction == GFX_DIR_AUTO) GFX_REQUIRE(do_a > 0 && do_b > 0, "do_a and do_b must be positive");
+  GFX_CK(cudaSetDevice(g->ctx->device));
+  return bfs_device_batch(g, sources, count, direction, do_a, do_b, mu_edge_based, labels_d,
+                          preds_d, ms);
 }
 
 extern "C" int gfx_estimate_mf_mu(int64_t n, int64_t m, int64_t n_f, int64_t n_u, int mu_edge,

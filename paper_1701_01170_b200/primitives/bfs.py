@@ -98,6 +98,27 @@ def bfs_device(dg, source: int, *, direction: str = PUSH, idempotent: bool = Fal
     return labels, preds, stats_from_records("bfs", recs, st)
 
 
+def bfs_batch(dg, sources, *, direction: str = "auto", do_a: float = 0.001, do_b: float = 0.2,
+              mu_edge_based: bool = False, labels=None, preds=None) -> float:
+    """Run one BFS per source back to back on the device (one synchronisation);
+    returns the device time in ms.  labels/preds hold the last run."""
+    import torch
+
+    n = dg.num_vertices
+    srcs = [int(s) for s in sources]
+    dev = dg.row.device
+    if labels is None:
+        labels = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    if preds is None:
+        preds = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    arr = (ctypes.c_int64 * len(srcs))(*srcs)
+    ms = ctypes.c_float()
+    _native.call("gfx_bfs_batch", dg.handle, arr, len(srcs), _DIRS[direction], float(do_a),
+                 float(do_b), int(bool(mu_edge_based)), _native.ptr(labels), _native.ptr(preds),
+                 ctypes.byref(ms))
+    return ms.value
+
+
 def bfs(g, source: int, idempotent: bool = False, direction: str = PUSH, strategy=None,
         do_a: float = 0.001, do_b: float = 0.2, mu_edge_based: bool = False,
         filter_mode=FilterMode.EXACT, culling=None, params=None,
