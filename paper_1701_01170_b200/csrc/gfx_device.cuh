@@ -58,6 +58,21 @@ __device__ __forceinline__ int32_t ld_stream_i32(const int32_t* p) {
   return v;
 }
 
+// L2 evict-first policy for read-once streams (adjacency / weights), so they
+// do not push the L2-resident bitmaps and label arrays out
+__device__ __forceinline__ unsigned long long l2_evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ int32_t ld_stream_i32(const int32_t* p, unsigned long long pol) {
+  int32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
+               : "=r"(v)
+               : "l"(p), "l"(pol));
+  return v;
+}
+
 __device__ __forceinline__ bool test_bit(const uint32_t* bm, int32_t v) {
   return (bm[v >> 5] >> (v & 31)) & 1u;
 }

@@ -82,6 +82,7 @@ __device__ __forceinline__ void expand_tasks(WarpSmem& W, Op& o, const int32_t* 
                                              int64_t task0, int64_t ntasks) {
   constexpr int B = Op::kBatch;
   const int lane = threadIdx.x & 31;
+  const unsigned long long pol = l2_evict_first_policy();
   int ocnt = 0;
   // software pipeline: the next tile's partition entry and first 32 items
   // are loaded while the current tile's column loads are in flight
@@ -190,8 +191,8 @@ __device__ __forceinline__ void expand_tasks(WarpSmem& W, Op& o, const int32_t* 
           if (j < ch) {
             const int it = W.owner[j];
             const int64_t e = W.delta[it] + s0 + j;
-            d[k] = ld_stream_i32(col + e);
-            if (Op::kWeights) w[Op::kWeights ? k : 0] = ld_stream_i32(wgt + e);
+            d[k] = ld_stream_i32(col + e, pol);
+            if (Op::kWeights) w[Op::kWeights ? k : 0] = ld_stream_i32(wgt + e, pol);
           }
         }
         o.prefetch(d);

@@ -31,35 +31,38 @@ struct SsspRelaxOp {
   static constexpr bool kWeights = true, kSrcVal = true, kEmitEdge = false;
   static constexpr int kBatch = 8;
   unsigned long long* dp;
+  uint32_t* dist;  // 32-bit mirror of dp's distance (half the probe footprint)
   int32_t* stamp;
   int32_t it;
-  unsigned long long cur[kBatch];
-  __device__ int32_t src_value(int32_t v) const { return (int32_t)(dp[v] >> 32); }
+  uint32_t cur[kBatch];
+  __device__ int32_t src_value(int32_t v) const { return (int32_t)dist[v]; }
   __device__ void prefetch(const int32_t* d) {
 #pragma unroll
-    for (int u = 0; u < kBatch; ++u) cur[u] = d[u] >= 0 ? dp[d[u]] : 0ull;
+    for (int u = 0; u < kBatch; ++u) cur[u] = d[u] >= 0 ? dist[d[u]] : 0u;
   }
   // atomic_min relax (operators.py:111-124): emit d once per iteration when
   // its distance strictly improved
   __device__ bool visit(int u, int32_t d, int32_t s, int32_t w, int32_t sdist, int64_t) {
     const unsigned long long nd = (unsigned long long)(uint32_t)sdist + (uint32_t)w;
-    if (nd >= (cur[u] >> 32)) return false;
+    if (nd >= cur[u]) return false;
     const unsigned long long key = (nd << 32) | (uint32_t)s;
     const unsigned long long old = atomicMin(&dp[d], key);
     if ((old >> 32) <= nd) return false;
+    atomicMin(&dist[d], (uint32_t)nd);
     return atomicExch(&stamp[d], it) != it;
   }
 };
 
-__global__ void k_sssp_seed(unsigned long long* dp, int32_t src, int32_t* near) {
+__global__ void k_sssp_seed(unsigned long long* dp, uint32_t* dist, int32_t src, int32_t* near) {
   dp[src] = 0xFFFFFFFFull;  // dist 0, pred -1
+  dist[src] = 0u;
   near[0] = src;
 }
 
 // split the improved vertices against the threshold (near_far.py:40-57)
 __global__ void __launch_bounds__(256)
     k_sssp_split(const int32_t* __restrict__ touched, const unsigned long long* __restrict__ n_d,
-                 const unsigned long long* __restrict__ dp, double threshold,
+                 const uint32_t* __restrict__ dist, double threshold,
                  int32_t* __restrict__ near, unsigned long long* __restrict__ near_len,
                  int32_t* __restrict__ far, int32_t* __restrict__ far_key,
                  unsigned long long* __restrict__ far_len) {
@@ -73,7 +76,7 @@ __global__ void __launch_bounds__(256)
     bool valid = i < n, is_near = false;
     if (valid) {
       v = touched[i];
-      key = (int32_t)(dp[v] >> 32);
+      key = (int32_t)dist[v];
       is_near = (double)key < threshold;
     }
     const unsigned nm = __ballot_sync(0xffffffffu, valid && is_near);
@@ -100,7 +103,7 @@ __global__ void __launch_bounds__(256)
 // (capacity compaction; everything fresh stays far).
 __global__ void __launch_bounds__(256)
     k_sssp_refar(const int32_t* __restrict__ far, const int32_t* __restrict__ far_key, int64_t n,
-                 const unsigned long long* __restrict__ dp, double threshold, int split,
+                 const uint32_t* __restrict__ dist, double threshold, int split,
                  int32_t* __restrict__ near, unsigned long long* __restrict__ near_len,
                  int32_t* __restrict__ far2, int32_t* __restrict__ far2_key,
                  unsigned long long* __restrict__ far2_len) {
@@ -113,7 +116,7 @@ __global__ void __launch_bounds__(256)
     if (i < n) {
       v = far[i];
       key = far_key[i];
-      const bool fresh = (int32_t)(dp[v] >> 32) == key;
+      const bool fresh = (int32_t)dist[v] == key;
       if (fresh) {
         if (split && (double)key < threshold) to_near = true; else to_far = true;
       }
@@ -153,9 +156,11 @@ int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t*
   gfx_ctx* ctx = g->ctx;
   const int64_t n = g->n;
   unsigned long long* dp;
+  uint32_t* dist32;
   int32_t *stamp, *nearA, *nearB, *touched, *far, *fkey, *far2, *fkey2, *part;
   int64_t *scan, *rowbase;
   GFX_TRY(scratch_t(g, "sssp_dp", n, &dp));
+  GFX_TRY(scratch_t(g, "sssp_dist", n, &dist32));
   GFX_TRY(scratch_t(g, "sssp_stamp", n, &stamp));
   GFX_TRY(scratch_t(g, "q_order", n + 1, &nearA));
   GFX_TRY(scratch_t(g, "sssp_nearB", n + 1, &nearB));
@@ -174,9 +179,10 @@ int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t*
 
   GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
   GFX_CK(cudaMemsetAsync(dp, 0xFF, n * sizeof(unsigned long long), ctx->stream));
+  GFX_CK(cudaMemsetAsync(dist32, 0xFF, n * sizeof(uint32_t), ctx->stream));
   GFX_CK(cudaMemsetAsync(stamp, 0, n * sizeof(int32_t), ctx->stream));
   GFX_CK(cudaMemsetAsync(C, 0, 4 * sizeof(Counters), ctx->stream));
-  GFX_LAUNCH(k_sssp_seed, 1, 1, 0, ctx->stream, dp, (int32_t)source, nearA);
+  GFX_LAUNCH(k_sssp_seed, 1, 1, 0, ctx->stream, dp, dist32, (int32_t)source, nearA);
   // near count lives in C[cur].out_len
   int curq = 0;
   unsigned long long one = 1;
@@ -193,7 +199,7 @@ int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t*
       GFX_CK(cudaMemsetAsync(nxt, 0, sizeof(Counters), ctx->stream));
       GFX_CK(cudaMemsetAsync(&C[3].aux1, 0, 8, ctx->stream));
       GFX_LAUNCH(k_sssp_refar, grid_for(nfar, 256, grid), 256, 0, ctx->stream, far, fkey, nfar,
-                 dp, threshold, 1, nearq[curq], &nxt->out_len, far2, fkey2, &C[3].aux1);
+                 dist32, threshold, 1, nearq[curq], &nxt->out_len, far2, fkey2, &C[3].aux1);
       GFX_CK(cudaMemcpyAsync(pin, C, 4 * sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
       GFX_CK(cudaStreamSynchronize(ctx->stream));
       bytes_total += 8 * nfar;
@@ -211,11 +217,11 @@ int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t*
     Counters* nxt = &C[curq ^ 1];
     GFX_CK(cudaMemsetAsync(&C[2], 0, sizeof(Counters), ctx->stream));
     GFX_CK(cudaMemsetAsync(nxt, 0, sizeof(Counters), ctx->stream));
-    SsspRelaxOp op{dp, stamp, (int32_t)it, {}};
+    SsspRelaxOp op{dp, dist32, stamp, (int32_t)it, {}};
     GFX_TRY(lb_advance(g, nearq[curq], &cur->out_len, nnear, &C[2], scan, rowbase, part, op,
                        touched, &C[2].out_len));
     GFX_LAUNCH(k_sssp_split, grid_for(n, 256, grid), 256, 0, ctx->stream, touched, &C[2].out_len,
-               dp, threshold, nearq[curq ^ 1], &nxt->out_len, far, fkey, &C[3].aux0);
+               dist32, threshold, nearq[curq ^ 1], &nxt->out_len, far, fkey, &C[3].aux0);
     GFX_CK(cudaGetLastError());
     if (ctx->timing) GFX_CK(cudaEventRecord(ctx->lev1, ctx->stream));
     GFX_CK(cudaMemcpyAsync(pin, C, 4 * sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
@@ -246,7 +252,7 @@ int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t*
       // capacity guard: drop stale far entries (each vertex then appears once)
       GFX_CK(cudaMemsetAsync(&C[3].aux1, 0, 8, ctx->stream));
       GFX_LAUNCH(k_sssp_refar, grid_for(nfar, 256, grid), 256, 0, ctx->stream, far, fkey, nfar,
-                 dp, threshold, 0, nearq[curq], &C[2].aux2, far2, fkey2, &C[3].aux1);
+                 dist32, threshold, 0, nearq[curq], &C[2].aux2, far2, fkey2, &C[3].aux1);
       GFX_CK(cudaMemcpyAsync(pin, C, 4 * sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
       GFX_CK(cudaStreamSynchronize(ctx->stream));
       nfar = (int64_t)pin[3].aux1;
