@@ -10,8 +10,10 @@
 //   items : lanes load up to 32 overlapping items (scan, delta = row[v] -
 //           scan, v) into the warp's shared-memory slice and mark each
 //           item's first slot;
-//   owner : a warp-wide inclusive max-scan over the 512 markers (16 per lane
-//           + shuffles) gives every slot its owning item;
+//   owner : chunks whose items average >= kItemModeSlots slots are walked
+//           item by item (no lookup); otherwise a warp-wide inclusive
+//           max-scan over the markers (16 per lane + shuffles) gives every
+//           slot its owning item;
 //   visit : lane l handles slots l, l+32, ... -- consecutive lanes read
 //           consecutive column ids (coalesced) -- with Op::kBatch column
 //           loads in flight per lane before the functor runs;
@@ -41,6 +43,7 @@ constexpr int kWarpsPerBlock = kExpandBlock / 32;
 constexpr int kLaneSlots = kTile / 32;  // 16 slots per lane per tile
 constexpr int kOutCap = 640;            // per-warp staged output (flushed past kOutCap - 32*kBatch)
 constexpr int kVisitBatch = 8;          // default Op::kBatch
+constexpr int kItemModeSlots = 24;      // chunks averaging >= this many slots per item walk items
 
 struct WarpSmem {
   int64_t delta[32];     // row[v] - scan[i]: col index = delta + global slot
@@ -141,6 +144,54 @@ __device__ __forceinline__ void expand_tasks(WarpSmem& W, Op& o, const int32_t* 
       const int last = 31 - __clz(vm);
       const int ch = (int)(__shfl_sync(0xffffffffu, hi, last) - s0);
       if (ch <= cl) continue;
+      const unsigned hm = __ballot_sync(0xffffffffu, has);
+      if ((ch - cl) >= kItemModeSlots * __popc(hm)) {
+        // long segments: walk the items one by one, lanes over consecutive
+        // slots -- no owner lookup at all (the common case on hub frontiers)
+        const int32_t my_sv = (Op::kSrcVal && has) ? o.src_value(v) : 0;
+        const int64_t my_del = rb - sc;
+        unsigned rem = hm;
+        while (rem) {
+          const int k = __ffs(rem) - 1;
+          rem &= rem - 1;
+          const int64_t klo = __shfl_sync(0xffffffffu, lo, k);
+          const int64_t khi = __shfl_sync(0xffffffffu, hi, k);
+          const int64_t kdel = __shfl_sync(0xffffffffu, my_del, k);
+          const int32_t ksrc = __shfl_sync(0xffffffffu, v, k);
+          const int32_t ksv = Op::kSrcVal ? __shfl_sync(0xffffffffu, my_sv, k) : 0;
+          const int32_t* cbase = col + kdel + klo + lane;
+          const int32_t* wbase = Op::kWeights ? wgt + kdel + klo + lane : nullptr;
+          const int klen = (int)(khi - klo);
+          for (int jb = 0; jb < klen; jb += 32 * B) {
+            int32_t d[B];
+            int32_t w[Op::kWeights ? B : 1];
+            const int lim = klen - jb - lane;  // this lane's slots remaining
+#pragma unroll
+            for (int q = 0; q < B; ++q) {
+              d[q] = -1;
+              if (Op::kWeights) w[Op::kWeights ? q : 0] = 0;
+              if (q * 32 < lim) {
+                d[q] = ld_stream_i32(cbase + jb + q * 32, pol);
+                if (Op::kWeights) w[Op::kWeights ? q : 0] = ld_stream_i32(wbase + jb + q * 32, pol);
+              }
+            }
+            o.prefetch(d);
+#pragma unroll
+            for (int q = 0; q < B; ++q) {
+              bool emit = false;
+              const int64_t e = Op::kEmitEdge ? kdel + klo + jb + q * 32 + lane : 0;
+              if (d[q] >= 0)
+                emit = o.visit(q, d[q], ksrc, Op::kWeights ? w[Op::kWeights ? q : 0] : 1, ksv, e);
+              const unsigned em = __ballot_sync(0xffffffffu, emit);
+              if (emit)
+                W.obuf[ocnt + __popc(em & ((1u << lane) - 1))] = Op::kEmitEdge ? (int32_t)e : d[q];
+              ocnt += __popc(em);
+            }
+            if (ocnt > kOutCap - 32 * B) warp_flush(W, ocnt, out, out_len);
+          }
+        }
+        continue;
+      }
       __syncwarp();
       for (int j = cl + lane; j < ch; j += 32) W.owner[j] = -1;
       __syncwarp();
@@ -220,7 +271,7 @@ __device__ __forceinline__ void expand_tasks(WarpSmem& W, Op& o, const int32_t* 
 }
 
 template <class Op>
-__global__ void __launch_bounds__(kExpandBlock)
+__global__ void __launch_bounds__(kExpandBlock, 2)
     k_lb_expand(const int32_t* __restrict__ F, const unsigned long long* __restrict__ nf_d,
                 const int64_t* __restrict__ scan, const int64_t* __restrict__ rowbase,
                 const int32_t* __restrict__ part, const Counters* __restrict__ plan,
