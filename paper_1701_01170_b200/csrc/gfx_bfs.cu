@@ -40,6 +40,7 @@ namespace gfx {
 struct BfsClaimOp {
   static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
   static constexpr int kBatch = kVisitBatch;
+  static constexpr int kMinBlocks = 3;
   uint32_t* visited;
   int32_t* labels;
   int32_t* preds;
@@ -63,6 +64,7 @@ struct BfsClaimOp {
 struct BfsIdempOp {
   static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
   static constexpr int kBatch = kVisitBatch;
+  static constexpr int kMinBlocks = 3;
   const uint32_t* visited;
   int32_t* labels;
   int32_t* preds;

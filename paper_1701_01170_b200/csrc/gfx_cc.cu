@@ -54,6 +54,7 @@ __device__ __forceinline__ void cc_unite(int32_t* p, int32_t a, int32_t b) {
 struct CcHookOp {
   static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
   static constexpr int kBatch = kVisitBatch;
+  static constexpr int kMinBlocks = 2;
   int32_t* parent;
   __device__ int32_t src_value(int32_t) const { return 0; }
   __device__ void prefetch(const int32_t*) {}

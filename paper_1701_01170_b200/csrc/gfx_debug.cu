@@ -15,6 +15,7 @@ template <int KB>
 struct StreamOpT {
   static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
   static constexpr int kBatch = KB;
+  static constexpr int kMinBlocks = 3;
   int32_t sentinel;
   __device__ int32_t src_value(int32_t) const { return 0; }
   __device__ void prefetch(const int32_t*) {}
@@ -27,6 +28,7 @@ struct StreamOpT {
 struct ProbeOp {
   static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
   static constexpr int kBatch = kVisitBatch;
+  static constexpr int kMinBlocks = 3;
   const uint32_t* visited;
   uint32_t wv[kBatch];
   __device__ int32_t src_value(int32_t) const { return 0; }
@@ -43,6 +45,7 @@ struct ProbeOp {
 struct ClaimOp {
   static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
   static constexpr int kBatch = kVisitBatch;
+  static constexpr int kMinBlocks = 3;
   uint32_t* visited;
   int32_t* labels;
   int32_t depth;

@@ -74,6 +74,7 @@ __global__ void k_part_copy(const int64_t* __restrict__ row, const int32_t* __re
 struct DistClaimOp {
   static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
   static constexpr int kBatch = kVisitBatch;
+  static constexpr int kMinBlocks = 3;
   uint32_t* visited;   // local bits
   uint32_t* sent;      // global bits
   int32_t* sent_src;   // global ids -> source of the emitted pair
@@ -430,11 +431,9 @@ int gfx_dbfs_push_expand(gfx_dbfs* db, int32_t depth, int64_t* send_counts, int6
   GFX_TRY(lb_advance(g, order + db->q_off, &C[0].out_len, db->nf, &C[1], scan, rowbase, part, op,
                      emit, &C[1].out_len));
   // pass 0: per-owner counts
-  unsigned long long* counts = reinterpret_cast<unsigned long long*>(&C[2]);  // up to 8
   unsigned long long* cnt64 = nullptr;
   GFX_TRY(scratch_t(g, "d_counts", 2 * 64, &cnt64));
   GFX_CK(cudaMemsetAsync(cnt64, 0, 2 * 64 * 8, ctx->stream));
-  (void)counts;
   const int grid = ctx->sm_count * 4;
   GFX_LAUNCH((k_dist_bucket<0>), grid, 256, 0, ctx->stream, emit, &C[1].out_len, db->P, db->r,
              cnt64, nullptr, sent_src, sent, db->send, nullptr, nullptr);

@@ -27,6 +27,7 @@
 //   static constexpr bool kSrcVal;     per-item src_value(v)
 //   static constexpr bool kEmitEdge;   emit edge ids instead of dst ids
 //   static constexpr int  kBatch;      slots in flight per lane (divides 16)
+//   static constexpr int  kMinBlocks;  CTAs per SM the register budget targets
 //   __device__ int32_t src_value(int32_t v) const;
 //   __device__ void prefetch(const int32_t* d);       // d[kBatch]
 //   __device__ bool visit(int u, int32_t dst, int32_t src, int32_t w,
@@ -271,7 +272,7 @@ __device__ __forceinline__ void expand_tasks(WarpSmem& W, Op& o, const int32_t* 
 }
 
 template <class Op>
-__global__ void __launch_bounds__(kExpandBlock, 2)
+__global__ void __launch_bounds__(kExpandBlock, Op::kMinBlocks)
     k_lb_expand(const int32_t* __restrict__ F, const unsigned long long* __restrict__ nf_d,
                 const int64_t* __restrict__ scan, const int64_t* __restrict__ rowbase,
                 const int32_t* __restrict__ part, const Counters* __restrict__ plan,

@@ -149,46 +149,43 @@ __global__ void k_upper_counts(const int64_t* __restrict__ row, const int32_t* _
     cnt[v] = row[v + 1] - upper_start(row, col, v);
 }
 
-// upper slots of v get lo + bounded(u32[rank]) with rank = base[v] + k
+// upper slots of v get lo + bounded(u32[rank]) with rank = base[v] + k.
+// One warp per row: lane l takes ranks base+l, base+l+32, ...; it jumps once
+// to its first draw, then every 32 ranks = 16 draws is one precomputed jump.
 __global__ void k_upper_weights(const int64_t* __restrict__ row, const int32_t* __restrict__ col,
                                 int64_t n, const int64_t* __restrict__ base, uint64_t s_hi,
                                 uint64_t s_lo, uint64_t i_hi, uint64_t i_lo, int64_t lo_w,
                                 uint64_t range1, int32_t* __restrict__ w) {
   const u128 inc = mk128(i_hi, i_lo);
-  const u128 mult = pcg_mult();
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
+  const u128 s0 = mk128(s_hi, s_lo);
+  const Jump j16 = jump_params(16, inc);
+  const int lane = threadIdx.x & 31;
+  for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < n;
+       v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t us = upper_start(row, col, v), ue = row[v + 1];
-    if (us == ue) continue;
-    int64_t rank = base[v];
-    // state after (rank/2) draws; the next draw yields u32 pair (2k, 2k+1)
-    u128 s = apply_jump(jump_params((uint64_t)(rank >> 1), inc), mk128(s_hi, s_lo));
-    uint64_t cur = 0;
-    if (rank & 1) {  // starts on the high half of draw rank/2
-      s = s * mult + inc;
-      cur = pcg_out(s);
-    }
-    for (int64_t e = us; e < ue; ++e, ++rank) {
-      uint32_t x;
-      if (!(rank & 1)) {
-        s = s * mult + inc;
-        cur = pcg_out(s);
-        x = (uint32_t)cur;
-      } else {
-        x = (uint32_t)(cur >> 32);
-      }
+    if (us + lane >= ue) continue;
+    const int64_t rank = base[v] + lane;
+    // state after rank/2 draws; one more step yields draw rank/2
+    u128 s = apply_jump(jump_params((uint64_t)(rank >> 1), inc), s0);
+    const bool high = rank & 1;
+    for (int64_t e = us + lane; e < ue; e += 32) {
+      const uint64_t x64 = pcg_out(s * pcg_mult() + inc);
+      const uint32_t x = high ? (uint32_t)(x64 >> 32) : (uint32_t)x64;
       w[e] = (int32_t)(lo_w + (int64_t)(((uint64_t)x * range1) >> 32));
+      s = apply_jump(j16, s);
     }
   }
 }
 
-// lower slots (s > d) copy the weight of their mirror slot (d -> s)
+// lower slots (s > d) copy the weight of their mirror slot (d -> s); one
+// warp per row, lanes binary-search their own mirrors
 __global__ void k_lower_weights(const int64_t* __restrict__ row, const int32_t* __restrict__ col,
                                 int64_t n, int32_t* __restrict__ w) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < n;
+       v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t us = upper_start(row, col, v);
-    for (int64_t e = row[v]; e < us; ++e) {
+    for (int64_t e = row[v] + lane; e < us; e += 32) {
       const int32_t d = col[e];
       int64_t lo = row[d], hi = row[d + 1];
       while (lo < hi) {
@@ -309,9 +306,10 @@ extern "C" int gfx_assign_weights(gfx_graph* g, int64_t lo, int64_t hi, uint64_t
   if (range1 == 1) {
     GFX_TRY(fill_i32(ctx, w_d, (int32_t)lo, g->m));
   } else {
-    GFX_LAUNCH(k_upper_weights, grid, 256, 0, ctx->stream, g->row, g->col, n, base, state_hi, state_lo,
-                                                   inc_hi, inc_lo, lo, range1, w_d);
-    GFX_LAUNCH(k_lower_weights, grid, 256, 0, ctx->stream, g->row, g->col, n, w_d);
+    const int wgrid = grid_for(n * 32, 256, ctx->sm_count * 16);
+    GFX_LAUNCH(k_upper_weights, wgrid, 256, 0, ctx->stream, g->row, g->col, n, base, state_hi,
+               state_lo, inc_hi, inc_lo, lo, range1, w_d);
+    GFX_LAUNCH(k_lower_weights, wgrid, 256, 0, ctx->stream, g->row, g->col, n, w_d);
   }
   GFX_CK(cudaGetLastError());
   GFX_CK(cudaStreamSynchronize(ctx->stream));

@@ -30,6 +30,7 @@ namespace gfx {
 struct SsspRelaxOp {
   static constexpr bool kWeights = true, kSrcVal = true, kEmitEdge = false;
   static constexpr int kBatch = 8;
+  static constexpr int kMinBlocks = 2;
   unsigned long long* dp;
   uint32_t* dist;  // 32-bit mirror of dp's distance (half the probe footprint)
   int32_t* stamp;
