@@ -44,7 +44,7 @@ constexpr int kWarpsPerBlock = kExpandBlock / 32;
 constexpr int kLaneSlots = kTile / 32;  // 16 slots per lane per tile
 constexpr int kOutCap = 640;            // per-warp staged output (flushed past kOutCap - 32*kBatch)
 constexpr int kVisitBatch = 8;          // default Op::kBatch
-constexpr int kItemModeSlots = 24;      // chunks averaging >= this many slots per item walk items
+constexpr int kItemModeSlots = 128;     // chunks averaging >= this many slots per item walk items
 
 struct WarpSmem {
   int64_t delta[32];     // row[v] - scan[i]: col index = delta + global slot
