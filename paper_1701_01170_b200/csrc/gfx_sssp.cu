@@ -10,8 +10,10 @@
 //   dp     uint64[n]  (dist << 32 | pred): one 64-bit atomicMin settles the
 //                     distance and a valid predecessor together, so preds are
 //                     always consistent with the final distances
-//   stamp  int32[n]   iteration id of the last enqueue (dedup: each improved
-//                     vertex is enqueued once per iteration, sssp.py:112-115)
+//   dist   uint32[n]  32-bit mirror of dp's distance: the probe array (L2-resident)
+//   mark   uint32[n/32] enqueued-this-iteration bits (the reference's stamp,
+//                     sssp.py:112-115): each improved vertex is enqueued once
+//                     per iteration; the split kernel clears the bits it reads
 //   near[2] int32[n]  near queues (double buffer)
 //   touched int32[n]  vertices improved this iteration
 //   far / far_key     far pile with enqueue keys, capacity 2n (compacted when
@@ -20,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "gfx_device.cuh"
 #include "gfx_expand.cuh"
@@ -29,12 +32,11 @@ namespace gfx {
 
 struct SsspRelaxOp {
   static constexpr bool kWeights = true, kSrcVal = true, kEmitEdge = false;
-  static constexpr int kBatch = 8;
-  static constexpr int kMinBlocks = 2;
+  static constexpr int kBatch = 4;
+  static constexpr int kMinBlocks = 3;
   unsigned long long* dp;
   uint32_t* dist;  // 32-bit mirror of dp's distance (half the probe footprint)
-  int32_t* stamp;
-  int32_t it;
+  uint32_t* mark;  // enqueued-this-iteration bitmap
   uint32_t cur[kBatch];
   __device__ int32_t src_value(int32_t v) const { return (int32_t)dist[v]; }
   __device__ void prefetch(const int32_t* d) {
@@ -50,7 +52,8 @@ struct SsspRelaxOp {
     const unsigned long long old = atomicMin(&dp[d], key);
     if ((old >> 32) <= nd) return false;
     atomicMin(&dist[d], (uint32_t)nd);
-    return atomicExch(&stamp[d], it) != it;
+    const uint32_t bit = 1u << (d & 31);
+    return !(atomicOr(&mark[d >> 5], bit) & bit);
   }
 };
 
@@ -63,7 +66,7 @@ __global__ void k_sssp_seed(unsigned long long* dp, uint32_t* dist, int32_t src,
 // split the improved vertices against the threshold (near_far.py:40-57)
 __global__ void __launch_bounds__(256)
     k_sssp_split(const int32_t* __restrict__ touched, const unsigned long long* __restrict__ n_d,
-                 const uint32_t* __restrict__ dist, double threshold,
+                 const uint32_t* __restrict__ dist, uint32_t* __restrict__ mark, double threshold,
                  int32_t* __restrict__ near, unsigned long long* __restrict__ near_len,
                  int32_t* __restrict__ far, int32_t* __restrict__ far_key,
                  unsigned long long* __restrict__ far_len) {
@@ -78,6 +81,7 @@ __global__ void __launch_bounds__(256)
     if (valid) {
       v = touched[i];
       key = (int32_t)dist[v];
+      atomicAnd(&mark[v >> 5], ~(1u << (v & 31)));  // re-arm for the next iteration
       is_near = (double)key < threshold;
     }
     const unsigned nm = __ballot_sync(0xffffffffu, valid && is_near);
@@ -152,17 +156,48 @@ __global__ void k_sssp_unpack(const unsigned long long* __restrict__ dp, int64_t
   }
 }
 
+// keep the 32-bit distance array (the random-probe target) L2-resident while
+// the adjacency and weights stream through with evict-first hints
+static void l2_persist(gfx_ctx* ctx, void* base, size_t bytes, bool on) {
+  static size_t max_persist = (size_t)-1;
+  if (max_persist == (size_t)-1) {
+    cudaDeviceProp prop{};
+    if (cudaGetDeviceProperties(&prop, ctx->device) != cudaSuccess) {
+      max_persist = 0;
+    } else {
+      max_persist = (size_t)prop.persistingL2CacheMaxSize;
+      if (max_persist) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, max_persist);
+    }
+    cudaGetLastError();
+  }
+  if (!max_persist || getenv("GFX_NO_L2_PERSIST")) return;
+  cudaStreamAttrValue attr{};
+  if (on) {
+    attr.accessPolicyWindow.base_ptr = base;
+    attr.accessPolicyWindow.num_bytes = bytes < max_persist ? bytes : max_persist;
+    attr.accessPolicyWindow.hitRatio = 1.0f;
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  } else {
+    attr.accessPolicyWindow.num_bytes = 0;
+  }
+  cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &attr);
+  if (!on) cudaCtxResetPersistingL2Cache();
+  cudaGetLastError();
+}
+
 int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t* preds,
              gfx_iter_rec* recs, int64_t rec_cap, gfx_stats* st) {
   gfx_ctx* ctx = g->ctx;
   const int64_t n = g->n;
   unsigned long long* dp;
   uint32_t* dist32;
-  int32_t *stamp, *nearA, *nearB, *touched, *far, *fkey, *far2, *fkey2, *part;
+  uint32_t* mark;
+  int32_t *nearA, *nearB, *touched, *far, *fkey, *far2, *fkey2, *part;
   int64_t *scan, *rowbase;
   GFX_TRY(scratch_t(g, "sssp_dp", n, &dp));
   GFX_TRY(scratch_t(g, "sssp_dist", n, &dist32));
-  GFX_TRY(scratch_t(g, "sssp_stamp", n, &stamp));
+  GFX_TRY(scratch_t(g, "sssp_mark", g->words + 1, &mark));
   GFX_TRY(scratch_t(g, "q_order", n + 1, &nearA));
   GFX_TRY(scratch_t(g, "sssp_nearB", n + 1, &nearB));
   GFX_TRY(scratch_t(g, "sssp_touched", n + 1, &touched));
@@ -178,10 +213,11 @@ int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t*
   auto* pin = static_cast<Counters*>(ctx->pinned);
   const int grid = ctx->sm_count * 8;
 
+  l2_persist(ctx, dist32, n * sizeof(uint32_t), true);
   GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
   GFX_CK(cudaMemsetAsync(dp, 0xFF, n * sizeof(unsigned long long), ctx->stream));
   GFX_CK(cudaMemsetAsync(dist32, 0xFF, n * sizeof(uint32_t), ctx->stream));
-  GFX_CK(cudaMemsetAsync(stamp, 0, n * sizeof(int32_t), ctx->stream));
+  GFX_CK(cudaMemsetAsync(mark, 0, (g->words + 1) * sizeof(uint32_t), ctx->stream));
   GFX_CK(cudaMemsetAsync(C, 0, 4 * sizeof(Counters), ctx->stream));
   GFX_LAUNCH(k_sssp_seed, 1, 1, 0, ctx->stream, dp, dist32, (int32_t)source, nearA);
   // near count lives in C[cur].out_len
@@ -218,11 +254,11 @@ int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t*
     Counters* nxt = &C[curq ^ 1];
     GFX_CK(cudaMemsetAsync(&C[2], 0, sizeof(Counters), ctx->stream));
     GFX_CK(cudaMemsetAsync(nxt, 0, sizeof(Counters), ctx->stream));
-    SsspRelaxOp op{dp, dist32, stamp, (int32_t)it, {}};
+    SsspRelaxOp op{dp, dist32, mark, {}};
     GFX_TRY(lb_advance(g, nearq[curq], &cur->out_len, nnear, &C[2], scan, rowbase, part, op,
                        touched, &C[2].out_len));
     GFX_LAUNCH(k_sssp_split, grid_for(n, 256, grid), 256, 0, ctx->stream, touched, &C[2].out_len,
-               dist32, threshold, nearq[curq ^ 1], &nxt->out_len, far, fkey, &C[3].aux0);
+               dist32, mark, threshold, nearq[curq ^ 1], &nxt->out_len, far, fkey, &C[3].aux0);
     GFX_CK(cudaGetLastError());
     if (ctx->timing) GFX_CK(cudaEventRecord(ctx->lev1, ctx->stream));
     GFX_CK(cudaMemcpyAsync(pin, C, 4 * sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
@@ -263,6 +299,7 @@ int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t*
     }
   }
   GFX_LAUNCH(k_sssp_unpack, grid_for(n, 256, grid), 256, 0, ctx->stream, dp, n, dist, preds);
+  l2_persist(ctx, nullptr, 0, false);
   GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));
   GFX_CK(cudaEventSynchronize(ctx->ev1));
   float ms = 0.f;

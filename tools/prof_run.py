@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--runs", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--delta", type=float, default=32)
+    ap.add_argument("--timing", action="store_true", help="per-iteration CUDA events")
     a = ap.parse_args()
     import torch
 
@@ -36,6 +37,8 @@ def main():
         fn = lambda: sssp_device(dg, 0, delta=a.delta)
     else:
         raise SystemExit(f"unknown primitive {a.prim}")
+    if a.timing:
+        dg.ctx.set_timing(True)
     for _ in range(a.warmup):
         fn()
     torch.cuda.synchronize()
