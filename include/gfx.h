@@ -189,8 +189,10 @@ GFX_API int gfx_segmented_intersect(gfx_graph* g, const int32_t* u_d, const int3
 #define GFX_FN_BFS_IDEMP 2   /* bfs.py:113-116 */
 #define GFX_FN_SSSP_RELAX 3  /* sssp.py:95-103 */
 #define GFX_FN_TC_ORIENT 4   /* tc.py:57-59 */
-#define GFX_FN_LABEL_EQ 5    /* vertex_cond labels[v] == value */
-#define GFX_FN_LABEL_NE 6    /* vertex_cond labels[v] != value */
+#define GFX_FN_LABEL_EQ 5    /* cond / vertex_cond labels[x] == value */
+#define GFX_FN_LABEL_NE 6    /* cond / vertex_cond labels[x] != value */
+#define GFX_FN_SET_LABEL 7   /* compute: labels[v] = value */
+#define GFX_FN_ADD_I64 8     /* compute: acc[v] += value (atomic_add, operators.py:127-128) */
 
 typedef struct gfx_functor_args {
   int32_t* labels_d;   /* int32 labels / distances */
@@ -214,6 +216,15 @@ GFX_API int gfx_advance(gfx_graph* g, const int32_t* fin_d, int64_t nin, int kin
 GFX_API int gfx_filter(gfx_graph* g, const int32_t* fin_d, int64_t nin, int mode,
                int functor_id, const gfx_functor_args* args, int64_t domain,
                int32_t* fout_d, int64_t* nout);
+/* compute (operators.py:528-533): apply a registry functor to every item,
+ * multiplicity included (acc_d: int64 array for GFX_FN_ADD_I64) */
+GFX_API int gfx_compute(gfx_graph* g, const int32_t* fin_d, int64_t nin, int functor_id,
+                        const gfx_functor_args* args, int64_t* acc_d);
+/* intersection elements per pair, in pair order, ascending within a pair
+ * (IntersectResult.intersections); offsets_d = exclusive scan of counts */
+GFX_API int gfx_segmented_intersect_list(gfx_graph* g, const int32_t* u_d, const int32_t* v_d,
+                                         int64_t num_pairs, const int64_t* offsets_d,
+                                         int32_t* out_d);
 
 /* ---- bit-exact R-MAT + canonical CSR builder ----------------------------
  * (reference generators.py:22-52, graph.py:158-203, graph.py:227-246)

@@ -110,6 +110,41 @@ def run_kat():
     print("kat done", len(graphs))
 
 
+def run_suite(stride: int = 5):
+    """Every stride-th graph of the reference acceptance suite
+    (pkg/tests/_graphs.py:55-91 build_suite(per_family=200, seed=20240)),
+    with the outputs acceptance criterion 1 compares (test_acceptance.py:89-109)
+    plus the DO trace (criterion 3) and idempotent labels (criterion 6)."""
+    from _graphs import build_suite
+
+    suite = build_suite(per_family=200)
+    picked = [sg for i, sg in enumerate(suite) if i % stride == 0 or sg.g.num_vertices >= 2048]
+    arrays, meta = {}, []
+    for i, sg in enumerate(picked):
+        p = f"g{i}_"
+        g, gw, src = sg.g, sg.weighted, sg.source
+        arrays[p + "row"] = g.row_offsets.astype(np.int64)
+        arrays[p + "col"] = g.column_indices.astype(np.int32)
+        arrays[p + "w"] = gw.edge_weights.astype(np.int8)
+        b = gx.bfs(g, src)
+        arrays[p + "bfs"] = b.labels
+        bd = gx.bfs(g, src, direction="auto")
+        arrays[p + "sssp"] = gx.sssp(gw, src).labels
+        arrays[p + "bc"] = gx.bc(g, src).bc_values
+        arrays[p + "cc"] = canon_cc(gx.cc(g).component)
+        arrays[p + "pr4"] = gx.pagerank(g, epsilon=0.0, max_iters=4).rank
+        t = gx.tc(g)
+        arrays[p + "tc_counts"] = t.per_edge_counts.astype(np.int32)
+        meta.append({"name": sg.name, "family": sg.family, "n": g.num_vertices,
+                     "m": g.num_edges, "source": int(src), "tc_total": int(t.total_triangles),
+                     "bfs_auto_trace": trace_rows(bd.stats.direction_trace)})
+    OUT.mkdir(parents=True, exist_ok=True)
+    np.savez_compressed(OUT / "suite_graphs.npz", **arrays)
+    (OUT / "suite_graphs.json").write_text(json.dumps(
+        {"numpy": np.__version__, "stride": stride, "graphs": meta}))
+    print("suite done", len(picked))
+
+
 def run_rmat(scale: int):
     t0 = time.time()
     rec = {"scale": scale, "edge_factor": 16, "seed": 0, "numpy": np.__version__}
@@ -204,6 +239,8 @@ if __name__ == "__main__":
     os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
     if sys.argv[1] == "kat":
         run_kat()
+    elif sys.argv[1] == "suite":
+        run_suite(int(sys.argv[2]) if len(sys.argv) > 2 else 5)
     else:
         for s in sys.argv[2:]:
             run_rmat(int(s))

@@ -22,7 +22,8 @@ DIR_PUSH, DIR_PULL, DIR_AUTO = 0, 1, 2
 FILTER_EXACT, FILTER_INEXACT = 0, 1
 LOOP_HOST, LOOP_DEVICE = 0, 1
 
-FN_NONE, FN_BFS_CLAIM, FN_BFS_IDEMP, FN_SSSP_RELAX, FN_TC_ORIENT, FN_LABEL_EQ, FN_LABEL_NE = range(7)
+(FN_NONE, FN_BFS_CLAIM, FN_BFS_IDEMP, FN_SSSP_RELAX, FN_TC_ORIENT, FN_LABEL_EQ, FN_LABEL_NE,
+ FN_SET_LABEL, FN_ADD_I64) = range(9)
 KIND_V2V, KIND_V2E, KIND_E2V, KIND_E2E = range(4)
 
 
@@ -85,6 +86,9 @@ _SIGS = {
                             c_void_p, c_int64, POINTER(c_int64), POINTER(c_int64)]),
     "gfx_filter": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, POINTER(FunctorArgs),
                            c_int64, c_void_p, POINTER(c_int64)]),
+    "gfx_compute": (c_int, [c_void_p, c_void_p, c_int64, c_int, POINTER(FunctorArgs), c_void_p]),
+    "gfx_segmented_intersect_list": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
+                                             c_void_p]),
     "gfx_rmat_keys": (c_int, [c_void_p, c_int, c_int, POINTER(c_double), c_uint64, c_uint64,
                               c_uint64, c_uint64, c_int, c_void_p, POINTER(c_int64)]),
     "gfx_keys_to_csr": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_void_p]),
