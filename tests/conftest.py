@@ -60,3 +60,20 @@ def host_graph(d, weighted=False):
     w = d["w"].astype(np.int64) if weighted else None
     return CsrGraph(int(d["n"]), d["row"].astype(np.int64), d["col"].astype(np.int64), w,
                     undirected=bool(d["undirected"]))
+
+
+@pytest.fixture(scope="session")
+def suite():
+    """Every 5th graph of the reference acceptance suite (+ its large tail),
+    with reference outputs (oracle/make_golden.py suite)."""
+    meta = json.loads((GOLDEN / "suite_graphs.json").read_text())
+    arrs = np.load(GOLDEN / "suite_graphs.npz")
+    out = []
+    for i, rec in enumerate(meta["graphs"]):
+        p = f"g{i}_"
+        d = dict(rec)
+        d["undirected"] = True
+        for k in ("row", "col", "w", "bfs", "sssp", "bc", "cc", "pr4", "tc_counts"):
+            d[k] = arrs[p + k]
+        out.append(d)
+    return out

@@ -80,3 +80,15 @@ def test_s16_outputs_oracles():
     assert np.array_equal(comp, arrays["cc"]) and k == rec["cc_num"]
     total, counts, _, _ = c_oracle.tc(row, col)
     assert total == rec["tc_total"] and np.array_equal(counts, arrays["tc_counts"])
+
+
+def test_suite_c_oracle(suite):
+    """C oracles vs the reference on its acceptance-suite graphs."""
+    for d in suite:
+        row, col = d["row"], d["col"].astype(np.int64)
+        assert np.array_equal(c_oracle.bfs(row, col, d["source"]), d["bfs"]), d["name"]
+        assert np.array_equal(c_oracle.dijkstra(row, col, d["w"], d["source"]), d["sssp"])
+        comp, _ = c_oracle.cc(row, col)
+        assert np.array_equal(comp, d["cc"]), d["name"]
+        total, counts, _, _ = c_oracle.tc(row, col)
+        assert total == d["tc_total"] and np.array_equal(counts, d["tc_counts"]), d["name"]
