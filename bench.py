@@ -164,6 +164,18 @@ class ClockSampler:
                 "samples": len(samples), "samples_under_load": len([s for s in samples if s[2] > 0])}
 
 
+def ncu_traffic(kernel: str, scale: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
+    from the committed `ncu --set full` summary (profiles/ncu_traffic.json,
+    written by tools/ncu_summary.py --traffic); None when not captured."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    try:
+        rec = json.loads(p.read_text())[f"{kernel}@s{scale}"]
+        return int(rec["dram_bytes"]), rec["source"]
+    except Exception:
+        return None, None
+
+
 def measured_peak_gbs() -> tuple[float, str]:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -246,22 +258,29 @@ def run_ours(args, dist: Dist):
     value = total_edges / (t_ms * 1e-3) / 1e9
     ms_per_step = t_ms / args.steps
 
-    # ---- roofline of the dominant kernel (per-level events, separate run)
+    # ---- roofline of the dominant kernel.  The whole DO-BFS is ONE
+    # cooperative launch (k_bfs_persistent), so the kernel's algorithmic
+    # bytes per launch are the whole BFS's (SURVEY 8(d) per-level formulas,
+    # counted by the kernel) and its launch duration is ms_per_step (CUDA
+    # events around the K back-to-back launches on the launching stream).
+    # The per-level split comes from a separate run with globaltimer stamps.
     ctx.set_timing(True)
     prof = step(args.direction)
     ctx.set_timing(False)
     peak, peak_kind = measured_peak_gbs()
+    achieved = prof.bytes_alg / (ms_per_step * 1e-3) / 1e9
     lv = max(prof.device_levels, key=lambda x: x["ms"])
-    achieved = lv["bytes_alg"] / (lv["ms"] * 1e-3) / 1e9
-    kernel = "k_bfs_pull" if lv["mode"] == "pull" else "k_degree_scan+k_lb_expand<BfsClaimOp>"
-    whole = prof.bytes_alg / (ms_per_step * 1e-3) / 1e9
+    traffic, traffic_src = ncu_traffic("k_bfs_persistent", args.scale)
     roofline = {
         "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-        "frac": round(achieved / peak, 4), "traffic": None,
-        "kernel": kernel, "level": lv["iteration"], "level_ms": round(lv["ms"], 4),
-        "bytes_alg_per_launch": lv["bytes_alg"], "peak_source": peak_kind,
-        "whole_bfs": {"bytes_alg": prof.bytes_alg, "achieved_gbs": round(whole, 1),
-                      "frac": round(whole / peak, 4)},
+        "frac": round(achieved / peak, 4), "traffic": traffic,
+        "kernel": "k_bfs_persistent", "bytes_alg_per_launch": prof.bytes_alg,
+        "launch_ms": round(ms_per_step, 4), "peak_source": peak_kind,
+        "traffic_source": traffic_src,
+        "init_ms": round(prof.init_ms, 4),
+        "heaviest_level": {"iteration": lv["iteration"], "mode": lv["mode"],
+                           "ms": round(lv["ms"], 4), "bytes_alg": lv["bytes_alg"],
+                           "achieved_gbs": round(lv["bytes_alg"] / (lv["ms"] * 1e-3) / 1e9, 1)},
         "levels": [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in d.items()}
                    for d in prof.device_levels],
     }

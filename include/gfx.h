@@ -276,6 +276,14 @@ GFX_API int gfx_dbfs_pull(gfx_dbfs* db, int32_t depth, int64_t* nf_local, int64_
 /* ---- kernel experiments (tools/expand_lab.py; not a product path) -------
  * One LB expansion of F_d with functor variant 0 (stream only), 1 (stream +
  * visited probe) or 2 (full claim); visited = {labels < depth}. */
+/* Diagnostics: microseconds per grid-wide barrier (variant 0: cooperative
+ * groups grid sync, 1: flag barrier) for a cooperative grid of blocks x threads. */
+GFX_API int gfx_debug_gridsync(gfx_ctx* ctx, int variant, int blocks, int threads, int iters,
+                               float* us_per_sync);
+/* Diagnostics: clock cycles per dependent load, chasing next = buf[next]
+ * (uint32 words, device buffer prepared by the caller) from `start`. */
+GFX_API int gfx_debug_chase(gfx_ctx* ctx, const uint32_t* buf_d, int iters, uint32_t start,
+                            double* cycles_per_load);
 GFX_API int gfx_debug_expand(gfx_graph* g, const int32_t* F_d, int64_t nf, int variant,
                              int32_t* labels_d, int32_t depth, float* ms, int64_t* out_count);
 

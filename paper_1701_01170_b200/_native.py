@@ -110,6 +110,8 @@ _SIGS = {
     "gfx_dbfs_pull_prepare": (c_int, [c_void_p]),
     "gfx_dbfs_pull": (c_int, [c_void_p, c_int32, POINTER(c_int64), POINTER(c_int64),
                               POINTER(c_int64)]),
+    "gfx_debug_gridsync": (c_int, [c_void_p, c_int, c_int, c_int, c_int, POINTER(c_float)]),
+    "gfx_debug_chase": (c_int, [c_void_p, c_void_p, c_int, ctypes.c_uint32, POINTER(c_double)]),
     "gfx_debug_expand": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_int32,
                                  POINTER(c_float), POINTER(c_int64)]),
 }
@@ -128,12 +130,18 @@ def load_library() -> ctypes.CDLL:
     with _lib_lock:
         if _lib is not None:
             return _lib
-        if not LIB_PATH.exists():
+        path = LIB_PATH
+        override = os.environ.get("GFX_LIB_PATH")  # A/B experiments against another build
+        if override:
+            path = Path(override)
+        if not path.exists():
             raise ImportError(
-                f"{LIB_PATH} is missing: build it with `python -m paper_1701_01170_b200._build` "
+                f"{path} is missing: build it with `python -m paper_1701_01170_b200._build` "
                 "(there is no CPU fallback)")
-        lib = ctypes.CDLL(str(LIB_PATH))
+        lib = ctypes.CDLL(str(path))
         for name, (res, args) in _SIGS.items():
+            if override and not hasattr(lib, name):
+                continue
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

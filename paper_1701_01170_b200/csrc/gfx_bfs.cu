@@ -718,8 +718,8 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
         queue_to_bitmap(a.order + c.q_off, nf, fcur, gtid, nthr);
         grid.sync();
       }
-      pull_groups(a.words, a.nz_in, a.visited, BitmapFront{fcur}, fnext, a.head, a.rrow, a.rcol, a.directed,
-                  a.labels, a.preds, depth, cur, gw, nw, PS);
+      pull_sweep(a.words, a.nz_in, a.visited, BitmapFront{fcur}, fnext, a.head, a.rrow, a.rcol,
+                 a.directed, LabelOut{a.labels, nullptr}, a.preds, depth, cur, nullptr, gw, nw, PS);
       grid.sync();
       nout = (long long)ld_ctr(&cur->out_len);
       work = (long long)ld_ctr(&cur->aux0);

@@ -1,6 +1,7 @@
 // Kernel-level experiment entry point (used by tools/expand_lab.py to break
 // the push expansion's time into streaming / probing / claiming parts).
 // Not on any product path.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "gfx_device.cuh"
@@ -74,9 +75,106 @@ __global__ void k_visited_from_labels(const int32_t* __restrict__ labels, int64_
   }
 }
 
+// grid-barrier microbenchmark: cg::grid sync vs a flag barrier (per-block
+// arrival words polled by block 0, one release word)
+__device__ __forceinline__ unsigned ld_acq(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rel(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void flag_barrier(unsigned* flags, unsigned* gen, unsigned g) {
+  __syncthreads();
+  if (threadIdx.x == 0) st_rel(&flags[blockIdx.x * 32], g);
+  if (blockIdx.x == 0) {
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x)
+      while (ld_acq(&flags[i * 32]) != g) {
+      }
+    __syncthreads();
+    if (threadIdx.x == 0) st_rel(gen, g);
+  } else if (threadIdx.x == 0) {
+    while (ld_acq(gen) != g) {
+    }
+  }
+  if (threadIdx.x == 0) __threadfence();
+  __syncthreads();
+}
+
+__global__ void k_gridsync_bench(int variant, int iters, unsigned* flags, unsigned* gen,
+                                 unsigned* sink) {
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  unsigned acc = 0;
+  for (int i = 0; i < iters; ++i) {
+    if (variant == 0) grid.sync();
+    else flag_barrier(flags, gen, (unsigned)i + 1);
+    acc += flags[(blockIdx.x * 7 + i) % gridDim.x * 32];
+  }
+  if (acc == 0xdeadbeef) sink[0] = acc;
+}
+
+// dependent-load latency: one thread chases next = buf[next] through a
+// random cyclic permutation of `span` words (stride-randomised), timing
+// `iters` hops with clock64
+__global__ void k_chase(const uint32_t* __restrict__ buf, int iters, long long* out,
+                        uint32_t start) {
+  uint32_t x = start;
+  const long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) x = buf[x];
+  const long long t1 = clock64();
+  out[0] = t1 - t0;
+  out[1] = x;
+}
+
 }  // namespace gfx
 
 using namespace gfx;
+
+// cycles per dependent load over a chase buffer prepared by the caller
+extern "C" int gfx_debug_chase(gfx_ctx* ctx, const uint32_t* buf_d, int iters, uint32_t start,
+                               double* cycles_per_load) {
+  GFX_REQUIRE(ctx && buf_d && cycles_per_load && iters > 0, "gfx_debug_chase: bad argument");
+  GFX_CK(cudaSetDevice(ctx->device));
+  long long* out = nullptr;
+  GFX_CK(cudaMalloc(&out, 16));
+  k_chase<<<1, 1, 0, ctx->stream>>>(buf_d, iters, out, start);  // warm (TLB, L2)
+  k_chase<<<1, 1, 0, ctx->stream>>>(buf_d, iters, out, start);
+  long long h[2];
+  GFX_CK(cudaMemcpyAsync(h, out, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  GFX_CK(cudaStreamSynchronize(ctx->stream));
+  GFX_CK(cudaFree(out));
+  *cycles_per_load = (double)h[0] / iters;
+  return GFX_OK;
+}
+
+extern "C" int gfx_debug_gridsync(gfx_ctx* ctx, int variant, int blocks, int threads, int iters,
+                                  float* us_per_sync) {
+  GFX_REQUIRE(ctx && us_per_sync && blocks > 0 && threads > 0, "gfx_debug_gridsync: bad argument");
+  GFX_CK(cudaSetDevice(ctx->device));
+  unsigned* buf = nullptr;
+  GFX_CK(cudaMalloc(&buf, (size_t)(blocks + 2) * 32 * 4));
+  GFX_CK(cudaMemset(buf, 0, (size_t)(blocks + 2) * 32 * 4));
+  unsigned* flags = buf;
+  unsigned* gen = buf + (size_t)blocks * 32;
+  unsigned* sink = gen + 32;
+  void* args[] = {&variant, &iters, &flags, &gen, &sink};
+  int one = 1;
+  void* args1[] = {&variant, &one, &flags, &gen, &sink};
+  GFX_CK(cudaLaunchCooperativeKernel((const void*)k_gridsync_bench, dim3(blocks), dim3(threads),
+                                     args1, 0, ctx->stream));
+  GFX_CK(cudaMemsetAsync(buf, 0, (size_t)(blocks + 2) * 32 * 4, ctx->stream));
+  GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  GFX_CK(cudaLaunchCooperativeKernel((const void*)k_gridsync_bench, dim3(blocks), dim3(threads),
+                                     args, 0, ctx->stream));
+  GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  GFX_CK(cudaEventSynchronize(ctx->ev1));
+  float ms = 0.f;
+  GFX_CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  *us_per_sync = ms * 1000.f / iters;
+  GFX_CK(cudaFree(buf));
+  return GFX_OK;
+}
 
 extern "C" int gfx_debug_expand(gfx_graph* g, const int32_t* F_d, int64_t nf, int variant,
                                         int32_t* labels_d, int32_t depth, float* ms,

@@ -79,11 +79,19 @@ def test_headline_config_golden(scale):
     from paper_1701_01170_b200.generators import rmat_device_graph
     from paper_1701_01170_b200.primitives.bfs import bfs_device
 
+    from paper_1701_01170_b200._results import preds_to_host
+
     rec, _ = rmat_golden(scale)
     dg = rmat_device_graph(scale, 16, 0)
+    host = None
     for direction in ("push", "auto"):
         labels, preds, st = bfs_device(dg, 0, direction=direction)
-        assert sha(labels_to_host(labels)) == rec["bfs_sha"], direction
+        lab = labels_to_host(labels)
+        assert sha(lab) == rec["bfs_sha"], direction
+        if scale <= 22:  # preds by property (reference _oracles.py:169-182)
+            if host is None:
+                host = (dg.row.cpu().numpy(), dg.col.cpu().numpy().astype(np.int64))
+            assert valid_bfs_preds(host[0], host[1], lab, preds_to_host(preds), 0), direction
         assert st.edges_reached == rec["E_r"]
         assert [it.frontier_in for it in st.per_iteration] == rec["bfs_levels"]
         if direction == "push":
@@ -122,3 +130,29 @@ def gfx_graph_s16(rec, arrays):
     import paper_1701_01170_b200 as gfx
 
     return gfx.CsrGraph(rec["n"], arrays["row"], arrays["col"].astype(np.int64), undirected=True)
+
+
+@pytest.mark.parametrize("direction", ["push", "pull", "auto"])
+def test_deep_graph_past_depth_255(direction):
+    """A 700-vertex path with side branches: more than 255 levels, so the
+    device loop's deferred depth bytes run out mid-traversal and it switches
+    to direct labels (gfx_bfs.cu materialize_labels); every pull level after
+    the first walks the candidate list (gfx_pull.cuh pull_list)."""
+    import paper_1701_01170_b200 as gfx
+    from oracle import c_oracle
+
+    rng = np.random.default_rng(5)
+    n_path = 700
+    src = list(range(n_path - 1))
+    dst = list(range(1, n_path))
+    extra = 300  # leaves hanging off random path vertices, plus isolated ids
+    for k in range(extra):
+        src.append(int(rng.integers(0, n_path)))
+        dst.append(n_path + k)
+    n = n_path + extra + 50
+    g = gfx.coo_to_csr(gfx.CooGraph(n, np.array(src), np.array(dst)), make_undirected=True)
+    for s0 in (0, 350):
+        want = c_oracle.bfs(g.row_offsets, g.column_indices, s0)
+        r = gfx.bfs(g, s0, direction=direction)
+        assert np.array_equal(r.labels, want), (direction, s0)
+        assert valid_bfs_preds(g.row_offsets, g.column_indices, r.labels, r.preds, s0)

@@ -60,6 +60,35 @@ def launches(path):
         print(f"{v/1000:10.1f} us  {name}")
 
 
+def traffic(rep, kernel, key, source):
+    """Record dram read+write bytes per launch of `kernel` (mean over the
+    captured launches) in profiles/ncu_traffic.json under `key`."""
+    import json
+    from pathlib import Path
+
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    hdr, units = rows[0], rows[1]
+    k, r_i, w_i = hdr.index("Kernel Name"), hdr.index("dram__bytes_read.sum"), hdr.index(
+        "dram__bytes_write.sum")
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    vals = []
+    for r in rows[2:]:
+        if kernel in r[k]:
+            vals.append(float(r[r_i].replace(",", "")) * scale[units[r_i]] +
+                        float(r[w_i].replace(",", "")) * scale[units[w_i]])
+    assert vals, f"{kernel} not in {rep}"
+    out = Path(__file__).resolve().parent.parent / "profiles" / "ncu_traffic.json"
+    db = json.loads(out.read_text()) if out.exists() else {}
+    db[key] = {"dram_bytes": int(sum(vals) / len(vals)), "launches": len(vals), "source": source}
+    out.write_text(json.dumps(db, indent=1, sort_keys=True) + "\n")
+    print(key, db[key])
+
+
 if __name__ == "__main__":
     p = sys.argv[1]
-    (launches if p.endswith(".csv") else details)(p)
+    if len(sys.argv) > 2 and sys.argv[2] == "--traffic":
+        traffic(p, sys.argv[3], sys.argv[4], sys.argv[5])
+    else:
+        (launches if p.endswith(".csv") else details)(p)
