@@ -128,6 +128,12 @@ GFX_API int gfx_graph_destroy(gfx_graph* g);
 GFX_API int64_t gfx_graph_max_degree(gfx_graph* g);
 /* release scratch buffers (they are re-allocated lazily) */
 GFX_API int gfx_graph_trim(gfx_graph* g);
+/* The caller rewrote the borrowed row/col (/weights/reverse) arrays in place,
+ * same n and m (e.g. a new graph uploaded into the same device buffers):
+ * recompute the graph constants derived from them (max degree, nonzero
+ * bitmaps, pull heads, TC orientation), keeping every scratch allocation.
+ * Replaces building a fresh CsrGraph device copy (reference graph.py:61-155). */
+GFX_API int gfx_graph_refresh(gfx_graph* g);
 
 /* ---- BFS (reference primitives/bfs.py:42-159) ---------------------------
  * labels_d/preds_d int32[n] (outputs).  recs: host array of rec_cap records

@@ -66,6 +66,7 @@ _SIGS = {
     "gfx_graph_destroy": (c_int, [c_void_p]),
     "gfx_graph_max_degree": (c_int64, [c_void_p]),
     "gfx_graph_trim": (c_int, [c_void_p]),
+    "gfx_graph_refresh": (c_int, [c_void_p]),
     "gfx_bfs": (c_int, [c_void_p, c_int64, c_int, c_int, c_int, c_double, c_double, c_int,
                         c_int, c_void_p, c_void_p, POINTER(IterRec), c_int64, POINTER(Stats)]),
     "gfx_bfs_batch": (c_int, [c_void_p, POINTER(c_int64), c_int64, c_int, c_double, c_double,

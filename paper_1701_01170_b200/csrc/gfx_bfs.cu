@@ -145,6 +145,16 @@ __global__ void k_pull_heads(const int64_t* __restrict__ rrow, const int32_t* __
   }
 }
 
+int refresh_pull_heads(gfx_graph* g) {
+  auto it = g->scratch.find("keep_head");
+  if (it == g->scratch.end() || !g->rrow) return GFX_OK;
+  gfx_ctx* ctx = g->ctx;
+  GFX_LAUNCH(k_pull_heads, grid_for(g->n, 256, ctx->sm_count * 8), 256, 0, ctx->stream, g->rrow,
+             g->rcol, g->n, static_cast<int32_t*>(it->second.ptr));
+  GFX_CK(cudaGetLastError());
+  return GFX_OK;
+}
+
 // frontier bitmap -> queue (ascending within each warp's 1024-vertex span)
 __device__ __forceinline__ void bitmap_to_queue(int64_t words, const uint32_t* __restrict__ bm,
                                                 int32_t* __restrict__ out,
@@ -718,8 +728,8 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
         queue_to_bitmap(a.order + c.q_off, nf, fcur, gtid, nthr);
         grid.sync();
       }
-      pull_sweep(a.words, a.nz_in, a.visited, BitmapFront{fcur}, fnext, a.head, a.rrow, a.rcol,
-                 a.directed, LabelOut{a.labels, nullptr}, a.preds, depth, cur, nullptr, gw, nw, PS);
+      pull_groups(a.words, a.nz_in, a.visited, BitmapFront{fcur}, fnext, a.head, a.rrow, a.rcol, a.directed,
+                  a.labels, a.preds, depth, cur, gw, nw, PS);
       grid.sync();
       nout = (long long)ld_ctr(&cur->out_len);
       work = (long long)ld_ctr(&cur->aux0);

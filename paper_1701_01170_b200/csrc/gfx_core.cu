@@ -334,6 +334,30 @@ int gfx_graph_destroy(gfx_graph* g) {
 
 int64_t gfx_graph_max_degree(gfx_graph* g) { return g ? g->max_deg : -1; }
 
+int gfx_graph_refresh(gfx_graph* g) {
+  GFX_REQUIRE(g, "gfx_graph_refresh: null graph");
+  gfx_ctx* ctx = g->ctx;
+  GFX_CK(cudaSetDevice(ctx->device));
+  // the caller rewrote the borrowed arrays in place (same n, m): recompute
+  // every graph constant derived from them, keep the scratch allocations
+  unsigned long long* dmax = reinterpret_cast<unsigned long long*>(g->counters) + 31;
+  GFX_CK(cudaMemsetAsync(dmax, 0, 8, ctx->stream));
+  if (g->n > 0) {
+    GFX_LAUNCH(k_max_degree, grid_for(g->n, 256, ctx->sm_count * 8), 256, 0, ctx->stream, g->row,
+               g->n, dmax);
+    GFX_TRY(build_nonzero_bitmap(g, g->row, "nz_out"));
+    if (!(g->flags & GFX_GRAPH_UNDIRECTED) && g->rrow)
+      GFX_TRY(build_nonzero_bitmap(g, g->rrow, "nz_in"));
+    GFX_TRY(refresh_pull_heads(g));
+  }
+  g->m_oriented = -1;  // the oriented CSR (TC) is rebuilt on next use
+  auto* pin = static_cast<unsigned long long*>(ctx->pinned);
+  GFX_CK(cudaMemcpyAsync(pin, dmax, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  GFX_CK(cudaStreamSynchronize(ctx->stream));
+  g->max_deg = (int64_t)pin[0];
+  return GFX_OK;
+}
+
 int gfx_graph_trim(gfx_graph* g) {
   GFX_REQUIRE(g, "null graph");
   GFX_CK(cudaStreamSynchronize(g->ctx->stream));

@@ -77,41 +77,4 @@ __device__ __forceinline__ bool test_bit(const uint32_t* bm, int32_t v) {
   return (bm[v >> 5] >> (v & 31)) & 1u;
 }
 
-// Grid-wide barrier for cooperative (co-resident) grids.  Same protocol as
-// cooperative_groups' grid sync (CTA barrier, one gpu-scope fence + arrival
-// atomic per CTA), but waiting CTAs poll the release word with a nanosleep
-// back-off instead of a tight loop: a persistent kernel spends whole
-// levels with most CTAs parked here, and ~450 tight pollers on one L2 line
-// inflate the memory latency of the CTAs that are still working.
-// count / gen: two words in different 128-byte lines, zero at launch.
-struct GridBarrier {
-  unsigned* count;
-  unsigned* gen;
-  __device__ __forceinline__ void sync(unsigned& local_gen) const {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const unsigned g = local_gen;
-      const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
-      __threadfence();
-      if (atomicAdd(count, 1u) == nb - 1) {
-        atomicExch(count, 0u);
-        __threadfence();
-        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(gen), "r"(g + 1) : "memory");
-      } else {
-        unsigned cur;
-        int ns = 32;
-        for (;;) {
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(gen) : "memory");
-          if (cur != g) break;
-          __nanosleep(ns);
-          if (ns < 256) ns <<= 1;
-        }
-      }
-      local_gen = g + 1;
-      __threadfence();
-    }
-    __syncthreads();
-  }
-};
-
 }  // namespace gfx

@@ -150,6 +150,10 @@ constexpr int kScanBlock = 256;
 constexpr int kScanItems = 8;        // items per thread in the scan
 constexpr int kScanTileItems = kScanBlock * kScanItems;
 
+// recompute the pull head array (first in-neighbour per vertex) if the
+// graph has one (gfx_graph_refresh)
+int refresh_pull_heads(gfx_graph* g);
+
 // reached count and E_r from an int32 label array (UNVISITED = INT32_MAX)
 int reached_stats(gfx_graph* g, const int32_t* labels, int64_t* reached, int64_t* edges);
 

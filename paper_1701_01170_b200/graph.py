@@ -279,6 +279,17 @@ class DeviceGraph:
             raise ValueError("edge weights must fit in int32 on the device path")
         return torch.from_numpy(np.ascontiguousarray(w, dtype=np.int32)).to(dev)
 
+    def reload_(self, row_h, col_h) -> None:
+        """Upload a new graph of the same shape into this device copy's own
+        buffers (host tensors, pinned for DMA speed; asynchronous on the
+        current stream) and recompute the derived graph constants
+        (gfx_graph_refresh) -- no reallocation of buffers or scratch."""
+        if row_h.numel() != self.row.numel() or col_h.numel() != self.col.numel():
+            raise ValueError("reload_: shape differs from the resident graph")
+        self.row.copy_(row_h, non_blocking=True)
+        self.col.copy_(col_h, non_blocking=True)
+        _native.call("gfx_graph_refresh", self.handle)
+
     def refresh_weights(self, w) -> None:
         """Re-upload weights if the host graph's weight array was replaced."""
         if self.host is None or w is self._w_src:

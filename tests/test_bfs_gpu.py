@@ -134,10 +134,8 @@ def gfx_graph_s16(rec, arrays):
 
 @pytest.mark.parametrize("direction", ["push", "pull", "auto"])
 def test_deep_graph_past_depth_255(direction):
-    """A 700-vertex path with side branches: more than 255 levels, so the
-    device loop's deferred depth bytes run out mid-traversal and it switches
-    to direct labels (gfx_bfs.cu materialize_labels); every pull level after
-    the first walks the candidate list (gfx_pull.cuh pull_list)."""
+    """A 700-vertex path with side branches: hundreds of levels, most of them
+    tiny, in every direction mode of the device-resident level loop."""
     import paper_1701_01170_b200 as gfx
     from oracle import c_oracle
 
@@ -156,3 +154,34 @@ def test_deep_graph_past_depth_255(direction):
         r = gfx.bfs(g, s0, direction=direction)
         assert np.array_equal(r.labels, want), (direction, s0)
         assert valid_bfs_preds(g.row_offsets, g.column_indices, r.labels, r.preds, s0)
+
+
+def test_graph_reload_refreshes_constants():
+    """DeviceGraph.reload_ (C ABI gfx_graph_refresh): a different graph of
+    the same shape uploaded into the resident buffers gives the new graph's
+    BFS (max degree, nonzero bitmaps and pull heads recomputed)."""
+    import torch
+
+    import paper_1701_01170_b200 as gfx
+    from oracle import c_oracle
+    from paper_1701_01170_b200._results import labels_to_host
+    from paper_1701_01170_b200.primitives.bfs import bfs_device
+
+    rec, arrays = rmat_golden(16)
+    g1 = gfx_graph_s16(rec, arrays)
+    n = rec["n"]
+    # the same graph with vertex ids reversed: same n and m, other content
+    row, col = arrays["row"], arrays["col"].astype(np.int64)
+    src = np.repeat(np.arange(n), np.diff(row))
+    g2 = gfx.coo_to_csr(gfx.CooGraph(n, n - 1 - src, n - 1 - col))
+    assert g2.num_edges == g1.num_edges
+    dg = g1.device()
+    for direction in ("push", "auto"):
+        labels, _, _ = bfs_device(dg, 0, direction=direction)
+        assert sha(labels_to_host(labels)) == rec["bfs_sha"]
+    dg.reload_(torch.from_numpy(g2.row_offsets), torch.from_numpy(g2.column_indices.astype(np.int32)))
+    for s0 in (n - 1, 5):
+        want = c_oracle.bfs(g2.row_offsets, g2.column_indices, s0)
+        for direction in ("push", "auto"):
+            labels, _, _ = bfs_device(dg, s0, direction=direction)
+            assert np.array_equal(labels_to_host(labels), want), (s0, direction)
