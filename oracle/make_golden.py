@@ -5,6 +5,7 @@ container (where /root/reference exists); its outputs are committed so the
 GPU box never needs the reference.
 
 Usage:  python oracle/make_golden.py kat            # mini suite + KAT graphs
+        python oracle/make_golden.py cache          # reference-written CSR cache files
         python oracle/make_golden.py rmat S [S ...] # R-MAT scale S, ef16, seed 0
 
 What is recorded (all arrays little-endian, hashes are SHA-256 of the raw
@@ -235,10 +236,30 @@ def run_rmat(scale: int):
     print("done scale", scale, time.time() - t0)
 
 
+def run_cache():
+    """Binary CSR cache files written by the reference's save_csr_cache
+    (io.py:121-130): an undirected weighted R-MAT s8 graph and a directed
+    unweighted one, plus the arrays they hold (tests/test_io_cache.py)."""
+    from graphfx.io import save_csr_cache
+
+    g = gx.coo_to_csr(gx.generate_rmat(8, 8, seed=3), make_undirected=True)
+    gw = gx.assign_random_weights(g, 1, 64, 0)
+    save_csr_cache(gw, OUT / "cache_rmat8_w.gfxcsr")
+    coo = gx.generate_rmat(7, 4, seed=5)
+    gd = gx.coo_to_csr(coo)
+    save_csr_cache(gd, OUT / "cache_rmat7_dir.gfxcsr")
+    np.savez_compressed(OUT / "cache_arrays.npz", w_row=gw.row_offsets, w_col=gw.column_indices,
+                        w_w=gw.edge_weights, d_row=gd.row_offsets, d_col=gd.column_indices,
+                        d_n=np.array([gd.num_vertices]), w_n=np.array([gw.num_vertices]))
+    print("cache files written", gw.num_edges, gd.num_edges)
+
+
 if __name__ == "__main__":
     os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
     if sys.argv[1] == "kat":
         run_kat()
+    elif sys.argv[1] == "cache":
+        run_cache()
     elif sys.argv[1] == "suite":
         run_suite(int(sys.argv[2]) if len(sys.argv) > 2 else 5)
     else:

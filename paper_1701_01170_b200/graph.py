@@ -286,6 +286,9 @@ class DeviceGraph:
         (gfx_graph_refresh) -- no reallocation of buffers or scratch."""
         if row_h.numel() != self.row.numel() or col_h.numel() != self.col.numel():
             raise ValueError("reload_: shape differs from the resident graph")
+        if not self.undirected:
+            raise ValueError("reload_: directed graphs carry a reverse adjacency; build a new "
+                             "DeviceGraph instead")
         self.row.copy_(row_h, non_blocking=True)
         self.col.copy_(col_h, non_blocking=True)
         _native.call("gfx_graph_refresh", self.handle)

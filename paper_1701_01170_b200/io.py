@@ -1,0 +1,182 @@
+"""Binary CSR cache: the reference's graph wire format, readable and writable
+from host numpy arrays and straight from / into HBM.
+
+Format (reference io.py:18-19, 121-159): magic ``GFXCSR\\0``, then
+``<BQQB`` = (version 1, n, m, flags: bit 0 weighted, bit 1 undirected), then
+little-endian int64 ``row_offsets[n+1]``, ``column_indices[m]`` and, when
+weighted, ``edge_weights[m]``.  ``save_csr_cache`` writes byte-identical
+files to the reference's; ``load_csr_cache`` returns the same ``CsrGraph``.
+
+The device variants move the arrays between the file and HBM without a
+host-side int64 -> int32 pass: the file's int64 column ids (and weights) are
+streamed to the GPU in chunks through pinned staging buffers and narrowed
+there, and written back the same way; the row offsets stay int64 end to
+end.  They are the input format around the hot path: a
+scale-24 graph built once (GPU R-MAT builder) is cached and reloaded in
+seconds instead of being regenerated.
+
+Matrix Market / edge-list text ingestion (reference io.py:22-118) is not a
+hot-path data format and is not provided here.
+"""
+from __future__ import annotations
+
+import struct
+from pathlib import Path
+
+import numpy as np
+
+from .graph import ID_DTYPE, WEIGHT_DTYPE, CsrGraph, DeviceGraph, GraphFormatError
+
+CACHE_MAGIC = b"GFXCSR\x00"
+CACHE_VERSION = 1
+_HDR = "<BQQB"
+_HDR_BYTES = struct.calcsize(_HDR)
+_DATA_OFF = len(CACHE_MAGIC) + _HDR_BYTES
+_CHUNK = 1 << 25  # elements per staged transfer (256 MB of int64)
+
+
+def _flags(weighted: bool, undirected: bool) -> int:
+    return (1 if weighted else 0) | (2 if undirected else 0)
+
+
+def _header(n: int, m: int, flags: int) -> bytes:
+    return CACHE_MAGIC + struct.pack(_HDR, CACHE_VERSION, n, m, flags)
+
+
+def read_header(path: str | Path) -> tuple[int, int, int]:
+    """(n, m, flags) of a cache file; GraphFormatError on a bad magic/version
+    (reference io.py:140-146)."""
+    with open(path, "rb") as fh:
+        head = fh.read(_DATA_OFF)
+    if not head.startswith(CACHE_MAGIC):
+        raise GraphFormatError("not a CSR cache file (bad magic)")
+    if len(head) < _DATA_OFF:
+        raise GraphFormatError("truncated CSR cache header")
+    version, n, m, flags = struct.unpack_from(_HDR, head, len(CACHE_MAGIC))
+    if version != CACHE_VERSION:
+        raise GraphFormatError(f"unsupported cache version {version}")
+    return int(n), int(m), int(flags)
+
+
+def _check_size(path: Path, n: int, m: int, flags: int) -> None:
+    want = _DATA_OFF + 8 * (n + 1 + m + (m if flags & 1 else 0))
+    have = path.stat().st_size
+    if have < want:
+        raise GraphFormatError(f"truncated CSR cache: {have} bytes, header needs {want}")
+
+
+# ---------------------------------------------------------------------------
+# host arrays (reference io.py:121-159)
+# ---------------------------------------------------------------------------
+def save_csr_cache(g: CsrGraph, path: str | Path) -> None:
+    """Write the binary CSR cache (byte-identical to reference save_csr_cache)."""
+    with open(path, "wb") as fh:
+        fh.write(_header(g.num_vertices, g.num_edges,
+                         _flags(g.edge_weights is not None, g.undirected)))
+        fh.write(np.ascontiguousarray(g.row_offsets, dtype="<i8").tobytes())
+        fh.write(np.ascontiguousarray(g.column_indices, dtype="<i8").tobytes())
+        if g.edge_weights is not None:
+            fh.write(np.ascontiguousarray(g.edge_weights, dtype="<i8").tobytes())
+
+
+def load_csr_cache(path: str | Path) -> CsrGraph:
+    """Read a cache file into a host ``CsrGraph`` (reference load_csr_cache)."""
+    path = Path(path)
+    n, m, flags = read_header(path)
+    _check_size(path, n, m, flags)
+    mm = np.memmap(path, dtype="<i8", mode="r", offset=_DATA_OFF)
+    row = np.array(mm[:n + 1], dtype=ID_DTYPE)
+    col = np.array(mm[n + 1:n + 1 + m], dtype=ID_DTYPE)
+    w = np.array(mm[n + 1 + m:n + 1 + 2 * m], dtype=WEIGHT_DTYPE) if flags & 1 else None
+    return CsrGraph(num_vertices=n, row_offsets=row, column_indices=col, edge_weights=w,
+                    undirected=bool(flags & 2))
+
+
+def load_graph(path: str | Path, make_undirected: bool = False) -> CsrGraph:
+    """Reference load_graph (io.py:162-175) for the cache format: a cache
+    file loads as stored; ``make_undirected`` symmetrises a directed one."""
+    g = load_csr_cache(path)
+    if make_undirected and not g.undirected:
+        from .graph import coo_to_csr, csr_to_coo
+
+        g = coo_to_csr(csr_to_coo(g), make_undirected=True)
+    return g
+
+
+# ---------------------------------------------------------------------------
+# HBM <-> file
+# ---------------------------------------------------------------------------
+def _stream_to_device(mm: np.ndarray, out, narrow: bool) -> None:
+    """Copy int64 file data into the device tensor `out` (int32 when
+    `narrow`) chunk by chunk: memmap -> pinned staging -> H2D -> narrow."""
+    import torch
+
+    total = len(mm)
+    if total == 0:
+        return
+    step = min(_CHUNK, total)
+    stage = [torch.empty(step, dtype=torch.int64, pin_memory=True) for _ in range(2)]
+    dev_tmp = torch.empty(step, dtype=torch.int64, device=out.device) if narrow else None
+    done = [None, None]
+    for k, a in enumerate(range(0, total, step)):
+        b = min(a + step, total)
+        buf = stage[k % 2]
+        if done[k % 2] is not None:
+            done[k % 2].synchronize()  # the DMA that last read this staging buffer
+        buf[:b - a].numpy()[:] = mm[a:b]
+        if narrow:
+            dev_tmp[:b - a].copy_(buf[:b - a], non_blocking=True)
+            out[a:b].copy_(dev_tmp[:b - a])
+        else:
+            out[a:b].copy_(buf[:b - a], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        done[k % 2] = ev
+    torch.cuda.synchronize(out.device)
+
+
+def load_csr_cache_device(path: str | Path, device: int | None = None) -> DeviceGraph:
+    """Load a cache file straight into HBM (int64 row, int32 col / weights).
+    Ids must fit int32 (the device layout); weights must fit int32."""
+    import torch
+
+    from . import _native
+
+    path = Path(path)
+    n, m, flags = read_header(path)
+    _check_size(path, n, m, flags)
+    if n >= 2**31 - 1:
+        raise ValueError("graphs with >= 2^31-1 vertices are not supported (int32 ids)")
+    ctx = _native.Context.get(device)
+    dev = torch.device("cuda", ctx.device)
+    mm = np.memmap(path, dtype="<i8", mode="r", offset=_DATA_OFF)
+    row = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    col = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
+    _stream_to_device(mm[:n + 1], row, narrow=False)
+    _stream_to_device(mm[n + 1:n + 1 + m], col, narrow=True)
+    w = None
+    if flags & 1:
+        w = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
+        _stream_to_device(mm[n + 1 + m:n + 1 + 2 * m], w, narrow=True)
+    if not flags & 2:
+        raise ValueError("load_csr_cache_device: directed caches need the reverse adjacency; "
+                         "load with load_csr_cache and upload via CsrGraph.device()")
+    if m and (int(row[-1]) != m or int(col.min()) < 0 or int(col.max()) >= n):
+        raise GraphFormatError("CSR cache arrays inconsistent with its header")
+    return DeviceGraph(ctx, n, m, row, col, w, True)
+
+
+def save_csr_cache_device(dg: DeviceGraph, path: str | Path) -> None:
+    """Write a device graph (e.g. from the GPU R-MAT builder) as a cache file:
+    widened to int64 on the GPU, read back chunk by chunk, appended."""
+    import torch
+
+    n, m = dg.num_vertices, dg.num_edges
+    with open(path, "wb") as fh:
+        fh.write(_header(n, m, _flags(dg.w is not None, dg.undirected)))
+        parts = [(dg.row, n + 1), (dg.col, m)] + ([(dg.w, m)] if dg.w is not None else [])
+        for t, count in parts:
+            for a in range(0, count, _CHUNK):
+                b = min(a + _CHUNK, count)
+                fh.write(t[a:b].to(torch.int64).cpu().numpy().astype("<i8", copy=False)
+                         .tobytes())
