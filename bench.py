@@ -446,7 +446,56 @@ def extras(args, dg, labels, preds, dist, peak):
         del dgw
     except Exception as exc:  # report, do not hide
         res["sssp_error"] = repr(exc)
+    try:
+        res.update(secondary(args, dg, peak))
+    except Exception as exc:
+        res["secondary_error"] = repr(exc)
     return res
+
+
+def secondary(args, dg, peak):
+    """BASELINE configs C3/C4 (parity-and-time configs): PageRank (d = 0.85,
+    20 iterations, eps = 0) and CC on the bench graph; BC from the source and
+    TC on the scale-2 graph (s22 for the s24 bench).  Device time per call
+    (CUDA events in the library), mean of 3 after a warm-up; bytes per SURVEY
+    8(d) (PR 4m + 40n per iteration, CC from the kernel's counters)."""
+    import torch
+
+    from paper_1701_01170_b200.generators import rmat_device_graph
+    from paper_1701_01170_b200.primitives.bc import bc_device
+    from paper_1701_01170_b200.primitives.cc import cc_device
+    from paper_1701_01170_b200.primitives.pagerank import pagerank_device
+    from paper_1701_01170_b200.primitives.tc import tc_device
+
+    def timed(fn, reps=3):
+        fn()
+        vals = []
+        for _ in range(reps):
+            st = fn()
+            vals.append(st.device_ms)
+        return st, sum(vals) / len(vals)
+
+    n, m = dg.num_vertices, dg.num_edges
+    out = {}
+    st, ms = timed(lambda: pagerank_device(dg, 0.85, 0.0, 20)[1])
+    b = (4 * m + 40 * n) * st.iterations
+    out[f"pagerank_s{args.scale}"] = {"ms": round(ms, 3), "iterations": st.iterations,
+                                      "bytes_alg": b,
+                                      "frac_of_hbm": round(b / (ms * 1e-3) / 1e9 / peak, 4)}
+    st, ms = timed(lambda: cc_device(dg)[2])
+    out[f"cc_s{args.scale}"] = {"ms": round(ms, 3), "iterations": st.iterations,
+                                "bytes_alg": st.bytes_alg,
+                                "frac_of_hbm": round(st.bytes_alg / (ms * 1e-3) / 1e9 / peak, 4)}
+    small = max(args.scale - 2, 10)
+    dg2 = rmat_device_graph(small, args.edge_factor, 0)
+    st, ms = timed(lambda: bc_device(dg2, [args.source])[1])
+    out[f"bc_s{small}"] = {"ms": round(ms, 3), "gteps_x2": round(
+        2 * st.edges_traversed / (ms * 1e-3) / 1e9, 2)}
+    st, ms = timed(lambda: tc_device(dg2)[4])
+    out[f"tc_s{small}"] = {"ms": round(ms, 3)}
+    del dg2
+    torch.cuda.empty_cache()
+    return out
 
 
 def e2e(args, dg, dist, e_r):

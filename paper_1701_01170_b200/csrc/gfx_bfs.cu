@@ -46,6 +46,7 @@ struct BfsClaimOp {
   int32_t* preds;
   int32_t depth;
   uint32_t wv[kBatch];
+  uint8_t* lvl8 = nullptr;  // optional: deferred labels (depth bytes, see LabelOut)
   __device__ int32_t src_value(int32_t) const { return 0; }
   __device__ void prefetch(const int32_t* d) {
 #pragma unroll
@@ -55,7 +56,8 @@ struct BfsClaimOp {
     const uint32_t bit = 1u << (d & 31);
     if (wv[u] & bit) return false;
     if (atomicOr(&visited[d >> 5], bit) & bit) return false;
-    labels[d] = depth;
+    if (lvl8) lvl8[d] = (uint8_t)depth;
+    else labels[d] = depth;
     preds[d] = s;
     return true;
   }
@@ -130,7 +132,7 @@ __global__ void __launch_bounds__(256)
                int count_in_edges, int32_t* __restrict__ labels, int32_t* __restrict__ preds,
                int32_t depth, Counters* __restrict__ ctr) {
   __shared__ PullSmem ps[8];
-  pull_groups(words, nz_in, visited, BitmapFront{front}, next, head, rrow, rcol, count_in_edges, labels,
+  pull_groups(words, nz_in, visited, BitmapFront{front}, next, head, rrow, rcol, count_in_edges, LabelOut{labels, nullptr},
               preds, depth, ctr, (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5,
               ((int64_t)gridDim.x * blockDim.x) >> 5, ps[threadIdx.x >> 5]);
 }
@@ -580,6 +582,8 @@ struct PBfsArgs {
   unsigned long long* status;
   int32_t* labels;
   int32_t* preds;
+  uint8_t* lvl8;  // depth bytes while labels are deferred (see LabelOut)
+  int vec_ok;     // labels/preds 16-byte aligned: vector stores
   Counters* C;  // 3 rotating counter blocks
   gfx_iter_rec* recs;
   int64_t rec_cap;
@@ -593,7 +597,7 @@ struct PBfsArgs {
 struct PCtl {
   long long nf, n_u, q_off, q_end, depth, reached, edges_total, bytes_total, work_total, switches,
       nrec;
-  int mode_state, queue_form, mode, fsel;
+  int mode_state, queue_form, mode, fsel, direct;
   double mf, mu;
   unsigned long long t0;
 };
@@ -625,6 +629,43 @@ __device__ __noinline__ void device_decide(long long n, long long m, long long n
     *mode = GFX_DIR_PUSH;
 }
 
+// Deferred labels: write labels[v] = depth byte of v if visited, else
+// UNVISITED, for every vertex (preds were set to -1 at launch and written at
+// discovery).  A warp covers 1024 vertices in 8 independent chunks of 128;
+// lane l of chunk k owns vertices 128k + 4l .. +3: one 4-byte depth load,
+// one visited-word load and one 16-byte label store per lane, so every
+// store instruction writes 512 contiguous bytes.
+__device__ __forceinline__ void materialize_labels(const PBfsArgs& a, int64_t gw, int64_t nw) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nfull = a.vec_ok ? (a.n & ~(int64_t)3) : 0;
+  for (int64_t base = gw * 1024; base < a.n; base += nw * 1024) {
+    uint32_t vw[8], d4[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int64_t v = base + 128 * k + 4 * lane;
+      vw[k] = v < a.n ? a.visited[v >> 5] : 0u;
+      d4[k] = v + 3 < a.n ? *reinterpret_cast<const uint32_t*>(a.lvl8 + v) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int64_t v = base + 128 * k + 4 * lane;
+      if (v >= a.n) continue;
+      const uint32_t bits = (vw[k] >> (v & 31)) & 0xFu;
+      if (v < nfull) {
+        int4 lab;
+        lab.x = (bits & 1u) ? (int32_t)(d4[k] & 0xFF) : GFX_UNVISITED;
+        lab.y = (bits & 2u) ? (int32_t)((d4[k] >> 8) & 0xFF) : GFX_UNVISITED;
+        lab.z = (bits & 4u) ? (int32_t)((d4[k] >> 16) & 0xFF) : GFX_UNVISITED;
+        lab.w = (bits & 8u) ? (int32_t)(d4[k] >> 24) : GFX_UNVISITED;
+        *reinterpret_cast<int4*>(a.labels + v) = lab;
+      } else {
+        for (int j = 0; v + j < a.n; ++j)
+          a.labels[v + j] = ((bits >> j) & 1u) ? (int32_t)a.lvl8[v + j] : GFX_UNVISITED;
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -638,10 +679,17 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
   const unsigned long long t_start = leader ? globaltimer() : 0ull;
 
-  // ---- initialise outputs and state
-  for (int64_t i = gtid; i < a.n; i += nthr) {
-    a.labels[i] = GFX_UNVISITED;
-    a.preds[i] = -1;
+  // ---- initialise outputs and state.  Labels are deferred: levels record
+  // depths in the L2-resident byte array lvl8 and materialize_labels writes
+  // every label once at the end (or at depth 255, after which labels are
+  // written directly).  preds start at -1 and are written at discovery.
+  if (a.vec_ok) {
+    const int64_t nq = a.n >> 2;
+    for (int64_t i = gtid; i < nq; i += nthr)
+      reinterpret_cast<int4*>(a.preds)[i] = make_int4(-1, -1, -1, -1);
+    for (int64_t i = (nq << 2) + gtid; i < a.n; i += nthr) a.preds[i] = -1;
+  } else {
+    for (int64_t i = gtid; i < a.n; i += nthr) a.preds[i] = -1;
   }
   for (int64_t i = gtid; i < a.words; i += nthr) a.visited[i] = 0u;
   for (int64_t i = gtid; i < 3 * (int64_t)(sizeof(Counters) / 8); i += nthr)
@@ -656,10 +704,11 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
     c.mode_state = GFX_DIR_PUSH;
     c.queue_form = 1;
     c.fsel = 0;
+    c.direct = 0;
   }
   grid.sync();
   if (leader) {
-    a.labels[a.source] = 0;
+    a.lvl8[a.source] = 0;
     a.visited[a.source >> 5] = 1u << (a.source & 31);
     a.order[0] = a.source;
   }
@@ -681,6 +730,14 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
       c.t0 = globaltimer();
     }
     __syncthreads();
+    if (!c.direct && c.depth == 255) {
+      // depth bytes exhausted: write the labels so far, label directly from here on
+      materialize_labels(a, gw, nw);
+      grid.sync();
+      if (threadIdx.x == 0) c.direct = 1;
+      __syncthreads();
+    }
+    const LabelOut lab{a.labels, c.direct ? nullptr : a.lvl8};
     const int32_t depth = (int32_t)c.depth;
     const int64_t nf = c.nf;
     Counters* cur = &a.C[c.depth % 3];
@@ -707,7 +764,7 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
       for (int64_t t = blockIdx.x; t < stiles; t += gridDim.x)
         scan_tile(t, stiles, F, nf, a.row, a.scan, a.rowbase, a.part, a.status, ep, cur, ss);
       grid.sync();
-      BfsClaimOp op{a.visited, a.labels, a.preds, depth, {}};
+      BfsClaimOp op{a.visited, a.labels, a.preds, depth, {}, lab.lvl8};
       expand_tasks(W, op, F, nf, a.scan, a.rowbase, a.part, (int64_t)ld_ctr(&cur->ntiles),
                    (int64_t)ld_ctr(&cur->total), a.col, nullptr, a.order + c.q_end,
                    &cur->out_len, gw, nw);
@@ -729,7 +786,7 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
         grid.sync();
       }
       pull_groups(a.words, a.nz_in, a.visited, BitmapFront{fcur}, fnext, a.head, a.rrow, a.rcol, a.directed,
-                  a.labels, a.preds, depth, cur, gw, nw, PS);
+                  lab, a.preds, depth, cur, gw, nw, PS);
       grid.sync();
       nout = (long long)ld_ctr(&cur->out_len);
       work = (long long)ld_ctr(&cur->aux0);
@@ -770,6 +827,7 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
     __syncthreads();
     if (c.nf == 0) break;
   }
+  if (!c.direct) materialize_labels(a, gw, nw);
   if (leader) {
     a.summary[0] = c.depth;
     a.summary[1] = c.edges_total;
@@ -825,6 +883,8 @@ static int pbfs_setup(gfx_graph* g, int64_t source, int direction, double do_a, 
   GFX_TRY(scratch_t(g, "pbfs_status", stiles_max + 1, &a.status));
   a.labels = labels;
   a.preds = preds;
+  a.vec_ok = ((reinterpret_cast<uintptr_t>(labels) | reinterpret_cast<uintptr_t>(preds)) & 15) == 0;
+  GFX_TRY(scratch_t(g, "bfs_lvl8", (size_t)n + 4, &a.lvl8));
   a.C = g->counters;
   const int64_t cap = 1 << 16;  // level records kept on device (stats)
   GFX_TRY(scratch_t(g, "pbfs_recs", cap, &a.recs));

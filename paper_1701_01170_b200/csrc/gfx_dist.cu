@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(256)
                 int32_t* __restrict__ labels, int32_t* __restrict__ preds, int32_t depth,
                 Counters* __restrict__ ctr) {
   __shared__ PullSmem ps[8];
-  pull_groups(words, nz, visited, front, next, head, lrow, lcol, 0, labels, preds, depth, ctr,
+  pull_groups(words, nz, visited, front, next, head, lrow, lcol, 0, LabelOut{labels, nullptr}, preds, depth, ctr,
               (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5,
               ((int64_t)gridDim.x * blockDim.x) >> 5, ps[threadIdx.x >> 5]);
 }

@@ -15,6 +15,19 @@ struct BitmapFront {
   __device__ __forceinline__ bool bit(uint32_t w, int32_t s) const { return (w >> (s & 31)) & 1u; }
 };
 
+// Where a discovered vertex's depth goes: straight into the int32 label
+// array, or (deferred labels, the single-GPU persistent BFS) into a
+// byte-per-vertex depth array that stays L2-resident; the int32 labels are
+// then written once, coalesced, after the last level.
+struct LabelOut {
+  int32_t* labels;
+  uint8_t* lvl8;  // non-null: deferred mode
+  __device__ __forceinline__ void set(int32_t v, int32_t d) const {
+    if (lvl8) lvl8[v] = (uint8_t)d;
+    else labels[v] = d;
+  }
+};
+
 constexpr int kPullBatch = 8;  // candidates per lane in flight
 
 // per-warp scratch of the pull phase (aliases the expansion's WarpSmem)
@@ -46,7 +59,7 @@ __device__ __forceinline__ void pull_groups(
     int64_t words, const uint32_t* __restrict__ nz_in, uint32_t* __restrict__ visited,
     const FrontT front, uint32_t* __restrict__ next,
     const int32_t* __restrict__ head, const int64_t* __restrict__ rrow,
-    const int32_t* __restrict__ rcol, int count_in_edges, int32_t* __restrict__ labels,
+    const int32_t* __restrict__ rcol, int count_in_edges, const LabelOut labels,
     int32_t* __restrict__ preds, int32_t depth, Counters* __restrict__ ctr, int64_t gw,
     int64_t nwarps, PullSmem& P) {
   const int lane = threadIdx.x & 31;
@@ -96,7 +109,7 @@ __device__ __forceinline__ void pull_groups(
         const bool hit = h[q] >= 0 && front.bit(fw[q], h[q]);
         const bool miss = h[q] >= 0 && !hit;
         if (hit) {
-          labels[u[q]] = depth;
+          labels.set(u[q], depth);
           preds[u[q]] = h[q];
           atomicOr(&P.newbits[(u[q] >> 5) - grp * 32], 1u << (u[q] & 31));
           ++found_cnt;
@@ -139,7 +152,7 @@ __device__ __forceinline__ void pull_groups(
       probes += (unsigned long long)(found ? p - b + 1 : e - b);
       in_edges += (unsigned long long)(e - b);
       if (found) {
-        labels[uu] = depth;
+        labels.set(uu, depth);
         preds[uu] = par;
         atomicOr(&P.newbits[(uu >> 5) - grp * 32], 1u << (uu & 31));
         ++found_cnt;
