@@ -130,20 +130,25 @@ __global__ void __launch_bounds__(256)
                uint32_t* __restrict__ next, const int32_t* __restrict__ head,
                const int64_t* __restrict__ rrow, const int32_t* __restrict__ rcol,
                int count_in_edges, int32_t* __restrict__ labels, int32_t* __restrict__ preds,
-               int32_t depth, Counters* __restrict__ ctr) {
+               int32_t depth, Counters* __restrict__ ctr, const int32_t* __restrict__ head2) {
   __shared__ PullSmem ps[8];
-  pull_groups(words, nz_in, visited, BitmapFront{front}, next, head, rrow, rcol, count_in_edges, LabelOut{labels, nullptr},
-              preds, depth, ctr, (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5,
-              ((int64_t)gridDim.x * blockDim.x) >> 5, ps[threadIdx.x >> 5]);
+  pull_groups(words, nz_in, visited, BitmapFront{front}, next, head, rrow, rcol, count_in_edges,
+              LabelOut{labels, nullptr}, preds, depth, ctr,
+              (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5,
+              ((int64_t)gridDim.x * blockDim.x) >> 5, ps[threadIdx.x >> 5], head2);
 }
 
-// graph-constant first in-neighbour per vertex (-1 when in-degree is 0)
+// graph-constant first / second in-neighbour per vertex, for the pull
+// probes: head[v] = first in-neighbour, bit 31 set when it is the only one
+// (-1: none); head2[v] = second in-neighbour, bit 31 set when there is no
+// third (-1: fewer than two)
 __global__ void k_pull_heads(const int64_t* __restrict__ rrow, const int32_t* __restrict__ rcol,
-                             int64_t n, int32_t* __restrict__ head) {
+                             int64_t n, int32_t* __restrict__ head, int32_t* __restrict__ head2) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = rrow[v];
-    head[v] = rrow[v + 1] > b ? rcol[b] : -1;
+    const int64_t b = rrow[v], d = rrow[v + 1] - b;
+    head[v] = d > 0 ? (int32_t)((uint32_t)rcol[b] | (d == 1 ? 0x80000000u : 0u)) : -1;
+    head2[v] = d > 1 ? (int32_t)((uint32_t)rcol[b + 1] | (d == 2 ? 0x80000000u : 0u)) : -1;
   }
 }
 
@@ -151,8 +156,9 @@ int refresh_pull_heads(gfx_graph* g) {
   auto it = g->scratch.find("keep_head");
   if (it == g->scratch.end() || !g->rrow) return GFX_OK;
   gfx_ctx* ctx = g->ctx;
+  int32_t* h = static_cast<int32_t*>(it->second.ptr);
   GFX_LAUNCH(k_pull_heads, grid_for(g->n, 256, ctx->sm_count * 8), 256, 0, ctx->stream, g->rrow,
-             g->rcol, g->n, static_cast<int32_t*>(it->second.ptr));
+             g->rcol, g->n, h, h + g->n + 1);
   GFX_CK(cudaGetLastError());
   return GFX_OK;
 }
@@ -411,11 +417,11 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
     nz_in = static_cast<const uint32_t*>(p);
     if (direction != GFX_DIR_PUSH) {
       bool fresh = false;
-      GFX_TRY(scratch(g, "keep_head", (size_t)(n + 1) * 4, &p, &fresh));
+      GFX_TRY(scratch(g, "keep_head", (size_t)(n + 1) * 8, &p, &fresh));
       head = static_cast<int32_t*>(p);
       if (fresh)
         GFX_LAUNCH(k_pull_heads, grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream,
-                   g->rrow, g->rcol, n, head);
+                   g->rrow, g->rcol, n, head, head + n + 1);
     }
   }
   Counters* C = g->counters;  // C[0], C[1]: per-level double buffer
@@ -489,7 +495,7 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
       }
       GFX_LAUNCH(k_bfs_pull, ctx->sm_count * 8, 256, 0, ctx->stream, W, nz_in, B.visited, fcur,
                  fnext, head, g->rrow, g->rcol, directed ? 1 : 0, labels, preds,
-                 (int32_t)depth, cur);
+                 (int32_t)depth, cur, head + n + 1);
       GFX_CK(cudaGetLastError());
       if (ctx->timing) GFX_CK(cudaEventRecord(ctx->lev1, ctx->stream));
       GFX_CK(cudaMemcpyAsync(pin, cur, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
@@ -786,7 +792,7 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
         grid.sync();
       }
       pull_groups(a.words, a.nz_in, a.visited, BitmapFront{fcur}, fnext, a.head, a.rrow, a.rcol, a.directed,
-                  lab, a.preds, depth, cur, gw, nw, PS);
+                  lab, a.preds, depth, cur, gw, nw, PS, a.head + a.n + 1);
       grid.sync();
       nout = (long long)ld_ctr(&cur->out_len);
       work = (long long)ld_ctr(&cur->aux0);
@@ -866,11 +872,11 @@ static int pbfs_setup(gfx_graph* g, int64_t source, int direction, double do_a, 
     GFX_TRY(scratch(g, directed ? "nz_in" : "nz_out", W * 4, &p));
     a.nz_in = static_cast<const uint32_t*>(p);
     bool fresh = false;
-    GFX_TRY(scratch(g, "keep_head", (size_t)(n + 1) * 4, &p, &fresh));
+    GFX_TRY(scratch(g, "keep_head", (size_t)(n + 1) * 8, &p, &fresh));
     a.head = static_cast<const int32_t*>(p);
     if (fresh)
       GFX_LAUNCH(k_pull_heads, grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream, a.rrow,
-                 a.rcol, n, static_cast<int32_t*>(p));
+                 a.rcol, n, static_cast<int32_t*>(p), static_cast<int32_t*>(p) + n + 1);
   }
   a.visited = B.visited;
   a.front[0] = B.front0;

@@ -373,7 +373,7 @@ int gfx_dbfs_reset(gfx_dbfs* db, int64_t source, int64_t* nf_local) {
   {
     bool fresh = false;
     void* p = nullptr;
-    GFX_TRY(scratch(g, "keep_head", (size_t)(db->nl + 1) * 4, &p, &fresh));
+    GFX_TRY(scratch(g, "keep_dhead", (size_t)(db->nl + 1) * 4, &p, &fresh));
     head = static_cast<int32_t*>(p);
     if (fresh && db->nl > 0)
       GFX_LAUNCH(k_first_neighbour, grid_for(db->nl, 256, ctx->sm_count * 8), 256, 0, ctx->stream,
@@ -517,7 +517,7 @@ int gfx_dbfs_pull(gfx_dbfs* db, int32_t depth, int64_t* nf_local, int64_t* probe
   gfx_ctx* ctx = db->ctx;
   GFX_CK(cudaSetDevice(ctx->device));
   uint32_t* visited = static_cast<uint32_t*>(g->scratch["d_visited"].ptr);
-  int32_t* head = static_cast<int32_t*>(g->scratch["keep_head"].ptr);
+  int32_t* head = static_cast<int32_t*>(g->scratch["keep_dhead"].ptr);
   void* nzp = nullptr;
   GFX_TRY(scratch(g, "nz_out", db->wl * 4, &nzp));
   uint32_t* next = nullptr;

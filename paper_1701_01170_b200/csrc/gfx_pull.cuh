@@ -34,6 +34,7 @@ constexpr int kPullBatch = 8;  // candidates per lane in flight
 struct PullSmem {
   int32_t cand[1024];    // compacted candidate vertices of the warp's 32 words
   uint32_t newbits[32];  // found bits per word of the group
+  uint32_t hitmask[32];  // head-probe hits, one ballot per 32 consecutive candidates
 };
 static_assert(sizeof(PullSmem) <= sizeof(WarpSmem) + 1024, "pull scratch must fit the warp slice");
 constexpr int kWarpScratch = sizeof(PullSmem) > sizeof(WarpSmem) ? sizeof(PullSmem) : sizeof(WarpSmem);
@@ -61,7 +62,7 @@ __device__ __forceinline__ void pull_groups(
     const int32_t* __restrict__ head, const int64_t* __restrict__ rrow,
     const int32_t* __restrict__ rcol, int count_in_edges, const LabelOut labels,
     int32_t* __restrict__ preds, int32_t depth, Counters* __restrict__ ctr, int64_t gw,
-    int64_t nwarps, PullSmem& P) {
+    int64_t nwarps, PullSmem& P, const int32_t* __restrict__ head2 = nullptr) {
   const int lane = threadIdx.x & 31;
   unsigned long long found_cnt = 0, in_edges = 0, probes = 0, cands = 0;
   for (int64_t grp = gw; grp * 32 < words; grp += nwarps) {
@@ -77,7 +78,6 @@ __device__ __forceinline__ void pull_groups(
       if (w < words) next[w] = 0u;  // the frontier buffer is reused across levels
       continue;
     }
-    P.newbits[lane] = 0u;
     {
       uint32_t x = cand;
       int k = off;
@@ -101,25 +101,59 @@ __device__ __forceinline__ void pull_groups(
         u[q] = k < total ? P.cand[k] : -1;
         h[q] = u[q] >= 0 ? head[u[q]] : -1;
       }
+      // with head2, head carries bit 31 = "in-degree is exactly 1" (-1 stays
+      // "no in-neighbour"): such a miss is settled without a second look
+      bool last[kPullBatch];
+#pragma unroll
+      for (int q = 0; q < kPullBatch; ++q) {
+        last[q] = head2 != nullptr && h[q] != -1 && h[q] < 0;
+        if (last[q]) h[q] &= 0x7fffffff;
+      }
 #pragma unroll
       for (int q = 0; q < kPullBatch; ++q) fw[q] = h[q] >= 0 ? front.word(h[q]) : 0u;
       __syncwarp();
 #pragma unroll
       for (int q = 0; q < kPullBatch; ++q) {
         const bool hit = h[q] >= 0 && front.bit(fw[q], h[q]);
-        const bool miss = h[q] >= 0 && !hit;
+        const bool miss = h[q] >= 0 && !hit && !last[q];
+        if (h[q] >= 0 && !hit && last[q]) {  // unfound, one probe, degree 1
+          ++probes;
+          ++in_edges;
+        }
         if (hit) {
           labels.set(u[q], depth);
           preds[u[q]] = h[q];
-          atomicOr(&P.newbits[(u[q] >> 5) - grp * 32], 1u << (u[q] & 31));
           ++found_cnt;
           ++probes;
           if (count_in_edges) in_edges += (unsigned long long)(rrow[u[q] + 1] - rrow[u[q]]);
         }
+        const unsigned hm = __ballot_sync(0xffffffffu, hit);
+        if (lane == 0) P.hitmask[(base >> 5) + q] = hm;
         const unsigned mm = __ballot_sync(0xffffffffu, miss);
         if (miss) P.cand[nmiss + __popc(mm & ((1u << lane) - 1))] = u[q];
         nmiss += __popc(mm);
       }
+    }
+    __syncwarp();
+    // each lane rebuilds its word's found bits: its candidates are entries
+    // [off, off + popc(cand)) of the list, whose hit bits are consecutive in
+    // hitmask; deposit them onto the candidate bit positions (no shared
+    // atomics -- lanes of one word would all hit the same address)
+    {
+      const int c = __popc(cand);
+      uint32_t nb = 0u;
+      if (c) {
+        const int r0 = off >> 5, sh = off & 31;
+        uint32_t comp = P.hitmask[r0] >> sh;
+        if (sh && off + c > (r0 + 1) * 32) comp |= P.hitmask[r0 + 1] << (32 - sh);
+        uint32_t x = cand;
+        for (int j = 0; x; ++j) {
+          const uint32_t b = x & (0u - x);
+          if ((comp >> j) & 1u) nb |= b;
+          x ^= b;
+        }
+      }
+      P.newbits[lane] = nb;
     }
     __syncwarp();
     // phase 2: misses, one per lane, scanning on from the second in-neighbour
@@ -128,10 +162,30 @@ __device__ __forceinline__ void pull_groups(
       const int k = base + lane;
       if (k >= nmiss) continue;
       const int32_t uu = P.cand[k];
+      if (head2 != nullptr && !count_in_edges) {
+        // second in-neighbour from the dense head2 array (bit 31 = "in-degree
+        // is exactly 2"): most misses settle here without the row bounds
+        int32_t h2 = head2[uu];
+        const bool deg2 = h2 < 0;
+        h2 &= 0x7fffffff;
+        if (front.bit(front.word(h2), h2)) {
+          labels.set(uu, depth);
+          preds[uu] = h2;
+          atomicOr(&P.newbits[(uu >> 5) - grp * 32], 1u << (uu & 31));
+          ++found_cnt;
+          probes += 2;
+          continue;
+        }
+        if (deg2) {
+          probes += 2;
+          in_edges += 2;
+          continue;
+        }
+      }
       const int64_t b = rrow[uu], e = rrow[uu + 1];
       bool found = false;
       int32_t par = -1;
-      int64_t p = b + 1;
+      int64_t p = b + ((head2 != nullptr && !count_in_edges) ? 2 : 1);
       while (p < e && !found) {
         int32_t sv[4];
         uint32_t wv[4];
