@@ -44,13 +44,17 @@ struct SsspRelaxOp {
     for (int u = 0; u < kBatch; ++u) cur[u] = d[u] >= 0 ? dist[d[u]] : 0u;
   }
   // atomic_min relax (operators.py:111-124): emit d once per iteration when
-  // its distance strictly improved
+  // its distance improves.  The gate is the prefetched distance; both minima
+  // are fire-and-forget reductions (no round trip on the 64-bit dp word,
+  // which lives in HBM), and only the L2-resident mark bit is read back, to
+  // emit each improved vertex once.  A vertex that passes the gate while a
+  // concurrent relaxation lowers it further is still (correctly) emitted:
+  // it did improve this iteration.
   __device__ bool visit(int u, int32_t d, int32_t s, int32_t w, int32_t sdist, int64_t) {
     const unsigned long long nd = (unsigned long long)(uint32_t)sdist + (uint32_t)w;
     if (nd >= cur[u]) return false;
     const unsigned long long key = (nd << 32) | (uint32_t)s;
-    const unsigned long long old = atomicMin(&dp[d], key);
-    if ((old >> 32) <= nd) return false;
+    atomicMin(&dp[d], key);
     atomicMin(&dist[d], (uint32_t)nd);
     const uint32_t bit = 1u << (d & 31);
     return !(atomicOr(&mark[d >> 5], bit) & bit);
