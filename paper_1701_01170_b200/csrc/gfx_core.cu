@@ -351,6 +351,7 @@ int gfx_graph_refresh(gfx_graph* g) {
     GFX_TRY(refresh_pull_heads(g));
   }
   g->m_oriented = -1;  // the oriented CSR (TC) is rebuilt on next use
+  g->w8_state = 0;     // and the compact weight copy (SSSP)
   auto* pin = static_cast<unsigned long long*>(ctx->pinned);
   GFX_CK(cudaMemcpyAsync(pin, dmax, 8, cudaMemcpyDeviceToHost, ctx->stream));
   GFX_CK(cudaStreamSynchronize(ctx->stream));

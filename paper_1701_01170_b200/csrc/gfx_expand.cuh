@@ -34,10 +34,36 @@
 //                         int32_t sval, int64_t edge);  // u = prefetch slot
 #pragma once
 
+#include <type_traits>
+
 #include "gfx_device.cuh"
 #include "gfx_internal.cuh"
 
 namespace gfx {
+
+// element type of the weight stream an Op reads (Op::WeightT, default int32)
+template <class Op, class = void>
+struct WeightOf {
+  using T = int32_t;
+};
+template <class Op>
+struct WeightOf<Op, std::void_t<typename Op::WeightT>> {
+  using T = typename Op::WeightT;
+};
+template <class T>
+__device__ __forceinline__ int32_t ld_weight(const T* p, unsigned long long pol);
+template <>
+__device__ __forceinline__ int32_t ld_weight<int32_t>(const int32_t* p, unsigned long long pol) {
+  return ld_stream_i32(p, pol);
+}
+template <>
+__device__ __forceinline__ int32_t ld_weight<uint8_t>(const uint8_t* p, unsigned long long pol) {
+  unsigned short v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;"
+               : "=h"(v)
+               : "l"(p), "l"(pol));
+  return (int32_t)v;
+}
 
 constexpr int kExpandBlock = 256;
 constexpr int kWarpsPerBlock = kExpandBlock / 32;
@@ -80,7 +106,7 @@ __device__ __forceinline__ void expand_tasks(WarpSmem& W, Op& o, const int32_t* 
                                              const int64_t* __restrict__ rowbase,
                                              const int32_t* __restrict__ part, int64_t ntiles,
                                              int64_t total, const int32_t* __restrict__ col,
-                                             const int32_t* __restrict__ wgt,
+                                             const typename WeightOf<Op>::T* __restrict__ wgt,
                                              int32_t* __restrict__ out,
                                              unsigned long long* __restrict__ out_len,
                                              int64_t task0, int64_t ntasks) {
@@ -161,7 +187,7 @@ __device__ __forceinline__ void expand_tasks(WarpSmem& W, Op& o, const int32_t* 
           const int32_t ksrc = __shfl_sync(0xffffffffu, v, k);
           const int32_t ksv = Op::kSrcVal ? __shfl_sync(0xffffffffu, my_sv, k) : 0;
           const int32_t* cbase = col + kdel + klo + lane;
-          const int32_t* wbase = Op::kWeights ? wgt + kdel + klo + lane : nullptr;
+          const typename WeightOf<Op>::T* wbase = Op::kWeights ? wgt + kdel + klo + lane : nullptr;
           const int klen = (int)(khi - klo);
           for (int jb = 0; jb < klen; jb += 32 * B) {
             int32_t d[B];
@@ -173,7 +199,7 @@ __device__ __forceinline__ void expand_tasks(WarpSmem& W, Op& o, const int32_t* 
               if (Op::kWeights) w[Op::kWeights ? q : 0] = 0;
               if (q * 32 < lim) {
                 d[q] = ld_stream_i32(cbase + jb + q * 32, pol);
-                if (Op::kWeights) w[Op::kWeights ? q : 0] = ld_stream_i32(wbase + jb + q * 32, pol);
+                if (Op::kWeights) w[Op::kWeights ? q : 0] = ld_weight(wbase + jb + q * 32, pol);
               }
             }
             o.prefetch(d);
@@ -244,7 +270,7 @@ __device__ __forceinline__ void expand_tasks(WarpSmem& W, Op& o, const int32_t* 
             const int it = W.owner[j];
             const int64_t e = W.delta[it] + s0 + j;
             d[k] = ld_stream_i32(col + e, pol);
-            if (Op::kWeights) w[Op::kWeights ? k : 0] = ld_stream_i32(wgt + e, pol);
+            if (Op::kWeights) w[Op::kWeights ? k : 0] = ld_weight(wgt + e, pol);
           }
         }
         o.prefetch(d);
@@ -276,7 +302,8 @@ __global__ void __launch_bounds__(kExpandBlock, Op::kMinBlocks)
     k_lb_expand(const int32_t* __restrict__ F, const unsigned long long* __restrict__ nf_d,
                 const int64_t* __restrict__ scan, const int64_t* __restrict__ rowbase,
                 const int32_t* __restrict__ part, const Counters* __restrict__ plan,
-                const int32_t* __restrict__ col, const int32_t* __restrict__ wgt, Op op,
+                const int32_t* __restrict__ col, const typename WeightOf<Op>::T* __restrict__ wgt,
+                Op op,
                 int32_t* __restrict__ out, unsigned long long* __restrict__ out_len) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WarpSmem& W = warp_smem(smem_raw);
@@ -303,7 +330,7 @@ int set_expand_smem() {
 template <class Op>
 int lb_advance(gfx_graph* g, const int32_t* F, const unsigned long long* nf_d, int64_t nf_max,
                Counters* plan_ctr, int64_t* scan, int64_t* rowbase, int32_t* part, const Op& op,
-               int32_t* out, unsigned long long* out_len) {
+               int32_t* out, unsigned long long* out_len, const void* wgt = nullptr) {
   gfx_ctx* ctx = g->ctx;
   GFX_TRY(launch_degree_scan(g, F, nf_d, nf_max, g->row, scan, rowbase, part, plan_ctr));
   GFX_TRY(set_expand_smem<Op>());
@@ -315,7 +342,8 @@ int lb_advance(gfx_graph* g, const int32_t* F, const unsigned long long* nf_d, i
   }
   const int grid = ctx->sm_count * per_sm;
   GFX_LAUNCH((k_lb_expand<Op>), grid, kExpandBlock, expand_smem_bytes(), ctx->stream, F, nf_d,
-             scan, rowbase, part, plan_ctr, g->col, g->w, op, out, out_len);
+             scan, rowbase, part, plan_ctr, g->col,
+             reinterpret_cast<const typename WeightOf<Op>::T*>(wgt ? wgt : g->w), op, out, out_len);
   GFX_CK(cudaGetLastError());
   return GFX_OK;
 }

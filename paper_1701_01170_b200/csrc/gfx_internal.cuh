@@ -96,6 +96,9 @@ struct gfx_graph {
   gfx::Counters* counters = nullptr;  // device
   // oriented CSR for TC
   int64_t m_oriented = -1;
+  // compact 8-bit copy of the weights (SSSP streams 5 instead of 8 bytes per
+  // slot when every weight fits 0..255): 0 unknown, 1 built ("keep_w8"), 2 no
+  int w8_state = 0;
   // decoupled look-back bookkeeping (per graph): epoch tags + per-epoch
   // dynamic tile counters, both cleared when the epoch wraps
   unsigned int epoch = 0;

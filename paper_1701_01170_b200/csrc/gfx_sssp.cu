@@ -30,7 +30,9 @@
 
 namespace gfx {
 
+template <class WT>
 struct SsspRelaxOp {
+  using WeightT = WT;  // weight stream element: int32 or the compact uint8 copy
   static constexpr bool kWeights = true, kSrcVal = true, kEmitEdge = false;
   static constexpr int kBatch = 4;
   static constexpr int kMinBlocks = 3;
@@ -60,6 +62,42 @@ struct SsspRelaxOp {
     return !(atomicOr(&mark[d >> 5], bit) & bit);
   }
 };
+
+// narrow the int32 weights to bytes; flag any weight outside 0..255
+__global__ void k_weights_u8(const int32_t* __restrict__ w, int64_t m, uint8_t* __restrict__ w8,
+                             unsigned* __restrict__ bad) {
+  unsigned any = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t x = w[i];
+    any |= (x < 0 || x > 255) ? 1u : 0u;
+    w8[i] = (uint8_t)x;
+  }
+  if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
+}
+
+// the graph's compact weight copy, built once (nullptr when a weight
+// exceeds a byte)
+static int weights_u8(gfx_graph* g, const uint8_t** out) {
+  *out = nullptr;
+  if (g->w8_state == 2) return GFX_OK;
+  void* p = nullptr;
+  GFX_TRY(scratch(g, "keep_w8", (size_t)g->m + 16, &p));
+  if (g->w8_state == 0) {
+    gfx_ctx* ctx = g->ctx;
+    unsigned* bad = reinterpret_cast<unsigned*>(g->counters) + 60;
+    GFX_CK(cudaMemsetAsync(bad, 0, 4, ctx->stream));
+    GFX_LAUNCH(k_weights_u8, grid_for(g->m, 256, ctx->sm_count * 8), 256, 0, ctx->stream, g->w,
+               g->m, static_cast<uint8_t*>(p), bad);
+    unsigned h = 0;
+    GFX_CK(cudaMemcpyAsync(&h, bad, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    GFX_CK(cudaStreamSynchronize(ctx->stream));
+    g->w8_state = h ? 2 : 1;
+    if (h) return GFX_OK;
+  }
+  *out = static_cast<const uint8_t*>(p);
+  return GFX_OK;
+}
 
 __global__ void k_sssp_seed(unsigned long long* dp, uint32_t* dist, int32_t src, int32_t* near) {
   dp[src] = 0xFFFFFFFFull;  // dist 0, pred -1
@@ -213,6 +251,8 @@ int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t*
   GFX_TRY(scratch_t(g, "q_rowbase", n + 1, &rowbase));
   GFX_TRY(scratch_t(g, "q_part", part_capacity(g->m, g->n), &part));
 
+  const uint8_t* w8 = nullptr;
+  if (!getenv("GFX_SSSP_W32")) GFX_TRY(weights_u8(g, &w8));
   Counters* C = g->counters;  // C[0]/C[1]: near sizes, C[2]: relax plan, C[3]: far
   auto* pin = static_cast<Counters*>(ctx->pinned);
   const int grid = ctx->sm_count * 8;
@@ -258,9 +298,15 @@ int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t*
     Counters* nxt = &C[curq ^ 1];
     GFX_CK(cudaMemsetAsync(&C[2], 0, sizeof(Counters), ctx->stream));
     GFX_CK(cudaMemsetAsync(nxt, 0, sizeof(Counters), ctx->stream));
-    SsspRelaxOp op{dp, dist32, mark, {}};
-    GFX_TRY(lb_advance(g, nearq[curq], &cur->out_len, nnear, &C[2], scan, rowbase, part, op,
-                       touched, &C[2].out_len));
+    if (w8) {
+      SsspRelaxOp<uint8_t> op{dp, dist32, mark, {}};
+      GFX_TRY(lb_advance(g, nearq[curq], &cur->out_len, nnear, &C[2], scan, rowbase, part, op,
+                         touched, &C[2].out_len, w8));
+    } else {
+      SsspRelaxOp<int32_t> op{dp, dist32, mark, {}};
+      GFX_TRY(lb_advance(g, nearq[curq], &cur->out_len, nnear, &C[2], scan, rowbase, part, op,
+                         touched, &C[2].out_len));
+    }
     GFX_LAUNCH(k_sssp_split, grid_for(n, 256, grid), 256, 0, ctx->stream, touched, &C[2].out_len,
                dist32, mark, threshold, nearq[curq ^ 1], &nxt->out_len, far, fkey, &C[3].aux0);
     GFX_CK(cudaGetLastError());
