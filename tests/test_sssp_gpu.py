@@ -67,8 +67,15 @@ def test_device_graph_golden(scale):
     from paper_1701_01170_b200.generators import rmat_device_graph
     from paper_1701_01170_b200.primitives.sssp import sssp_device
 
+    from paper_1701_01170_b200._results import preds_to_host
+
     rec, _ = rmat_golden(scale)
     dg = rmat_device_graph(scale, 16, 0, weights=(1, 64), weight_seed=0)
+    host = (dg.row.cpu().numpy(), dg.col.cpu().numpy().astype(np.int64),
+            dg.w.cpu().numpy().astype(np.int64))
     for delta, key in ((32, "sssp_d32"), (None, "sssp_default")):
         dist, preds, st = sssp_device(dg, 0, delta=delta)
-        assert sha(labels_to_host(dist)) == rec[key + "_sha"], (scale, delta)
+        lab = labels_to_host(dist)
+        assert sha(lab) == rec[key + "_sha"], (scale, delta)
+        # preds recovered from the final distances (undirected path)
+        assert valid_sssp_preds(*host, lab, preds_to_host(preds), 0), (scale, delta)
