@@ -590,6 +590,7 @@ struct PBfsArgs {
   int32_t* preds;
   uint8_t* lvl8;  // depth bytes while labels are deferred (see LabelOut)
   int vec_ok;     // labels/preds 16-byte aligned: vector stores
+  int64_t nnz;    // vertices with out-degree > 0 (graph constant)
   Counters* C;  // 3 rotating counter blocks
   gfx_iter_rec* recs;
   int64_t rec_cap;
@@ -792,7 +793,10 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
         grid.sync();
       }
       pull_groups(a.words, a.nz_in, a.visited, BitmapFront{fcur}, fnext, a.head, a.rrow, a.rcol, a.directed,
-                  lab, a.preds, depth, cur, gw, nw, PS, a.head + a.n + 1);
+                  lab, a.preds, depth, cur, gw, nw, PS, a.head + a.n + 1,
+                  // dynamic tail only on dense levels (unvisited non-isolated
+                  // vertices above n/8); sparse levels keep the static deal
+                  (c.n_u - (a.n - a.nnz)) * 8 > a.n ? &cur->aux2 : nullptr);
       grid.sync();
       nout = (long long)ld_ctr(&cur->out_len);
       work = (long long)ld_ctr(&cur->aux0);
@@ -890,6 +894,7 @@ static int pbfs_setup(gfx_graph* g, int64_t source, int direction, double do_a, 
   a.labels = labels;
   a.preds = preds;
   a.vec_ok = ((reinterpret_cast<uintptr_t>(labels) | reinterpret_cast<uintptr_t>(preds)) & 15) == 0;
+  a.nnz = g->nnz_vertices;
   GFX_TRY(scratch_t(g, "bfs_lvl8", (size_t)n + 4, &a.lvl8));
   a.C = g->counters;
   const int64_t cap = 1 << 16;  // level records kept on device (stats)

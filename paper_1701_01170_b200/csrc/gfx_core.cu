@@ -158,20 +158,26 @@ __global__ void k_nonzero_bitmap(const int64_t* __restrict__ row, int64_t n, int
   }
 }
 
+// max out-degree -> out[0], number of vertices with out-degree > 0 -> out[-1]
 __global__ void k_max_degree(const int64_t* __restrict__ row, int64_t n,
                              unsigned long long* __restrict__ out) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  unsigned long long best = 0;
+  unsigned long long best = 0, nnz = 0;
   for (; i < n; i += stride) {
     unsigned long long d = (unsigned long long)(row[i + 1] - row[i]);
     best = d > best ? d : best;
+    nnz += d > 0;
   }
   for (int o = 16; o; o >>= 1) {
     unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
     best = y > best ? y : best;
+    nnz += __shfl_xor_sync(0xffffffffu, nnz, o);
   }
-  if ((threadIdx.x & 31) == 0) atomicMax(out, best);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out, best);
+    atomicAdd(out - 1, nnz);
+  }
 }
 
 int build_nonzero_bitmap(gfx_graph* g, const int64_t* row, const char* name) {
@@ -292,7 +298,7 @@ int gfx_graph_create(gfx_ctx* ctx, int64_t n, int64_t m, const int64_t* row_d,
   // max degree + nonzero bitmaps (graph constants)
   auto* pin = static_cast<unsigned long long*>(ctx->pinned);
   unsigned long long* dmax = reinterpret_cast<unsigned long long*>(g->counters) + 31;
-  cudaMemsetAsync(dmax, 0, 8, ctx->stream);
+  cudaMemsetAsync(dmax - 1, 0, 16, ctx->stream);
   if (n > 0) {
     GFX_LAUNCH(k_max_degree, grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream, row_d, n, dmax);
     st = build_nonzero_bitmap(g, row_d, "nz_out");
@@ -301,13 +307,14 @@ int gfx_graph_create(gfx_ctx* ctx, int64_t n, int64_t m, const int64_t* row_d,
       return st;
     }
   }
-  cudaMemcpyAsync(pin, dmax, 8, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaMemcpyAsync(pin, dmax - 1, 16, cudaMemcpyDeviceToHost, ctx->stream);
   cudaError_t e = cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) {
     delete g;
     return cuda_status(e, "graph create", __FILE__, __LINE__);
   }
-  g->max_deg = (int64_t)pin[0];
+  g->nnz_vertices = (int64_t)pin[0];
+  g->max_deg = (int64_t)pin[1];
   *out = g;
   return GFX_OK;
 }
@@ -341,7 +348,7 @@ int gfx_graph_refresh(gfx_graph* g) {
   // the caller rewrote the borrowed arrays in place (same n, m): recompute
   // every graph constant derived from them, keep the scratch allocations
   unsigned long long* dmax = reinterpret_cast<unsigned long long*>(g->counters) + 31;
-  GFX_CK(cudaMemsetAsync(dmax, 0, 8, ctx->stream));
+  GFX_CK(cudaMemsetAsync(dmax - 1, 0, 16, ctx->stream));
   if (g->n > 0) {
     GFX_LAUNCH(k_max_degree, grid_for(g->n, 256, ctx->sm_count * 8), 256, 0, ctx->stream, g->row,
                g->n, dmax);
@@ -353,9 +360,10 @@ int gfx_graph_refresh(gfx_graph* g) {
   g->m_oriented = -1;  // the oriented CSR (TC) is rebuilt on next use
   g->w8_state = 0;     // and the compact weight copy (SSSP)
   auto* pin = static_cast<unsigned long long*>(ctx->pinned);
-  GFX_CK(cudaMemcpyAsync(pin, dmax, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  GFX_CK(cudaMemcpyAsync(pin, dmax - 1, 16, cudaMemcpyDeviceToHost, ctx->stream));
   GFX_CK(cudaStreamSynchronize(ctx->stream));
-  g->max_deg = (int64_t)pin[0];
+  g->nnz_vertices = (int64_t)pin[0];
+  g->max_deg = (int64_t)pin[1];
   return GFX_OK;
 }
 

@@ -91,6 +91,7 @@ struct gfx_graph {
   const int32_t* rcol = nullptr;
   int flags = 0;
   int64_t max_deg = 0;
+  int64_t nnz_vertices = 0;       // vertices with out-degree > 0
   int64_t words = 0;              // ceil(n/32)
   std::unordered_map<std::string, gfx::gfx_buffer> scratch;
   gfx::Counters* counters = nullptr;  // device

@@ -62,10 +62,21 @@ __device__ __forceinline__ void pull_groups(
     const int32_t* __restrict__ head, const int64_t* __restrict__ rrow,
     const int32_t* __restrict__ rcol, int count_in_edges, const LabelOut labels,
     int32_t* __restrict__ preds, int32_t depth, Counters* __restrict__ ctr, int64_t gw,
-    int64_t nwarps, PullSmem& P, const int32_t* __restrict__ head2 = nullptr) {
+    int64_t nwarps, PullSmem& P, const int32_t* __restrict__ head2 = nullptr,
+    unsigned long long* __restrict__ grab = nullptr) {
   const int lane = threadIdx.x & 31;
   unsigned long long found_cnt = 0, in_edges = 0, probes = 0, cands = 0;
-  for (int64_t grp = gw; grp * 32 < words; grp += nwarps) {
+  // groups are dealt out statically for all but the last ~1.5 rounds; the
+  // rest are handed out dynamically when `grab` (a zeroed counter) is given
+  // -- the next group is claimed while this one is processed -- so warps
+  // with slow groups do not set the level's tail
+  const int64_t ngroups = (words + 31) / 32;
+  // (every warp's first group is static: the dynamic range starts after them)
+  const int64_t nstatic = grab ? max(ngroups / nwarps - 1, (int64_t)1) * nwarps : ngroups;
+  unsigned long long nxt = 0;
+  for (int64_t grp = gw; grp < ngroups;) {
+    const bool dyn_next = grp + nwarps >= nstatic;
+    if (grab && dyn_next && lane == 0) nxt = atomicAdd(grab, 1ull);
     const int64_t w = grp * 32 + lane;
     uint32_t vis = 0xffffffffu, cand = 0;
     if (w < words) {
@@ -76,6 +87,7 @@ __device__ __forceinline__ void pull_groups(
     const int off = warp_excl_scan(__popc(cand), lane, &total);
     if (total == 0) {
       if (w < words) next[w] = 0u;  // the frontier buffer is reused across levels
+      grp = (grab && dyn_next) ? nstatic + (int64_t)__shfl_sync(0xffffffffu, nxt, 0) : grp + nwarps;
       continue;
     }
     {
@@ -217,10 +229,9 @@ __device__ __forceinline__ void pull_groups(
       const uint32_t nb = P.newbits[lane];
       next[w] = nb;
       if (nb) visited[w] = vis | nb;
-    } else {
-      (void)0;
     }
     __syncwarp();
+    grp = (grab && dyn_next) ? nstatic + (int64_t)__shfl_sync(0xffffffffu, nxt, 0) : grp + nwarps;
   }
   found_cnt = warp_sum_u64(found_cnt);
   in_edges = warp_sum_u64(in_edges);
