@@ -27,9 +27,13 @@ __device__ __forceinline__ unsigned long long pack_status(unsigned long long fla
   return flag | ((unsigned long long)(epoch & 0x3FFF) << 48) | (v & kValMask);
 }
 
+constexpr int kLongFill = 16;  // items owning more tiles than this are filled by the whole block
 struct ScanSmem {
   int64_t warp[kScanBlock / 32];
   int64_t prefix;
+  int64_t lk0[kLongFill], lk1[kLongFill];  // long partition ranges [k0, k1] of item li
+  int32_t li[kLongFill];
+  int nlong;
 };
 
 // one tile of kScanTileItems frontier items (blockDim == kScanBlock)
@@ -41,6 +45,7 @@ __device__ __forceinline__ void scan_tile(int64_t tile, int64_t ntiles,
                                           int32_t* __restrict__ part, unsigned long long* status,
                                           unsigned ep, Counters* __restrict__ ctr, ScanSmem& sm) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) sm.nlong = 0;
   const int64_t base = tile * kScanTileItems + (int64_t)threadIdx.x * kScanItems;
   int64_t deg[kScanItems];
   int64_t rb[kScanItems];
@@ -125,10 +130,23 @@ __device__ __forceinline__ void scan_tile(int64_t tile, int64_t ntiles,
       const int64_t ub = run + (int64_t)kItemUnits * i;
       const int64_t k0 = (ub + kTile - 1) / kTile;
       const int64_t k1 = (ub + kItemUnits + deg[k] - 1) / kTile;
-      for (int64_t t = k0; t <= k1; ++t) part[t] = (int32_t)i;
+      int slot = -1;
+      if (k1 - k0 >= kLongFill) {  // a hub: the block fills its range below
+        slot = atomicAdd(&sm.nlong, 1);
+        if (slot < kLongFill) {
+          sm.lk0[slot] = k0;
+          sm.lk1[slot] = k1;
+          sm.li[slot] = (int32_t)i;
+        }
+      }
+      if (slot < 0 || slot >= kLongFill)
+        for (int64_t t = k0; t <= k1; ++t) part[t] = (int32_t)i;
     }
     run += deg[k];
   }
+  __syncthreads();
+  for (int j = 0; j < min(sm.nlong, kLongFill); ++j)
+    for (int64_t t = sm.lk0[j] + threadIdx.x; t <= sm.lk1[j]; t += kScanBlock) part[t] = sm.li[j];
   if (tile == ntiles - 1 && threadIdx.x == kScanBlock - 1) {
     // the last thread of the last tile holds the grand total
     scan[nf] = run;
