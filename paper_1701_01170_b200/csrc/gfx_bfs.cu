@@ -636,6 +636,76 @@ __device__ __noinline__ void device_decide(long long n, long long m, long long n
     *mode = GFX_DIR_PUSH;
 }
 
+// Push expansion of a frontier of at most 32 items without a scan pass:
+// each warp loads every item's row bounds (one per lane), scans the degrees
+// with shuffles, and expands its own chunks of 32 * Op::kBatch consecutive
+// slots (chunk c = gw, gw + nw, ...); a slot's item comes from a binary
+// search over the <= 32 prefix offsets kept in the warp's shared memory.
+// Output and claims as expand_tasks; *total receives the slot count.
+template <class Op>
+__device__ __forceinline__ void small_push(WarpSmem& W, Op& o, const int32_t* __restrict__ F,
+                                           int64_t nf, const int64_t* __restrict__ row,
+                                           const int32_t* __restrict__ col,
+                                           int32_t* __restrict__ out,
+                                           unsigned long long* __restrict__ out_len,
+                                           unsigned long long* __restrict__ total_out,
+                                           int64_t gw, int64_t nw) {
+  constexpr int B = Op::kBatch;
+  const int lane = threadIdx.x & 31;
+  int64_t* ex = reinterpret_cast<int64_t*>(W.owner);  // exclusive prefix, 33 entries
+  int32_t v = 0;
+  int64_t rb = 0, deg = 0;
+  if (lane < nf) {
+    v = F[lane];
+    rb = row[v];
+    deg = row[v + 1] - rb;
+  }
+  int64_t incl = deg;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += y;
+  }
+  const int64_t total = __shfl_sync(0xffffffffu, incl, 31);
+  ex[lane] = incl - deg;
+  W.delta[lane] = rb - (incl - deg);
+  W.src[lane] = v;
+  __syncwarp();
+  if (gw == 0 && lane == 0) *total_out = (unsigned long long)total;
+  const unsigned long long pol = l2_evict_first_policy();
+  const int nitems = (int)nf;
+  int ocnt = 0;
+  for (int64_t c0 = gw * 32 * B; c0 < total; c0 += nw * 32 * B) {
+    int32_t d[B];
+    int it[B];
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      const int64_t sl = c0 + q * 32 + lane;
+      d[q] = -1;
+      it[q] = 0;
+      if (sl < total) {
+        int lo = 0, hi = nitems - 1;  // last item with ex[item] <= sl
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (ex[mid] <= sl) lo = mid; else hi = mid - 1;
+        }
+        it[q] = lo;
+        d[q] = ld_stream_i32(col + W.delta[lo] + sl, pol);
+      }
+    }
+    o.prefetch(d);
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      const bool emit = d[q] >= 0 && o.visit(q, d[q], W.src[it[q]], 1, 0, 0);
+      const unsigned em = __ballot_sync(0xffffffffu, emit);
+      if (emit) W.obuf[ocnt + __popc(em & ((1u << lane) - 1))] = d[q];
+      ocnt += __popc(em);
+    }
+    if (ocnt > kOutCap - 32 * B) warp_flush(W, ocnt, out, out_len);
+  }
+  warp_flush(W, ocnt, out, out_len);
+}
+
 // Deferred labels: write labels[v] = depth byte of v if visited, else
 // UNVISITED, for every vertex (preds were set to -1 at launch and written at
 // discovery).  A warp covers 1024 vertices in 8 independent chunks of 128;
@@ -766,16 +836,24 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
         __syncthreads();
       }
       const int32_t* F = a.order + c.q_off;
-      const int64_t stiles = nf > 0 ? (nf + kScanTileItems - 1) / kScanTileItems : 1;
-      const unsigned ep = a.epoch_base + (unsigned)c.depth;
-      for (int64_t t = blockIdx.x; t < stiles; t += gridDim.x)
-        scan_tile(t, stiles, F, nf, a.row, a.scan, a.rowbase, a.part, a.status, ep, cur, ss);
-      grid.sync();
       BfsClaimOp op{a.visited, a.labels, a.preds, depth, {}, lab.lvl8};
-      expand_tasks(W, op, F, nf, a.scan, a.rowbase, a.part, (int64_t)ld_ctr(&cur->ntiles),
-                   (int64_t)ld_ctr(&cur->total), a.col, nullptr, a.order + c.q_end,
-                   &cur->out_len, gw, nw);
-      for (int64_t i = gtid; i < stiles; i += nthr) a.status[i] = 0ull;
+      if (nf <= 32) {
+        // tiny frontier (the hub's level, the tail levels): every warp derives
+        // the whole expansion plan itself -- no scan pass, no grid barrier
+        // between plan and expansion
+        small_push(W, op, F, nf, a.row, a.col, a.order + c.q_end, &cur->out_len, &cur->total,
+                   gw, nw);
+      } else {
+        const int64_t stiles = (nf + kScanTileItems - 1) / kScanTileItems;
+        const unsigned ep = a.epoch_base + (unsigned)c.depth;
+        for (int64_t t = blockIdx.x; t < stiles; t += gridDim.x)
+          scan_tile(t, stiles, F, nf, a.row, a.scan, a.rowbase, a.part, a.status, ep, cur, ss);
+        grid.sync();
+        expand_tasks(W, op, F, nf, a.scan, a.rowbase, a.part, (int64_t)ld_ctr(&cur->ntiles),
+                     (int64_t)ld_ctr(&cur->total), a.col, nullptr, a.order + c.q_end,
+                     &cur->out_len, gw, nw);
+        for (int64_t i = gtid; i < stiles; i += nthr) a.status[i] = 0ull;
+      }
       grid.sync();
       level_edges = (long long)ld_ctr(&cur->total);
       nout = (long long)ld_ctr(&cur->out_len);
