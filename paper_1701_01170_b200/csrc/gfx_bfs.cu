@@ -636,30 +636,22 @@ __device__ __noinline__ void device_decide(long long n, long long m, long long n
     *mode = GFX_DIR_PUSH;
 }
 
-// Push expansion of a frontier of at most 32 items without a scan pass:
-// each warp loads every item's row bounds (one per lane), scans the degrees
-// with shuffles, and expands its own chunks of 32 * Op::kBatch consecutive
-// slots (chunk c = gw, gw + nw, ...); a slot's item comes from a binary
-// search over the <= 32 prefix offsets kept in the warp's shared memory.
-// Output and claims as expand_tasks; *total receives the slot count.
+// Expansion of at most 32 items held one per lane (v, row base, degree; 0
+// for empty lanes) without any scan pass: the degrees are scanned with
+// shuffles, the exclusive offsets parked in the warp's shared memory, and
+// the slots [c0, c0 + 32 * Op::kBatch) for c0 = chunk0, chunk0 + stride, ...
+// expanded by this warp; a slot's item comes from a binary search over the
+// <= 32 offsets.  Returns the item set's slot count.  Output and claims as
+// expand_tasks (staged in the warp buffer, ocnt carried by the caller).
 template <class Op>
-__device__ __forceinline__ void small_push(WarpSmem& W, Op& o, const int32_t* __restrict__ F,
-                                           int64_t nf, const int64_t* __restrict__ row,
-                                           const int32_t* __restrict__ col,
-                                           int32_t* __restrict__ out,
-                                           unsigned long long* __restrict__ out_len,
-                                           unsigned long long* __restrict__ total_out,
-                                           int64_t gw, int64_t nw) {
+__device__ __forceinline__ int64_t expand_items32(WarpSmem& W, Op& o, int32_t v, int64_t rb,
+                                                  int64_t deg, const int32_t* __restrict__ col,
+                                                  int32_t* __restrict__ out,
+                                                  unsigned long long* __restrict__ out_len,
+                                                  int& ocnt, int64_t chunk0, int64_t stride) {
   constexpr int B = Op::kBatch;
   const int lane = threadIdx.x & 31;
-  int64_t* ex = reinterpret_cast<int64_t*>(W.owner);  // exclusive prefix, 33 entries
-  int32_t v = 0;
-  int64_t rb = 0, deg = 0;
-  if (lane < nf) {
-    v = F[lane];
-    rb = row[v];
-    deg = row[v + 1] - rb;
-  }
+  int64_t* ex = reinterpret_cast<int64_t*>(W.owner);  // exclusive offsets
   int64_t incl = deg;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
@@ -667,15 +659,13 @@ __device__ __forceinline__ void small_push(WarpSmem& W, Op& o, const int32_t* __
     if (lane >= off) incl += y;
   }
   const int64_t total = __shfl_sync(0xffffffffu, incl, 31);
+  __syncwarp();
   ex[lane] = incl - deg;
   W.delta[lane] = rb - (incl - deg);
   W.src[lane] = v;
   __syncwarp();
-  if (gw == 0 && lane == 0) *total_out = (unsigned long long)total;
   const unsigned long long pol = l2_evict_first_policy();
-  const int nitems = (int)nf;
-  int ocnt = 0;
-  for (int64_t c0 = gw * 32 * B; c0 < total; c0 += nw * 32 * B) {
+  for (int64_t c0 = chunk0; c0 < total; c0 += stride) {
     int32_t d[B];
     int it[B];
 #pragma unroll
@@ -684,7 +674,7 @@ __device__ __forceinline__ void small_push(WarpSmem& W, Op& o, const int32_t* __
       d[q] = -1;
       it[q] = 0;
       if (sl < total) {
-        int lo = 0, hi = nitems - 1;  // last item with ex[item] <= sl
+        int lo = 0, hi = 31;  // last item with ex[item] <= sl (empty items repeat offsets)
         while (lo < hi) {
           const int mid = (lo + hi + 1) >> 1;
           if (ex[mid] <= sl) lo = mid; else hi = mid - 1;
@@ -703,7 +693,76 @@ __device__ __forceinline__ void small_push(WarpSmem& W, Op& o, const int32_t* __
     }
     if (ocnt > kOutCap - 32 * B) warp_flush(W, ocnt, out, out_len);
   }
+  __syncwarp();
+  return total;
+}
+
+// A frontier of <= 32 items: every warp derives the whole plan and takes
+// its own slot chunks (the hub's level, the last levels).
+template <class Op>
+__device__ __forceinline__ void push_tiny(WarpSmem& W, Op& o, const int32_t* __restrict__ F,
+                                          int64_t nf, const int64_t* __restrict__ row,
+                                          const int32_t* __restrict__ col,
+                                          int32_t* __restrict__ out,
+                                          unsigned long long* __restrict__ out_len,
+                                          unsigned long long* __restrict__ total_out, int64_t gw,
+                                          int64_t nw) {
+  const int lane = threadIdx.x & 31;
+  int32_t v = 0;
+  int64_t rb = 0, deg = 0;
+  if (lane < nf) {
+    v = F[lane];
+    rb = row[v];
+    deg = row[v + 1] - rb;
+  }
+  int ocnt = 0;
+  const int64_t total = expand_items32(W, o, v, rb, deg, col, out, out_len, ocnt,
+                                       gw * 32 * Op::kBatch, nw * 32 * Op::kBatch);
   warp_flush(W, ocnt, out, out_len);
+  if (gw == 0 && lane == 0) *total_out = (unsigned long long)total;
+}
+
+// A frontier of up to kMidItems items: each warp expands 32 consecutive
+// items by itself (no scan pass, no plan barrier); items with more than
+// kHeavyDeg slots are set aside in `heavy` (count in *nheavy) for a second,
+// cooperative pass after the caller's barrier.
+constexpr int64_t kMidItems = 1 << 16;
+constexpr int64_t kHeavyDeg = 1024;
+template <class Op>
+__device__ __forceinline__ void push_mid(WarpSmem& W, Op& o, const int32_t* __restrict__ F,
+                                         int64_t nf, const int64_t* __restrict__ row,
+                                         const int32_t* __restrict__ col,
+                                         int32_t* __restrict__ out,
+                                         unsigned long long* __restrict__ out_len,
+                                         unsigned long long* __restrict__ total_out,
+                                         int32_t* __restrict__ heavy,
+                                         unsigned long long* __restrict__ nheavy, int64_t gw,
+                                         int64_t nw) {
+  const int lane = threadIdx.x & 31;
+  int ocnt = 0;
+  unsigned long long tot = 0;
+  for (int64_t base = gw * 32; base < nf; base += nw * 32) {
+    const int64_t i = base + lane;
+    int32_t v = 0;
+    int64_t rb = 0, deg = 0;
+    if (i < nf) {
+      v = F[i];
+      rb = row[v];
+      deg = row[v + 1] - rb;
+    }
+    const bool hv = deg > kHeavyDeg;
+    const unsigned hm = __ballot_sync(0xffffffffu, hv);
+    if (hm) {
+      unsigned long long at = 0;
+      if (lane == __ffs(hm) - 1) at = atomicAdd(nheavy, (unsigned long long)__popc(hm));
+      at = __shfl_sync(0xffffffffu, at, __ffs(hm) - 1);
+      if (hv) heavy[at + __popc(hm & ((1u << lane) - 1))] = i;
+    }
+    tot += (unsigned long long)expand_items32(W, o, v, rb, hv ? 0 : deg, col, out, out_len, ocnt,
+                                              0, 32 * Op::kBatch);
+  }
+  warp_flush(W, ocnt, out, out_len);
+  if (lane == 0 && tot) atomicAdd(total_out, tot);
 }
 
 // Deferred labels: write labels[v] = depth byte of v if visited, else
@@ -841,8 +900,31 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
         // tiny frontier (the hub's level, the tail levels): every warp derives
         // the whole expansion plan itself -- no scan pass, no grid barrier
         // between plan and expansion
-        small_push(W, op, F, nf, a.row, a.col, a.order + c.q_end, &cur->out_len, &cur->total,
-                   gw, nw);
+        push_tiny(W, op, F, nf, a.row, a.col, a.order + c.q_end, &cur->out_len, &cur->total, gw,
+                  nw);
+      } else if (nf <= kMidItems) {
+        // mid-size frontier: warps expand 32 items each; hubs (rare) are set
+        // aside and expanded cooperatively after one barrier
+        push_mid(W, op, F, nf, a.row, a.col, a.order + c.q_end, &cur->out_len, &cur->total,
+                 a.part, &cur->aux3, gw, nw);
+        grid.sync();
+        const int64_t nh = (int64_t)ld_ctr(&cur->aux3);
+        for (int64_t h0 = 0; h0 < nh; h0 += 32) {  // heavy items, 32 at a time
+          const int lane = threadIdx.x & 31;
+          int32_t v = 0;
+          int64_t rb = 0, deg = 0;
+          if (h0 + lane < nh) {
+            v = F[a.part[h0 + lane]];
+            rb = a.row[v];
+            deg = a.row[v + 1] - rb;
+          }
+          int ocnt = 0;
+          const int64_t t = expand_items32(W, op, v, rb, deg, a.col, a.order + c.q_end,
+                                           &cur->out_len, ocnt, gw * 32 * BfsClaimOp::kBatch,
+                                           nw * 32 * BfsClaimOp::kBatch);
+          warp_flush(W, ocnt, a.order + c.q_end, &cur->out_len);
+          if (gtid == 0) atomicAdd(&cur->total, (unsigned long long)t);
+        }
       } else {
         const int64_t stiles = (nf + kScanTileItems - 1) / kScanTileItems;
         const unsigned ep = a.epoch_base + (unsigned)c.depth;

@@ -185,3 +185,32 @@ def test_graph_reload_refreshes_constants():
         for direction in ("push", "auto"):
             labels, _, _ = bfs_device(dg, s0, direction=direction)
             assert np.array_equal(labels_to_host(labels), want), (s0, direction)
+
+
+@pytest.mark.parametrize("direction", ["push", "auto"])
+def test_mid_frontier_with_hubs(direction):
+    """Push levels of 33..65536 items expand 32 items per warp and set hubs
+    (> 1024 slots) aside for a cooperative pass (gfx_bfs.cu push_mid): a
+    level of 200 items holding three hubs of 3000-6000 leaves each."""
+    import paper_1701_01170_b200 as gfx
+    from oracle import c_oracle
+
+    src, dst = [], []
+    mids = list(range(1, 201))
+    src += [0] * len(mids)
+    dst += mids
+    nxt = 201
+    for hub, leaves in ((5, 3000), (77, 6000), (150, 4500)):
+        src += [hub] * leaves
+        dst += list(range(nxt, nxt + leaves))
+        nxt += leaves
+    for k, m in enumerate(mids):  # light items: a couple of leaves each
+        src += [m, m]
+        dst += [nxt + 2 * k, nxt + 2 * k + 1]
+    n = nxt + 2 * len(mids) + 10
+    g = gfx.coo_to_csr(gfx.CooGraph(n, np.array(src), np.array(dst)), make_undirected=True)
+    want = c_oracle.bfs(g.row_offsets, g.column_indices, 0)
+    r = gfx.bfs(g, 0, direction=direction)
+    assert np.array_equal(r.labels, want)
+    assert valid_bfs_preds(g.row_offsets, g.column_indices, r.labels, r.preds, 0)
+    assert r.stats.edges_traversed > 0
