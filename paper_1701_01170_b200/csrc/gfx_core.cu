@@ -358,6 +358,15 @@ int gfx_graph_refresh(gfx_graph* g) {
     GFX_TRY(refresh_pull_heads(g));
   }
   g->m_oriented = -1;  // the oriented CSR (TC) is rebuilt on next use
+  GFX_CK(cudaStreamSynchronize(ctx->stream));
+  for (auto it = g->scratch.begin(); it != g->scratch.end();) {  // PageRank chunk table
+    if (it->first.rfind("keep_pr_", 0) == 0) {
+      cudaFree(it->second.ptr);
+      it = g->scratch.erase(it);
+    } else {
+      ++it;
+    }
+  }
   g->w8_state = 0;     // and the compact weight copy (SSSP)
   auto* pin = static_cast<unsigned long long*>(ctx->pinned);
   GFX_CK(cudaMemcpyAsync(pin, dmax - 1, 16, cudaMemcpyDeviceToHost, ctx->stream));

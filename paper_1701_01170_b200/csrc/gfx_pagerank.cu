@@ -8,10 +8,12 @@
 // Here the scatter becomes a gather over in-neighbours (no fp64 atomics, so
 // runs are reproducible): contrib[u] = d*rank[u]/outdeg[u] for active u (0
 // otherwise), rank_next[v] = base + sum contrib[u] in ascending u.  Vertices
-// with in-degree <= 32 are summed sequentially by one thread in exactly the
+// with in-degree <= 64 are summed sequentially by one thread in exactly the
 // reference's slot order (bit-identical terms and order); heavier rows are
 // reduced by a whole warp (tolerance: L1 <= 1e-6, north_star).
 #include <cuda_runtime.h>
+
+#include <vector>
 
 #include "gfx_device.cuh"
 #include "gfx_internal.cuh"
@@ -69,8 +71,14 @@ __global__ void k_pr_base(const double* __restrict__ partials, int nparts, int64
   }
 }
 
-// warp per 32 consecutive vertices: light rows sequential per lane, heavy
-// rows (in-degree > 32) cooperative across the warp
+// Warp per 32 consecutive vertices.  Light rows (in-degree <= kPrLight):
+// one lane per row, summed in the reference's slot order, with the row's
+// column ids and then their contributions fetched kPrBatch at a time (the
+// loads of a batch are in flight together; the adds stay sequential, so the
+// terms and their order are the reference's).  Heavy rows: the whole warp,
+// kPrBatch loads per lane in flight, tree-reduced (L1 <= 1e-6 tolerance).
+constexpr int kPrLight = 64;
+constexpr int kPrBatch = 8;
 __global__ void __launch_bounds__(kPrBlock)
     k_pr_gather(const int64_t* __restrict__ rrow, const int32_t* __restrict__ rcol, int64_t n,
                 const double* __restrict__ contrib, const double* __restrict__ base_p,
@@ -86,22 +94,68 @@ __global__ void __launch_bounds__(kPrBlock)
       b = rrow[v];
       e = rrow[v + 1];
     }
-    const bool heavy = (e - b) > 32;
+    const bool heavy = (e - b) > kPrLight;
     double s = base;
     if (v < n && !heavy) {
-      for (int64_t p = b; p < e; ++p) s = __dadd_rn(s, contrib[rcol[p]]);
+      for (int64_t p = b; p < e; p += kPrBatch) {
+        int32_t u[kPrBatch];
+        double c[kPrBatch];
+#pragma unroll
+        for (int k = 0; k < kPrBatch; ++k) u[k] = p + k < e ? ld_stream_i32(rcol + p + k) : -1;
+#pragma unroll
+        for (int k = 0; k < kPrBatch; ++k) c[k] = u[k] >= 0 ? contrib[u[k]] : 0.0;
+#pragma unroll
+        for (int k = 0; k < kPrBatch; ++k)
+          if (u[k] >= 0) s = __dadd_rn(s, c[k]);
+      }
     }
-    unsigned hm = __ballot_sync(0xffffffffu, heavy);
-    while (hm) {
-      const int k = __ffs(hm) - 1;
-      hm &= hm - 1;
-      const int64_t kb = __shfl_sync(0xffffffffu, b, k), ke = __shfl_sync(0xffffffffu, e, k);
-      double part = 0.0;
-      for (int64_t p = kb + lane; p < ke; p += 32) part = __dadd_rn(part, contrib[rcol[p]]);
-      part = warp_sum_f64(part);
-      if (lane == k) s = __dadd_rn(base, part);
+    if (v < n && !heavy) out[v] = s;  // heavy rows: k_pr_chunks + k_pr_heavy
+  }
+}
+
+// Heavy rows (in-degree > kPrLight) are cut into chunks of kPrChunk slots
+// (graph-constant table, built once): one warp sums a chunk (kPrBatch loads
+// per lane in flight, tree-reduced) into partial[k] ...
+constexpr int64_t kPrChunk = 4096;
+__global__ void __launch_bounds__(kPrBlock)
+    k_pr_chunks(const int64_t* __restrict__ cstart, int64_t nchunks, const int64_t* __restrict__ cend,
+                const int32_t* __restrict__ rcol, const double* __restrict__ contrib,
+                double* __restrict__ partial) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; k < nchunks;
+       k += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t kb = cstart[k], ke = cend[k];
+    double part = 0.0;
+    for (int64_t p0 = kb; p0 < ke; p0 += 32 * kPrBatch) {
+      int32_t u[kPrBatch];
+      double c[kPrBatch];
+#pragma unroll
+      for (int j = 0; j < kPrBatch; ++j) {
+        const int64_t p = p0 + j * 32 + lane;
+        u[j] = p < ke ? ld_stream_i32(rcol + p) : -1;
+      }
+#pragma unroll
+      for (int j = 0; j < kPrBatch; ++j) c[j] = u[j] >= 0 ? contrib[u[j]] : 0.0;
+#pragma unroll
+      for (int j = 0; j < kPrBatch; ++j) part = __dadd_rn(part, c[j]);
     }
-    if (v < n) out[v] = s;
+    part = warp_sum_f64(part);
+    if (lane == 0) partial[k] = part;
+  }
+}
+
+// ... and each heavy row adds its chunks' partials in chunk order (the
+// result is reproducible run to run)
+__global__ void __launch_bounds__(kPrBlock)
+    k_pr_heavy(const int32_t* __restrict__ hrow, const int64_t* __restrict__ hfirst, int64_t nheavy,
+               const double* __restrict__ partial, const double* __restrict__ base_p,
+               double* __restrict__ out) {
+  const double base = *base_p;
+  for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < nheavy;
+       h += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t k = hfirst[h]; k < hfirst[h + 1]; ++k) s = __dadd_rn(s, partial[k]);
+    out[hrow[h]] = __dadd_rn(base, s);
   }
 }
 
@@ -147,6 +201,63 @@ extern "C" int gfx_pagerank(gfx_graph* g, double damping, double epsilon, int64_
   Counters* C = g->counters + 2;
   auto* pin = static_cast<Counters*>(ctx->pinned);
 
+  // graph-constant heavy-row chunk table (reverse adjacency), built once:
+  // keep_pr_meta = {nheavy, nchunks}; rows, first chunk per row, chunk bounds
+  int64_t nheavy = 0, nchunks = 0;
+  int32_t* hrow = nullptr;
+  int64_t *hfirst = nullptr, *cstart = nullptr, *cend = nullptr;
+  double* partial = nullptr;
+  {
+    bool fresh = false;
+    void* meta = nullptr;
+    GFX_TRY(scratch(g, "keep_pr_meta", 16, &meta, &fresh));
+    int64_t hm[2] = {0, 0};
+    if (fresh) {
+      std::vector<int64_t> rr((size_t)n + 1);
+      GFX_CK(cudaMemcpyAsync(rr.data(), g->rrow, (n + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      GFX_CK(cudaStreamSynchronize(ctx->stream));
+      std::vector<int32_t> rows;
+      std::vector<int64_t> first, cs, ce;
+      for (int64_t v = 0; v < n; ++v) {
+        const int64_t b = rr[v], e = rr[v + 1];
+        if (e - b <= kPrLight) continue;
+        rows.push_back((int32_t)v);
+        first.push_back((int64_t)cs.size());
+        for (int64_t p = b; p < e; p += kPrChunk) {
+          cs.push_back(p);
+          ce.push_back(p + kPrChunk < e ? p + kPrChunk : e);
+        }
+      }
+      first.push_back((int64_t)cs.size());
+      hm[0] = (int64_t)rows.size();
+      hm[1] = (int64_t)cs.size();
+      void* q = nullptr;
+      GFX_TRY(scratch(g, "keep_pr_rows", (rows.size() + 1) * 4, &q));
+      GFX_CK(cudaMemcpy(q, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice));
+      GFX_TRY(scratch(g, "keep_pr_first", first.size() * 8, &q));
+      GFX_CK(cudaMemcpy(q, first.data(), first.size() * 8, cudaMemcpyHostToDevice));
+      GFX_TRY(scratch(g, "keep_pr_cs", (cs.size() + 1) * 8, &q));
+      GFX_CK(cudaMemcpy(q, cs.data(), cs.size() * 8, cudaMemcpyHostToDevice));
+      GFX_TRY(scratch(g, "keep_pr_ce", (ce.size() + 1) * 8, &q));
+      GFX_CK(cudaMemcpy(q, ce.data(), ce.size() * 8, cudaMemcpyHostToDevice));
+      GFX_CK(cudaMemcpy(meta, hm, 16, cudaMemcpyHostToDevice));
+    } else {
+      GFX_CK(cudaMemcpy(hm, meta, 16, cudaMemcpyDeviceToHost));
+    }
+    nheavy = hm[0];
+    nchunks = hm[1];
+    void* q = nullptr;
+    GFX_TRY(scratch(g, "keep_pr_rows", (nheavy + 1) * 4, &q));
+    hrow = static_cast<int32_t*>(q);
+    GFX_TRY(scratch(g, "keep_pr_first", (nheavy + 1) * 8, &q));
+    hfirst = static_cast<int64_t*>(q);
+    GFX_TRY(scratch(g, "keep_pr_cs", (nchunks + 1) * 8, &q));
+    cstart = static_cast<int64_t*>(q);
+    GFX_TRY(scratch(g, "keep_pr_ce", (nchunks + 1) * 8, &q));
+    cend = static_cast<int64_t*>(q);
+    GFX_TRY(scratch_t(g, "pr_partial", nchunks + 1, &partial));
+  }
+
   GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
   GFX_TRY(fill_f64(ctx, rank_d, 1.0 / (double)n, n));
   GFX_CK(cudaMemsetAsync(active, 1, n, ctx->stream));
@@ -162,6 +273,12 @@ extern "C" int gfx_pagerank(gfx_graph* g, double damping, double epsilon, int64_
     GFX_LAUNCH(k_pr_base, 1, 256, 0, ctx->stream, partials, cgrid, n, damping, base);
     GFX_LAUNCH(k_pr_gather, ggrid, kPrBlock, 0, ctx->stream, g->rrow, g->rcol, n, contrib, base,
                nx);
+    if (nchunks) {
+      GFX_LAUNCH(k_pr_chunks, grid_for(nchunks * 32, kPrBlock, ctx->sm_count * 16), kPrBlock, 0,
+                 ctx->stream, cstart, nchunks, cend, g->rcol, contrib, partial);
+      GFX_LAUNCH(k_pr_heavy, grid_for(nheavy, kPrBlock, ctx->sm_count * 4), kPrBlock, 0,
+                 ctx->stream, hrow, hfirst, nheavy, partial, base, nx);
+    }
     if (epsilon > 0.0) {
       GFX_CK(cudaMemsetAsync(&C->out_len, 0, 8, ctx->stream));
       GFX_LAUNCH(k_pr_moved, cgrid, kPrBlock, 0, ctx->stream, nx, cur, n, epsilon, active,

@@ -1,8 +1,10 @@
+# round evidence: GPU tests, default bench, reference arm, launch list, ncu of the persistent BFS
 set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -30 > gpurun_out/pytest_gpu.txt
-timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
-timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -5 > gpurun_out/pytest_gpu.txt
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-extras --no-e2e --no-cpu-baseline > gpurun_out/b_ncu.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_bfs_persistent -c 1 -o gpurun_out/bfs_full python tools/prof_run.py --prim bfs --direction auto --scale 24 --runs 1 > gpurun_out/ncu_full.log 2>&1
-tail -3 gpurun_out/pytest_gpu.txt; cat gpurun_out/bench.json
+python tools/ncu_summary.py gpurun_out/launches.csv > gpurun_out/launches_summary.txt 2>&1
+bash tools/gpu_ncu_bfs.sh
+bash tools/gpu_ncu_sssp.sh
+cat gpurun_out/pytest_gpu.txt
