@@ -238,8 +238,11 @@ int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t*
   int32_t *nearA, *nearB, *touched, *far, *fkey, *far2, *fkey2, *part;
   int64_t *scan, *rowbase;
   GFX_TRY(scratch_t(g, "sssp_dp", n, &dp));
-  GFX_TRY(scratch_t(g, "sssp_dist", n, &dist32));
-  GFX_TRY(scratch_t(g, "sssp_mark", g->words + 1, &mark));
+  // distances and the mark bitmap in one allocation: one persisting L2
+  // window covers both random-probe targets
+  const int64_t dist_words = (n + 63) / 64 * 64;
+  GFX_TRY(scratch_t(g, "sssp_dist_mark", dist_words + g->words + 1, &dist32));
+  mark = dist32 + dist_words;
   GFX_TRY(scratch_t(g, "q_order", n + 1, &nearA));
   GFX_TRY(scratch_t(g, "sssp_nearB", n + 1, &nearB));
   GFX_TRY(scratch_t(g, "sssp_touched", n + 1, &touched));
@@ -257,7 +260,7 @@ int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t*
   auto* pin = static_cast<Counters*>(ctx->pinned);
   const int grid = ctx->sm_count * 8;
 
-  l2_persist(ctx, dist32, n * sizeof(uint32_t), true);
+  l2_persist(ctx, dist32, (dist_words + g->words + 1) * sizeof(uint32_t), true);
   GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
   GFX_CK(cudaMemsetAsync(dp, 0xFF, n * sizeof(unsigned long long), ctx->stream));
   GFX_CK(cudaMemsetAsync(dist32, 0xFF, n * sizeof(uint32_t), ctx->stream));
