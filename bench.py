@@ -46,6 +46,7 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip push-only / SSSP lines")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-s27", action="store_true", help="skip the single-GPU scale-27 extra")
     ap.add_argument("--partitioned", action="store_true",
                     help="use the partitioned multi-GPU engine even at N=1 (default: N>1)")
     return ap.parse_args()
@@ -407,17 +408,13 @@ def extras(args, dg, labels, preds, dist, peak):
     from paper_1701_01170_b200.primitives.bfs import bfs_device
 
     res = {}
-    # push-only BFS
+    # push-only BFS: the same batched device-resident launches as the headline
+    from paper_1701_01170_b200.primitives.bfs import bfs_batch
+
     for _ in range(2):
         st = bfs_device(dg, args.source, direction="push", labels=labels, preds=preds)[2]
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     k = max(3, args.steps // 2)
-    ev0.record()
-    for _ in range(k):
-        bfs_device(dg, args.source, direction="push", labels=labels, preds=preds)
-    ev1.record()
-    torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1) / k
+    ms = bfs_batch(dg, [args.source] * k, direction="push", labels=labels, preds=preds) / k
     res["bfs_push"] = {"gteps": round(st.edges_reached / (ms * 1e-3) / 1e9, 2),
                        "ms": round(ms, 4), "bytes_alg": st.bytes_alg,
                        "frac_of_hbm": round(st.bytes_alg / (ms * 1e-3) / 1e9 / peak, 4)}
@@ -432,12 +429,11 @@ def extras(args, dg, labels, preds, dist, peak):
         for delta in (32, None):
             for _ in range(2):
                 st = sssp_device(dgw, args.source, delta=delta)[2]
-            ev0.record()
-            for _ in range(k):
-                sssp_device(dgw, args.source, delta=delta)
-            ev1.record()
-            torch.cuda.synchronize()
-            ms = ev0.elapsed_time(ev1) / k
+            # device time of the primitive as the library measures it (CUDA
+            # events around its loop, the host-read iteration counters
+            # included), mean of k calls
+            times = [sssp_device(dgw, args.source, delta=delta)[2].device_ms for _ in range(k)]
+            ms = sum(times) / len(times)
             res[f"sssp_delta{delta or 'default'}"] = {
                 "gteps": round(st.edges_reached / (ms * 1e-3) / 1e9, 2), "ms": round(ms, 4),
                 "relaxed_slots": st.work_slots, "work_inflation": round(st.work_slots / max(st.edges_reached, 1), 3),
@@ -450,7 +446,45 @@ def extras(args, dg, labels, preds, dist, peak):
         res.update(secondary(args, dg, peak))
     except Exception as exc:
         res["secondary_error"] = repr(exc)
+    if args.scale == 24 and not args.no_s27:
+        try:
+            res.update(scale27(args, peak))
+        except Exception as exc:  # e.g. not enough free HBM next to the s24 graph
+            res["s27_error"] = repr(exc)
     return res
+
+
+def scale27(args, peak):
+    """BASELINE config C5's input (R-MAT s27 ef16, 134M vertices, 4.2B
+    directed slots) on ONE GPU: GPU-built, then the same device-resident
+    DO-BFS from vertex 0, K launches back to back."""
+    import torch
+
+    from paper_1701_01170_b200.generators import rmat_device_graph
+    from paper_1701_01170_b200.primitives.bfs import bfs_batch, bfs_device
+
+    torch.cuda.empty_cache()
+    t0 = time.perf_counter()
+    dg = rmat_device_graph(27, args.edge_factor, 0)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    labels = torch.empty(dg.num_vertices, dtype=torch.int32, device="cuda")
+    preds = torch.empty(dg.num_vertices, dtype=torch.int32, device="cuda")
+    st = None
+    for _ in range(3):
+        st = bfs_device(dg, args.source, direction="auto", labels=labels, preds=preds)[2]
+    k = 5
+    ms = bfs_batch(dg, [args.source] * k, direction="auto", labels=labels, preds=preds) / k
+    out = {"bfs_do_s27_1gpu": {
+        "gteps": round(st.edges_reached / (ms * 1e-3) / 1e9, 2), "ms": round(ms, 4),
+        "n": dg.num_vertices, "m": dg.num_edges, "E_r": st.edges_reached,
+        "reached": st.reached, "bytes_alg": st.bytes_alg,
+        "frac_of_hbm": round(st.bytes_alg / (ms * 1e-3) / 1e9 / peak, 4),
+        "graph_build_s": round(build_s, 2),
+        "trace": [[t["iteration"], t["decision"], t["n_f"]] for t in st.direction_trace]}}
+    del dg, labels, preds
+    torch.cuda.empty_cache()
+    return out
 
 
 def secondary(args, dg, peak):

@@ -208,7 +208,6 @@ static void l2_persist(gfx_ctx* ctx, void* base, size_t bytes, bool on) {
       max_persist = 0;
     } else {
       max_persist = (size_t)prop.persistingL2CacheMaxSize;
-      if (max_persist) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, max_persist);
     }
     cudaGetLastError();
   }
@@ -223,8 +222,14 @@ static void l2_persist(gfx_ctx* ctx, void* base, size_t bytes, bool on) {
   } else {
     attr.accessPolicyWindow.num_bytes = 0;
   }
+  // the set-aside is taken for the duration of the call only: a persisting
+  // carve-out left behind would shrink L2 for every later kernel
+  if (on) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, max_persist);
   cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &attr);
-  if (!on) cudaCtxResetPersistingL2Cache();
+  if (!on) {
+    cudaCtxResetPersistingL2Cache();
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+  }
   cudaGetLastError();
 }
 

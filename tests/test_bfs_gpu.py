@@ -214,3 +214,28 @@ def test_mid_frontier_with_hubs(direction):
     assert np.array_equal(r.labels, want)
     assert valid_bfs_preds(g.row_offsets, g.column_indices, r.labels, r.preds, 0)
     assert r.stats.edges_traversed > 0
+
+
+def test_scale27_push_and_do_agree():
+    """BASELINE config C5's input size on one GPU (R-MAT s27 ef16, GPU-built,
+    4.2B slots): the direction-optimising run (pull sweeps) and the push-only
+    run (load-balanced expansion) are independent code paths and must give
+    identical labels; every reached vertex's pred sits one level up."""
+    import torch
+
+    from paper_1701_01170_b200.generators import rmat_device_graph
+    from paper_1701_01170_b200.primitives.bfs import bfs_device
+
+    free, _ = torch.cuda.mem_get_info()
+    if free < 120 * 2**30:
+        pytest.skip("needs ~120 GB of free HBM for the s27 build")
+    dg = rmat_device_graph(27, 16, 0)
+    la, pa, sa = bfs_device(dg, 0, direction="auto")
+    lp, _, sp = bfs_device(dg, 0, direction="push")
+    assert torch.equal(la, lp)
+    assert sa.edges_reached == sp.edges_reached > 4_000_000_000
+    reached = (la != 2**31 - 1).nonzero().squeeze(1)
+    reached = reached[reached != 0]
+    par = pa[reached].long()
+    assert bool((par >= 0).all())
+    assert torch.equal(la[par], la[reached] - 1)
