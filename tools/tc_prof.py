@@ -1,0 +1,16 @@
+"""TC on the GPU-built R-MAT graph (default s22): per-kernel launch list under
+ncu, or plain timing."""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import torch  # noqa: E402
+
+from paper_1701_01170_b200.generators import rmat_device_graph  # noqa: E402
+from paper_1701_01170_b200.primitives.tc import tc_device  # noqa: E402
+
+scale = int(sys.argv[1]) if len(sys.argv) > 1 else 22
+dg = rmat_device_graph(scale, 16, 0)
+for _ in range(2):
+    total, counts, osrc, odst, st = tc_device(dg)
+print("tc scale", scale, "triangles", total, "ms", round(st.device_ms, 3), "oriented", counts.numel())
