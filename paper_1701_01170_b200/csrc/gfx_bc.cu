@@ -23,13 +23,19 @@
 
 namespace gfx {
 
+// Each term loads everything it needs for neighbour u in one go (the label
+// and the value arrays in parallel), then evaluates -- so a batch of
+// neighbours costs two dependent round trips (column ids, then their data).
 struct SigmaTerm {
   const int32_t* labels;
   const double* sigma;
   int32_t want;  // level of contributing neighbours
-  __device__ double term(int32_t, int32_t u) const {
-    return labels[u] == want ? sigma[u] : 0.0;
-  }
+  struct V {
+    int32_t l;
+    double s;
+  };
+  __device__ V load(int32_t u) const { return V{labels[u], sigma[u]}; }
+  __device__ double eval(int32_t, const V& x) const { return x.l == want ? x.s : 0.0; }
 };
 
 struct DeltaTerm {
@@ -37,17 +43,29 @@ struct DeltaTerm {
   const double* sigma;
   const double* delta;
   int32_t want;
-  __device__ double term(int32_t v, int32_t w) const {
-    if (labels[w] != want) return 0.0;
-    return __dmul_rn(__ddiv_rn(sigma[v], sigma[w]), __dadd_rn(1.0, delta[w]));
+  struct V {
+    int32_t l;
+    double s, d;
+  };
+  __device__ V load(int32_t u) const { return V{labels[u], sigma[u], delta[u]}; }
+  __device__ double eval(int32_t v, const V& x) const {
+    if (x.l != want) return 0.0;
+    return __dmul_rn(__ddiv_rn(sigma[v], x.s), __dadd_rn(1.0, x.d));
   }
 };
 
-// out[v] = sum_{u in adj(v)} T.term(v, u) for v in items[0..cnt)
+// out[v] = sum_{u in adj(v)} T(v, u) for v in items[0..cnt).  Light rows
+// (<= kGatherLight): one lane per row, kGatherBatch neighbours' loads in
+// flight, terms added sequentially in ascending neighbour order (the
+// reference's slot order); heavy rows: the whole warp, kGatherBatch loads
+// per lane in flight, tree-reduced.
+constexpr int kGatherLight = 32;
+constexpr int kGatherBatch = 8;
 template <class T>
 __global__ void __launch_bounds__(256)
     k_level_gather(const int32_t* __restrict__ items, int64_t cnt, const int64_t* __restrict__ rows,
                    const int32_t* __restrict__ cols, T term, double* __restrict__ out) {
+  constexpr int B = kGatherBatch;
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -60,12 +78,23 @@ __global__ void __launch_bounds__(256)
       b = rows[v];
       e = rows[v + 1];
     }
-    const bool heavy = (e - b) > 32;
+    const bool heavy = (e - b) > kGatherLight;
     double acc = 0.0;
     if (i < cnt && !heavy)
-      for (int64_t p = b; p < e; ++p) {
-        const double t = term.term(v, cols[p]);
-        if (t != 0.0) acc = __dadd_rn(acc, t);
+      for (int64_t p0 = b; p0 < e; p0 += B) {
+        int32_t u[B];
+        typename T::V x[B];
+#pragma unroll
+        for (int k = 0; k < B; ++k) u[k] = p0 + k < e ? ld_stream_i32(cols + p0 + k) : -1;
+#pragma unroll
+        for (int k = 0; k < B; ++k)
+          if (u[k] >= 0) x[k] = term.load(u[k]);
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+          if (u[k] < 0) continue;
+          const double t = term.eval(v, x[k]);
+          if (t != 0.0) acc = __dadd_rn(acc, t);
+        }
       }
     unsigned hm = __ballot_sync(0xffffffffu, heavy);
     while (hm) {
@@ -74,7 +103,21 @@ __global__ void __launch_bounds__(256)
       const int32_t kv = __shfl_sync(0xffffffffu, v, k);
       const int64_t kb = __shfl_sync(0xffffffffu, b, k), ke = __shfl_sync(0xffffffffu, e, k);
       double part = 0.0;
-      for (int64_t p = kb + lane; p < ke; p += 32) part = __dadd_rn(part, term.term(kv, cols[p]));
+      for (int64_t p0 = kb; p0 < ke; p0 += 32 * B) {
+        int32_t u[B];
+        typename T::V x[B];
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+          const int64_t p = p0 + j * 32 + lane;
+          u[j] = p < ke ? ld_stream_i32(cols + p) : -1;
+        }
+#pragma unroll
+        for (int j = 0; j < B; ++j)
+          if (u[j] >= 0) x[j] = term.load(u[j]);
+#pragma unroll
+        for (int j = 0; j < B; ++j)
+          if (u[j] >= 0) part = __dadd_rn(part, term.eval(kv, x[j]));
+      }
       part = warp_sum_f64(part);
       if (lane == k) acc = part;
     }
@@ -133,9 +176,10 @@ extern "C" int gfx_bc(gfx_graph* g, const int64_t* sources, int64_t num_sources,
       GFX_LAUNCH((k_level_gather<SigmaTerm>), grid_for(cnt * 32, 256, grid), 256, 0, ctx->stream,
                  order + off[d], cnt, g->rrow, g->rcol, t, sigma);
     }
-    // backward: delta deepest level first (bc.py:98-116)
+    // backward: delta deepest level first (bc.py:98-116); the source's own
+    // delta is 0 by definition (bc.py:110), so level 0 is not gathered
     GFX_CK(cudaMemsetAsync(delta, 0, n * sizeof(double), ctx->stream));
-    for (int64_t d = L - 2; d >= 0; --d) {
+    for (int64_t d = L - 2; d >= 1; --d) {
       const int64_t cnt = off[d + 1] - off[d];
       if (cnt <= 0) continue;
       DeltaTerm t{labels, sigma, delta, (int32_t)(d + 1)};
