@@ -41,15 +41,26 @@ __global__ void __launch_bounds__(256)
     }
     const bool heavy = (e - b) > 32;
     if (v < n && !heavy) {
+      // 8 neighbours' ids, then their row bounds, in flight per batch
       int64_t k = WRITE ? orow[v] : 0;
-      for (int64_t p = b; p < e; ++p) {
-        const int32_t d = col[p];
-        if (keep_slot(row, e - b, (int32_t)v, d)) {
-          if (WRITE) {
-            ocol[k] = d;
-            osrc[k] = (int32_t)v;
+      for (int64_t p0 = b; p0 < e; p0 += 8) {
+        int32_t d[8];
+        int64_t dd[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) d[t] = p0 + t < e ? col[p0 + t] : -1;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) dd[t] = d[t] >= 0 ? row[d[t] + 1] - row[d[t]] : 0;
+        const int64_t ds = e - b;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          if (d[t] < 0) continue;
+          if (ds > dd[t] || (ds == dd[t] && (int32_t)v < d[t])) {  // keep_slot
+            if (WRITE) {
+              ocol[k] = d[t];
+              osrc[k] = (int32_t)v;
+            }
+            ++k;
           }
-          ++k;
         }
       }
       if (!WRITE) ocnt[v] = k;
@@ -61,21 +72,29 @@ __global__ void __launch_bounds__(256)
       const int64_t kv = grp * 32 + k;
       const int64_t kb = __shfl_sync(0xffffffffu, b, k), ke = __shfl_sync(0xffffffffu, e, k);
       int64_t pos = WRITE ? orow[kv] : 0;
-      for (int64_t p0 = kb; p0 < ke; p0 += 32) {
-        const int64_t p = p0 + lane;
-        int32_t d = 0;
-        bool keep = false;
-        if (p < ke) {
-          d = col[p];
-          keep = keep_slot(row, ke - kb, (int32_t)kv, d);
+      // 8 rows of 32 slots per step: ids, then their row bounds, in flight
+      for (int64_t p0 = kb; p0 < ke; p0 += 256) {
+        int32_t d[8];
+        int64_t dd[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int64_t p = p0 + t * 32 + lane;
+          d[t] = p < ke ? col[p] : -1;
         }
-        const unsigned km = __ballot_sync(0xffffffffu, keep);
-        if (WRITE && keep) {
-          const int64_t at = pos + __popc(km & ((1u << lane) - 1));
-          ocol[at] = d;
-          osrc[at] = (int32_t)kv;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) dd[t] = d[t] >= 0 ? row[d[t] + 1] - row[d[t]] : 0;
+        const int64_t ds = ke - kb;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const bool keep = d[t] >= 0 && (ds > dd[t] || (ds == dd[t] && (int32_t)kv < d[t]));
+          const unsigned km = __ballot_sync(0xffffffffu, keep);
+          if (WRITE && keep) {
+            const int64_t at = pos + __popc(km & ((1u << lane) - 1));
+            ocol[at] = d[t];
+            osrc[at] = (int32_t)kv;
+          }
+          pos += __popc(km);
         }
-        pos += __popc(km);
       }
       if (!WRITE && lane == 0) ocnt[kv] = pos;
     }
