@@ -1,6 +1,7 @@
 // libgfx core: errors, context, graph handle, scratch, fills, and the fused
 // degree-scan + tile partition shared by every load-balanced expansion.
 #include <cuda_runtime.h>
+#include <cstdlib>
 
 #include <algorithm>
 #include <atomic>
@@ -188,6 +189,51 @@ int build_nonzero_bitmap(gfx_graph* g, const int64_t* row, const char* name) {
       row, g->n, g->words, bm);
   GFX_CK(cudaGetLastError());
   return GFX_OK;
+}
+
+// Persisting-L2 access window on the stream for [base, base + bytes): random-
+// probe targets (SSSP distances, PageRank contributions) stay L2-resident
+// while the adjacency streams through with evict-first hints.  When bytes
+// exceed the persisting capacity, hitRatio spreads the capacity over the
+// whole window.  on == false removes the window and the carve-out.
+void l2_window(gfx_ctx* ctx, void* base, size_t bytes, bool on) {
+  static size_t max_persist = (size_t)-1;
+  if (max_persist == (size_t)-1) {
+    cudaDeviceProp prop{};
+    if (cudaGetDeviceProperties(&prop, ctx->device) != cudaSuccess) {
+      max_persist = 0;
+    } else {
+      max_persist = (size_t)prop.persistingL2CacheMaxSize;
+    }
+    cudaGetLastError();
+  }
+  if (!max_persist || getenv("GFX_NO_L2_PERSIST")) return;
+  cudaStreamAttrValue attr{};
+  if (on) {
+    attr.accessPolicyWindow.base_ptr = base;
+    static size_t max_window = 0;
+    if (!max_window) {
+      int w = 0;
+      cudaDeviceGetAttribute(&w, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device);
+      max_window = w > 0 ? (size_t)w : max_persist;
+    }
+    const size_t win = bytes < max_window ? bytes : max_window;
+    attr.accessPolicyWindow.num_bytes = win;
+    attr.accessPolicyWindow.hitRatio = win <= max_persist ? 1.0f : (float)max_persist / (float)win;
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  } else {
+    attr.accessPolicyWindow.num_bytes = 0;
+  }
+  // the set-aside is taken for the duration of the call only: a persisting
+  // carve-out left behind would shrink L2 for every later kernel
+  if (on) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, max_persist);
+  cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &attr);
+  if (!on) {
+    cudaCtxResetPersistingL2Cache();
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+  }
+  cudaGetLastError();
 }
 
 }  // namespace gfx

@@ -154,6 +154,9 @@ constexpr int kScanBlock = 256;
 constexpr int kScanItems = 8;        // items per thread in the scan
 constexpr int kScanTileItems = kScanBlock * kScanItems;
 
+// persisting-L2 window over a random-probe target (on/off, see gfx_core.cu)
+void l2_window(gfx_ctx* ctx, void* base, size_t bytes, bool on);
+
 // recompute the pull head array (first in-neighbour per vertex) if the
 // graph has one (gfx_graph_refresh)
 int refresh_pull_heads(gfx_graph* g);

@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(kPrBlock)
                 double* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const double base = *base_p;
+  const unsigned long long pol = l2_evict_first_policy();  // column ids stream past contrib
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t grp = gw; grp * 32 < n; grp += nw) {
@@ -101,7 +102,7 @@ __global__ void __launch_bounds__(kPrBlock)
         int32_t u[kPrBatch];
         double c[kPrBatch];
 #pragma unroll
-        for (int k = 0; k < kPrBatch; ++k) u[k] = p + k < e ? ld_stream_i32(rcol + p + k) : -1;
+        for (int k = 0; k < kPrBatch; ++k) u[k] = p + k < e ? ld_stream_i32(rcol + p + k, pol) : -1;
 #pragma unroll
         for (int k = 0; k < kPrBatch; ++k) c[k] = u[k] >= 0 ? contrib[u[k]] : 0.0;
 #pragma unroll
@@ -122,6 +123,7 @@ __global__ void __launch_bounds__(kPrBlock)
                 const int32_t* __restrict__ rcol, const double* __restrict__ contrib,
                 double* __restrict__ partial) {
   const int lane = threadIdx.x & 31;
+  const unsigned long long pol = l2_evict_first_policy();
   for (int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; k < nchunks;
        k += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t kb = cstart[k], ke = cend[k];
@@ -132,7 +134,7 @@ __global__ void __launch_bounds__(kPrBlock)
 #pragma unroll
       for (int j = 0; j < kPrBatch; ++j) {
         const int64_t p = p0 + j * 32 + lane;
-        u[j] = p < ke ? ld_stream_i32(rcol + p) : -1;
+        u[j] = p < ke ? ld_stream_i32(rcol + p, pol) : -1;
       }
 #pragma unroll
       for (int j = 0; j < kPrBatch; ++j) c[j] = u[j] >= 0 ? contrib[u[j]] : 0.0;

@@ -198,41 +198,6 @@ __global__ void k_sssp_unpack(const unsigned long long* __restrict__ dp, int64_t
   }
 }
 
-// keep the 32-bit distance array (the random-probe target) L2-resident while
-// the adjacency and weights stream through with evict-first hints
-static void l2_persist(gfx_ctx* ctx, void* base, size_t bytes, bool on) {
-  static size_t max_persist = (size_t)-1;
-  if (max_persist == (size_t)-1) {
-    cudaDeviceProp prop{};
-    if (cudaGetDeviceProperties(&prop, ctx->device) != cudaSuccess) {
-      max_persist = 0;
-    } else {
-      max_persist = (size_t)prop.persistingL2CacheMaxSize;
-    }
-    cudaGetLastError();
-  }
-  if (!max_persist || getenv("GFX_NO_L2_PERSIST")) return;
-  cudaStreamAttrValue attr{};
-  if (on) {
-    attr.accessPolicyWindow.base_ptr = base;
-    attr.accessPolicyWindow.num_bytes = bytes < max_persist ? bytes : max_persist;
-    attr.accessPolicyWindow.hitRatio = 1.0f;
-    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-  } else {
-    attr.accessPolicyWindow.num_bytes = 0;
-  }
-  // the set-aside is taken for the duration of the call only: a persisting
-  // carve-out left behind would shrink L2 for every later kernel
-  if (on) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, max_persist);
-  cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &attr);
-  if (!on) {
-    cudaCtxResetPersistingL2Cache();
-    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
-  }
-  cudaGetLastError();
-}
-
 int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t* preds,
              gfx_iter_rec* recs, int64_t rec_cap, gfx_stats* st) {
   gfx_ctx* ctx = g->ctx;
@@ -265,7 +230,7 @@ int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t*
   auto* pin = static_cast<Counters*>(ctx->pinned);
   const int grid = ctx->sm_count * 8;
 
-  l2_persist(ctx, dist32, (dist_words + g->words + 1) * sizeof(uint32_t), true);
+  l2_window(ctx, dist32, (dist_words + g->words + 1) * sizeof(uint32_t), true);
   GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
   GFX_CK(cudaMemsetAsync(dp, 0xFF, n * sizeof(unsigned long long), ctx->stream));
   GFX_CK(cudaMemsetAsync(dist32, 0xFF, n * sizeof(uint32_t), ctx->stream));
@@ -357,7 +322,7 @@ int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t*
     }
   }
   GFX_LAUNCH(k_sssp_unpack, grid_for(n, 256, grid), 256, 0, ctx->stream, dp, n, dist, preds);
-  l2_persist(ctx, nullptr, 0, false);
+  l2_window(ctx, nullptr, 0, false);
   GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));
   GFX_CK(cudaEventSynchronize(ctx->ev1));
   float ms = 0.f;
