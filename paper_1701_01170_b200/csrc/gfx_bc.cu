@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "gfx_device.cuh"
+#include "gfx_expand.cuh"
 #include "gfx_internal.cuh"
 
 namespace gfx {
@@ -125,6 +126,52 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Push forms, used on undirected graphs for a level whose neighbour level
+// has fewer slots than the level itself (the load-balanced expansion then
+// splits hubs across warps).  Forward: sigma values are path counts --
+// integers held exactly in fp64 -- so the atomic sums are exact in any
+// order.  Backward: the atomic fp64 sums are order-dependent in the last
+// bits only (north_star tolerance rel <= 1e-5).
+struct SigmaPushOp {
+  static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
+  static constexpr int kBatch = kVisitBatch;
+  static constexpr int kMinBlocks = 3;
+  const int32_t* labels;
+  double* sigma;
+  int32_t want;  // level of the receiving neighbours
+  int32_t lv[kBatch];
+  __device__ int32_t src_value(int32_t) const { return 0; }
+  __device__ void prefetch(const int32_t* d) {
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) lv[u] = d[u] >= 0 ? labels[d[u]] : -1;
+  }
+  __device__ bool visit(int u, int32_t d, int32_t s, int32_t, int32_t, int64_t) {
+    if (lv[u] == want) atomicAdd(&sigma[d], sigma[s]);
+    return false;
+  }
+};
+
+struct DeltaPushOp {  // frontier: level want + 1; receivers: neighbours at level want
+  static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
+  static constexpr int kBatch = kVisitBatch;
+  static constexpr int kMinBlocks = 3;
+  const int32_t* labels;
+  const double* sigma;
+  double* delta;
+  int32_t want;
+  int32_t lv[kBatch];
+  __device__ int32_t src_value(int32_t) const { return 0; }
+  __device__ void prefetch(const int32_t* d) {
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) lv[u] = d[u] >= 0 ? labels[d[u]] : -1;
+  }
+  __device__ bool visit(int u, int32_t s, int32_t w, int32_t, int32_t, int64_t) {
+    if (lv[u] == want)
+      atomicAdd(&delta[s], __dmul_rn(__ddiv_rn(sigma[s], sigma[w]), __dadd_rn(1.0, delta[w])));
+    return false;
+  }
+};
+
 __global__ void k_bc_seed(double* sigma, int32_t src) { sigma[src] = 1.0; }
 
 __global__ void k_bc_accumulate(const int32_t* __restrict__ items, int64_t cnt,
@@ -158,13 +205,30 @@ extern "C" int gfx_bc(gfx_graph* g, const int64_t* sources, int64_t num_sources,
   GFX_TRY(scratch_t(g, "bc_sigma", n + 1, &sigma));
   GFX_TRY(scratch_t(g, "bc_delta", n + 1, &delta));
   const int grid = ctx->sm_count * 8;
+  int32_t* part;
+  int64_t *scan, *rowbase;
+  GFX_TRY(scratch_t(g, "q_scan", n + 2, &scan));
+  GFX_TRY(scratch_t(g, "q_rowbase", n + 1, &rowbase));
+  GFX_TRY(scratch_t(g, "q_part", part_capacity(g->m, g->n), &part));
+  Counters* pc = g->counters + 2;  // push plans (C[2], C[3])
   int64_t iterations = 0, edges = 0;
   std::vector<int64_t> off;
   GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
   for (int64_t si = 0; si < num_sources; ++si) {
     const int32_t src = (int32_t)sources[si];
     int32_t* order = nullptr;
-    GFX_TRY(bfs_push_levels(g, src, labels, preds, &off, &order));
+    std::vector<int64_t> slots;
+    GFX_TRY(bfs_push_levels(g, src, labels, preds, &off, &order, &slots));
+    const bool undirected = (g->flags & GFX_GRAPH_UNDIRECTED) != 0;
+    // push a level from its neighbour level when that is fewer slots
+    auto push_from = [&](int64_t lvl, auto op) -> int {
+      const int64_t cnt = off[lvl + 1] - off[lvl];
+      const unsigned long long c = (unsigned long long)cnt;
+      GFX_CK(cudaMemcpyAsync(&pc[0].out_len, &c, 8, cudaMemcpyHostToDevice, ctx->stream));
+      GFX_CK(cudaMemsetAsync(&pc[1], 0, sizeof(Counters), ctx->stream));
+      return lb_advance(g, order + off[lvl], &pc[0].out_len, cnt, &pc[1], scan, rowbase, part, op,
+                        nullptr, &pc[1].out_len);
+    };
     const int64_t L = (int64_t)off.size() - 1;  // levels 0..L-1 (last is empty)
     // forward: sigma level by level (bc.py:87-92)
     GFX_CK(cudaMemsetAsync(sigma, 0, n * sizeof(double), ctx->stream));
@@ -172,6 +236,10 @@ extern "C" int gfx_bc(gfx_graph* g, const int64_t* sources, int64_t num_sources,
     for (int64_t d = 1; d < L; ++d) {
       const int64_t cnt = off[d + 1] - off[d];
       if (cnt <= 0) continue;
+      if (undirected && slots[d - 1] < slots[d]) {
+        GFX_TRY(push_from(d - 1, SigmaPushOp{labels, sigma, (int32_t)d, {}}));
+        continue;
+      }
       SigmaTerm t{labels, sigma, (int32_t)(d - 1)};
       GFX_LAUNCH((k_level_gather<SigmaTerm>), grid_for(cnt * 32, 256, grid), 256, 0, ctx->stream,
                  order + off[d], cnt, g->rrow, g->rcol, t, sigma);
@@ -182,6 +250,11 @@ extern "C" int gfx_bc(gfx_graph* g, const int64_t* sources, int64_t num_sources,
     for (int64_t d = L - 2; d >= 1; --d) {
       const int64_t cnt = off[d + 1] - off[d];
       if (cnt <= 0) continue;
+      if (undirected && d + 1 < (int64_t)slots.size() && slots[d + 1] < slots[d] &&
+          off[d + 2] > off[d + 1]) {
+        GFX_TRY(push_from(d + 1, DeltaPushOp{labels, sigma, delta, (int32_t)d, {}}));
+        continue;
+      }
       DeltaTerm t{labels, sigma, delta, (int32_t)(d + 1)};
       GFX_LAUNCH((k_level_gather<DeltaTerm>), grid_for(cnt * 32, 256, grid), 256, 0, ctx->stream,
                  order + off[d], cnt, g->row, g->col, t, delta);

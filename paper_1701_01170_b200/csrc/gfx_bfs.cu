@@ -365,7 +365,8 @@ static int push_level(gfx_graph* g, const BfsBuffers& B, const int32_t* F,
 // order array: level d occupies order[off[d], off[d+1]) (used by BC, which
 // replays the levels like reference bc.py:73-116)
 int bfs_push_levels(gfx_graph* g, int64_t source, int32_t* labels, int32_t* preds,
-                    std::vector<int64_t>* off, int32_t** order_out) {
+                    std::vector<int64_t>* off, int32_t** order_out,
+                    std::vector<int64_t>* slots) {
   gfx_ctx* ctx = g->ctx;
   const int64_t n = g->n;
   BfsBuffers B;
@@ -378,6 +379,7 @@ int bfs_push_levels(gfx_graph* g, int64_t source, int32_t* labels, int32_t* pred
   GFX_CK(cudaMemsetAsync(C, 0, 2 * sizeof(Counters), ctx->stream));
   GFX_LAUNCH(k_bfs_seed, 1, 1, 0, ctx->stream, (int32_t)source, labels, B.visited, B.order, &C[0]);
   off->assign(1, 0);
+  if (slots) slots->clear();
   int64_t nf = 1, q_off = 0, depth = 0;
   while (nf > 0) {
     ++depth;
@@ -389,6 +391,7 @@ int bfs_push_levels(gfx_graph* g, int64_t source, int32_t* labels, int32_t* pred
                        preds, B.order + q_off + nf));
     GFX_CK(cudaMemcpyAsync(pin, cur, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
     GFX_CK(cudaStreamSynchronize(ctx->stream));
+    if (slots) slots->push_back((int64_t)pin->total);  // sum of degrees of this level
     q_off += nf;
     nf = (int64_t)pin->out_len;
   }
