@@ -13,6 +13,9 @@
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <vector>
+
 #include "gfx_device.cuh"
 #include "gfx_internal.cuh"
 
@@ -106,7 +109,8 @@ __global__ void __launch_bounds__(256)
     k_tc_small(const int32_t* __restrict__ us, const int32_t* __restrict__ vs, int64_t npairs,
                const int64_t* __restrict__ rows, const int32_t* __restrict__ cols,
                int32_t* __restrict__ counts, int32_t* __restrict__ heavy,
-               unsigned long long* __restrict__ nheavy, unsigned long long* __restrict__ total) {
+               unsigned long long* __restrict__ nheavy, unsigned long long* __restrict__ total,
+               int64_t hub_deg = 0) {
   const int lane = threadIdx.x & 31;
   unsigned long long sum = 0;
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < npairs;
@@ -116,7 +120,9 @@ __global__ void __launch_bounds__(256)
     if (i < npairs) {
       const int32_t u = us[i], v = vs[i];
       int64_t a = rows[u], ae = rows[u + 1], b = rows[v], be = rows[v + 1];
-      if (ae - a + be - b > 64) {
+      if (hub_deg && ae - a > hub_deg) {
+        // a hub source: counted by k_tc_hubs
+      } else if (ae - a + be - b > 64) {
         big = true;
       } else {
         int c = 0;
@@ -176,6 +182,69 @@ __global__ void __launch_bounds__(256)
       sum += (unsigned long long)c;
     }
   }
+  if (lane == 0 && sum) atomicAdd(total, sum);
+}
+
+// Hub rows of the oriented CSR (out-degree > kTcHub): one CTA per hub at a
+// time keeps N+(u) as bits of its own bitmap slot (n bits, L2-resident for
+// the scales benchmarked), then each warp counts, for one out-neighbour v,
+// the elements of N+(v) whose bit is set -- one bitmap probe per element
+// instead of a binary search over the hub's long list -- and clears the
+// bits again.  Hubs are handed out dynamically.
+constexpr int64_t kTcHub = 512;
+__global__ void k_tc_hub_list(const int64_t* __restrict__ orow, int64_t n, int32_t* __restrict__ hubs,
+                              unsigned long long* __restrict__ nhubs) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+       u += (int64_t)gridDim.x * blockDim.x)
+    if (orow[u + 1] - orow[u] > kTcHub) hubs[atomicAdd(nhubs, 1ull)] = (int32_t)u;
+}
+
+// work item k: hub hub_of[k], its out-neighbours [j0[k], j1[k]) (a hub's
+// pairs are cut into kTcHubChunk-pair items so the largest hubs spread over
+// many CTAs; every item rebuilds the hub's bits in its CTA's slot)
+constexpr int64_t kTcHubChunk = 4096;
+__global__ void __launch_bounds__(256)
+    k_tc_hubs(const int64_t* __restrict__ orow, const int32_t* __restrict__ ocol,
+              const int32_t* __restrict__ hub_of, const int64_t* __restrict__ j0s,
+              const int64_t* __restrict__ j1s, int64_t nitems, uint32_t* __restrict__ bitmaps,
+              int64_t words, int32_t* __restrict__ counts, unsigned long long* __restrict__ total,
+              unsigned long long* __restrict__ cursor) {
+  __shared__ long long s_h;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  uint32_t* bm = bitmaps + (int64_t)blockIdx.x * words;
+  unsigned long long sum = 0;
+  for (;;) {
+    if (threadIdx.x == 0) s_h = (long long)atomicAdd(cursor, 1ull);
+    __syncthreads();
+    const int64_t h = s_h;
+    __syncthreads();
+    if (h >= nitems) break;
+    const int32_t u = hub_of[h];
+    const int64_t ub = orow[u], ue = orow[u + 1];
+    for (int64_t p = ub + threadIdx.x; p < ue; p += blockDim.x) {
+      const int32_t x = ocol[p];
+      atomicOr(&bm[x >> 5], 1u << (x & 31));
+    }
+    __syncthreads();
+    for (int64_t j = j0s[h] + warp; j < j1s[h]; j += nwarp) {
+      const int32_t v = ocol[j];
+      const int64_t vb = orow[v], ve = orow[v + 1];
+      int c = 0;
+      for (int64_t p = vb + lane; p < ve; p += 32) {
+        const int32_t w = ocol[p];
+        c += (__ldcg(&bm[w >> 5]) >> (w & 31)) & 1u;  // L2: the bits were set by atomics
+      }
+      for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if (lane == 0) {
+        counts[j] = c;
+        sum += (unsigned long long)c;
+      }
+    }
+    __syncthreads();
+    for (int64_t p = ub + threadIdx.x; p < ue; p += blockDim.x) bm[ocol[p] >> 5] = 0u;
+    __syncthreads();
+  }
+  sum = warp_sum_u64(sum);
   if (lane == 0 && sum) atomicAdd(total, sum);
 }
 
@@ -248,9 +317,67 @@ extern "C" int gfx_tc_count(gfx_graph* g, int32_t* osrc_d, int32_t* odst_d, int3
   int32_t* osrc = static_cast<int32_t*>(g->scratch["tc_osrc"].ptr);
   int32_t* counts = counts_d;
   if (!counts) GFX_TRY(scratch_t(g, "tc_counts", mo + 1, &counts));
+  // hub rows first (bitmap counting), then every other pair
+  int32_t *hubs = nullptr, *heavy = nullptr;
+  GFX_TRY(scratch_t(g, "tc_hubs", g->n + 1, &hubs));
+  GFX_TRY(scratch_t(g, "tc_heavy", mo + 1, &heavy));
+  const int hub_ctas = ctx->sm_count;
+  uint32_t* bitmaps = nullptr;
+  GFX_TRY(scratch_t(g, "tc_hub_bm", (size_t)hub_ctas * g->words, &bitmaps));
+  Counters* C = g->counters + 3;
   GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
-  GFX_TRY(intersect_pairs(g, osrc, ocol, mo, orow, ocol, counts, total));
+  GFX_CK(cudaMemsetAsync(C, 0, sizeof(Counters), ctx->stream));
+  GFX_CK(cudaMemsetAsync(bitmaps, 0, (size_t)hub_ctas * g->words * 4, ctx->stream));
+  GFX_LAUNCH(k_tc_hub_list, grid_for(g->n, 256, ctx->sm_count * 8), 256, 0, ctx->stream, orow,
+             g->n, hubs, &C->aux2);
+  {
+    // items: each hub's pairs in chunks of kTcHubChunk (host-built, small)
+    auto* pin = static_cast<Counters*>(ctx->pinned);
+    GFX_CK(cudaMemcpyAsync(pin, C, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+    GFX_CK(cudaStreamSynchronize(ctx->stream));
+    const int64_t nh = (int64_t)pin->aux2;
+    std::vector<int32_t> hh((size_t)nh);
+    std::vector<int64_t> rows((size_t)g->n + 1);
+    if (nh) {
+      GFX_CK(cudaMemcpy(hh.data(), hubs, nh * 4, cudaMemcpyDeviceToHost));
+      GFX_CK(cudaMemcpy(rows.data(), orow, (g->n + 1) * 8, cudaMemcpyDeviceToHost));
+    }
+    std::vector<int32_t> item_hub;
+    std::vector<int64_t> item_j0, item_j1;
+    for (int32_t u : hh)
+      for (int64_t j = rows[u]; j < rows[u + 1]; j += kTcHubChunk) {
+        item_hub.push_back(u);
+        item_j0.push_back(j);
+        item_j1.push_back(std::min(j + kTcHubChunk, rows[u + 1]));
+      }
+    const int64_t ni = (int64_t)item_hub.size();
+    if (ni) {
+      int32_t* ih = nullptr;
+      int64_t *ij0 = nullptr, *ij1 = nullptr;
+      GFX_TRY(scratch_t(g, "tc_item_hub", ni, &ih));
+      GFX_TRY(scratch_t(g, "tc_item_j0", ni, &ij0));
+      GFX_TRY(scratch_t(g, "tc_item_j1", ni, &ij1));
+      GFX_CK(cudaMemcpyAsync(ih, item_hub.data(), ni * 4, cudaMemcpyHostToDevice, ctx->stream));
+      GFX_CK(cudaMemcpyAsync(ij0, item_j0.data(), ni * 8, cudaMemcpyHostToDevice, ctx->stream));
+      GFX_CK(cudaMemcpyAsync(ij1, item_j1.data(), ni * 8, cudaMemcpyHostToDevice, ctx->stream));
+      GFX_LAUNCH(k_tc_hubs, hub_ctas, 256, 0, ctx->stream, orow, ocol, ih, ij0, ij1, ni, bitmaps,
+                 g->words, counts, &C->total, &C->aux3);
+      GFX_CK(cudaStreamSynchronize(ctx->stream));  // host item vectors go out of scope
+    }
+  }
+  const int grid = ctx->sm_count * 8;
+  GFX_LAUNCH(k_tc_small, grid_for(mo, 256, grid), 256, 0, ctx->stream, osrc, ocol, mo, orow, ocol,
+             counts, heavy, &C->aux0, &C->total, kTcHub);
+  GFX_LAUNCH(k_tc_heavy, grid, 256, 0, ctx->stream, osrc, ocol, heavy, &C->aux0, orow, ocol,
+             counts, &C->total);
+  GFX_CK(cudaGetLastError());
   GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  {
+    auto* pin = static_cast<Counters*>(ctx->pinned);
+    GFX_CK(cudaMemcpyAsync(pin, C, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+    GFX_CK(cudaStreamSynchronize(ctx->stream));
+    *total = (int64_t)pin->total;
+  }
   if (osrc_d)
     GFX_CK(cudaMemcpyAsync(osrc_d, osrc, mo * 4, cudaMemcpyDeviceToDevice, ctx->stream));
   if (odst_d)
