@@ -5,6 +5,7 @@ container (where /root/reference exists); its outputs are committed so the
 GPU box never needs the reference.
 
 Usage:  python oracle/make_golden.py kat            # mini suite + KAT graphs
+        GOLDEN_S24_FULL=1 python oracle/make_golden.py rmat 24   # + SSSP / CC / PageRank at s24
         python oracle/make_golden.py cache          # reference-written CSR cache files
         python oracle/make_golden.py rmat S [S ...] # R-MAT scale S, ef16, seed 0
 
@@ -185,7 +186,7 @@ def run_rmat(scale: int):
     rec["bfs_auto_trace"] = trace_rows(bd.stats.direction_trace)
     rec["bfs_auto_ms"] = bd.stats.total_runtime_ms
     save()
-    if scale >= 24:
+    if scale >= 24 and not os.environ.get("GOLDEN_S24_FULL"):
         print("s24: graph + bfs only", time.time() - t0)
         return
     for delta in (32, None):
@@ -196,6 +197,21 @@ def run_rmat(scale: int):
         if small:
             arrays[key] = s.labels
     save()
+    if scale >= 24:  # C3 / M3 pins: SSSP above, then CC and PageRank (BC/TC: C4 is s22)
+        c = canon_cc(gx.cc(g).component)
+        rec["cc_canon_sha"] = sha(c)
+        rec["cc_num"] = int(len(np.unique(c)))
+        save()
+        pr = gx.pagerank(g, epsilon=0.0, max_iters=20).rank
+        rec["pr20_sum"] = float(pr.sum())
+        idx = np.random.default_rng(2).choice(n, 4096, replace=False)
+        arrays["pr_idx"] = idx
+        arrays["pr_vals"] = pr[idx]
+        rec["total_s"] = time.time() - t0
+        save()
+        np.savez_compressed(OUT / f"rmat_s{scale}.npz", **arrays)
+        print("done scale", scale, time.time() - t0)
+        return
     c = canon_cc(gx.cc(g).component)
     rec["cc_canon_sha"] = sha(c)
     rec["cc_num"] = int(len(np.unique(c)))

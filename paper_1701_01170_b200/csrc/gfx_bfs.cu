@@ -13,6 +13,11 @@
 //   scan     int64[n+1]      exclusive degree prefix of the current queue
 //   rowbase  int64[n]        row[F[i]] (saves a scattered re-read)
 //   part     int32[m/T+2]    tile -> first item (LB partition)
+//   lvl8     uint8[n]        depth bytes while labels are deferred (the
+//                            persistent loop writes the int32 labels once,
+//                            coalesced, at the end: materialize_labels)
+//   head     int32[2(n+1)]   first / second in-neighbour per vertex with
+//                            degree-1 / degree-2 flags (graph constant)
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -570,7 +575,10 @@ int bfs_host_loop(gfx_graph* g, int64_t source, int direction, bool idemp, bool 
 // replica in gfx_direction.cuh) itself; phases are separated by grid-wide
 // barriers instead of kernel boundaries and host round trips.  The grid
 // barrier's gpu-scope fence also invalidates L1, so every phase reads the
-// previous phase's bitmaps fresh.
+// previous phase's bitmaps fresh.  Push levels pick their expansion by
+// frontier size: <= 32 items (push_tiny: no scan, no plan barrier), <= 64K
+// items (push_mid: 32 items per warp, hubs in a second cooperative pass),
+// else the fused degree scan + load-balanced tiles (expand_tasks).
 // ---------------------------------------------------------------------------
 namespace cg = cooperative_groups;
 

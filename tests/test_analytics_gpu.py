@@ -150,3 +150,31 @@ def test_tc_s22_vs_c_oracle():
     assert total == want_total
     assert np.array_equal(counts.to(torch.int64).cpu().numpy(), want_counts)
     assert np.array_equal(odst.to(torch.int64).cpu().numpy(), want_dst)
+
+
+def test_s24_sssp_cc_pagerank_golden():
+    """C3 (PageRank 20 iterations and CC on R-MAT s24) and M3 (SSSP s24,
+    delta 32 and default) against the reference's own s24 run
+    (GOLDEN_S24_FULL=1 oracle/make_golden.py rmat 24): distances and
+    canonical CC labels bit-exact, PageRank sum and 4096 sampled ranks."""
+    import torch
+
+    from paper_1701_01170_b200._results import labels_to_host
+    from paper_1701_01170_b200.generators import rmat_device_graph
+    from paper_1701_01170_b200.primitives.cc import cc_device
+    from paper_1701_01170_b200.primitives.pagerank import pagerank_device
+    from paper_1701_01170_b200.primitives.sssp import sssp_device
+
+    rec, arrays = rmat_golden(24)
+    if "sssp_d32_sha" not in rec:
+        pytest.skip("s24 SSSP/CC/PageRank goldens not generated")
+    dg = rmat_device_graph(24, 16, 0, weights=(1, 64), weight_seed=0)
+    for delta, key in ((32, "sssp_d32"), (None, "sssp_default")):
+        dist, _, _ = sssp_device(dg, 0, delta=delta)
+        assert sha(labels_to_host(dist)) == rec[key + "_sha"], delta
+    comp, k, _ = cc_device(dg)
+    assert sha(comp.to(torch.int64).cpu().numpy()) == rec["cc_canon_sha"] and k == rec["cc_num"]
+    rank, _ = pagerank_device(dg, 0.85, 0.0, 20)
+    rank = rank.cpu().numpy()
+    assert abs(rank.sum() - rec["pr20_sum"]) < 1e-9
+    assert np.allclose(rank[arrays["pr_idx"]], arrays["pr_vals"], rtol=1e-9, atol=1e-15)
