@@ -277,12 +277,32 @@ __global__ void __launch_bounds__(256)
   if (small)
     for (int i = threadIdx.x; i < kLevelSmem; i += blockDim.x) hist[i] = 0ull;
   __syncthreads();
+  // depths 0..7 (nearly every vertex of a small-world graph) are summed in
+  // registers and reduced per warp; deeper ones go to the histogram
+  constexpr int kReg = 8;
+  unsigned long long acc[kReg];
+#pragma unroll
+  for (int k = 0; k < kReg; ++k) acc[k] = 0ull;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int32_t l = labels[v];
     if (l == GFX_UNVISITED || l >= levels) continue;
     const unsigned long long d = (unsigned long long)(row[v + 1] - row[v]);
-    if (small) atomicAdd(&hist[l], d); else atomicAdd(&out_deg[l], d);
+    if (l < kReg) {
+#pragma unroll
+      for (int k = 0; k < kReg; ++k) acc[k] += (l == k) ? d : 0ull;
+    } else if (small) {
+      atomicAdd(&hist[l], d);
+    } else {
+      atomicAdd(&out_deg[l], d);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kReg; ++k) {
+    const unsigned long long w = warp_sum_u64(acc[k]);
+    if ((threadIdx.x & 31) == 0 && w && k < levels) {
+      if (small) atomicAdd(&hist[k], w); else atomicAdd(&out_deg[k], w);
+    }
   }
   __syncthreads();
   if (small)
