@@ -105,6 +105,38 @@ __global__ void k_sssp_seed(unsigned long long* dp, uint32_t* dist, int32_t src,
   near[0] = src;
 }
 
+// Block-staged appends for the near / far piles: each CTA collects its
+// items in shared memory (block-local atomics) and appends them to the
+// global pile with ONE atomicAdd per flush, instead of two same-address
+// global atomics per warp and tile.
+constexpr int kPileStage = 2048;
+struct PileStage {
+  int32_t nv[kPileStage];
+  int32_t fv[kPileStage], fk[kPileStage];
+  int nn, nfar;
+  unsigned long long base;
+};
+
+__device__ __forceinline__ void pile_flush(PileStage& S, int32_t* __restrict__ near,
+                                           unsigned long long* __restrict__ near_len,
+                                           int32_t* __restrict__ far, int32_t* __restrict__ far_key,
+                                           unsigned long long* __restrict__ far_len) {
+  __syncthreads();
+  if (threadIdx.x == 0) S.base = S.nn ? atomicAdd(near_len, (unsigned long long)S.nn) : 0ull;
+  __syncthreads();
+  for (int i = threadIdx.x; i < S.nn; i += blockDim.x) near[S.base + i] = S.nv[i];
+  __syncthreads();
+  if (threadIdx.x == 0) S.base = S.nfar ? atomicAdd(far_len, (unsigned long long)S.nfar) : 0ull;
+  __syncthreads();
+  for (int i = threadIdx.x; i < S.nfar; i += blockDim.x) {
+    far[S.base + i] = S.fv[i];
+    far_key[S.base + i] = S.fk[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) S.nn = S.nfar = 0;
+  __syncthreads();
+}
+
 // split the improved vertices against the threshold (near_far.py:40-57)
 __global__ void __launch_bounds__(256)
     k_sssp_split(const int32_t* __restrict__ touched, const unsigned long long* __restrict__ n_d,
@@ -112,37 +144,30 @@ __global__ void __launch_bounds__(256)
                  int32_t* __restrict__ near, unsigned long long* __restrict__ near_len,
                  int32_t* __restrict__ far, int32_t* __restrict__ far_key,
                  unsigned long long* __restrict__ far_len) {
+  __shared__ PileStage S;
   const int64_t n = (int64_t)*n_d;
-  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) S.nn = S.nfar = 0;
+  __syncthreads();
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n;
        base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = base + threadIdx.x;
-    int32_t v = 0;
-    int32_t key = 0;
-    bool valid = i < n, is_near = false;
-    if (valid) {
-      v = touched[i];
-      key = (int32_t)dist[v];
+    if (i < n) {
+      const int32_t v = touched[i];
+      const int32_t key = (int32_t)dist[v];
       atomicAnd(&mark[v >> 5], ~(1u << (v & 31)));  // re-arm for the next iteration
-      is_near = (double)key < threshold;
+      if ((double)key < threshold) {
+        S.nv[atomicAdd(&S.nn, 1)] = v;
+      } else {
+        const int at = atomicAdd(&S.nfar, 1);
+        S.fv[at] = v;
+        S.fk[at] = key;
+      }
     }
-    const unsigned nm = __ballot_sync(0xffffffffu, valid && is_near);
-    const unsigned fm = __ballot_sync(0xffffffffu, valid && !is_near);
-    unsigned long long nb = 0, fb = 0;
-    if (lane == 0) {
-      if (nm) nb = atomicAdd(near_len, (unsigned long long)__popc(nm));
-      if (fm) fb = atomicAdd(far_len, (unsigned long long)__popc(fm));
-    }
-    nb = __shfl_sync(0xffffffffu, nb, 0);
-    fb = __shfl_sync(0xffffffffu, fb, 0);
-    const unsigned below = (1u << lane) - 1;
-    if (valid && is_near) near[nb + __popc(nm & below)] = v;
-    if (valid && !is_near) {
-      const unsigned long long p = fb + __popc(fm & below);
-      far[p] = v;
-      far_key[p] = key;
-    }
+    __syncthreads();
+    if (S.nn > kPileStage - (int)blockDim.x || S.nfar > kPileStage - (int)blockDim.x)
+      pile_flush(S, near, near_len, far, far_key, far_len);
   }
+  pile_flush(S, near, near_len, far, far_key, far_len);
 }
 
 // advance_bucket (near_far.py:68-85): drop stale far entries, split the rest
@@ -154,37 +179,30 @@ __global__ void __launch_bounds__(256)
                  int32_t* __restrict__ near, unsigned long long* __restrict__ near_len,
                  int32_t* __restrict__ far2, int32_t* __restrict__ far2_key,
                  unsigned long long* __restrict__ far2_len) {
-  const int lane = threadIdx.x & 31;
+  __shared__ PileStage S;
+  if (threadIdx.x == 0) S.nn = S.nfar = 0;
+  __syncthreads();
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n;
        base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = base + threadIdx.x;
-    bool to_near = false, to_far = false;
-    int32_t v = 0, key = 0;
     if (i < n) {
-      v = far[i];
-      key = far_key[i];
-      const bool fresh = (int32_t)dist[v] == key;
-      if (fresh) {
-        if (split && (double)key < threshold) to_near = true; else to_far = true;
+      const int32_t v = far[i];
+      const int32_t key = far_key[i];
+      if ((int32_t)dist[v] == key) {  // fresh
+        if (split && (double)key < threshold) {
+          S.nv[atomicAdd(&S.nn, 1)] = v;
+        } else {
+          const int at = atomicAdd(&S.nfar, 1);
+          S.fv[at] = v;
+          S.fk[at] = key;
+        }
       }
     }
-    const unsigned nm = __ballot_sync(0xffffffffu, to_near);
-    const unsigned fm = __ballot_sync(0xffffffffu, to_far);
-    unsigned long long nb = 0, fb = 0;
-    if (lane == 0) {
-      if (nm) nb = atomicAdd(near_len, (unsigned long long)__popc(nm));
-      if (fm) fb = atomicAdd(far2_len, (unsigned long long)__popc(fm));
-    }
-    nb = __shfl_sync(0xffffffffu, nb, 0);
-    fb = __shfl_sync(0xffffffffu, fb, 0);
-    const unsigned below = (1u << lane) - 1;
-    if (to_near) near[nb + __popc(nm & below)] = v;
-    if (to_far) {
-      const unsigned long long p = fb + __popc(fm & below);
-      far2[p] = v;
-      far2_key[p] = key;
-    }
+    __syncthreads();
+    if (S.nn > kPileStage - (int)blockDim.x || S.nfar > kPileStage - (int)blockDim.x)
+      pile_flush(S, near, near_len, far2, far2_key, far2_len);
   }
+  pile_flush(S, near, near_len, far2, far2_key, far2_len);
 }
 
 __global__ void k_sssp_unpack(const unsigned long long* __restrict__ dp, int64_t n,

@@ -82,7 +82,7 @@ def sssp_device(dg, source: int, delta=None, use_priority_queue: bool = True,
         stats.device_levels.append({"iteration": int(r.iteration), "ms": float(r.ms),
                                     "bytes_alg": int(r.bytes_alg), "work": int(r.work),
                                     "frontier_in": int(r.frontier_in),
-                                    "frontier_out": int(r.frontier_out)})
+                                    "frontier_out": int(r.frontier_out), "far": int(r.n_u)})
     stats.iterations = int(st.iterations)
     stats.edges_traversed = int(st.edges_traversed)
     stats.work_slots = int(st.work_slots)
