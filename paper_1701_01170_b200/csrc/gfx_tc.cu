@@ -277,6 +277,10 @@ extern "C" int gfx_tc_orient(gfx_graph* g, int64_t* m_oriented) {
   GFX_REQUIRE(g->flags & GFX_GRAPH_UNDIRECTED, "tc expects a canonical undirected graph");
   gfx_ctx* ctx = g->ctx;
   GFX_CK(cudaSetDevice(ctx->device));
+  if (g->m_oriented >= 0) {  // graph constant, already built (gfx_graph_refresh resets it)
+    *m_oriented = g->m_oriented;
+    return GFX_OK;
+  }
   const int64_t n = g->n;
   int64_t *ocnt, *orow;
   int32_t *ocol, *osrc;
