@@ -205,10 +205,26 @@ __global__ void __launch_bounds__(256)
   pile_flush(S, near, near_len, far2, far2_key, far2_len);
 }
 
+// (dist | pred) words -> the two int32 outputs; two vertices per thread with
+// 16-byte loads and 8-byte stores when the outputs are 8-byte aligned
 __global__ void k_sssp_unpack(const unsigned long long* __restrict__ dp, int64_t n,
-                              int32_t* __restrict__ dist, int32_t* __restrict__ preds) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
+                              int32_t* __restrict__ dist, int32_t* __restrict__ preds, int vec) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t done = 0;
+  if (vec) {
+    const int64_t pairs = n >> 1;
+    for (int64_t p = t0; p < pairs; p += stride) {
+      const ulonglong2 x = reinterpret_cast<const ulonglong2*>(dp)[p];
+      const uint32_t d0 = (uint32_t)(x.x >> 32), d1 = (uint32_t)(x.y >> 32);
+      reinterpret_cast<int2*>(dist)[p] =
+          make_int2(d0 == 0xFFFFFFFFu ? GFX_UNVISITED : (int32_t)d0,
+                    d1 == 0xFFFFFFFFu ? GFX_UNVISITED : (int32_t)d1);
+      reinterpret_cast<int2*>(preds)[p] = make_int2((int32_t)(uint32_t)x.x, (int32_t)(uint32_t)x.y);
+    }
+    done = pairs << 1;
+  }
+  for (int64_t v = done + t0; v < n; v += stride) {
     const unsigned long long x = dp[v];
     const uint32_t d = (uint32_t)(x >> 32);
     dist[v] = d == 0xFFFFFFFFu ? GFX_UNVISITED : (int32_t)d;
@@ -339,7 +355,9 @@ int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t*
       GFX_CK(cudaMemcpyAsync(&C[3].aux0, &pin[3].aux1, 8, cudaMemcpyHostToDevice, ctx->stream));
     }
   }
-  GFX_LAUNCH(k_sssp_unpack, grid_for(n, 256, grid), 256, 0, ctx->stream, dp, n, dist, preds);
+  const int vec = ((reinterpret_cast<uintptr_t>(dist) | reinterpret_cast<uintptr_t>(preds) |
+                    reinterpret_cast<uintptr_t>(dp)) & 15) == 0 ? 1 : 0;
+  GFX_LAUNCH(k_sssp_unpack, grid_for(n, 256, grid), 256, 0, ctx->stream, dp, n, dist, preds, vec);
   l2_window(ctx, nullptr, 0, false);
   GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));
   GFX_CK(cudaEventSynchronize(ctx->ev1));
