@@ -49,6 +49,9 @@ def parse_args():
     ap.add_argument("--no-s27", action="store_true", help="skip the single-GPU scale-27 extra")
     ap.add_argument("--partitioned", action="store_true",
                     help="use the partitioned multi-GPU engine even at N=1 (default: N>1)")
+    ap.add_argument("--python-loop", action="store_true",
+                    help="partitioned engine: drive the levels from Python (dist.bfs_partitioned) "
+                         "instead of the native loop (gfx_dbfs_run)")
     return ap.parse_args()
 
 
@@ -317,7 +320,7 @@ def run_ours(args, dist: Dist):
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, dg, e_r)
     if dist.rank == 0:
-        print(json.dumps(out), flush=True)
+        emit(out)
     dist.close()
 
 
@@ -325,12 +328,7 @@ def run_partitioned(args, dist: Dist):
     """N GPUs, one process each: the s24 graph 1D-partitioned (owner = v mod N),
     per-level NCCL exchange (paper_1701_01170_b200/dist.py).  Strong scaling:
     the same graph and BFS at every N."""
-    import torch
     import torch.distributed as tdist
-
-    from paper_1701_01170_b200 import _native
-    from paper_1701_01170_b200.dist import DeviceEngine, ProcessComm, bfs_partitioned, partition_graph
-    from paper_1701_01170_b200.generators import rmat_device_graph
 
     if dist.pg is None:  # --partitioned at N=1: a one-rank NCCL group
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -340,40 +338,29 @@ def run_partitioned(args, dist: Dist):
         tdist.init_process_group("nccl")
         dist.pg = tdist
     P, r = dist.world, dist.rank
-    t_build = time.perf_counter()
-    dg = rmat_device_graph(args.scale, args.edge_factor, 0)
-    n, m = dg.num_vertices, dg.num_edges
-    lrow, lcol = partition_graph(dg, P, r)
-    del dg
-    torch.cuda.empty_cache()
-    eng = DeviceEngine(lrow, lcol, n, m, P, r)
-    comm = ProcessComm(eng)
-    torch.cuda.synchronize()
-    build_s = time.perf_counter() - t_build
-
-    def step():
-        return bfs_partitioned(comm, n, m, args.source, direction=args.direction)
-
     sampler = ClockSampler(dist.local)
     sampler.start()
-    for _ in range(max(args.warmup, 3)):
-        st = step()
-    reached, deg = eng.reached_degree_sum()
-    e_r = int(dist.sum(float(deg)))
-    dist.barrier()
-    torch.cuda.synchronize()
-    l0 = _native.launch_count()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    for _ in range(args.steps):
-        step()
-    ev1.record()
-    torch.cuda.synchronize()
-    launches = _native.launch_count() - l0
-    dist.barrier()
-    t_ms = dist.max(ev0.elapsed_time(ev1))
+    run = _partitioned_run(args, dist, args.scale, args.steps, max(args.warmup, 3))
     clocks = sampler.stop()
+    st, t_ms, e_r, n, m, launches, build_s, loop = (run[k] for k in (
+        "st", "t_ms", "e_r", "n", "m", "launches", "build_s", "loop"))
+    extra = {}
+    if args.scale == 24 and not args.no_s27:
+        try:
+            r27 = _partitioned_run(args, dist, 27, 5, 3, with_1gpu=True)
+            ms27 = r27["t_ms"] / 5
+            extra["bfs_do_s27_partitioned"] = {
+                "gteps": round(r27["e_r"] / (ms27 * 1e-3) / 1e9, 2), "ms": round(ms27, 4),
+                "n_gpus": P, "n": r27["n"], "m": r27["m"], "E_r": r27["e_r"],
+                "level_loop": r27["loop"],
+                "single_gpu_same_graph": r27.get("one_gpu"),
+                "what": "BASELINE config C5: R-MAT s27 ef16 1D-partitioned over the N ranks, "
+                        "5 BFS from vertex 0 timed (max over ranks); single_gpu_same_graph = "
+                        "rank 0's device-resident DO-BFS on the whole s27 graph before partitioning",
+                "trace": [[t["iteration"], t["decision"], t["n_f"]]
+                          for t in r27["st"].direction_trace]}
+        except Exception as exc:  # noqa: BLE001 -- report, keep the headline line
+            extra["s27_error"] = repr(exc)
     peak, peak_kind = measured_peak_gbs()
     ms = t_ms / args.steps
     achieved = st.bytes_alg / (ms * 1e-3) / 1e9 / P
@@ -387,7 +374,9 @@ def run_partitioned(args, dist: Dist):
                    "scale": args.scale, "edge_factor": args.edge_factor, "seed": 0,
                    "source": args.source, "direction": args.direction, "n": n, "m": m, "E_r": e_r,
                    "parallelism": f"1d-cyclic-partition{P}",
-                   "exchange": "NCCL allreduce(n_f) + all_to_all(dst,src pairs) push / all_gather(frontier bitmaps) pull",
+                   "exchange": "NCCL all_to_all(pair counts) + send/recv(dst,src pairs) push / "
+                               "all_gather(frontier bitmaps) pull / allreduce(level counters)",
+                   "level_loop": loop,
                    "l2": "inputs larger than L2; per-BFS state re-initialised each step",
                    "graph_build_s": round(build_s, 3)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -396,10 +385,86 @@ def run_partitioned(args, dist: Dist):
                      "peak_source": peak_kind},
         "gpu_launches": int(launches), "clocks": clocks,
         "trace": [[t["iteration"], t["decision"], t["n_f"]] for t in st.direction_trace],
+        "extras": extra,
     }
     if dist.rank == 0:
-        print(json.dumps(out), flush=True)
+        emit(out)
     dist.close()
+
+
+def _partitioned_run(args, dist, scale: int, steps: int, warmup: int, with_1gpu: bool = False):
+    """Build R-MAT ``scale`` on every rank, keep this rank's partition, and
+    time ``steps`` partitioned BFS (CUDA events, max over ranks)."""
+    import torch
+
+    from paper_1701_01170_b200 import _native
+    from paper_1701_01170_b200.dist import (DeviceEngine, NativeComm, ProcessComm, bfs_partitioned,
+                                            bfs_partitioned_native, partition_graph)
+    from paper_1701_01170_b200.generators import rmat_device_graph
+
+    P, r = dist.world, dist.rank
+    torch.cuda.empty_cache()
+    t_build = time.perf_counter()
+    dg = rmat_device_graph(scale, args.edge_factor, 0)
+    n, m = dg.num_vertices, dg.num_edges
+    one_gpu = None
+    if with_1gpu and r == 0:
+        from paper_1701_01170_b200.primitives.bfs import bfs_batch, bfs_device
+
+        lab = torch.empty(n, dtype=torch.int32, device=dg.row.device)
+        prd = torch.empty(n, dtype=torch.int32, device=dg.row.device)
+        for _ in range(3):
+            st1 = bfs_device(dg, args.source, direction=args.direction, labels=lab, preds=prd)[2]
+        ms1 = bfs_batch(dg, [args.source] * 5, direction=args.direction, labels=lab, preds=prd) / 5
+        one_gpu = {"gteps": round(st1.edges_reached / (ms1 * 1e-3) / 1e9, 2), "ms": round(ms1, 4)}
+        del lab, prd
+    lrow, lcol = partition_graph(dg, P, r)
+    del dg
+    torch.cuda.empty_cache()
+    eng = DeviceEngine(lrow, lcol, n, m, P, r)
+    comm = ProcessComm(eng)
+    ncomm, loop = None, "python"
+    if not args.python_loop:
+        err = None
+        try:
+            ncomm = NativeComm(eng)
+        except Exception as exc:  # noqa: BLE001 -- agreed on below, reported in the line
+            err = repr(exc)
+        if dist.sum(0.0 if err is None else 1.0) == 0:
+            loop = "native"
+        else:
+            loop = f"python (native communicator unavailable: {err})"
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t_build
+
+    def step():
+        if loop == "native":
+            return bfs_partitioned_native(eng, ncomm, n, m, args.source, direction=args.direction)
+        return bfs_partitioned(comm, n, m, args.source, direction=args.direction)
+
+    for _ in range(warmup):
+        st = step()
+    reached, deg = eng.reached_degree_sum()
+    e_r = int(dist.sum(float(deg)))
+    dist.barrier()
+    torch.cuda.synchronize()
+    l0 = _native.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    launches = _native.launch_count() - l0
+    dist.barrier()
+    t_ms = dist.max(ev0.elapsed_time(ev1))
+    if ncomm is not None:
+        ncomm.close()
+    del eng, comm, lrow, lcol
+    torch.cuda.empty_cache()
+    return {"st": st, "t_ms": t_ms, "e_r": e_r, "n": n, "m": m, "launches": launches,
+            "build_s": build_s, "one_gpu": one_gpu, "loop": loop}
 
 
 def extras(args, dg, labels, preds, dist, peak):
@@ -686,11 +751,27 @@ def run_reference(args, dist: Dist):
                                       "restatement of reference bfs.py), 1 thread"},
            "e2e": {"value": round(v, 6), "unit": "GTEPS", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    emit(out)
+
+
+_JSON_OUT = None
+
+
+def emit(out: dict) -> None:
+    """The one JSON line, on the process's original stdout."""
+    f = _JSON_OUT or sys.stdout
+    f.write(json.dumps(out) + "\n")
+    f.flush()
 
 
 def main():
+    global _JSON_OUT
     args = parse_args()
+    # libraries (NCCL's version banner, ...) may print to fd 1: point fd 1 at
+    # stderr and keep a private handle on the real stdout for the JSON line
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     dist = Dist()
     if args.impl == "reference":
         run_reference(args, dist)

@@ -253,10 +253,14 @@ GFX_API int gfx_assign_weights(gfx_graph* g, int64_t lo, int64_t hi, uint64_t st
 /* ---- partitioned multi-GPU BFS (1D cyclic partition) -------
  * Rank r of P owns vertices v = l*P + r (local id l); its local CSR holds
  * the owned rows with GLOBAL column ids.  The host drives the levels and the
- * collectives (allreduce of n_f, all_to_all of (dst, src) pairs for push
- * levels, all_gather of local frontier bitmaps for pull levels) on buffers it
- * owns and binds here; the direction decision is the reference formula on the
- * global counts (direction.py:52-70).  Undirected graphs only. */
+ * collectives (allreduce of the level counters, all_to_all of (dst, src)
+ * pairs for push levels, all_gather of local frontier bitmaps for pull
+ * levels) on buffers it owns and binds here; the direction decision is the
+ * reference formula on the global counts (direction.py:52-70).  Undirected
+ * graphs only.  Every level entry point only ENQUEUES work on the context
+ * stream (no host synchronisation): per-level counts land in the bound
+ * device arrays, the host reduces / reads them once per level and hands the
+ * rank's new frontier size back with gfx_dbfs_commit. */
 typedef struct gfx_dbfs gfx_dbfs;
 GFX_API int gfx_dist_partition_sizes(gfx_graph* g, int P, int r, int64_t* n_local,
                                      int64_t* m_local);
@@ -267,17 +271,47 @@ GFX_API int gfx_dbfs_create(gfx_ctx* ctx, int64_t n, int64_t m, int P, int r,
 GFX_API int gfx_dbfs_destroy(gfx_dbfs* db);
 GFX_API int gfx_dbfs_words(gfx_dbfs* db, int64_t* words_local, int64_t* words_max);
 /* labels/preds: int32[n_local]; send/recv: uint64 pairs (dst << 32 | src);
- * front_local: uint32[words_max]; gathered: uint32[P * words_max] */
+ * front_local: uint32[words_max]; gathered: uint32[P * words_max];
+ * send_counts: int64[2P]: [0, P) pairs per destination rank (own rank 0),
+ * [P, 2P) the counts received from each rank (written by the exchange);
+ * stats: int64[8] = {local new frontier, local slots expanded, pull probes,
+ * pull candidates} of the last level, written twice (stats[4..7] is the copy
+ * the host allreduces in place) */
 GFX_API int gfx_dbfs_bind(gfx_dbfs* db, int32_t* labels_d, int32_t* preds_d, void* send_d,
                           int64_t send_cap, void* recv_d, int64_t recv_cap,
-                          uint32_t* front_local_d, uint32_t* gathered_d);
+                          uint32_t* front_local_d, uint32_t* gathered_d,
+                          int64_t* send_counts_d, int64_t* stats_d);
+/* *nf_local = 1 if this rank owns the source, else 0 (known on the host) */
 GFX_API int gfx_dbfs_reset(gfx_dbfs* db, int64_t source, int64_t* nf_local);
-GFX_API int gfx_dbfs_push_expand(gfx_dbfs* db, int32_t depth, int64_t* send_counts,
-                                 int64_t* local_new, int64_t* edges);
-GFX_API int gfx_dbfs_push_claim(gfx_dbfs* db, int64_t nrecv, int32_t depth, int64_t* nf_local);
+/* push level: expand, claim owned targets, bucket remote (dst, src) pairs
+ * into send (grouped by destination rank) and their counts into send_counts */
+GFX_API int gfx_dbfs_push_expand(gfx_dbfs* db, int32_t depth);
+/* push level, after the all_to_all: claim the nrecv received pairs */
+GFX_API int gfx_dbfs_push_claim(gfx_dbfs* db, int64_t nrecv, int32_t depth);
+/* pull level: local frontier -> front_local (before the all_gather) */
 GFX_API int gfx_dbfs_pull_prepare(gfx_dbfs* db);
-GFX_API int gfx_dbfs_pull(gfx_dbfs* db, int32_t depth, int64_t* nf_local, int64_t* probes,
-                          int64_t* candidates);
+/* pull level, after the all_gather into gathered */
+GFX_API int gfx_dbfs_pull(gfx_dbfs* db, int32_t depth);
+/* end of level: the rank's new frontier size (stats[0] as read by the host) */
+GFX_API int gfx_dbfs_commit(gfx_dbfs* db, int64_t nf_local);
+
+/* Native level loop: one whole partitioned BFS from `source` with the
+ * per-level protocol above, NCCL called from C++ on the context stream (one
+ * host synchronisation per pull level, two per push level).  `comm` may be
+ * NULL only when P == 1.  recs (rec_cap records) receives the direction
+ * trace; stats the totals (edges_traversed = push slots, bytes_alg,
+ * device_ms = CUDA-event time of the whole BFS on this rank). */
+typedef struct gfx_nccl gfx_nccl;
+/* resolve NCCL from the library already loaded in the process (path: its
+ * file, e.g. torch's nvidia/nccl/lib/libnccl.so.2; NULL: by soname) */
+GFX_API int gfx_nccl_load(const char* path);
+GFX_API int gfx_nccl_unique_id(uint8_t* id_out /* 128 bytes */);
+GFX_API int gfx_nccl_comm_create(gfx_ctx* ctx, int nranks, int rank, const uint8_t* id,
+                                 gfx_nccl** out);
+GFX_API int gfx_nccl_comm_destroy(gfx_nccl* comm);
+GFX_API int gfx_dbfs_run(gfx_dbfs* db, gfx_nccl* comm, int64_t source, int direction,
+                         double do_a, double do_b, int mu_edge_based, gfx_iter_rec* recs,
+                         int64_t rec_cap, gfx_stats* stats);
 
 /* ---- kernel experiments (tools/expand_lab.py; not a product path) -------
  * One LB expansion of F_d with functor variant 0 (stream only), 1 (stream +

@@ -103,14 +103,19 @@ _SIGS = {
     "gfx_dbfs_destroy": (c_int, [c_void_p]),
     "gfx_dbfs_words": (c_int, [c_void_p, POINTER(c_int64), POINTER(c_int64)]),
     "gfx_dbfs_bind": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int64,
-                              c_void_p, c_void_p]),
+                              c_void_p, c_void_p, c_void_p, c_void_p]),
     "gfx_dbfs_reset": (c_int, [c_void_p, c_int64, POINTER(c_int64)]),
-    "gfx_dbfs_push_expand": (c_int, [c_void_p, c_int32, POINTER(c_int64), POINTER(c_int64),
-                                     POINTER(c_int64)]),
-    "gfx_dbfs_push_claim": (c_int, [c_void_p, c_int64, c_int32, POINTER(c_int64)]),
+    "gfx_dbfs_push_expand": (c_int, [c_void_p, c_int32]),
+    "gfx_dbfs_push_claim": (c_int, [c_void_p, c_int64, c_int32]),
     "gfx_dbfs_pull_prepare": (c_int, [c_void_p]),
-    "gfx_dbfs_pull": (c_int, [c_void_p, c_int32, POINTER(c_int64), POINTER(c_int64),
-                              POINTER(c_int64)]),
+    "gfx_dbfs_pull": (c_int, [c_void_p, c_int32]),
+    "gfx_dbfs_commit": (c_int, [c_void_p, c_int64]),
+    "gfx_nccl_load": (c_int, [c_char_p]),
+    "gfx_nccl_unique_id": (c_int, [c_void_p]),
+    "gfx_nccl_comm_create": (c_int, [c_void_p, c_int, c_int, c_void_p, POINTER(c_void_p)]),
+    "gfx_nccl_comm_destroy": (c_int, [c_void_p]),
+    "gfx_dbfs_run": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_double, c_double, c_int,
+                             POINTER(IterRec), c_int64, POINTER(Stats)]),
     "gfx_debug_gridsync": (c_int, [c_void_p, c_int, c_int, c_int, c_int, POINTER(c_float)]),
     "gfx_debug_chase": (c_int, [c_void_p, c_void_p, c_int, ctypes.c_uint32, POINTER(c_double)]),
     "gfx_debug_expand": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_int32,

@@ -18,10 +18,15 @@
 // torch tensors and passes their device pointers in.
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstring>
 
 #include <vector>
 
 #include "gfx_device.cuh"
+#include "gfx_direction.cuh"
 #include "gfx_expand.cuh"
 #include "gfx_internal.cuh"
 #include "gfx_pull.cuh"
@@ -38,11 +43,13 @@ struct gfx_dbfs {
   unsigned long long* recv = nullptr;
   uint32_t* front_local = nullptr;  // wmax words: local frontier bitmap (pull levels)
   uint32_t* gathered = nullptr;     // P * wmax words
+  int64_t* send_counts = nullptr;   // P: pairs per destination rank
+  int64_t* stats = nullptr;         // 4: new frontier, slots, probes, candidates
   int64_t send_cap = 0, recv_cap = 0;
-  // engine state
-  int64_t nf = 0, q_off = 0, q_end = 0, local_new = 0;
+  // engine state (host mirror; nf arrives through gfx_dbfs_commit)
+  int64_t nf = 0, q_off = 0, q_end = 0;
   bool queue_form = true;
-  std::vector<long long> bucket_off;
+  bool pending_push = false;  // the level in flight appends to the queue
 };
 
 namespace gfx {
@@ -127,23 +134,37 @@ __global__ void __launch_bounds__(256)
                   uint32_t* __restrict__ sent, unsigned long long* __restrict__ send,
                   int32_t* __restrict__ next_q, unsigned long long* __restrict__ next_len) {
   __shared__ unsigned long long hist[64];
+  const int lane = threadIdx.x & 31;
   const int64_t n = (int64_t)*n_d;
   if (PASS == 0) {
     for (int i = threadIdx.x; i < P; i += blockDim.x) hist[i] = 0;
     __syncthreads();
   }
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t d = emit[i];
-    const int o = d % P;
+  // warp-uniform trip count so the match / shuffle below see full warps
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + lane;
+    const bool ok = i < n;
+    const int32_t d = ok ? emit[i] : 0;
+    const int o = ok ? d % P : 64;  // 64: idle lanes form their own group
+    const unsigned peers = __match_any_sync(0xffffffffu, o);
+    const int leader = __ffs(peers) - 1;
+    const int rank_in = __popc(peers & ((1u << lane) - 1));
     if (PASS == 0) {
-      atomicAdd(&hist[o], 1ull);
-    } else if (o == r) {
-      next_q[atomicAdd(next_len, 1ull)] = d / P;
+      if (ok && lane == leader) atomicAdd(&hist[o], (unsigned long long)__popc(peers));
     } else {
-      const unsigned long long at = atomicAdd(&cursors[o], 1ull);
-      send[at] = ((unsigned long long)(uint32_t)d << 32) | (uint32_t)sent_src[d];
-      atomicAnd(&sent[d >> 5], ~(1u << (d & 31)));
+      unsigned long long at = 0;
+      if (ok && lane == leader)
+        at = atomicAdd(o == r ? next_len : &cursors[o], (unsigned long long)__popc(peers));
+      at = __shfl_sync(0xffffffffu, at, leader) + rank_in;
+      if (ok) {
+        if (o == r) {
+          next_q[at] = d / P;
+        } else {
+          send[at] = ((unsigned long long)(uint32_t)d << 32) | (uint32_t)sent_src[d];
+          atomicAnd(&sent[d >> 5], ~(1u << (d & 31)));
+        }
+      }
     }
   }
   if (PASS == 0) {
@@ -247,6 +268,50 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// remote-owner cursors (exclusive scan, own bucket excluded) and the
+// host-visible per-destination counts; clears the owned-append counter
+__global__ void k_dist_cursors(int P, int r, const unsigned long long* __restrict__ hist,
+                               unsigned long long* __restrict__ cursors,
+                               int64_t* __restrict__ send_counts,
+                               unsigned long long* __restrict__ next_len) {
+  if (threadIdx.x != 0) return;
+  unsigned long long acc = 0;
+  for (int o = 0; o < P; ++o) {
+    cursors[o] = acc;
+    const unsigned long long c = o == r ? 0ull : hist[o];
+    send_counts[o] = (int64_t)c;
+    acc += c;
+  }
+  *next_len = 0;
+}
+
+// zero the three level counters and seed the frontier length
+__global__ void k_dist_level_init(Counters* C, unsigned long long nf) {
+  unsigned long long* w = reinterpret_cast<unsigned long long*>(C);
+  for (int i = threadIdx.x; i < 3 * (int)(sizeof(Counters) / 8); i += blockDim.x) w[i] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) C[0].out_len = nf;
+}
+
+// level counters -> the host-bound stats array, twice: st[0..3] stay this
+// rank's, st[4..7] are the copy the host allreduces in place
+__global__ void k_dist_stats(const Counters* __restrict__ C, int which, int64_t* __restrict__ st) {
+  if (threadIdx.x != 0) return;
+  int64_t v[4];
+  if (which == 0) {  // push: new frontier = owned claims + received claims; slots
+    v[0] = (int64_t)C[2].out_len;
+    v[1] = (int64_t)C[1].total;
+    v[2] = 0;
+    v[3] = 0;
+  } else {  // pull
+    v[0] = (int64_t)C[0].out_len;
+    v[1] = 0;
+    v[2] = (int64_t)C[0].aux0;
+    v[3] = (int64_t)C[0].aux1;
+  }
+  for (int k = 0; k < 4; ++k) st[k] = st[4 + k] = v[k];
+}
+
 __global__ void k_dist_q2bm(const int32_t* __restrict__ F, int64_t nf, uint32_t* __restrict__ bm) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nf;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -344,9 +409,13 @@ int gfx_dbfs_words(gfx_dbfs* db, int64_t* words_local, int64_t* words_max) {
 
 int gfx_dbfs_bind(gfx_dbfs* db, int32_t* labels_d, int32_t* preds_d, void* send_d,
                   int64_t send_cap, void* recv_d, int64_t recv_cap, uint32_t* front_local_d,
-                  uint32_t* gathered_d) {
-  GFX_REQUIRE(db && labels_d && preds_d && send_d && recv_d && front_local_d && gathered_d,
+                  uint32_t* gathered_d, int64_t* send_counts_d, int64_t* stats_d) {
+  GFX_REQUIRE(db && labels_d && preds_d && send_d && recv_d && front_local_d && gathered_d &&
+                  send_counts_d && stats_d,
               "gfx_dbfs_bind: null argument");
+  GFX_REQUIRE(send_cap >= db->n && recv_cap >= db->n,
+              "exchange buffers need n pairs (send %lld, recv %lld, n %lld)", (long long)send_cap,
+              (long long)recv_cap, (long long)db->n);
   db->labels = labels_d;
   db->preds = preds_d;
   db->send = static_cast<unsigned long long*>(send_d);
@@ -355,6 +424,8 @@ int gfx_dbfs_bind(gfx_dbfs* db, int32_t* labels_d, int32_t* preds_d, void* send_
   db->recv_cap = recv_cap;
   db->front_local = front_local_d;
   db->gathered = gathered_d;
+  db->send_counts = send_counts_d;
+  db->stats = stats_d;
   return GFX_OK;
 }
 
@@ -387,21 +458,20 @@ int gfx_dbfs_reset(gfx_dbfs* db, int64_t source, int64_t* nf_local) {
   db->q_end = 0;
   db->nf = 0;
   db->queue_form = true;
+  db->pending_push = false;
   if (source % db->P == db->r) {
     GFX_LAUNCH(k_dist_seed, 1, 1, 0, ctx->stream, source / db->P, db->labels, visited, order);
     db->nf = 1;
     db->q_end = 1;
   }
-  GFX_CK(cudaStreamSynchronize(ctx->stream));
+  GFX_CK(cudaGetLastError());
   *nf_local = db->nf;
   return GFX_OK;
 }
 
-// push: expand the local frontier; returns per-destination-rank pair counts
-// (host array of P) and the number of owned vertices claimed locally
-int gfx_dbfs_push_expand(gfx_dbfs* db, int32_t depth, int64_t* send_counts, int64_t* local_new,
-                         int64_t* edges) {
-  GFX_REQUIRE(db && send_counts && local_new && edges, "gfx_dbfs_push_expand: null argument");
+// push: expand the local frontier, claim owned targets, bucket remote pairs
+int gfx_dbfs_push_expand(gfx_dbfs* db, int32_t depth) {
+  GFX_REQUIRE(db && db->stats, "gfx_dbfs_push_expand: unbound engine");
   gfx_graph* g = db->lg;
   gfx_ctx* ctx = db->ctx;
   GFX_CK(cudaSetDevice(ctx->device));
@@ -415,9 +485,10 @@ int gfx_dbfs_push_expand(gfx_dbfs* db, int32_t depth, int64_t* send_counts, int6
   GFX_TRY(scratch_t(g, "q_scan", db->nl + 2, &scan));
   GFX_TRY(scratch_t(g, "q_rowbase", db->nl + 1, &rowbase));
   GFX_TRY(scratch_t(g, "q_part", part_capacity(db->ml, db->nl), &part));
+  unsigned long long* cnt64 = nullptr;
+  GFX_TRY(scratch_t(g, "d_counts", 2 * 64, &cnt64));
   Counters* C = g->counters;
-  auto* pin = static_cast<Counters*>(ctx->pinned);
-  GFX_CK(cudaMemsetAsync(C, 0, 3 * sizeof(Counters), ctx->stream));
+  GFX_LAUNCH(k_dist_level_init, 1, 32, 0, ctx->stream, C, (unsigned long long)db->nf);
   if (!db->queue_form) {
     GFX_LAUNCH(k_dist_bm2q, grid_for(db->wl * 32, 256, ctx->sm_count * 8), 256, 0, ctx->stream,
                db->wl, db->front_local, order + db->q_end, &C[2].aux0);
@@ -425,47 +496,25 @@ int gfx_dbfs_push_expand(gfx_dbfs* db, int32_t depth, int64_t* send_counts, int6
     db->q_end += db->nf;
     db->queue_form = true;
   }
-  const unsigned long long nf = (unsigned long long)db->nf;
-  GFX_CK(cudaMemcpyAsync(&C[0].out_len, &nf, 8, cudaMemcpyHostToDevice, ctx->stream));
   DistClaimOp op{visited, sent, sent_src, db->labels, db->preds, depth, db->P, db->r, {}};
   GFX_TRY(lb_advance(g, order + db->q_off, &C[0].out_len, db->nf, &C[1], scan, rowbase, part, op,
                      emit, &C[1].out_len));
-  // pass 0: per-owner counts
-  unsigned long long* cnt64 = nullptr;
-  GFX_TRY(scratch_t(g, "d_counts", 2 * 64, &cnt64));
-  GFX_CK(cudaMemsetAsync(cnt64, 0, 2 * 64 * 8, ctx->stream));
+  // pass 0: per-owner counts; cursors on the device; pass 1: scatter
+  GFX_CK(cudaMemsetAsync(cnt64, 0, 64 * 8, ctx->stream));
   const int grid = ctx->sm_count * 4;
   GFX_LAUNCH((k_dist_bucket<0>), grid, 256, 0, ctx->stream, emit, &C[1].out_len, db->P, db->r,
              cnt64, nullptr, sent_src, sent, db->send, nullptr, nullptr);
-  std::vector<unsigned long long> hc(db->P);
-  GFX_CK(cudaMemcpyAsync(hc.data(), cnt64, db->P * 8, cudaMemcpyDeviceToHost, ctx->stream));
-  GFX_CK(cudaMemcpyAsync(pin, C, 2 * sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
-  GFX_CK(cudaStreamSynchronize(ctx->stream));
-  const int64_t total_slots = (int64_t)pin[1].total;
-  // cursors = exclusive scan over remote owners (own bucket excluded)
-  std::vector<unsigned long long> cur(db->P, 0);
-  unsigned long long acc = 0;
-  for (int o = 0; o < db->P; ++o) {
-    cur[o] = acc;
-    send_counts[o] = (o == db->r) ? 0 : (int64_t)hc[o];
-    if (o != db->r) acc += hc[o];
-  }
-  GFX_REQUIRE((int64_t)acc <= db->send_cap, "send buffer too small (%llu > %lld)",
-              (unsigned long long)acc, (long long)db->send_cap);
-  GFX_CK(cudaMemcpyAsync(cnt64 + 64, cur.data(), db->P * 8, cudaMemcpyHostToDevice, ctx->stream));
-  GFX_CK(cudaMemsetAsync(&C[2].out_len, 0, 8, ctx->stream));
+  GFX_LAUNCH(k_dist_cursors, 1, 32, 0, ctx->stream, db->P, db->r, cnt64, cnt64 + 64,
+             db->send_counts, &C[2].out_len);
   GFX_LAUNCH((k_dist_bucket<1>), grid, 256, 0, ctx->stream, emit, &C[1].out_len, db->P, db->r,
              nullptr, cnt64 + 64, sent_src, sent, db->send, order + db->q_end, &C[2].out_len);
   GFX_CK(cudaGetLastError());
-  GFX_CK(cudaStreamSynchronize(ctx->stream));
-  db->local_new = (int64_t)hc[db->r];
-  *local_new = db->local_new;
-  *edges = total_slots;
+  db->pending_push = true;
   return GFX_OK;
 }
 
-int gfx_dbfs_push_claim(gfx_dbfs* db, int64_t nrecv, int32_t depth, int64_t* nf_local) {
-  GFX_REQUIRE(db && nf_local, "gfx_dbfs_push_claim: null argument");
+int gfx_dbfs_push_claim(gfx_dbfs* db, int64_t nrecv, int32_t depth) {
+  GFX_REQUIRE(db && db->stats, "gfx_dbfs_push_claim: unbound engine");
   GFX_REQUIRE(nrecv >= 0 && nrecv <= db->recv_cap, "received %lld pairs, capacity %lld",
               (long long)nrecv, (long long)db->recv_cap);
   gfx_graph* g = db->lg;
@@ -474,20 +523,12 @@ int gfx_dbfs_push_claim(gfx_dbfs* db, int64_t nrecv, int32_t depth, int64_t* nf_
   uint32_t* visited = static_cast<uint32_t*>(g->scratch["d_visited"].ptr);
   int32_t* order = static_cast<int32_t*>(g->scratch["q_order"].ptr);
   Counters* C = g->counters;
-  auto* pin = static_cast<Counters*>(ctx->pinned);
-  const unsigned long long ln = (unsigned long long)db->local_new;
-  GFX_CK(cudaMemcpyAsync(&C[2].out_len, &ln, 8, cudaMemcpyHostToDevice, ctx->stream));
   if (nrecv > 0)
     GFX_LAUNCH(k_dist_claim, grid_for(nrecv, 256, ctx->sm_count * 8), 256, 0, ctx->stream,
                db->recv, nrecv, db->P, visited, db->labels, db->preds, depth, order + db->q_end,
                &C[2].out_len);
-  GFX_CK(cudaMemcpyAsync(pin, &C[2], sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
-  GFX_CK(cudaStreamSynchronize(ctx->stream));
-  db->nf = (int64_t)pin->out_len;
-  db->q_off = db->q_end;
-  db->q_end += db->nf;
-  db->queue_form = true;
-  *nf_local = db->nf;
+  GFX_LAUNCH(k_dist_stats, 1, 32, 0, ctx->stream, C, 0, db->stats);
+  GFX_CK(cudaGetLastError());
   return GFX_OK;
 }
 
@@ -505,14 +546,13 @@ int gfx_dbfs_pull_prepare(gfx_dbfs* db) {
                  order + db->q_off, db->nf, db->front_local);
     db->queue_form = false;
   }
-  GFX_CK(cudaStreamSynchronize(ctx->stream));
+  GFX_CK(cudaGetLastError());
   return GFX_OK;
 }
 
 // pull, step 2 (after the host all-gathered front_local into gathered)
-int gfx_dbfs_pull(gfx_dbfs* db, int32_t depth, int64_t* nf_local, int64_t* probes,
-                  int64_t* candidates) {
-  GFX_REQUIRE(db && nf_local && probes && candidates, "gfx_dbfs_pull: null argument");
+int gfx_dbfs_pull(gfx_dbfs* db, int32_t depth) {
+  GFX_REQUIRE(db && db->stats, "gfx_dbfs_pull: unbound engine");
   gfx_graph* g = db->lg;
   gfx_ctx* ctx = db->ctx;
   GFX_CK(cudaSetDevice(ctx->device));
@@ -520,26 +560,277 @@ int gfx_dbfs_pull(gfx_dbfs* db, int32_t depth, int64_t* nf_local, int64_t* probe
   int32_t* head = static_cast<int32_t*>(g->scratch["keep_dhead"].ptr);
   void* nzp = nullptr;
   GFX_TRY(scratch(g, "nz_out", db->wl * 4, &nzp));
-  uint32_t* next = nullptr;
-  GFX_TRY(scratch_t(g, "d_next", db->wmax + 1, &next));
   Counters* C = g->counters;
-  auto* pin = static_cast<Counters*>(ctx->pinned);
-  GFX_CK(cudaMemsetAsync(C, 0, sizeof(Counters), ctx->stream));
+  GFX_LAUNCH(k_dist_level_init, 1, 32, 0, ctx->stream, C, 0ull);
+  // the new frontier is written straight into the local bitmap (the pull
+  // reads only the gathered copy); words past wl stay zero
+  GFX_CK(cudaMemsetAsync(db->front_local, 0, db->wmax * 4, ctx->stream));
   GatheredFront front{db->gathered, db->wmax, db->P};
   GFX_LAUNCH(k_dist_pull, ctx->sm_count * 8, 256, 0, ctx->stream, db->wl,
-             static_cast<const uint32_t*>(nzp), visited, front, next, head, g->row, g->col,
-             db->labels, db->preds, depth, C);
-  // the new frontier becomes the local bitmap
-  GFX_CK(cudaMemsetAsync(db->front_local, 0, db->wmax * 4, ctx->stream));
-  GFX_CK(cudaMemcpyAsync(db->front_local, next, db->wl * 4, cudaMemcpyDeviceToDevice,
-                         ctx->stream));
-  GFX_CK(cudaMemcpyAsync(pin, C, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
-  GFX_CK(cudaStreamSynchronize(ctx->stream));
-  db->nf = (int64_t)pin->out_len;
-  db->queue_form = false;
-  *nf_local = db->nf;
-  *probes = (int64_t)pin->aux0;
-  *candidates = (int64_t)pin->aux1;
+             static_cast<const uint32_t*>(nzp), visited, front, db->front_local, head, g->row,
+             g->col, db->labels, db->preds, depth, C);
+  GFX_LAUNCH(k_dist_stats, 1, 32, 0, ctx->stream, C, 1, db->stats);
+  GFX_CK(cudaGetLastError());
+  db->pending_push = false;
+  return GFX_OK;
+}
+
+int gfx_dbfs_commit(gfx_dbfs* db, int64_t nf_local) {
+  GFX_REQUIRE(db, "gfx_dbfs_commit: null engine");
+  GFX_REQUIRE(nf_local >= 0 && nf_local <= db->nl, "frontier %lld out of range",
+              (long long)nf_local);
+  db->nf = nf_local;
+  if (db->pending_push) {
+    GFX_REQUIRE(db->q_end + nf_local <= db->nl + 1, "queue overflow");
+    db->q_off = db->q_end;
+    db->q_end += nf_local;
+    db->queue_form = true;
+  } else {
+    db->queue_form = false;
+  }
+  db->pending_push = false;
+  return GFX_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Native level loop: the same per-level protocol as
+// dist.py:bfs_partitioned, driven from C++ with NCCL called directly on the
+// context stream -- one host synchronisation per pull level (the allreduced
+// level counters), two per push level (pair counts, then counters).  NCCL is
+// the library torch already loaded in this process (resolved with dlopen /
+// dlsym, so libgfx carries no link-time NCCL dependency and cannot pick up a
+// second, different NCCL).
+// ---------------------------------------------------------------------------
+namespace {
+
+struct NcclUid {
+  char internal[128];
+};
+using nres_t = int;
+constexpr int kNcclInt32 = 2, kNcclInt64 = 4, kNcclUint64 = 5, kNcclSum = 0;
+
+struct NcclApi {
+  void* lib = nullptr;
+  nres_t (*GetUniqueId)(NcclUid*) = nullptr;
+  nres_t (*CommInitRank)(void**, int, NcclUid, int) = nullptr;
+  nres_t (*CommDestroy)(void*) = nullptr;
+  nres_t (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  nres_t (*AllGather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+  nres_t (*Send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  nres_t (*Recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  nres_t (*GroupStart)() = nullptr;
+  nres_t (*GroupEnd)() = nullptr;
+  const char* (*ErrorString)(nres_t) = nullptr;
+};
+NcclApi g_nccl;
+
+template <class F>
+bool nccl_sym(F& f, const char* name) {
+  f = reinterpret_cast<F>(dlsym(g_nccl.lib, name));
+  return f != nullptr;
+}
+
+}  // namespace
+
+struct gfx_nccl {
+  void* comm = nullptr;
+  int nranks = 1, rank = 0;
+};
+
+#define GFX_NCCL(call)                                                                        \
+  do {                                                                                         \
+    const nres_t rc_ = (call);                                                                 \
+    GFX_REQUIRE(rc_ == 0, "NCCL error %d (%s) at %s:%d", rc_,                                  \
+                g_nccl.ErrorString ? g_nccl.ErrorString(rc_) : "?", __FILE__, __LINE__);      \
+  } while (0)
+
+extern "C" {
+
+int gfx_nccl_load(const char* path) {
+  if (g_nccl.lib) return GFX_OK;
+  void* h = nullptr;
+  if (path && *path) h = dlopen(path, RTLD_NOW | RTLD_NOLOAD);
+  if (!h && path && *path) h = dlopen(path, RTLD_NOW);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  GFX_REQUIRE(h, "gfx_nccl_load: NCCL is not loaded in this process (%s)",
+              path ? path : "no path given");
+  g_nccl.lib = h;
+  bool ok = nccl_sym(g_nccl.GetUniqueId, "ncclGetUniqueId") &&
+            nccl_sym(g_nccl.CommInitRank, "ncclCommInitRank") &&
+            nccl_sym(g_nccl.CommDestroy, "ncclCommDestroy") &&
+            nccl_sym(g_nccl.AllReduce, "ncclAllReduce") &&
+            nccl_sym(g_nccl.AllGather, "ncclAllGather") && nccl_sym(g_nccl.Send, "ncclSend") &&
+            nccl_sym(g_nccl.Recv, "ncclRecv") && nccl_sym(g_nccl.GroupStart, "ncclGroupStart") &&
+            nccl_sym(g_nccl.GroupEnd, "ncclGroupEnd") &&
+            nccl_sym(g_nccl.ErrorString, "ncclGetErrorString");
+  if (!ok) {
+    g_nccl = NcclApi{};
+    GFX_REQUIRE(false, "gfx_nccl_load: NCCL symbols missing");
+  }
+  return GFX_OK;
+}
+
+int gfx_nccl_unique_id(uint8_t* id_out) {
+  GFX_REQUIRE(id_out, "gfx_nccl_unique_id: null argument");
+  GFX_REQUIRE(g_nccl.lib, "gfx_nccl_unique_id: call gfx_nccl_load first");
+  NcclUid uid;
+  GFX_NCCL(g_nccl.GetUniqueId(&uid));
+  std::memcpy(id_out, uid.internal, sizeof(uid.internal));
+  return GFX_OK;
+}
+
+int gfx_nccl_comm_create(gfx_ctx* ctx, int nranks, int rank, const uint8_t* id, gfx_nccl** out) {
+  GFX_REQUIRE(ctx && id && out, "gfx_nccl_comm_create: null argument");
+  GFX_REQUIRE(g_nccl.lib, "gfx_nccl_comm_create: call gfx_nccl_load first");
+  GFX_REQUIRE(nranks >= 1 && nranks <= 64 && rank >= 0 && rank < nranks, "bad rank %d of %d",
+              rank, nranks);
+  GFX_CK(cudaSetDevice(ctx->device));
+  NcclUid uid;
+  std::memcpy(uid.internal, id, sizeof(uid.internal));
+  auto* c = new gfx_nccl();
+  c->nranks = nranks;
+  c->rank = rank;
+  const nres_t rc = g_nccl.CommInitRank(&c->comm, nranks, uid, rank);
+  if (rc != 0) {
+    delete c;
+    GFX_NCCL(rc);
+  }
+  *out = c;
+  return GFX_OK;
+}
+
+int gfx_nccl_comm_destroy(gfx_nccl* c) {
+  if (!c) return GFX_OK;
+  if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  delete c;
+  return GFX_OK;
+}
+
+int gfx_dbfs_run(gfx_dbfs* db, gfx_nccl* comm, int64_t source, int direction, double do_a,
+                 double do_b, int mu_edge_based, gfx_iter_rec* recs, int64_t rec_cap,
+                 gfx_stats* stats) {
+  GFX_REQUIRE(db && stats && db->stats, "gfx_dbfs_run: unbound engine");
+  GFX_REQUIRE(direction == GFX_DIR_PUSH || direction == GFX_DIR_PULL || direction == GFX_DIR_AUTO,
+              "bad direction %d", direction);
+  GFX_REQUIRE(do_a > 0 && do_b > 0, "do_a and do_b must be positive");
+  const int P = db->P, r = db->r;
+  GFX_REQUIRE(P == 1 || (comm && comm->comm && comm->nranks == P && comm->rank == r),
+              "gfx_dbfs_run: P = %d needs a communicator of P ranks with this rank", P);
+  gfx_ctx* ctx = db->ctx;
+  cudaStream_t st = ctx->stream;
+  void* nc = P > 1 ? comm->comm : nullptr;
+  auto* pin = static_cast<int64_t*>(ctx->pinned);  // 4 KB: 2P counts or 8 stats
+  std::memset(stats, 0, sizeof(*stats));
+  cudaEvent_t e0, e1;
+  GFX_CK(cudaEventCreate(&e0));
+  GFX_CK(cudaEventCreate(&e1));
+  GFX_CK(cudaEventRecord(e0, st));
+  int64_t nf_local = 0;
+  GFX_TRY(gfx_dbfs_reset(db, source, &nf_local));
+  int64_t nf = 1, n_u = db->n, depth = 0, nrec = 0;
+  int mode = GFX_DIR_PUSH;
+  std::vector<int64_t> sc(P), rc(P), soff(P), roff(P);
+  while (nf > 0) {
+    ++depth;
+    n_u -= nf;
+    const DirEstimate est = estimate_mf_mu(db->n, db->m, nf, n_u, mu_edge_based);
+    int dec;
+    if (direction == GFX_DIR_AUTO)
+      dec = decide_direction(mode == GFX_DIR_PULL ? 1 : 0, est, do_a, do_b) ? GFX_DIR_PULL
+                                                                            : GFX_DIR_PUSH;
+    else if (direction == GFX_DIR_PULL)
+      dec = depth > 1 ? GFX_DIR_PULL : GFX_DIR_PUSH;
+    else
+      dec = GFX_DIR_PUSH;
+    int64_t edges = 0, work = 0;
+    if (dec == GFX_DIR_PUSH) {
+      GFX_TRY(gfx_dbfs_push_expand(db, (int32_t)depth));
+      int64_t nrecv = 0;
+      if (P > 1) {
+        GFX_NCCL(g_nccl.GroupStart());
+        for (int o = 0; o < P; ++o) {
+          GFX_NCCL(g_nccl.Send(db->send_counts + o, 1, kNcclInt64, o, nc, st));
+          GFX_NCCL(g_nccl.Recv(db->send_counts + P + o, 1, kNcclInt64, o, nc, st));
+        }
+        GFX_NCCL(g_nccl.GroupEnd());
+        GFX_CK(cudaMemcpyAsync(pin, db->send_counts, 2 * P * 8, cudaMemcpyDeviceToHost, st));
+        GFX_CK(cudaStreamSynchronize(st));
+        int64_t sa = 0, ra = 0;
+        for (int o = 0; o < P; ++o) {
+          sc[o] = pin[o];
+          rc[o] = pin[P + o];
+          soff[o] = sa;
+          roff[o] = ra;
+          sa += sc[o];
+          ra += rc[o];
+        }
+        GFX_REQUIRE(ra <= db->recv_cap, "received %lld pairs, capacity %lld", (long long)ra,
+                    (long long)db->recv_cap);
+        GFX_NCCL(g_nccl.GroupStart());
+        for (int o = 0; o < P; ++o) {
+          if (o == r) continue;
+          if (sc[o]) GFX_NCCL(g_nccl.Send(db->send + soff[o], sc[o], kNcclUint64, o, nc, st));
+          if (rc[o]) GFX_NCCL(g_nccl.Recv(db->recv + roff[o], rc[o], kNcclUint64, o, nc, st));
+        }
+        GFX_NCCL(g_nccl.GroupEnd());
+        nrecv = ra;
+      }
+      GFX_TRY(gfx_dbfs_push_claim(db, nrecv, (int32_t)depth));
+    } else {
+      GFX_TRY(gfx_dbfs_pull_prepare(db));
+      if (P > 1)
+        GFX_NCCL(g_nccl.AllGather(db->front_local, db->gathered, (size_t)db->wmax, kNcclInt32,
+                                  nc, st));
+      else
+        GFX_CK(cudaMemcpyAsync(db->gathered, db->front_local, db->wmax * 4,
+                               cudaMemcpyDeviceToDevice, st));
+      GFX_TRY(gfx_dbfs_pull(db, (int32_t)depth));
+    }
+    if (P > 1)
+      GFX_NCCL(g_nccl.AllReduce(db->stats + 4, db->stats + 4, 4, kNcclInt64, kNcclSum, nc, st));
+    GFX_CK(cudaMemcpyAsync(pin, db->stats, 8 * 8, cudaMemcpyDeviceToHost, st));
+    GFX_CK(cudaStreamSynchronize(st));
+    const int64_t local_out = pin[0], nout = pin[4];
+    if (dec == GFX_DIR_PUSH) {
+      edges = pin[5];
+      work = 20 * nf + 4 * edges;
+      stats->edges_traversed += edges;
+    } else {
+      work = 12 * pin[7] + 4 * pin[6];
+    }
+    GFX_TRY(gfx_dbfs_commit(db, local_out));
+    if (recs && nrec < rec_cap) {
+      gfx_iter_rec& x = recs[nrec++];
+      std::memset(&x, 0, sizeof(x));
+      x.iteration = depth;
+      x.frontier_in = nf;
+      x.frontier_out = nout;
+      x.n_u = n_u;
+      x.edges = edges;
+      x.m_f = est.m_f;
+      x.m_u = est.m_u;
+      x.mode_before = mode;
+      x.decision = dec;
+      x.candidates = dec == GFX_DIR_PULL ? pin[7] : 0;
+      x.work = dec == GFX_DIR_PULL ? pin[6] : edges;
+      x.bytes_alg = work + 8 * nout;
+    }
+    if (dec != mode) stats->direction_switches += 1;
+    stats->bytes_alg += work + 8 * nout;
+    mode = dec;
+    nf = nout;
+  }
+  GFX_CK(cudaEventRecord(e1, st));
+  GFX_CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  GFX_CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  stats->iterations = depth;
+  stats->device_ms = ms;
+  stats->num_records = nrec;
   return GFX_OK;
 }
 

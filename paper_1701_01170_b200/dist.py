@@ -6,12 +6,14 @@ over every rank.  Each rank keeps the rows of its owned vertices with GLOBAL
 column ids plus its own labels / preds / visited bits (csrc/gfx_dist.cu).
 
 Per level, on every rank in lockstep:
-  * the global frontier size comes from an allreduce, and the direction is
+  * the level counters (new frontier, slots, pull probes / candidates) are
+    allreduced on the device and read by the host once, and the direction is
     the reference decision (direction.py:52-70) on those global counts -- the
     trace therefore equals the single-GPU and the reference trace;
   * push levels expand the local frontier, claim owned destinations locally,
     and exchange (dst, src) pairs for remote ones with an all_to_all
-    (de-duplicated per level on the sender); owners claim what they receive;
+    (de-duplicated per level on the sender, pair counts exchanged first with
+    an all_to_all); owners claim what they receive;
   * pull levels all-gather every rank's local frontier bitmap (n/8 bytes in
     total) and pull the rank's unvisited vertices against it.
 
@@ -38,37 +40,46 @@ class VirtualComm:
     def __init__(self, engines):
         self.engines = engines
 
-    def allreduce_sum(self, values):
-        return int(sum(int(v) for v in values))
+    def exchange_counts(self):
+        sc = [[int(k) for k in e.send_counts.tolist()] for e in self.engines]
+        P = len(self.engines)
+        rc = [[sc[i][j] for i in range(P)] for j in range(P)]
+        return sc, rc
 
-    def exchange_pairs(self, counts):
+    def exchange_pairs(self, sc, rc):
         P = len(self.engines)
         offs = []
-        for c in counts:  # per sender: offsets of each destination bucket
+        for c in sc:  # per sender: offsets of each destination bucket
             o, acc = [], 0
             for k in c:
                 o.append(acc)
-                acc += int(k)
+                acc += k
             offs.append(o)
-        recv_counts = []
+        recv = []
         for j, dst in enumerate(self.engines):
-            parts = [self.engines[i].send[offs[i][j]: offs[i][j] + int(counts[i][j])]
-                     for i in range(P) if int(counts[i][j])]
-            total = sum(int(counts[i][j]) for i in range(P))
+            parts = [self.engines[i].send[offs[i][j]: offs[i][j] + sc[i][j]]
+                     for i in range(P) if sc[i][j]]
+            total = sum(rc[j])
             if parts:
                 dst.recv[:total].copy_(_cat(parts))
-            recv_counts.append(total)
-        return recv_counts
+            recv.append(total)
+        return recv
 
     def allgather_frontier(self):
         g = _cat([e.front_local for e in self.engines])
         for e in self.engines:
             e.gathered.copy_(g)
 
+    def allreduce_stats(self):
+        loc = [[int(x) for x in e.stats[:4].tolist()] for e in self.engines]
+        return loc, [sum(col) for col in zip(*loc)]
+
 
 class ProcessComm:
     """One engine per process, collectives over a torch.distributed group
-    (NCCL on GPUs; gloo for the CPU tests)."""
+    (NCCL on GPUs; gloo for the CPU tests).  Collectives are enqueued on the
+    stream the engine's kernels run on; the host reads device values twice
+    per push level (pair counts, level counters) and once per pull level."""
 
     def __init__(self, engine, group=None):
         import torch.distributed as dist
@@ -77,30 +88,29 @@ class ProcessComm:
         self.engines = [engine]
         self.group = group
 
-    def _tensor(self, values):
-        import torch
-
-        return torch.tensor(values, dtype=torch.int64, device=self.engines[0].device)
-
-    def allreduce_sum(self, values):
-        t = self._tensor([int(sum(values))])
-        self.dist.all_reduce(t, group=self.group)
-        return int(t.item())
-
-    def exchange_pairs(self, counts):
+    def exchange_counts(self):
         e = self.engines[0]
-        send_counts = self._tensor([int(k) for k in counts[0]])
-        recv_counts = send_counts.clone()
-        self.dist.all_to_all_single(recv_counts, send_counts, group=self.group)
-        rc = [int(k) for k in recv_counts.tolist()]
-        sc = [int(k) for k in counts[0]]
-        self.dist.all_to_all_single(e.recv[: sum(rc)], e.send[: sum(sc)], output_split_sizes=rc,
-                                    input_split_sizes=sc, group=self.group)
-        return [sum(rc)]
+        P = e.send_counts.numel()
+        self.dist.all_to_all_single(e.recv_counts, e.send_counts, group=self.group)
+        both = [int(k) for k in e.counts.tolist()]
+        return [both[:P]], [both[P:]]
+
+    def exchange_pairs(self, sc, rc):
+        e = self.engines[0]
+        s, r = sc[0], rc[0]
+        self.dist.all_to_all_single(e.recv[: sum(r)], e.send[: sum(s)], output_split_sizes=r,
+                                    input_split_sizes=s, group=self.group)
+        return [sum(r)]
 
     def allgather_frontier(self):
         e = self.engines[0]
         self.dist.all_gather_into_tensor(e.gathered, e.front_local, group=self.group)
+
+    def allreduce_stats(self):
+        e = self.engines[0]
+        self.dist.all_reduce(e.stats[4:], group=self.group)
+        vals = [int(x) for x in e.stats.tolist()]
+        return [vals[:4]], vals[4:]
 
 
 def _cat(parts):
@@ -152,9 +162,13 @@ class DeviceEngine:
         self.recv = torch.empty(cap, dtype=torch.int64, device=dev)
         self.front_local = torch.zeros(self.wmax, dtype=torch.int32, device=dev)
         self.gathered = torch.zeros(P * self.wmax, dtype=torch.int32, device=dev)
+        self.counts = torch.zeros(2 * P, dtype=torch.int64, device=dev)  # send | recv
+        self.send_counts, self.recv_counts = self.counts[:P], self.counts[P:]
+        self.stats = torch.zeros(8, dtype=torch.int64, device=dev)  # local | to reduce
         _native.call("gfx_dbfs_bind", h, _native.ptr(self.labels), _native.ptr(self.preds),
                      _native.ptr(self.send), cap, _native.ptr(self.recv), cap,
-                     _native.ptr(self.front_local), _native.ptr(self.gathered))
+                     _native.ptr(self.front_local), _native.ptr(self.gathered),
+                     _native.ptr(self.send_counts), _native.ptr(self.stats))
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -167,26 +181,20 @@ class DeviceEngine:
         _native.call("gfx_dbfs_reset", self.handle, int(source), ctypes.byref(nf))
         return nf.value
 
-    def push_expand(self, depth: int):
-        counts = (ctypes.c_int64 * self.P)()
-        local_new, edges = ctypes.c_int64(), ctypes.c_int64()
-        _native.call("gfx_dbfs_push_expand", self.handle, depth, counts, ctypes.byref(local_new),
-                     ctypes.byref(edges))
-        return list(counts), local_new.value, edges.value
+    def push_expand(self, depth: int) -> None:
+        _native.call("gfx_dbfs_push_expand", self.handle, depth)
 
-    def push_claim(self, nrecv: int, depth: int) -> int:
-        nf = ctypes.c_int64()
-        _native.call("gfx_dbfs_push_claim", self.handle, int(nrecv), depth, ctypes.byref(nf))
-        return nf.value
+    def push_claim(self, nrecv: int, depth: int) -> None:
+        _native.call("gfx_dbfs_push_claim", self.handle, int(nrecv), depth)
 
     def pull_prepare(self) -> None:
         _native.call("gfx_dbfs_pull_prepare", self.handle)
 
-    def pull(self, depth: int):
-        nf, probes, cands = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
-        _native.call("gfx_dbfs_pull", self.handle, depth, ctypes.byref(nf), ctypes.byref(probes),
-                     ctypes.byref(cands))
-        return nf.value, probes.value, cands.value
+    def pull(self, depth: int) -> None:
+        _native.call("gfx_dbfs_pull", self.handle, depth)
+
+    def commit(self, nf_local: int) -> None:
+        _native.call("gfx_dbfs_commit", self.handle, int(nf_local))
 
     def local_labels(self):
         return self.labels[: self.nl], self.preds[: self.nl]
@@ -211,6 +219,7 @@ class DistBfsStats:
     per_level: list = field(default_factory=list)
     edges_push: int = 0
     bytes_alg: int = 0   # SURVEY 8(d) formulas summed over ranks and levels
+    device_ms: float = 0.0  # native loop: CUDA-event time of the BFS on this rank
 
 
 def bfs_partitioned(comm, n: int, m: int, source: int, direction: str = PUSH,
@@ -224,7 +233,8 @@ def bfs_partitioned(comm, n: int, m: int, source: int, direction: str = PUSH,
         raise ValueError(f"unknown direction {direction!r}")
     engines = comm.engines
     st = DistBfsStats()
-    nf = comm.allreduce_sum([e.reset(source) for e in engines])
+    local = [e.reset(source) for e in engines]
+    nf = 1  # exactly one rank owns the source
     state = DirectionState(n=n, m=m, do_a=do_a, do_b=do_b, mu_edge_based=mu_edge_based)
     depth = 0
     while nf > 0:
@@ -241,27 +251,115 @@ def bfs_partitioned(comm, n: int, m: int, source: int, direction: str = PUSH,
         st.direction_trace.append({"iteration": depth, "mode_before": state.mode, "n_f": nf,
                                    "n_u": state.n_u, "m_f": m_f, "m_u": m_u, "decision": mode})
         if mode == PUSH:
-            outs = [e.push_expand(depth) for e in engines]
-            recv = comm.exchange_pairs([o[0] for o in outs])
-            local = [e.push_claim(rc, depth) for e, rc in zip(engines, recv)]
-            edges = comm.allreduce_sum([o[2] for o in outs])
-            st.edges_push += edges
-            work = 20 * nf + 4 * edges
+            for e in engines:
+                e.push_expand(depth)
+            sc, rc = comm.exchange_counts()
+            recv = comm.exchange_pairs(sc, rc)
+            for e, nr in zip(engines, recv):
+                e.push_claim(nr, depth)
+            loc, glob = comm.allreduce_stats()
+            st.edges_push += glob[1]
+            work = 20 * nf + 4 * glob[1]
         else:
             for e in engines:
                 e.pull_prepare()
             comm.allgather_frontier()
-            res = [e.pull(depth) for e in engines]
-            local = [x[0] for x in res]
-            work = 12 * comm.allreduce_sum([x[2] for x in res]) + \
-                4 * comm.allreduce_sum([x[1] for x in res])
-        nout = comm.allreduce_sum(local)
+            for e in engines:
+                e.pull(depth)
+            loc, glob = comm.allreduce_stats()
+            work = 12 * glob[3] + 4 * glob[2]
+        for e, lv in zip(engines, loc):
+            e.commit(lv[0])
+        nout = glob[0]
         st.bytes_alg += work + 8 * nout
         st.per_level.append({"iteration": depth, "mode": mode, "frontier_in": nf,
                              "frontier_out": nout})
         state.mode = mode
         nf = nout
     st.iterations = depth
+    return st
+
+
+_DIR_CODE = {PUSH: 0, PULL: 1, "auto": 2}
+
+
+def _nccl_library_path() -> str | None:
+    """File of the NCCL library torch loaded into this process."""
+    try:
+        with open("/proc/self/maps") as fh:
+            for line in fh:
+                if "libnccl.so" in line:
+                    return line.split()[-1]
+    except OSError:
+        pass
+    return None
+
+
+class NativeComm:
+    """A NCCL communicator owned by libgfx (gfx_nccl_comm_create), for the
+    native level loop.  Created collectively: rank 0 draws the unique id and
+    the torch.distributed group broadcasts it.  ``None`` handle at P = 1."""
+
+    def __init__(self, engine, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.handle = None
+        P, r = engine.P, engine.r
+        if P == 1:
+            return
+        path = _nccl_library_path()
+        _native.call("gfx_nccl_load", path.encode() if path else None)
+        uid = (ctypes.c_uint8 * 128)()
+        if r == 0:
+            _native.call("gfx_nccl_unique_id", uid)
+        dev = engine.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+        t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
+        dist.broadcast(t, src=0, group=group)
+        uid = (ctypes.c_uint8 * 128)(*t.cpu().tolist())
+        ctx = _native.Context.get(engine.device.index)
+        h = ctypes.c_void_p()
+        _native.call("gfx_nccl_comm_create", ctx.handle, P, r, uid, ctypes.byref(h))
+        self.handle = h
+
+    def close(self):
+        if self.handle is not None and _native._lib is not None:
+            _native._lib.gfx_nccl_comm_destroy(self.handle)
+        self.handle = None
+
+    def __del__(self):
+        self.close()
+
+
+def bfs_partitioned_native(engine, ncomm, n: int, m: int, source: int, direction: str = PUSH,
+                           do_a: float = 0.001, do_b: float = 0.2,
+                           mu_edge_based: bool = False) -> DistBfsStats:
+    """``bfs_partitioned`` with the level loop in libgfx (gfx_dbfs_run):
+    the same protocol, decisions and trace, without a Python round trip per
+    collective.  ``engine`` is this rank's DeviceEngine."""
+    if not 0 <= source < n:
+        raise ValueError(f"source {source} out of range")
+    if direction not in _DIR_CODE:
+        raise ValueError(f"unknown direction {direction!r}")
+    cap = 4096
+    recs = (_native.IterRec * cap)()
+    stats = _native.Stats()
+    _native.call("gfx_dbfs_run", engine.handle, ncomm.handle if ncomm else None, int(source),
+                 _DIR_CODE[direction], float(do_a), float(do_b), int(bool(mu_edge_based)), recs,
+                 cap, ctypes.byref(stats))
+    st = DistBfsStats()
+    mode = {0: PUSH, 1: PULL}
+    for i in range(stats.num_records):
+        x = recs[i]
+        st.direction_trace.append({"iteration": x.iteration, "mode_before": mode[x.mode_before],
+                                   "n_f": x.frontier_in, "n_u": x.n_u, "m_f": x.m_f,
+                                   "m_u": x.m_u, "decision": mode[x.decision]})
+        st.per_level.append({"iteration": x.iteration, "mode": mode[x.decision],
+                             "frontier_in": x.frontier_in, "frontier_out": x.frontier_out})
+    st.iterations = stats.iterations
+    st.edges_push = stats.edges_traversed
+    st.bytes_alg = stats.bytes_alg
+    st.device_ms = stats.device_ms
     return st
 
 

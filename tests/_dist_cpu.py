@@ -27,6 +27,9 @@ class CpuEngine:
         self.recv = torch.zeros(n + 64, dtype=torch.int64)
         self.front_local = torch.zeros(self.wmax, dtype=torch.int32)
         self.gathered = torch.zeros(P * self.wmax, dtype=torch.int32)
+        self.counts = torch.zeros(2 * P, dtype=torch.int64)
+        self.send_counts, self.recv_counts = self.counts[:P], self.counts[P:]
+        self.stats = torch.zeros(8, dtype=torch.int64)
 
     def reset(self, source):
         self.labels = np.full(self.nl, UNV, dtype=np.int64)
@@ -68,14 +71,15 @@ class CpuEngine:
             pairs.append((rd[sel] << 32) | rs[sel])
         flat = np.concatenate(pairs) if pairs else np.zeros(0, dtype=np.int64)
         self.send[: len(flat)] = torch.from_numpy(flat)
-        return counts, len(self.local_new), int(deg.sum())
+        self.send_counts[:] = torch.tensor(counts, dtype=torch.int64)
+        self.stats[:] = torch.tensor([0, int(deg.sum()), 0, 0] * 2)
 
     def push_claim(self, nrecv, depth):
         x = self.recv[:nrecv].numpy()
         d, s = x >> 32, x & 0xFFFFFFFF
         got = self._claim(d // self.P, s, depth)
         self.frontier = np.concatenate([self.local_new, got])
-        return len(self.frontier)
+        self.stats[0] = self.stats[4] = len(self.frontier)
 
     def pull_prepare(self):
         bits = np.zeros(self.wmax * 32, dtype=bool)
@@ -104,7 +108,10 @@ class CpuEngine:
         self.labels[found] = depth
         self.preds[found] = np.array(par, dtype=np.int64)
         self.frontier = found
-        return len(found), probes, cands
+        self.stats[:] = torch.tensor([len(found), 0, probes, cands] * 2)
+
+    def commit(self, nf_local):
+        assert nf_local == len(self.frontier)
 
 
 def _pack(bits):

@@ -66,3 +66,49 @@ def test_rmat_partitioned(scale, P):
     lab, _ = gather_labels(engines, dg.num_vertices)
     assert sha(labels_to_host(lab)) == rec["bfs_sha"]
     assert st.edges_push == rec["bfs_edges_traversed"]
+
+
+def test_kat_native_loop_single_rank(kat):
+    """The native level loop (gfx_dbfs_run) at P = 1: labels and trace equal
+    the reference's, for every direction."""
+    from paper_1701_01170_b200._results import labels_to_host
+    from paper_1701_01170_b200.dist import bfs_partitioned_native, gather_labels
+
+    for d in kat:
+        if not d["undirected"]:
+            continue
+        dg = host_graph(d).device()
+        (eng,) = _engines(dg, 1)
+        for direction in ("auto", "push", "pull"):
+            st = bfs_partitioned_native(eng, None, d["n"], d["m"], d["source"],
+                                        direction=direction)
+            lab, _ = gather_labels([eng], d["n"])
+            assert np.array_equal(labels_to_host(lab), d["bfs"]), (d["name"], direction)
+            if direction == "auto":
+                assert _rows(st.direction_trace) == [list(x) for x in d["bfs_auto_trace"]]
+
+
+@pytest.mark.parametrize("scale", [16, 20, 22])
+def test_rmat_native_loop_single_rank(scale):
+    from _checks import valid_bfs_preds
+    from paper_1701_01170_b200._results import labels_to_host, preds_to_host
+    from paper_1701_01170_b200.dist import bfs_partitioned_native, gather_labels
+    from paper_1701_01170_b200.generators import rmat_device_graph
+
+    rec, _ = rmat_golden(scale)
+    dg = rmat_device_graph(scale, 16, 0)
+    (eng,) = _engines(dg, 1)
+    for _ in range(2):  # engine reuse across BFS runs
+        st = bfs_partitioned_native(eng, None, dg.num_vertices, dg.num_edges, 0, direction="auto")
+        lab, prd = gather_labels([eng], dg.num_vertices)
+        labels = labels_to_host(lab)
+        assert sha(labels) == rec["bfs_sha"]
+        assert _rows(st.direction_trace) == [list(x) for x in rec["bfs_auto_trace"]]
+    if scale <= 16:
+        row = dg.row.cpu().numpy()
+        col = dg.col.cpu().numpy().astype(np.int64)
+        assert valid_bfs_preds(row, col, labels, preds_to_host(prd), 0)
+    st = bfs_partitioned_native(eng, None, dg.num_vertices, dg.num_edges, 0, direction="push")
+    lab, _ = gather_labels([eng], dg.num_vertices)
+    assert sha(labels_to_host(lab)) == rec["bfs_sha"]
+    assert st.edges_push == rec["bfs_edges_traversed"]
