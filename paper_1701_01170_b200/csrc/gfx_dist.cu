@@ -89,15 +89,18 @@ struct DistClaimOp {
   int32_t* preds;
   int32_t depth;
   int P, r;
+  int sh;  // log2(P) when P is a power of two, else -1
   uint32_t wv[kBatch];
+  __device__ __forceinline__ int owner(int32_t d) const { return sh >= 0 ? (d & (P - 1)) : d % P; }
+  __device__ __forceinline__ int32_t local(int32_t d) const { return sh >= 0 ? (d >> sh) : d / P; }
   __device__ int32_t src_value(int32_t) const { return 0; }
   __device__ void prefetch(const int32_t* d) {
 #pragma unroll
     for (int u = 0; u < kBatch; ++u) {
       if (d[u] < 0) {
         wv[u] = 0xffffffffu;
-      } else if (d[u] % P == r) {
-        const int32_t l = d[u] / P;
+      } else if (owner(d[u]) == r) {
+        const int32_t l = local(d[u]);
         wv[u] = visited[l >> 5];
       } else {
         wv[u] = sent[d[u] >> 5];
@@ -106,8 +109,8 @@ struct DistClaimOp {
   }
   __device__ bool visit(int u, int32_t d, int32_t s, int32_t, int32_t, int64_t) {
     const int32_t sg = s * P + r;  // frontier items are local ids
-    if (d % P == r) {
-      const int32_t l = d / P;
+    if (owner(d) == r) {
+      const int32_t l = local(d);
       const uint32_t bit = 1u << (l & 31);
       if (wv[u] & bit) return false;
       if (atomicOr(&visited[l >> 5], bit) & bit) return false;
@@ -206,17 +209,27 @@ __global__ void __launch_bounds__(256)
 }
 
 // frontier membership against the all-gathered per-rank local bitmaps
+// (P a power of two -- 1, 2, 4, 8 GPUs -- replaces the divisions by shifts)
 struct GatheredFront {
   const uint32_t* g;
   int64_t wmax;
   int P;
+  int sh;  // log2(P) when P is a power of two, else -1
   __device__ __forceinline__ uint32_t word(int32_t s) const {
+    if (sh >= 0) return g[(int64_t)(s & (P - 1)) * wmax + ((s >> sh) >> 5)];
     return g[(int64_t)(s % P) * wmax + ((s / P) >> 5)];
   }
   __device__ __forceinline__ bool bit(uint32_t w, int32_t s) const {
-    return (w >> ((s / P) & 31)) & 1u;
+    return (w >> (((sh >= 0) ? (s >> sh) : (s / P)) & 31)) & 1u;
   }
 };
+
+static int pow2_shift(int P) {
+  if (P <= 0 || (P & (P - 1))) return -1;
+  int sh = 0;
+  while ((1 << sh) < P) ++sh;
+  return sh;
+}
 
 __global__ void __launch_bounds__(256)
     k_dist_pull(int64_t words, const uint32_t* __restrict__ nz, uint32_t* __restrict__ visited,
@@ -496,7 +509,8 @@ int gfx_dbfs_push_expand(gfx_dbfs* db, int32_t depth) {
     db->q_end += db->nf;
     db->queue_form = true;
   }
-  DistClaimOp op{visited, sent, sent_src, db->labels, db->preds, depth, db->P, db->r, {}};
+  DistClaimOp op{visited, sent, sent_src, db->labels, db->preds, depth, db->P, db->r,
+                 pow2_shift(db->P), {}};
   GFX_TRY(lb_advance(g, order + db->q_off, &C[0].out_len, db->nf, &C[1], scan, rowbase, part, op,
                      emit, &C[1].out_len));
   // pass 0: per-owner counts; cursors on the device; pass 1: scatter
@@ -565,7 +579,7 @@ int gfx_dbfs_pull(gfx_dbfs* db, int32_t depth) {
   // the new frontier is written straight into the local bitmap (the pull
   // reads only the gathered copy); words past wl stay zero
   GFX_CK(cudaMemsetAsync(db->front_local, 0, db->wmax * 4, ctx->stream));
-  GatheredFront front{db->gathered, db->wmax, db->P};
+  GatheredFront front{db->gathered, db->wmax, db->P, pow2_shift(db->P)};
   GFX_LAUNCH(k_dist_pull, ctx->sm_count * 8, 256, 0, ctx->stream, db->wl,
              static_cast<const uint32_t*>(nzp), visited, front, db->front_local, head, g->row,
              g->col, db->labels, db->preds, depth, C);
