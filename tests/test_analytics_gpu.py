@@ -130,6 +130,8 @@ def test_rmat_golden_large(scale):
         total, counts, osrc, odst, _ = tc_device(dg)
         assert total == rec["tc_total"]
         assert sha(counts.to(torch.int64).cpu().numpy()) == rec["tc_counts_sha"]
+        assert sha(osrc.to(torch.int64).cpu().numpy()) == rec["tc_src_sha"]
+        assert sha(odst.to(torch.int64).cpu().numpy()) == rec["tc_dst_sha"]
 
 
 @pytest.mark.skipif(not __import__("os").environ.get("GFX_SLOW_TESTS"),
