@@ -7,6 +7,13 @@ little-endian int64 ``row_offsets[n+1]``, ``column_indices[m]`` and, when
 weighted, ``edge_weights[m]``.  ``save_csr_cache`` writes byte-identical
 files to the reference's; ``load_csr_cache`` returns the same ``CsrGraph``.
 
+Compact variant ("an int32-col variant for GPU
+upload"): version 2 of the same header, row offsets still int64 but column
+ids and weights int32 -- the device layout, so a load is a straight copy of
+half the bytes.  The reference rejects version-2 files ("unsupported cache
+version"), which is the intended behaviour for a format it cannot read;
+``save_csr_cache(..., compact=False)`` (the default) stays byte-identical.
+
 The device variants move the arrays between the file and HBM without a
 host-side int64 -> int32 pass: the file's int64 column ids (and weights) are
 streamed to the GPU in chunks through pinned staging buffers and narrowed
@@ -29,6 +36,7 @@ from .graph import ID_DTYPE, WEIGHT_DTYPE, CsrGraph, DeviceGraph, GraphFormatErr
 
 CACHE_MAGIC = b"GFXCSR\x00"
 CACHE_VERSION = 1
+COMPACT_VERSION = 2  # int32 column ids / weights
 _HDR = "<BQQB"
 _HDR_BYTES = struct.calcsize(_HDR)
 _DATA_OFF = len(CACHE_MAGIC) + _HDR_BYTES
@@ -39,13 +47,13 @@ def _flags(weighted: bool, undirected: bool) -> int:
     return (1 if weighted else 0) | (2 if undirected else 0)
 
 
-def _header(n: int, m: int, flags: int) -> bytes:
-    return CACHE_MAGIC + struct.pack(_HDR, CACHE_VERSION, n, m, flags)
+def _header(n: int, m: int, flags: int, version: int = CACHE_VERSION) -> bytes:
+    return CACHE_MAGIC + struct.pack(_HDR, version, n, m, flags)
 
 
-def read_header(path: str | Path) -> tuple[int, int, int]:
-    """(n, m, flags) of a cache file; GraphFormatError on a bad magic/version
-    (reference io.py:140-146)."""
+def read_header_version(path: str | Path) -> tuple[int, int, int, int]:
+    """(version, n, m, flags) of a cache file; GraphFormatError on a bad
+    magic/version (reference io.py:140-146)."""
     with open(path, "rb") as fh:
         head = fh.read(_DATA_OFF)
     if not head.startswith(CACHE_MAGIC):
@@ -53,41 +61,75 @@ def read_header(path: str | Path) -> tuple[int, int, int]:
     if len(head) < _DATA_OFF:
         raise GraphFormatError("truncated CSR cache header")
     version, n, m, flags = struct.unpack_from(_HDR, head, len(CACHE_MAGIC))
-    if version != CACHE_VERSION:
+    if version not in (CACHE_VERSION, COMPACT_VERSION):
         raise GraphFormatError(f"unsupported cache version {version}")
-    return int(n), int(m), int(flags)
+    return int(version), int(n), int(m), int(flags)
 
 
-def _check_size(path: Path, n: int, m: int, flags: int) -> None:
-    want = _DATA_OFF + 8 * (n + 1 + m + (m if flags & 1 else 0))
+def read_header(path: str | Path) -> tuple[int, int, int]:
+    """(n, m, flags) of a cache file (either version)."""
+    return read_header_version(path)[1:]
+
+
+def _layout(version: int, n: int, m: int, flags: int):
+    """[(name, dtype, offset, count)] of the arrays after the header."""
+    el = "<i8" if version == CACHE_VERSION else "<i4"
+    parts = [("row", "<i8", _DATA_OFF, n + 1)]
+    off = _DATA_OFF + 8 * (n + 1)
+    parts.append(("col", el, off, m))
+    if flags & 1:
+        parts.append(("w", el, off + np.dtype(el).itemsize * m, m))
+    return parts
+
+
+def _check_size(path: Path, version: int, n: int, m: int, flags: int) -> None:
+    name, dt, off, count = _layout(version, n, m, flags)[-1]
+    want = off + np.dtype(dt).itemsize * count
     have = path.stat().st_size
     if have < want:
         raise GraphFormatError(f"truncated CSR cache: {have} bytes, header needs {want}")
 
 
+def _arrays(path: Path, version: int, n: int, m: int, flags: int) -> dict:
+    return {name: np.memmap(path, dtype=dt, mode="r", offset=off, shape=(count,))
+            if count else np.zeros(0, dtype=dt)
+            for name, dt, off, count in _layout(version, n, m, flags)}
+
+
 # ---------------------------------------------------------------------------
 # host arrays (reference io.py:121-159)
 # ---------------------------------------------------------------------------
-def save_csr_cache(g: CsrGraph, path: str | Path) -> None:
-    """Write the binary CSR cache (byte-identical to reference save_csr_cache)."""
+def _int32_or_raise(a: np.ndarray, what: str) -> np.ndarray:
+    if len(a) and (int(a.min()) < -2**31 or int(a.max()) >= 2**31):
+        raise ValueError(f"compact cache: {what} do not fit int32")
+    return np.ascontiguousarray(a, dtype="<i4")
+
+
+def save_csr_cache(g: CsrGraph, path: str | Path, compact: bool = False) -> None:
+    """Write the binary CSR cache: byte-identical to reference save_csr_cache,
+    or (``compact=True``) the version-2 file with int32 columns / weights."""
+    el = (lambda a, what: _int32_or_raise(np.asarray(a), what)) if compact else \
+        (lambda a, what: np.ascontiguousarray(a, dtype="<i8"))
     with open(path, "wb") as fh:
         fh.write(_header(g.num_vertices, g.num_edges,
-                         _flags(g.edge_weights is not None, g.undirected)))
+                         _flags(g.edge_weights is not None, g.undirected),
+                         COMPACT_VERSION if compact else CACHE_VERSION))
         fh.write(np.ascontiguousarray(g.row_offsets, dtype="<i8").tobytes())
-        fh.write(np.ascontiguousarray(g.column_indices, dtype="<i8").tobytes())
+        fh.write(el(g.column_indices, "column ids").tobytes())
         if g.edge_weights is not None:
-            fh.write(np.ascontiguousarray(g.edge_weights, dtype="<i8").tobytes())
+            fh.write(el(g.edge_weights, "weights").tobytes())
 
 
 def load_csr_cache(path: str | Path) -> CsrGraph:
-    """Read a cache file into a host ``CsrGraph`` (reference load_csr_cache)."""
+    """Read a cache file (either version) into a host ``CsrGraph`` in the
+    reference layout (reference load_csr_cache)."""
     path = Path(path)
-    n, m, flags = read_header(path)
-    _check_size(path, n, m, flags)
-    mm = np.memmap(path, dtype="<i8", mode="r", offset=_DATA_OFF)
-    row = np.array(mm[:n + 1], dtype=ID_DTYPE)
-    col = np.array(mm[n + 1:n + 1 + m], dtype=ID_DTYPE)
-    w = np.array(mm[n + 1 + m:n + 1 + 2 * m], dtype=WEIGHT_DTYPE) if flags & 1 else None
+    version, n, m, flags = read_header_version(path)
+    _check_size(path, version, n, m, flags)
+    a = _arrays(path, version, n, m, flags)
+    row = np.array(a["row"], dtype=ID_DTYPE)
+    col = np.array(a["col"], dtype=ID_DTYPE)
+    w = np.array(a["w"], dtype=WEIGHT_DTYPE) if flags & 1 else None
     return CsrGraph(num_vertices=n, row_offsets=row, column_indices=col, edge_weights=w,
                     undirected=bool(flags & 2))
 
@@ -107,15 +149,17 @@ def load_graph(path: str | Path, make_undirected: bool = False) -> CsrGraph:
 # HBM <-> file
 # ---------------------------------------------------------------------------
 def _stream_to_device(mm: np.ndarray, out, narrow: bool) -> None:
-    """Copy int64 file data into the device tensor `out` (int32 when
-    `narrow`) chunk by chunk: memmap -> pinned staging -> H2D -> narrow."""
+    """Copy file data into the device tensor `out` chunk by chunk: memmap ->
+    pinned staging -> H2D (-> int64 to int32 narrowing on the GPU when
+    `narrow`)."""
     import torch
 
     total = len(mm)
     if total == 0:
         return
     step = min(_CHUNK, total)
-    stage = [torch.empty(step, dtype=torch.int64, pin_memory=True) for _ in range(2)]
+    sdt = torch.int64 if (narrow or out.dtype == torch.int64) else out.dtype
+    stage = [torch.empty(step, dtype=sdt, pin_memory=True) for _ in range(2)]
     dev_tmp = torch.empty(step, dtype=torch.int64, device=out.device) if narrow else None
     done = [None, None]
     for k, a in enumerate(range(0, total, step)):
@@ -143,21 +187,22 @@ def load_csr_cache_device(path: str | Path, device: int | None = None) -> Device
     from . import _native
 
     path = Path(path)
-    n, m, flags = read_header(path)
-    _check_size(path, n, m, flags)
+    version, n, m, flags = read_header_version(path)
+    _check_size(path, version, n, m, flags)
     if n >= 2**31 - 1:
         raise ValueError("graphs with >= 2^31-1 vertices are not supported (int32 ids)")
     ctx = _native.Context.get(device)
     dev = torch.device("cuda", ctx.device)
-    mm = np.memmap(path, dtype="<i8", mode="r", offset=_DATA_OFF)
+    a = _arrays(path, version, n, m, flags)
+    narrow = version == CACHE_VERSION  # the compact file is already int32
     row = torch.empty(n + 1, dtype=torch.int64, device=dev)
     col = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
-    _stream_to_device(mm[:n + 1], row, narrow=False)
-    _stream_to_device(mm[n + 1:n + 1 + m], col, narrow=True)
+    _stream_to_device(a["row"], row, narrow=False)
+    _stream_to_device(a["col"], col, narrow=narrow)
     w = None
     if flags & 1:
         w = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
-        _stream_to_device(mm[n + 1 + m:n + 1 + 2 * m], w, narrow=True)
+        _stream_to_device(a["w"], w, narrow=narrow)
     if not flags & 2:
         raise ValueError("load_csr_cache_device: directed caches need the reverse adjacency; "
                          "load with load_csr_cache and upload via CsrGraph.device()")
@@ -166,17 +211,22 @@ def load_csr_cache_device(path: str | Path, device: int | None = None) -> Device
     return DeviceGraph(ctx, n, m, row, col, w, True)
 
 
-def save_csr_cache_device(dg: DeviceGraph, path: str | Path) -> None:
-    """Write a device graph (e.g. from the GPU R-MAT builder) as a cache file:
-    widened to int64 on the GPU, read back chunk by chunk, appended."""
+def save_csr_cache_device(dg: DeviceGraph, path: str | Path, compact: bool = False) -> None:
+    """Write a device graph (e.g. from the GPU R-MAT builder) as a cache file,
+    read back chunk by chunk: columns / weights widened to int64 on the GPU
+    (reference format) or written as they are (``compact=True``)."""
     import torch
 
     n, m = dg.num_vertices, dg.num_edges
     with open(path, "wb") as fh:
-        fh.write(_header(n, m, _flags(dg.w is not None, dg.undirected)))
-        parts = [(dg.row, n + 1), (dg.col, m)] + ([(dg.w, m)] if dg.w is not None else [])
-        for t, count in parts:
+        fh.write(_header(n, m, _flags(dg.w is not None, dg.undirected),
+                         COMPACT_VERSION if compact else CACHE_VERSION))
+        parts = [(dg.row, n + 1, torch.int64, "<i8")]
+        el = (torch.int32, "<i4") if compact else (torch.int64, "<i8")
+        parts.append((dg.col, m) + el)
+        if dg.w is not None:
+            parts.append((dg.w, m) + el)
+        for t, count, tdt, ndt in parts:
             for a in range(0, count, _CHUNK):
                 b = min(a + _CHUNK, count)
-                fh.write(t[a:b].to(torch.int64).cpu().numpy().astype("<i8", copy=False)
-                         .tobytes())
+                fh.write(t[a:b].to(tdt).cpu().numpy().astype(ndt, copy=False).tobytes())

@@ -51,11 +51,55 @@ def test_bad_files(tmp_path):
 
     blob = W_FILE.read_bytes()
     (tmp_path / "magic").write_bytes(b"NOTCSR\x00" + blob[7:])
-    (tmp_path / "version").write_bytes(blob[:7] + b"\x02" + blob[8:])
+    (tmp_path / "version").write_bytes(blob[:7] + b"\x03" + blob[8:])
     (tmp_path / "short").write_bytes(blob[:-8])
     for name in ("magic", "version", "short"):
         with pytest.raises(GraphFormatError):
             load_csr_cache(tmp_path / name)
+
+
+def test_compact_variant(tmp_path):
+    """Version-2 file (int32 columns / weights): half the
+    column bytes, loads to the same reference-layout CsrGraph."""
+    import paper_1701_01170_b200 as gfx
+    from paper_1701_01170_b200.io import load_csr_cache, read_header_version, save_csr_cache
+
+    a = _arrays()
+    g = gfx.CsrGraph(int(a["w_n"][0]), a["w_row"], a["w_col"], a["w_w"], undirected=True)
+    p = tmp_path / "w2.gfxcsr"
+    save_csr_cache(g, p, compact=True)
+    n, m = g.num_vertices, g.num_edges
+    assert read_header_version(p) == (2, n, m, 3)
+    assert p.stat().st_size == 7 + 18 + 8 * (n + 1) + 4 * m + 4 * m
+    h = load_csr_cache(p)
+    assert h.undirected and h.column_indices.dtype == np.int64
+    assert np.array_equal(h.row_offsets, g.row_offsets)
+    assert np.array_equal(h.column_indices, g.column_indices)
+    assert np.array_equal(h.edge_weights, g.edge_weights)
+    big = gfx.CsrGraph(2, np.array([0, 1, 2]), np.array([1, 0]), np.array([2**31, 2**31]),
+                       undirected=True)
+    with pytest.raises(ValueError):
+        save_csr_cache(big, tmp_path / "big.gfxcsr", compact=True)
+
+
+@pytest.mark.gpu
+def test_device_compact_variant(tmp_path):
+    """Compact file -> HBM is a straight int32 copy equal to the reference
+    file's load; HBM -> compact file equals the host writer's bytes."""
+    import paper_1701_01170_b200 as gfx
+    from paper_1701_01170_b200.io import load_csr_cache, load_csr_cache_device, save_csr_cache, \
+        save_csr_cache_device
+
+    host = load_csr_cache(W_FILE)
+    p = tmp_path / "w2.gfxcsr"
+    save_csr_cache(host, p, compact=True)
+    dg = load_csr_cache_device(p)
+    ref = load_csr_cache_device(W_FILE)
+    for x, y in ((dg.row, ref.row), (dg.col, ref.col), (dg.w, ref.w)):
+        assert x.dtype == y.dtype and bool((x == y).all())
+    save_csr_cache_device(dg, tmp_path / "back.gfxcsr", compact=True)
+    assert (tmp_path / "back.gfxcsr").read_bytes() == p.read_bytes()
+    assert gfx.bfs(load_csr_cache(p), 0).labels.tolist() == gfx.bfs(host, 0).labels.tolist()
 
 
 @pytest.mark.gpu
