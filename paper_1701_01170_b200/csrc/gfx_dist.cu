@@ -236,11 +236,11 @@ __global__ void __launch_bounds__(256)
                 GatheredFront front, uint32_t* __restrict__ next, const int32_t* __restrict__ head,
                 const int64_t* __restrict__ lrow, const int32_t* __restrict__ lcol,
                 int32_t* __restrict__ labels, int32_t* __restrict__ preds, int32_t depth,
-                Counters* __restrict__ ctr) {
+                Counters* __restrict__ ctr, const int32_t* __restrict__ head2) {
   __shared__ PullSmem ps[8];
-  pull_groups(words, nz, visited, front, next, head, lrow, lcol, 0, LabelOut{labels, nullptr}, preds, depth, ctr,
-              (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5,
-              ((int64_t)gridDim.x * blockDim.x) >> 5, ps[threadIdx.x >> 5]);
+  pull_groups(words, nz, visited, front, next, head, lrow, lcol, 0, LabelOut{labels, nullptr},
+              preds, depth, ctr, (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5,
+              ((int64_t)gridDim.x * blockDim.x) >> 5, ps[threadIdx.x >> 5], head2);
 }
 
 __global__ void k_dist_seed(int64_t l, int32_t* labels, uint32_t* visited, int32_t* order) {
@@ -249,12 +249,15 @@ __global__ void k_dist_seed(int64_t l, int32_t* labels, uint32_t* visited, int32
   order[0] = (int32_t)l;
 }
 
-__global__ void k_first_neighbour(const int64_t* __restrict__ row, const int32_t* __restrict__ col,
-                                  int64_t n, int32_t* __restrict__ head) {
+// first two neighbours of every owned row, bit 31 flagging "degree is
+// exactly 1 / 2" (the single-GPU pull's head / head2 arrays)
+__global__ void k_dist_heads(const int64_t* __restrict__ row, const int32_t* __restrict__ col,
+                             int64_t n, int32_t* __restrict__ head, int32_t* __restrict__ head2) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = row[v];
-    head[v] = row[v + 1] > b ? col[b] : -1;
+    const int64_t b = row[v], d = row[v + 1] - b;
+    head[v] = d > 0 ? (int32_t)((uint32_t)col[b] | (d == 1 ? 0x80000000u : 0u)) : -1;
+    head2[v] = d > 1 ? (int32_t)((uint32_t)col[b + 1] | (d == 2 ? 0x80000000u : 0u)) : -1;
   }
 }
 
@@ -457,11 +460,11 @@ int gfx_dbfs_reset(gfx_dbfs* db, int64_t source, int64_t* nf_local) {
   {
     bool fresh = false;
     void* p = nullptr;
-    GFX_TRY(scratch(g, "keep_dhead", (size_t)(db->nl + 1) * 4, &p, &fresh));
+    GFX_TRY(scratch(g, "keep_dhead", (size_t)(db->nl + 1) * 8, &p, &fresh));
     head = static_cast<int32_t*>(p);
     if (fresh && db->nl > 0)
-      GFX_LAUNCH(k_first_neighbour, grid_for(db->nl, 256, ctx->sm_count * 8), 256, 0, ctx->stream,
-                 g->row, g->col, db->nl, head);
+      GFX_LAUNCH(k_dist_heads, grid_for(db->nl, 256, ctx->sm_count * 8), 256, 0, ctx->stream,
+                 g->row, g->col, db->nl, head, head + db->nl + 1);
   }
   GFX_TRY(fill_i32(ctx, db->labels, GFX_UNVISITED, db->nl));
   GFX_CK(cudaMemsetAsync(db->preds, 0xFF, db->nl * 4, ctx->stream));
@@ -582,7 +585,7 @@ int gfx_dbfs_pull(gfx_dbfs* db, int32_t depth) {
   GatheredFront front{db->gathered, db->wmax, db->P, pow2_shift(db->P)};
   GFX_LAUNCH(k_dist_pull, ctx->sm_count * 8, 256, 0, ctx->stream, db->wl,
              static_cast<const uint32_t*>(nzp), visited, front, db->front_local, head, g->row,
-             g->col, db->labels, db->preds, depth, C);
+             g->col, db->labels, db->preds, depth, C, head + db->nl + 1);
   GFX_LAUNCH(k_dist_stats, 1, 32, 0, ctx->stream, C, 1, db->stats);
   GFX_CK(cudaGetLastError());
   db->pending_push = false;
