@@ -7,13 +7,29 @@
 //
 // Device: orientation keeps each row's surviving slots in order, so the
 // compacted rows ARE the canonical oriented CSR (sorted by (src, dst)).
-// Intersections: one thread merges both lists when they are short; longer
-// pairs go to a list handled warp-cooperatively (each lane binary-searches
-// elements of the shorter list in the longer one).  Counts are exact int32.
+// Counting (default): every triangle {x, y, z} with rank x < y < z (rank =
+// the reference's orientation order: degree, then smaller id higher) is
+// found ONCE from the rank-increasing side -- for the edge x => y of the
+// REVERSED orientation, z is a common element of the two (short) reversed
+// rows x and y -- and credited to the reference's oriented edge z -> y, the
+// only one of its three edges whose endpoints' out-lists both hold the third
+// vertex (tc.py:57-59: x is a common out-neighbour of z and y).  The
+// reversed CSR and the map from its slots to the reference's oriented slots
+// are built once with the orientation (preprocessing, like the reference's
+// oriented-adjacency build).  Reversed rows are bounded by O(sqrt(m)), so
+// the work is the optimal sum over vertices of d+(v)^2 instead of the
+// reference orientation's hub-sized out-lists.  Counts stay exact int32, in
+// the reference's oriented CSR order.  GFX_TC_LEGACY=1 selects the direct
+// intersection of the reference orientation (below) for comparison:
+// one thread merges both lists when they are short; longer pairs go to a
+// list handled warp-cooperatively (each lane binary-searches elements of the
+// shorter list in the longer one), hub rows through per-CTA bitmaps.
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "gfx_device.cuh"
@@ -268,6 +284,140 @@ int intersect_pairs(gfx_graph* g, const int32_t* us, const int32_t* vs, int64_t 
   return GFX_OK;
 }
 
+// reversed-orientation build: (dst << 32 | src) keys of the oriented slots
+__global__ void k_tc_rev_keys(const int32_t* __restrict__ osrc, const int32_t* __restrict__ ocol,
+                              int64_t mo, unsigned long long* __restrict__ keys,
+                              int32_t* __restrict__ slot, int64_t* __restrict__ rcnt) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < mo;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t d = ocol[j];
+    keys[j] = ((unsigned long long)(uint32_t)d << 32) | (uint32_t)osrc[j];
+    slot[j] = (int32_t)j;
+    atomicAdd(reinterpret_cast<unsigned long long*>(&rcnt[d]), 1ull);
+  }
+}
+
+__global__ void k_tc_rev_split(const unsigned long long* __restrict__ keys, int64_t mo,
+                               int32_t* __restrict__ rsrc, int32_t* __restrict__ rcol) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < mo;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = keys[j];
+    rsrc[j] = (int32_t)(k >> 32);
+    rcol[j] = (int32_t)(uint32_t)k;
+  }
+}
+
+__device__ __forceinline__ int64_t lower_bound_i32(const int32_t* __restrict__ a, int64_t lo,
+                                                   int64_t hi, int32_t v) {
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// one thread per reversed edge x => y: common elements z of rows x and y;
+// each credits the reference slot of z -> y (xslot of (y => z))
+__global__ void __launch_bounds__(256)
+    k_tc_rev_count(const int32_t* __restrict__ rsrc, const int32_t* __restrict__ rcol, int64_t mo,
+                   const int64_t* __restrict__ rrow, const int32_t* __restrict__ xslot,
+                   int32_t* __restrict__ counts, unsigned long long* __restrict__ total) {
+  unsigned long long local = 0;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < mo;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t x = rsrc[p], y = rcol[p];
+    int64_t i = rrow[x];
+    const int64_t ie = rrow[x + 1];
+    int64_t j = rrow[y];
+    const int64_t je = rrow[y + 1];
+    const int64_t la = ie - i, lb = je - j;
+    if (lb == 0) continue;
+    if (la * 16 < lb) {  // few elements of x: binary-search each in y's row
+      for (; i < ie; ++i) {
+        const int32_t z = rcol[i];
+        j = lower_bound_i32(rcol, j, je, z);
+        if (j == je) break;
+        if (rcol[j] == z) {
+          atomicAdd(&counts[xslot[j]], 1);
+          ++local;
+        }
+      }
+    } else if (lb * 16 < la) {  // few elements of y: search each in x's row
+      for (; j < je; ++j) {
+        const int32_t z = rcol[j];
+        i = lower_bound_i32(rcol, i, ie, z);
+        if (i == ie) break;
+        if (rcol[i] == z) {
+          atomicAdd(&counts[xslot[j]], 1);
+          ++local;
+        }
+      }
+    } else {
+      int32_t a = rcol[i], b = rcol[j];
+      for (;;) {
+        if (a < b) {
+          if (++i == ie) break;
+          a = rcol[i];
+        } else if (a > b) {
+          if (++j == je) break;
+          b = rcol[j];
+        } else {
+          atomicAdd(&counts[xslot[j]], 1);
+          ++local;
+          if (++i == ie || ++j == je) break;
+          a = rcol[i];
+          b = rcol[j];
+        }
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(total, local);
+}
+
+// reversed CSR of the oriented graph + slot map (graph constant, cached)
+static int build_reverse(gfx_graph* g, int64_t mo) {
+  gfx_ctx* ctx = g->ctx;
+  const int64_t n = g->n;
+  int64_t *rcnt, *rrow;
+  int32_t *rsrc, *rcol, *xslot;
+  GFX_TRY(scratch_t(g, "tc_rcnt", n + 1, &rcnt));
+  GFX_TRY(scratch_t(g, "tc_rrow", n + 1, &rrow));
+  GFX_TRY(scratch_t(g, "tc_rsrc", mo + 1, &rsrc));
+  GFX_TRY(scratch_t(g, "tc_rcol", mo + 1, &rcol));
+  GFX_TRY(scratch_t(g, "tc_xslot", mo + 1, &xslot));
+  const int32_t* osrc = static_cast<const int32_t*>(g->scratch["tc_osrc"].ptr);
+  const int32_t* ocol = static_cast<const int32_t*>(g->scratch["tc_ocol"].ptr);
+  unsigned long long *k0 = nullptr, *k1 = nullptr;
+  int32_t* v0 = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  int end_bit = 32;
+  while (end_bit < 64 && (1ll << (end_bit - 32)) < n) ++end_bit;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, v0, xslot, mo, 0, end_bit, ctx->stream);
+  GFX_CK(cudaMallocAsync(&k0, (mo + 1) * 8, ctx->stream));
+  GFX_CK(cudaMallocAsync(&k1, (mo + 1) * 8, ctx->stream));
+  GFX_CK(cudaMallocAsync(&v0, (mo + 1) * 4, ctx->stream));
+  GFX_CK(cudaMallocAsync(&tmp, tb + 16, ctx->stream));
+  GFX_CK(cudaMemsetAsync(rcnt, 0, (n + 1) * 8, ctx->stream));
+  const int grid = grid_for(mo, 256, ctx->sm_count * 16);
+  GFX_LAUNCH(k_tc_rev_keys, grid, 256, 0, ctx->stream, osrc, ocol, mo, k0, v0, rcnt);
+  cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, v0, xslot, mo, 0, end_bit, ctx->stream);
+  GFX_LAUNCH(k_tc_rev_split, grid, 256, 0, ctx->stream, k1, mo, rsrc, rcol);
+  size_t sb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, sb, rcnt, rrow, n + 1, ctx->stream);
+  void* stmp = nullptr;
+  GFX_TRY(scratch(g, "tc_scan_tmp2", sb, &stmp));
+  cub::DeviceScan::ExclusiveSum(stmp, sb, rcnt, rrow, n + 1, ctx->stream);
+  GFX_CK(cudaFreeAsync(k0, ctx->stream));
+  GFX_CK(cudaFreeAsync(k1, ctx->stream));
+  GFX_CK(cudaFreeAsync(v0, ctx->stream));
+  GFX_CK(cudaFreeAsync(tmp, ctx->stream));
+  GFX_CK(cudaGetLastError());
+  GFX_CK(cudaStreamSynchronize(ctx->stream));
+  return GFX_OK;
+}
+
 }  // namespace gfx
 
 using namespace gfx;
@@ -304,6 +454,7 @@ extern "C" int gfx_tc_orient(gfx_graph* g, int64_t* m_oriented) {
              ocol, osrc);
   GFX_CK(cudaGetLastError());
   GFX_CK(cudaStreamSynchronize(ctx->stream));
+  if (mo > 0) GFX_TRY(build_reverse(g, mo));
   g->m_oriented = mo;
   *m_oriented = mo;
   return GFX_OK;
@@ -321,7 +472,40 @@ extern "C" int gfx_tc_count(gfx_graph* g, int32_t* osrc_d, int32_t* odst_d, int3
   int32_t* osrc = static_cast<int32_t*>(g->scratch["tc_osrc"].ptr);
   int32_t* counts = counts_d;
   if (!counts) GFX_TRY(scratch_t(g, "tc_counts", mo + 1, &counts));
-  // hub rows first (bitmap counting), then every other pair
+  if (!getenv("GFX_TC_LEGACY")) {
+    Counters* C = g->counters + 3;
+    GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
+    GFX_CK(cudaMemsetAsync(C, 0, sizeof(Counters), ctx->stream));
+    GFX_CK(cudaMemsetAsync(counts, 0, (mo + 1) * 4, ctx->stream));
+    if (mo > 0) {
+      auto* rrow = static_cast<const int64_t*>(g->scratch["tc_rrow"].ptr);
+      auto* rsrc = static_cast<const int32_t*>(g->scratch["tc_rsrc"].ptr);
+      auto* rcol = static_cast<const int32_t*>(g->scratch["tc_rcol"].ptr);
+      auto* xslot = static_cast<const int32_t*>(g->scratch["tc_xslot"].ptr);
+      GFX_LAUNCH(k_tc_rev_count, grid_for(mo, 256, ctx->sm_count * 8), 256, 0, ctx->stream, rsrc,
+                 rcol, mo, rrow, xslot, counts, &C->total);
+    }
+    GFX_CK(cudaGetLastError());
+    GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));
+    auto* pin = static_cast<Counters*>(ctx->pinned);
+    GFX_CK(cudaMemcpyAsync(pin, C, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+    GFX_CK(cudaStreamSynchronize(ctx->stream));
+    *total = (int64_t)pin->total;
+    if (osrc_d)
+      GFX_CK(cudaMemcpyAsync(osrc_d, osrc, mo * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (odst_d)
+      GFX_CK(cudaMemcpyAsync(odst_d, ocol, mo * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    GFX_CK(cudaStreamSynchronize(ctx->stream));
+    float ms = 0.f;
+    GFX_CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    if (stats) {
+      *stats = gfx_stats{};
+      stats->iterations = 1;
+      stats->device_ms = ms;
+    }
+    return GFX_OK;
+  }
+  // legacy: hub rows first (bitmap counting), then every other pair
   int32_t *hubs = nullptr, *heavy = nullptr;
   GFX_TRY(scratch_t(g, "tc_hubs", g->n + 1, &hubs));
   GFX_TRY(scratch_t(g, "tc_heavy", mo + 1, &heavy));
