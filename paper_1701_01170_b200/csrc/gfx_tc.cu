@@ -316,63 +316,101 @@ __device__ __forceinline__ int64_t lower_bound_i32(const int32_t* __restrict__ a
   return lo;
 }
 
-// one thread per reversed edge x => y: common elements z of rows x and y;
-// each credits the reference slot of z -> y (xslot of (y => z))
+// reversed edge x => y: common elements z of rows x and y; each credits the
+// reference slot of z -> y (xslot of (y => z)).  Short pairs (both rows
+// together <= kRevShort) are merged by one thread; longer ones are appended
+// to a list that k_tc_rev_heavy takes a warp per pair.
+constexpr int kRevShort = 64;
+
 __global__ void __launch_bounds__(256)
     k_tc_rev_count(const int32_t* __restrict__ rsrc, const int32_t* __restrict__ rcol, int64_t mo,
                    const int64_t* __restrict__ rrow, const int32_t* __restrict__ xslot,
-                   int32_t* __restrict__ counts, unsigned long long* __restrict__ total) {
+                   int32_t* __restrict__ counts, unsigned long long* __restrict__ total,
+                   int32_t* __restrict__ heavy, unsigned long long* __restrict__ nheavy) {
+  const int lane = threadIdx.x & 31;
   unsigned long long local = 0;
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < mo;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t x = rsrc[p], y = rcol[p];
-    int64_t i = rrow[x];
-    const int64_t ie = rrow[x + 1];
-    int64_t j = rrow[y];
-    const int64_t je = rrow[y + 1];
-    const int64_t la = ie - i, lb = je - j;
-    if (lb == 0) continue;
-    if (la * 16 < lb) {  // few elements of x: binary-search each in y's row
-      for (; i < ie; ++i) {
-        const int32_t z = rcol[i];
-        j = lower_bound_i32(rcol, j, je, z);
-        if (j == je) break;
-        if (rcol[j] == z) {
-          atomicAdd(&counts[xslot[j]], 1);
-          ++local;
-        }
-      }
-    } else if (lb * 16 < la) {  // few elements of y: search each in x's row
-      for (; j < je; ++j) {
-        const int32_t z = rcol[j];
-        i = lower_bound_i32(rcol, i, ie, z);
-        if (i == ie) break;
-        if (rcol[i] == z) {
-          atomicAdd(&counts[xslot[j]], 1);
-          ++local;
-        }
-      }
-    } else {
-      int32_t a = rcol[i], b = rcol[j];
-      for (;;) {
-        if (a < b) {
-          if (++i == ie) break;
-          a = rcol[i];
-        } else if (a > b) {
-          if (++j == je) break;
-          b = rcol[j];
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; base < mo;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = base + lane;
+    bool is_heavy = false;
+    if (p < mo) {
+      const int32_t x = rsrc[p], y = rcol[p];
+      int64_t i = rrow[x];
+      const int64_t ie = rrow[x + 1];
+      int64_t j = rrow[y];
+      const int64_t je = rrow[y + 1];
+      if (j < je) {
+        if ((ie - i) + (je - j) > kRevShort) {
+          is_heavy = true;
         } else {
+          int32_t a = rcol[i], b = rcol[j];
+          for (;;) {
+            if (a < b) {
+              if (++i == ie) break;
+              a = rcol[i];
+            } else if (a > b) {
+              if (++j == je) break;
+              b = rcol[j];
+            } else {
+              atomicAdd(&counts[xslot[j]], 1);
+              ++local;
+              if (++i == ie || ++j == je) break;
+              a = rcol[i];
+              b = rcol[j];
+            }
+          }
+        }
+      }
+    }
+    const unsigned hm = __ballot_sync(0xffffffffu, is_heavy);
+    if (hm) {
+      unsigned long long at = 0;
+      if (lane == 0) at = atomicAdd(nheavy, (unsigned long long)__popc(hm));
+      at = __shfl_sync(0xffffffffu, at, 0);
+      if (is_heavy) heavy[at + __popc(hm & ((1u << lane) - 1))] = (int32_t)p;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  if (lane == 0 && local) atomicAdd(total, local);
+}
+
+// warp per heavy pair: lanes take elements of the shorter row and
+// binary-search them in the longer one
+__global__ void __launch_bounds__(256)
+    k_tc_rev_heavy(const int32_t* __restrict__ rsrc, const int32_t* __restrict__ rcol,
+                   const int64_t* __restrict__ rrow, const int32_t* __restrict__ xslot,
+                   const int32_t* __restrict__ heavy, const unsigned long long* __restrict__ nheavy,
+                   int32_t* __restrict__ counts, unsigned long long* __restrict__ total) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nh = (int64_t)*nheavy;
+  unsigned long long local = 0;
+  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nh;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t p = heavy[w];
+    const int32_t x = rsrc[p], y = rcol[p];
+    const int64_t i0 = rrow[x], ie = rrow[x + 1], j0 = rrow[y], je = rrow[y + 1];
+    if (ie - i0 <= je - j0) {  // elements of x searched in y's row
+      for (int64_t i = i0 + lane; i < ie; i += 32) {
+        const int32_t z = rcol[i];
+        const int64_t j = lower_bound_i32(rcol, j0, je, z);
+        if (j < je && rcol[j] == z) {
           atomicAdd(&counts[xslot[j]], 1);
           ++local;
-          if (++i == ie || ++j == je) break;
-          a = rcol[i];
-          b = rcol[j];
+        }
+      }
+    } else {  // elements of y searched in x's row
+      for (int64_t j = j0 + lane; j < je; j += 32) {
+        const int32_t z = rcol[j];
+        const int64_t i = lower_bound_i32(rcol, i0, ie, z);
+        if (i < ie && rcol[i] == z) {
+          atomicAdd(&counts[xslot[j]], 1);
+          ++local;
         }
       }
     }
   }
   for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
-  if ((threadIdx.x & 31) == 0 && local) atomicAdd(total, local);
+  if (lane == 0 && local) atomicAdd(total, local);
 }
 
 // reversed CSR of the oriented graph + slot map (graph constant, cached)
@@ -482,8 +520,12 @@ extern "C" int gfx_tc_count(gfx_graph* g, int32_t* osrc_d, int32_t* odst_d, int3
       auto* rsrc = static_cast<const int32_t*>(g->scratch["tc_rsrc"].ptr);
       auto* rcol = static_cast<const int32_t*>(g->scratch["tc_rcol"].ptr);
       auto* xslot = static_cast<const int32_t*>(g->scratch["tc_xslot"].ptr);
+      int32_t* heavy = nullptr;
+      GFX_TRY(scratch_t(g, "tc_heavy", mo + 1, &heavy));
       GFX_LAUNCH(k_tc_rev_count, grid_for(mo, 256, ctx->sm_count * 8), 256, 0, ctx->stream, rsrc,
-                 rcol, mo, rrow, xslot, counts, &C->total);
+                 rcol, mo, rrow, xslot, counts, &C->total, heavy, &C->aux0);
+      GFX_LAUNCH(k_tc_rev_heavy, ctx->sm_count * 8, 256, 0, ctx->stream, rsrc, rcol, rrow, xslot,
+                 heavy, &C->aux0, counts, &C->total);
     }
     GFX_CK(cudaGetLastError());
     GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));

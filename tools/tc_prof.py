@@ -1,16 +1,14 @@
-"""TC on the GPU-built R-MAT graph (default s22): per-kernel launch list under
-ncu, or plain timing."""
+"""One TC count on R-MAT s<scale> for ncu captures: python tools/tc_prof.py 22"""
+import os
 import sys
-from pathlib import Path
 
-sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 from paper_1701_01170_b200.generators import rmat_device_graph  # noqa: E402
 from paper_1701_01170_b200.primitives.tc import tc_device  # noqa: E402
 
-scale = int(sys.argv[1]) if len(sys.argv) > 1 else 22
-dg = rmat_device_graph(scale, 16, 0)
-for _ in range(2):
-    total, counts, osrc, odst, st = tc_device(dg)
-print("tc scale", scale, "triangles", total, "ms", round(st.device_ms, 3), "oriented", counts.numel())
+dg = rmat_device_graph(int(sys.argv[1]) if len(sys.argv) > 1 else 22, 16, 0)
+total, counts, osrc, odst, st = tc_device(dg)
+torch.cuda.synchronize()
+print("total", total, "ms", st.device_ms)
