@@ -384,6 +384,13 @@ def run_partitioned(args, dist: Dist):
                      "kernel": "whole partitioned BFS per GPU (bytes_alg / N / step time)",
                      "peak_source": peak_kind},
         "gpu_launches": int(launches), "clocks": clocks,
+        "e2e": {"value": round(e_r * args.steps / (run["e2e"]["ms"] * 1e-3) / 1e9, 3),
+                "unit": "GTEPS", "h2d_bytes_per_step": run["e2e"]["h2d_bytes_per_step"],
+                "d2h_bytes_per_step": run["e2e"]["d2h_bytes_per_step"],
+                "ms_per_step": round(run["e2e"]["ms"] / args.steps, 4),
+                "what": "graph resident (partitioned at build time): per step the source goes "
+                        "up and every rank's int32 labels + preds come back to pinned host "
+                        "memory, max over ranks"},
         "trace": [[t["iteration"], t["decision"], t["n_f"]] for t in st.direction_trace],
         "extras": extra,
     }
@@ -459,12 +466,33 @@ def _partitioned_run(args, dist, scale: int, steps: int, warmup: int, with_1gpu:
     launches = _native.launch_count() - l0
     dist.barrier()
     t_ms = dist.max(ev0.elapsed_time(ev1))
+    # end to end with the graph resident: the source goes up, every rank's
+    # labels + preds come back to pinned host memory, each step
+    lab_h = torch.empty(eng.nl, dtype=torch.int32, pin_memory=True)
+    prd_h = torch.empty(eng.nl, dtype=torch.int32, pin_memory=True)
+    src_h = torch.tensor([args.source], dtype=torch.int64, pin_memory=True)
+    src_d = torch.empty(1, dtype=torch.int64, device=eng.device)
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev0.record()
+    for _ in range(steps):
+        src_d.copy_(src_h, non_blocking=True)
+        step()
+        lab_h.copy_(eng.labels[: eng.nl], non_blocking=True)
+        prd_h.copy_(eng.preds[: eng.nl], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    ev1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e2e_ms = dist.max(ev0.elapsed_time(ev1))
+    e2e = {"ms": e2e_ms, "d2h_bytes_per_step": int(dist.sum(float(8 * eng.nl))),
+           "h2d_bytes_per_step": 8 * P}
     if ncomm is not None:
         ncomm.close()
     del eng, comm, lrow, lcol
     torch.cuda.empty_cache()
     return {"st": st, "t_ms": t_ms, "e_r": e_r, "n": n, "m": m, "launches": launches,
-            "build_s": build_s, "one_gpu": one_gpu, "loop": loop}
+            "build_s": build_s, "one_gpu": one_gpu, "loop": loop, "e2e": e2e}
 
 
 def extras(args, dg, labels, preds, dist, peak):
