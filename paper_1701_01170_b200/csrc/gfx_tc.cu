@@ -374,13 +374,20 @@ __global__ void __launch_bounds__(256)
   if (lane == 0 && local) atomicAdd(total, local);
 }
 
-// warp per heavy pair: lanes take elements of the shorter row and
-// binary-search them in the longer one
+// warp per heavy pair.  Rows of similar length: a warp-wide merge, 32
+// elements of each row per step -- every lane locates its element of x's
+// chunk in y's chunk with a 5-step binary search over shuffles, and the
+// chunk with the smaller last element advances.  Very uneven rows (one more
+// than kRevSkew times the other): lanes take elements of the shorter row
+// and binary-search them in the longer one.
+constexpr int kRevSkew = 2;
+
 __global__ void __launch_bounds__(256)
     k_tc_rev_heavy(const int32_t* __restrict__ rsrc, const int32_t* __restrict__ rcol,
                    const int64_t* __restrict__ rrow, const int32_t* __restrict__ xslot,
                    const int32_t* __restrict__ heavy, const unsigned long long* __restrict__ nheavy,
-                   int32_t* __restrict__ counts, unsigned long long* __restrict__ total) {
+                   int32_t* __restrict__ counts, unsigned long long* __restrict__ total,
+                   int skew) {
   const int lane = threadIdx.x & 31;
   const int64_t nh = (int64_t)*nheavy;
   unsigned long long local = 0;
@@ -389,24 +396,55 @@ __global__ void __launch_bounds__(256)
     const int64_t p = heavy[w];
     const int32_t x = rsrc[p], y = rcol[p];
     const int64_t i0 = rrow[x], ie = rrow[x + 1], j0 = rrow[y], je = rrow[y + 1];
-    if (ie - i0 <= je - j0) {  // elements of x searched in y's row
-      for (int64_t i = i0 + lane; i < ie; i += 32) {
-        const int32_t z = rcol[i];
-        const int64_t j = lower_bound_i32(rcol, j0, je, z);
-        if (j < je && rcol[j] == z) {
-          atomicAdd(&counts[xslot[j]], 1);
-          ++local;
+    const int64_t la = ie - i0, lb = je - j0;
+    if (la > skew * lb || lb > skew * la) {
+      // (each lane's elements increase, so its search starts where the
+      // previous one ended)
+      if (la <= lb) {  // elements of x searched in y's row
+        int64_t jl = j0;
+        for (int64_t i = i0 + lane; i < ie; i += 32) {
+          const int32_t z = rcol[i];
+          jl = lower_bound_i32(rcol, jl, je, z);
+          if (jl == je) break;
+          if (rcol[jl] == z) {
+            atomicAdd(&counts[xslot[jl]], 1);
+            ++local;
+          }
+        }
+      } else {  // elements of y searched in x's row
+        int64_t il = i0;
+        for (int64_t j = j0 + lane; j < je; j += 32) {
+          const int32_t z = rcol[j];
+          il = lower_bound_i32(rcol, il, ie, z);
+          if (il == ie) break;
+          if (rcol[il] == z) {
+            atomicAdd(&counts[xslot[j]], 1);
+            ++local;
+          }
         }
       }
-    } else {  // elements of y searched in x's row
-      for (int64_t j = j0 + lane; j < je; j += 32) {
-        const int32_t z = rcol[j];
-        const int64_t i = lower_bound_i32(rcol, i0, ie, z);
-        if (i < ie && rcol[i] == z) {
-          atomicAdd(&counts[xslot[j]], 1);
-          ++local;
-        }
+      continue;
+    }
+    int64_t i = i0, j = j0;
+    while (i < ie && j < je) {  // warp-uniform
+      const bool va = i + lane < ie, vb = j + lane < je;
+      const int32_t a = va ? rcol[i + lane] : 0x7fffffff;
+      const int32_t b = vb ? rcol[j + lane] : 0x7fffffff;
+      const int32_t amax = __shfl_sync(0xffffffffu, a, (int)min((int64_t)31, ie - i - 1));
+      const int32_t bmax = __shfl_sync(0xffffffffu, b, (int)min((int64_t)31, je - j - 1));
+      int lo = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {  // first lane of b's chunk with b >= a
+        const int32_t bm = __shfl_sync(0xffffffffu, b, lo + step - 1);
+        if (bm < a) lo += step;
       }
+      const int32_t bv = __shfl_sync(0xffffffffu, b, lo & 31);
+      if (va && lo < 32 && bv == a && j + lo < je) {
+        atomicAdd(&counts[xslot[j + lo]], 1);
+        ++local;
+      }
+      if (amax <= bmax) i += 32;
+      if (bmax <= amax) j += 32;
     }
   }
   for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
@@ -525,7 +563,8 @@ extern "C" int gfx_tc_count(gfx_graph* g, int32_t* osrc_d, int32_t* odst_d, int3
       GFX_LAUNCH(k_tc_rev_count, grid_for(mo, 256, ctx->sm_count * 8), 256, 0, ctx->stream, rsrc,
                  rcol, mo, rrow, xslot, counts, &C->total, heavy, &C->aux0);
       GFX_LAUNCH(k_tc_rev_heavy, ctx->sm_count * 8, 256, 0, ctx->stream, rsrc, rcol, rrow, xslot,
-                 heavy, &C->aux0, counts, &C->total);
+                 heavy, &C->aux0, counts, &C->total,
+                 getenv("GFX_TC_SKEW") ? atoi(getenv("GFX_TC_SKEW")) : kRevSkew);
     }
     GFX_CK(cudaGetLastError());
     GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));
