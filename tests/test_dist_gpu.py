@@ -112,3 +112,115 @@ def test_rmat_native_loop_single_rank(scale):
     lab, _ = gather_labels([eng], dg.num_vertices)
     assert sha(labels_to_host(lab)) == rec["bfs_sha"]
     assert st.edges_push == rec["bfs_edges_traversed"]
+
+
+class _StagedComm:
+    """Test-only: ProcessComm's protocol with each collective staged through
+    host memory so gloo can carry it -- two real processes share the one
+    GPU a gpurun box has, each driving its own DeviceEngine."""
+
+    def __init__(self, engine):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.engines = [engine]
+
+    def _a2a(self, out, inp, out_splits=None, in_splits=None):
+        import torch
+
+        o = torch.empty(out.shape, dtype=out.dtype)
+        self.dist.all_to_all_single(o, inp.cpu(), output_split_sizes=out_splits,
+                                    input_split_sizes=in_splits)
+        out.copy_(o)
+
+    def exchange_counts(self):
+        e = self.engines[0]
+        P = e.send_counts.numel()
+        self._a2a(e.recv_counts, e.send_counts)
+        both = [int(k) for k in e.counts.tolist()]
+        return [both[:P]], [both[P:]]
+
+    def exchange_pairs(self, sc, rc):
+        e = self.engines[0]
+        s, r = sc[0], rc[0]
+        self._a2a(e.recv[: sum(r)], e.send[: sum(s)], r, s)
+        return [sum(r)]
+
+    def allgather_frontier(self):
+        import torch
+
+        e = self.engines[0]
+        o = torch.empty(e.gathered.shape, dtype=e.gathered.dtype)
+        self.dist.all_gather_into_tensor(o, e.front_local.cpu())
+        e.gathered.copy_(o)
+
+    def allreduce_stats(self):
+        e = self.engines[0]
+        t = e.stats[4:].cpu()
+        self.dist.all_reduce(t)
+        e.stats[4:].copy_(t)
+        vals = [int(x) for x in e.stats.tolist()]
+        return [vals[:4]], vals[4:]
+
+
+def _two_proc_worker(rank, world, port, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1701_01170_b200._results import labels_to_host
+        from paper_1701_01170_b200.dist import DeviceEngine, bfs_partitioned, partition_graph
+        from paper_1701_01170_b200.generators import rmat_device_graph
+
+        dg = rmat_device_graph(16, 16, 0)
+        n, m = dg.num_vertices, dg.num_edges
+        lrow, lcol = partition_graph(dg, world, rank)
+        eng = DeviceEngine(lrow, lcol, n, m, world, rank)
+        comm = _StagedComm(eng)
+        out = {}
+        for direction in ("auto", "push", "pull"):
+            st = bfs_partitioned(comm, n, m, 0, direction=direction)
+            lab = labels_to_host(eng.labels[: eng.nl])
+            parts = [None] * world
+            dist.all_gather_object(parts, lab)
+            if rank == 0:
+                full = np.empty(n, dtype=np.int64)
+                for r, part in enumerate(parts):
+                    full[r::world] = part
+                out[direction] = (full, _rows(st.direction_trace), st.edges_push)
+        if rank == 0:
+            q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_processes_share_one_gpu():
+    """The partitioned BFS as two real processes (P = 2, one DeviceEngine
+    each, collectives over gloo staged through host memory): labels, trace
+    and push slot totals equal the reference's s16 goldens."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_two_proc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    rec, _ = rmat_golden(16)
+    for direction, (labels, trace, edges_push) in out.items():
+        assert sha(labels) == rec["bfs_sha"], direction
+    assert out["auto"][1] == [list(x) for x in rec["bfs_auto_trace"]]
+    assert out["push"][2] == rec["bfs_edges_traversed"]
