@@ -312,6 +312,24 @@ GFX_API int gfx_nccl_comm_destroy(gfx_nccl* comm);
 GFX_API int gfx_dbfs_run(gfx_dbfs* db, gfx_nccl* comm, int64_t source, int direction,
                          double do_a, double do_b, int mu_edge_based, gfx_iter_rec* recs,
                          int64_t rec_cap, gfx_stats* stats);
+/* The same loop over a caller-supplied collective table (the NCCL one above
+ * is one implementation).  Each callback acts on the buffers bound with
+ * gfx_dbfs_bind, ordered on the context stream, and returns 0 on success:
+ * exchange_counts fills send_counts[P..2P) from every rank's [0..P);
+ * exchange_pairs moves each rank's send buckets (host counts sc[P], rc[P],
+ * own rank 0) into the receivers' recv arrays in rank order;
+ * allgather_frontier fills gathered from every rank's front_local;
+ * allreduce_stats sums stats[4..8) over the ranks in place. */
+typedef struct gfx_dbfs_comm {
+  void* user;
+  int (*exchange_counts)(void* user);
+  int (*exchange_pairs)(void* user, const int64_t* send_counts, const int64_t* recv_counts);
+  int (*allgather_frontier)(void* user);
+  int (*allreduce_stats)(void* user);
+} gfx_dbfs_comm;
+GFX_API int gfx_dbfs_run_comm(gfx_dbfs* db, const gfx_dbfs_comm* comm, int64_t source,
+                              int direction, double do_a, double do_b, int mu_edge_based,
+                              gfx_iter_rec* recs, int64_t rec_cap, gfx_stats* stats);
 
 /* ---- kernel experiments (tools/expand_lab.py; not a product path) -------
  * One LB expansion of F_d with functor variant 0 (stream only), 1 (stream +

@@ -45,6 +45,17 @@ class Stats(Structure):
     ]
 
 
+DBFS_CB0 = ctypes.CFUNCTYPE(c_int, c_void_p)
+DBFS_CB_PAIRS = ctypes.CFUNCTYPE(c_int, c_void_p, POINTER(c_int64), POINTER(c_int64))
+
+
+class DbfsComm(Structure):
+    """gfx_dbfs_comm: the collective table of gfx_dbfs_run_comm."""
+    _fields_ = [("user", c_void_p), ("exchange_counts", DBFS_CB0),
+                ("exchange_pairs", DBFS_CB_PAIRS), ("allgather_frontier", DBFS_CB0),
+                ("allreduce_stats", DBFS_CB0)]
+
+
 class FunctorArgs(Structure):
     _fields_ = [("labels_d", c_void_p), ("preds_d", c_void_p), ("value", c_int64)]
 
@@ -116,6 +127,8 @@ _SIGS = {
     "gfx_nccl_comm_destroy": (c_int, [c_void_p]),
     "gfx_dbfs_run": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_double, c_double, c_int,
                              POINTER(IterRec), c_int64, POINTER(Stats)]),
+    "gfx_dbfs_run_comm": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_double, c_double, c_int,
+                                  POINTER(IterRec), c_int64, POINTER(Stats)]),
     "gfx_debug_gridsync": (c_int, [c_void_p, c_int, c_int, c_int, c_int, POINTER(c_float)]),
     "gfx_debug_chase": (c_int, [c_void_p, c_void_p, c_int, ctypes.c_uint32, POINTER(c_double)]),
     "gfx_debug_expand": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_int32,

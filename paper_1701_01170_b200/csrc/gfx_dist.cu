@@ -725,19 +725,81 @@ int gfx_nccl_comm_destroy(gfx_nccl* c) {
   return GFX_OK;
 }
 
-int gfx_dbfs_run(gfx_dbfs* db, gfx_nccl* comm, int64_t source, int direction, double do_a,
-                 double do_b, int mu_edge_based, gfx_iter_rec* recs, int64_t rec_cap,
-                 gfx_stats* stats) {
+}  // extern "C"
+
+namespace {
+
+// NCCL implementation of the collective table (user = NcclCtx)
+struct NcclCtx {
+  gfx_dbfs* db;
+  void* comm;
+};
+
+int nccl_counts(void* user) {
+  auto* c = static_cast<NcclCtx*>(user);
+  gfx_dbfs* db = c->db;
+  const int P = db->P;
+  cudaStream_t st = db->ctx->stream;
+  GFX_NCCL(g_nccl.GroupStart());
+  for (int o = 0; o < P; ++o) {
+    GFX_NCCL(g_nccl.Send(db->send_counts + o, 1, kNcclInt64, o, c->comm, st));
+    GFX_NCCL(g_nccl.Recv(db->send_counts + P + o, 1, kNcclInt64, o, c->comm, st));
+  }
+  GFX_NCCL(g_nccl.GroupEnd());
+  return GFX_OK;
+}
+
+int nccl_pairs(void* user, const int64_t* sc, const int64_t* rc) {
+  auto* c = static_cast<NcclCtx*>(user);
+  gfx_dbfs* db = c->db;
+  cudaStream_t st = db->ctx->stream;
+  int64_t so = 0, ro = 0;
+  GFX_NCCL(g_nccl.GroupStart());
+  for (int o = 0; o < db->P; ++o) {
+    if (o != db->r) {
+      if (sc[o]) GFX_NCCL(g_nccl.Send(db->send + so, sc[o], kNcclUint64, o, c->comm, st));
+      if (rc[o]) GFX_NCCL(g_nccl.Recv(db->recv + ro, rc[o], kNcclUint64, o, c->comm, st));
+    }
+    so += sc[o];
+    ro += rc[o];
+  }
+  GFX_NCCL(g_nccl.GroupEnd());
+  return GFX_OK;
+}
+
+int nccl_gather(void* user) {
+  auto* c = static_cast<NcclCtx*>(user);
+  gfx_dbfs* db = c->db;
+  GFX_NCCL(g_nccl.AllGather(db->front_local, db->gathered, (size_t)db->wmax, kNcclInt32, c->comm,
+                            db->ctx->stream));
+  return GFX_OK;
+}
+
+int nccl_reduce(void* user) {
+  auto* c = static_cast<NcclCtx*>(user);
+  gfx_dbfs* db = c->db;
+  GFX_NCCL(g_nccl.AllReduce(db->stats + 4, db->stats + 4, 4, kNcclInt64, kNcclSum, c->comm,
+                            db->ctx->stream));
+  return GFX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gfx_dbfs_run_comm(gfx_dbfs* db, const gfx_dbfs_comm* comm, int64_t source, int direction,
+                      double do_a, double do_b, int mu_edge_based, gfx_iter_rec* recs,
+                      int64_t rec_cap, gfx_stats* stats) {
   GFX_REQUIRE(db && stats && db->stats, "gfx_dbfs_run: unbound engine");
   GFX_REQUIRE(direction == GFX_DIR_PUSH || direction == GFX_DIR_PULL || direction == GFX_DIR_AUTO,
               "bad direction %d", direction);
   GFX_REQUIRE(do_a > 0 && do_b > 0, "do_a and do_b must be positive");
-  const int P = db->P, r = db->r;
-  GFX_REQUIRE(P == 1 || (comm && comm->comm && comm->nranks == P && comm->rank == r),
-              "gfx_dbfs_run: P = %d needs a communicator of P ranks with this rank", P);
+  const int P = db->P;
+  GFX_REQUIRE(P == 1 || (comm && comm->exchange_counts && comm->exchange_pairs &&
+                         comm->allgather_frontier && comm->allreduce_stats),
+              "gfx_dbfs_run: P = %d needs a collective table", P);
   gfx_ctx* ctx = db->ctx;
   cudaStream_t st = ctx->stream;
-  void* nc = P > 1 ? comm->comm : nullptr;
   auto* pin = static_cast<int64_t*>(ctx->pinned);  // 4 KB: 2P counts or 8 stats
   std::memset(stats, 0, sizeof(*stats));
   cudaEvent_t e0, e1;
@@ -748,7 +810,7 @@ int gfx_dbfs_run(gfx_dbfs* db, gfx_nccl* comm, int64_t source, int direction, do
   GFX_TRY(gfx_dbfs_reset(db, source, &nf_local));
   int64_t nf = 1, n_u = db->n, depth = 0, nrec = 0;
   int mode = GFX_DIR_PUSH;
-  std::vector<int64_t> sc(P), rc(P), soff(P), roff(P);
+  std::vector<int64_t> sc(P), rc(P);
   while (nf > 0) {
     ++depth;
     n_u -= nf;
@@ -766,47 +828,30 @@ int gfx_dbfs_run(gfx_dbfs* db, gfx_nccl* comm, int64_t source, int direction, do
       GFX_TRY(gfx_dbfs_push_expand(db, (int32_t)depth));
       int64_t nrecv = 0;
       if (P > 1) {
-        GFX_NCCL(g_nccl.GroupStart());
-        for (int o = 0; o < P; ++o) {
-          GFX_NCCL(g_nccl.Send(db->send_counts + o, 1, kNcclInt64, o, nc, st));
-          GFX_NCCL(g_nccl.Recv(db->send_counts + P + o, 1, kNcclInt64, o, nc, st));
-        }
-        GFX_NCCL(g_nccl.GroupEnd());
+        GFX_REQUIRE(comm->exchange_counts(comm->user) == 0, "exchange_counts failed");
         GFX_CK(cudaMemcpyAsync(pin, db->send_counts, 2 * P * 8, cudaMemcpyDeviceToHost, st));
         GFX_CK(cudaStreamSynchronize(st));
-        int64_t sa = 0, ra = 0;
         for (int o = 0; o < P; ++o) {
           sc[o] = pin[o];
           rc[o] = pin[P + o];
-          soff[o] = sa;
-          roff[o] = ra;
-          sa += sc[o];
-          ra += rc[o];
+          nrecv += rc[o];
         }
-        GFX_REQUIRE(ra <= db->recv_cap, "received %lld pairs, capacity %lld", (long long)ra,
-                    (long long)db->recv_cap);
-        GFX_NCCL(g_nccl.GroupStart());
-        for (int o = 0; o < P; ++o) {
-          if (o == r) continue;
-          if (sc[o]) GFX_NCCL(g_nccl.Send(db->send + soff[o], sc[o], kNcclUint64, o, nc, st));
-          if (rc[o]) GFX_NCCL(g_nccl.Recv(db->recv + roff[o], rc[o], kNcclUint64, o, nc, st));
-        }
-        GFX_NCCL(g_nccl.GroupEnd());
-        nrecv = ra;
+        GFX_REQUIRE(nrecv <= db->recv_cap, "received %lld pairs, capacity %lld",
+                    (long long)nrecv, (long long)db->recv_cap);
+        GFX_REQUIRE(comm->exchange_pairs(comm->user, sc.data(), rc.data()) == 0,
+                    "exchange_pairs failed");
       }
       GFX_TRY(gfx_dbfs_push_claim(db, nrecv, (int32_t)depth));
     } else {
       GFX_TRY(gfx_dbfs_pull_prepare(db));
       if (P > 1)
-        GFX_NCCL(g_nccl.AllGather(db->front_local, db->gathered, (size_t)db->wmax, kNcclInt32,
-                                  nc, st));
+        GFX_REQUIRE(comm->allgather_frontier(comm->user) == 0, "allgather_frontier failed");
       else
         GFX_CK(cudaMemcpyAsync(db->gathered, db->front_local, db->wmax * 4,
                                cudaMemcpyDeviceToDevice, st));
       GFX_TRY(gfx_dbfs_pull(db, (int32_t)depth));
     }
-    if (P > 1)
-      GFX_NCCL(g_nccl.AllReduce(db->stats + 4, db->stats + 4, 4, kNcclInt64, kNcclSum, nc, st));
+    if (P > 1) GFX_REQUIRE(comm->allreduce_stats(comm->user) == 0, "allreduce_stats failed");
     GFX_CK(cudaMemcpyAsync(pin, db->stats, 8 * 8, cudaMemcpyDeviceToHost, st));
     GFX_CK(cudaStreamSynchronize(st));
     const int64_t local_out = pin[0], nout = pin[4];
@@ -849,6 +894,21 @@ int gfx_dbfs_run(gfx_dbfs* db, gfx_nccl* comm, int64_t source, int direction, do
   stats->device_ms = ms;
   stats->num_records = nrec;
   return GFX_OK;
+}
+
+int gfx_dbfs_run(gfx_dbfs* db, gfx_nccl* comm, int64_t source, int direction, double do_a,
+                 double do_b, int mu_edge_based, gfx_iter_rec* recs, int64_t rec_cap,
+                 gfx_stats* stats) {
+  GFX_REQUIRE(db, "gfx_dbfs_run: null engine");
+  if (db->P == 1)
+    return gfx_dbfs_run_comm(db, nullptr, source, direction, do_a, do_b, mu_edge_based, recs,
+                             rec_cap, stats);
+  GFX_REQUIRE(comm && comm->comm && comm->nranks == db->P && comm->rank == db->r,
+              "gfx_dbfs_run: P = %d needs a communicator of P ranks with this rank", db->P);
+  NcclCtx c{db, comm->comm};
+  gfx_dbfs_comm ops{&c, nccl_counts, nccl_pairs, nccl_gather, nccl_reduce};
+  return gfx_dbfs_run_comm(db, &ops, source, direction, do_a, do_b, mu_edge_based, recs, rec_cap,
+                           stats);
 }
 
 }  // extern "C"

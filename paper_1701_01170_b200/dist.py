@@ -331,12 +331,41 @@ class NativeComm:
         self.close()
 
 
+def _comm_table(collectives):
+    """gfx_dbfs_comm over a Python object with exchange_counts(),
+    exchange_pairs(sc, rc), allgather_frontier(), allreduce_stats_inplace()
+    acting on the engine's bound tensors (returns the struct and the ctypes
+    callbacks, which must stay alive for the call)."""
+    def wrap(fn):
+        def cb(*args):
+            try:
+                fn(*args)
+                return 0
+            except Exception:  # noqa: BLE001 -- reported through the status code
+                import traceback
+
+                traceback.print_exc()
+                return 1
+        return cb
+
+    P = collectives.P
+    cbs = (_native.DBFS_CB0(wrap(lambda u: collectives.exchange_counts())),
+           _native.DBFS_CB_PAIRS(wrap(lambda u, sc, rc: collectives.exchange_pairs(
+               [int(sc[k]) for k in range(P)], [int(rc[k]) for k in range(P)]))),
+           _native.DBFS_CB0(wrap(lambda u: collectives.allgather_frontier())),
+           _native.DBFS_CB0(wrap(lambda u: collectives.allreduce_stats_inplace())))
+    return _native.DbfsComm(None, *cbs), cbs
+
+
 def bfs_partitioned_native(engine, ncomm, n: int, m: int, source: int, direction: str = PUSH,
                            do_a: float = 0.001, do_b: float = 0.2,
-                           mu_edge_based: bool = False) -> DistBfsStats:
+                           mu_edge_based: bool = False, collectives=None) -> DistBfsStats:
     """``bfs_partitioned`` with the level loop in libgfx (gfx_dbfs_run):
     the same protocol, decisions and trace, without a Python round trip per
-    collective.  ``engine`` is this rank's DeviceEngine."""
+    collective.  ``engine`` is this rank's DeviceEngine; the collectives are
+    NCCL (``ncomm``, a NativeComm; None at P = 1) or, with ``collectives``,
+    a Python implementation called back from the C loop
+    (gfx_dbfs_run_comm; used by the tests to run P > 1 on one GPU)."""
     if not 0 <= source < n:
         raise ValueError(f"source {source} out of range")
     if direction not in _DIR_CODE:
@@ -344,9 +373,14 @@ def bfs_partitioned_native(engine, ncomm, n: int, m: int, source: int, direction
     cap = 4096
     recs = (_native.IterRec * cap)()
     stats = _native.Stats()
-    _native.call("gfx_dbfs_run", engine.handle, ncomm.handle if ncomm else None, int(source),
-                 _DIR_CODE[direction], float(do_a), float(do_b), int(bool(mu_edge_based)), recs,
-                 cap, ctypes.byref(stats))
+    args = (int(source), _DIR_CODE[direction], float(do_a), float(do_b),
+            int(bool(mu_edge_based)), recs, cap, ctypes.byref(stats))
+    if collectives is not None:
+        table, keep = _comm_table(collectives)
+        _native.call("gfx_dbfs_run_comm", engine.handle, ctypes.byref(table), *args)
+        del keep
+    else:
+        _native.call("gfx_dbfs_run", engine.handle, ncomm.handle if ncomm else None, *args)
     st = DistBfsStats()
     mode = {0: PUSH, 1: PULL}
     for i in range(stats.num_records):

@@ -224,3 +224,96 @@ def test_two_processes_share_one_gpu():
         assert sha(labels) == rec["bfs_sha"], direction
     assert out["auto"][1] == [list(x) for x in rec["bfs_auto_trace"]]
     assert out["push"][2] == rec["bfs_edges_traversed"]
+
+
+class _StagedCollectives:
+    """Test-only collective table for the NATIVE loop (gfx_dbfs_run_comm):
+    the C loop calls back into Python, which stages each collective through
+    host memory over gloo."""
+
+    def __init__(self, engine):
+        self.comm = _StagedComm(engine)
+        self.e = engine
+        self.P = engine.P
+
+    def exchange_counts(self):
+        self.comm._a2a(self.e.recv_counts, self.e.send_counts)
+
+    def exchange_pairs(self, sc, rc):
+        self.comm._a2a(self.e.recv[: sum(rc)], self.e.send[: sum(sc)], rc, sc)
+
+    def allgather_frontier(self):
+        self.comm.allgather_frontier()
+
+    def allreduce_stats_inplace(self):
+        import torch
+
+        t = self.e.stats[4:].cpu()
+        self.comm.dist.all_reduce(t)
+        self.e.stats[4:].copy_(t)
+        torch.cuda.synchronize()
+
+
+def _two_proc_native_worker(rank, world, port, q):
+    import os
+
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1701_01170_b200._results import labels_to_host
+        from paper_1701_01170_b200.dist import DeviceEngine, bfs_partitioned_native, partition_graph
+        from paper_1701_01170_b200.generators import rmat_device_graph
+
+        dg = rmat_device_graph(16, 16, 0)
+        n, m = dg.num_vertices, dg.num_edges
+        lrow, lcol = partition_graph(dg, world, rank)
+        eng = DeviceEngine(lrow, lcol, n, m, world, rank)
+        coll = _StagedCollectives(eng)
+        out = {}
+        for direction in ("auto", "push", "pull"):
+            st = bfs_partitioned_native(eng, None, n, m, 0, direction=direction, collectives=coll)
+            lab = labels_to_host(eng.labels[: eng.nl])
+            parts = [None] * world
+            dist.all_gather_object(parts, lab)
+            if rank == 0:
+                full = np.empty(n, dtype=np.int64)
+                for r, part in enumerate(parts):
+                    full[r::world] = part
+                out[direction] = (full, _rows(st.direction_trace), st.edges_push)
+        if rank == 0:
+            q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_native_loop_two_processes_share_one_gpu(world):
+    """The NATIVE level loop (gfx_dbfs_run_comm: the C++ protocol the NCCL
+    path runs) with P = 2 / 3 real processes on one GPU, collectives called
+    back into Python and staged over gloo: labels, trace and push totals
+    equal the reference's s16 goldens."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_two_proc_native_worker, args=(r, world, port, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    rec, _ = rmat_golden(16)
+    for direction, (labels, trace, edges_push) in out.items():
+        assert sha(labels) == rec["bfs_sha"], direction
+    assert out["auto"][1] == [list(x) for x in rec["bfs_auto_trace"]]
+    assert out["push"][2] == rec["bfs_edges_traversed"]
