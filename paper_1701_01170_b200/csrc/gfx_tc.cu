@@ -381,18 +381,27 @@ __global__ void __launch_bounds__(256)
 // than kRevSkew times the other): lanes take elements of the shorter row
 // and binary-search them in the longer one.
 constexpr int kRevSkew = 2;
+constexpr int64_t kRevGrab = 16;  // heavy pairs per dynamic hand-out
 
 __global__ void __launch_bounds__(256)
     k_tc_rev_heavy(const int32_t* __restrict__ rsrc, const int32_t* __restrict__ rcol,
                    const int64_t* __restrict__ rrow, const int32_t* __restrict__ xslot,
                    const int32_t* __restrict__ heavy, const unsigned long long* __restrict__ nheavy,
                    int32_t* __restrict__ counts, unsigned long long* __restrict__ total,
-                   int skew) {
+                   int skew, unsigned long long* __restrict__ grab) {
   const int lane = threadIdx.x & 31;
   const int64_t nh = (int64_t)*nheavy;
   unsigned long long local = 0;
-  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nh;
-       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+  // pairs handed out dynamically in chunks of kRevGrab (their costs vary
+  // by orders of magnitude; one counter update per chunk)
+  int64_t w = 0, wend = 0;
+  for (;;) {
+    if (w == wend) {
+      if (lane == 0) w = (int64_t)atomicAdd(grab, (unsigned long long)kRevGrab);
+      w = __shfl_sync(0xffffffffu, w, 0);
+      wend = min(w + kRevGrab, nh);
+    }
+    if (w >= nh) break;
     const int64_t p = heavy[w];
     const int32_t x = rsrc[p], y = rcol[p];
     const int64_t i0 = rrow[x], ie = rrow[x + 1], j0 = rrow[y], je = rrow[y + 1];
@@ -423,6 +432,7 @@ __global__ void __launch_bounds__(256)
           }
         }
       }
+      ++w;
       continue;
     }
     int64_t i = i0, j = j0;
@@ -446,6 +456,7 @@ __global__ void __launch_bounds__(256)
       if (amax <= bmax) i += 32;
       if (bmax <= amax) j += 32;
     }
+    ++w;
   }
   for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
   if (lane == 0 && local) atomicAdd(total, local);
@@ -564,7 +575,7 @@ extern "C" int gfx_tc_count(gfx_graph* g, int32_t* osrc_d, int32_t* odst_d, int3
                  rcol, mo, rrow, xslot, counts, &C->total, heavy, &C->aux0);
       GFX_LAUNCH(k_tc_rev_heavy, ctx->sm_count * 8, 256, 0, ctx->stream, rsrc, rcol, rrow, xslot,
                  heavy, &C->aux0, counts, &C->total,
-                 getenv("GFX_TC_SKEW") ? atoi(getenv("GFX_TC_SKEW")) : kRevSkew);
+                 getenv("GFX_TC_SKEW") ? atoi(getenv("GFX_TC_SKEW")) : kRevSkew, &C->aux1);
     }
     GFX_CK(cudaGetLastError());
     GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));
