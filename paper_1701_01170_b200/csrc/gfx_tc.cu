@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(256)
                    const int64_t* __restrict__ rrow, const int32_t* __restrict__ xslot,
                    const int32_t* __restrict__ heavy, const unsigned long long* __restrict__ nheavy,
                    int32_t* __restrict__ counts, unsigned long long* __restrict__ total,
-                   int skew, unsigned long long* __restrict__ grab) {
+                   int skew, unsigned long long* __restrict__ grab, int64_t grab_chunk) {
   const int lane = threadIdx.x & 31;
   const int64_t nh = (int64_t)*nheavy;
   unsigned long long local = 0;
@@ -397,9 +397,9 @@ __global__ void __launch_bounds__(256)
   int64_t w = 0, wend = 0;
   for (;;) {
     if (w == wend) {
-      if (lane == 0) w = (int64_t)atomicAdd(grab, (unsigned long long)kRevGrab);
+      if (lane == 0) w = (int64_t)atomicAdd(grab, (unsigned long long)grab_chunk);
       w = __shfl_sync(0xffffffffu, w, 0);
-      wend = min(w + kRevGrab, nh);
+      wend = min(w + grab_chunk, nh);
     }
     if (w >= nh) break;
     const int64_t p = heavy[w];
@@ -575,7 +575,8 @@ extern "C" int gfx_tc_count(gfx_graph* g, int32_t* osrc_d, int32_t* odst_d, int3
                  rcol, mo, rrow, xslot, counts, &C->total, heavy, &C->aux0);
       GFX_LAUNCH(k_tc_rev_heavy, ctx->sm_count * 8, 256, 0, ctx->stream, rsrc, rcol, rrow, xslot,
                  heavy, &C->aux0, counts, &C->total,
-                 getenv("GFX_TC_SKEW") ? atoi(getenv("GFX_TC_SKEW")) : kRevSkew, &C->aux1);
+                 getenv("GFX_TC_SKEW") ? atoi(getenv("GFX_TC_SKEW")) : kRevSkew, &C->aux1,
+                 (int64_t)(getenv("GFX_TC_GRAB") ? atoi(getenv("GFX_TC_GRAB")) : kRevGrab));
     }
     GFX_CK(cudaGetLastError());
     GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));
