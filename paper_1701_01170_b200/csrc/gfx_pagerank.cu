@@ -8,7 +8,7 @@
 // Here the scatter becomes a gather over in-neighbours (no fp64 atomics, so
 // runs are reproducible): contrib[u] = d*rank[u]/outdeg[u] for active u (0
 // otherwise), rank_next[v] = base + sum contrib[u] in ascending u.  Vertices
-// with in-degree <= 64 are summed sequentially by one thread in exactly the
+// with in-degree <= 16 are summed sequentially by one thread in exactly the
 // reference's slot order (bit-identical terms and order); heavier rows are
 // reduced by a whole warp (tolerance: L1 <= 1e-6, north_star).
 #include <cuda_runtime.h>
@@ -77,7 +77,7 @@ __global__ void k_pr_base(const double* __restrict__ partials, int nparts, int64
 // loads of a batch are in flight together; the adds stay sequential, so the
 // terms and their order are the reference's).  Heavy rows: the whole warp,
 // kPrBatch loads per lane in flight, tree-reduced (L1 <= 1e-6 tolerance).
-constexpr int kPrLight = 64;
+constexpr int kPrLight = 16;
 constexpr int kPrBatch = 8;
 __global__ void __launch_bounds__(kPrBlock)
     k_pr_gather(const int64_t* __restrict__ rrow, const int32_t* __restrict__ rcol, int64_t n,
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kPrBlock)
 // Heavy rows (in-degree > kPrLight) are cut into chunks of kPrChunk slots
 // (graph-constant table, built once): one warp sums a chunk (kPrBatch loads
 // per lane in flight, tree-reduced) into partial[k] ...
-constexpr int64_t kPrChunk = 4096;
+constexpr int64_t kPrChunk = 1024;
 __global__ void __launch_bounds__(kPrBlock)
     k_pr_chunks(const int64_t* __restrict__ cstart, int64_t nchunks, const int64_t* __restrict__ cend,
                 const int32_t* __restrict__ rcol, const double* __restrict__ contrib,
