@@ -983,11 +983,17 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
         queue_to_bitmap(a.order + c.q_off, nf, fcur, gtid, nthr);
         grid.sync();
       }
-      pull_groups(a.words, a.nz_in, a.visited, BitmapFront{fcur}, fnext, a.head, a.rrow, a.rcol, a.directed,
-                  lab, a.preds, depth, cur, gw, nw, PS, a.head + a.n + 1,
-                  // dynamic tail only on dense levels (unvisited non-isolated
-                  // vertices above n/8); sparse levels keep the static deal
-                  (c.n_u - (a.n - a.nnz)) * 8 > a.n ? &cur->aux2 : nullptr);
+      // dense levels (unvisited non-isolated vertices above n/8): 8
+      // candidates per lane in flight and a dynamic tail; sparse levels: 4
+      // in flight and the static deal
+      if ((c.n_u - (a.n - a.nnz)) * 8 > a.n)
+        pull_groups<BitmapFront, 8>(a.words, a.nz_in, a.visited, BitmapFront{fcur}, fnext, a.head,
+                                    a.rrow, a.rcol, a.directed, lab, a.preds, depth, cur, gw, nw,
+                                    PS, a.head + a.n + 1, &cur->aux2);
+      else
+        pull_groups<BitmapFront, 4>(a.words, a.nz_in, a.visited, BitmapFront{fcur}, fnext, a.head,
+                                    a.rrow, a.rcol, a.directed, lab, a.preds, depth, cur, gw, nw,
+                                    PS, a.head + a.n + 1, nullptr);
       grid.sync();
       nout = (long long)ld_ctr(&cur->out_len);
       work = (long long)ld_ctr(&cur->aux0);

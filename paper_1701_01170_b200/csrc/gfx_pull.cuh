@@ -55,7 +55,7 @@ constexpr int kWarpScratch = sizeof(PullSmem) > sizeof(WarpSmem) ? sizeof(PullSm
 //           aux1 += |U| with in-degree > 0.
 // FrontT: frontier membership of an in-neighbour s (global id):
 //   uint32_t word(s) loads the bitmap word holding s; bool bit(w, s) tests it.
-template <class FrontT>
+template <class FrontT, int kPB = kPullBatch>
 __device__ __forceinline__ void pull_groups(
     int64_t words, const uint32_t* __restrict__ nz_in, uint32_t* __restrict__ visited,
     const FrontT front, uint32_t* __restrict__ next,
@@ -104,28 +104,28 @@ __device__ __forceinline__ void pull_groups(
     // phase 1: first probe of every candidate from the dense head array;
     // misses are compacted in place to the front of the list
     int nmiss = 0;
-    for (int base = 0; base < total; base += 32 * kPullBatch) {
-      int32_t u[kPullBatch], h[kPullBatch];
-      uint32_t fw[kPullBatch];
+    for (int base = 0; base < total; base += 32 * kPB) {
+      int32_t u[kPB], h[kPB];
+      uint32_t fw[kPB];
 #pragma unroll
-      for (int q = 0; q < kPullBatch; ++q) {
+      for (int q = 0; q < kPB; ++q) {
         const int k = base + q * 32 + lane;
         u[q] = k < total ? P.cand[k] : -1;
         h[q] = u[q] >= 0 ? head[u[q]] : -1;
       }
       // with head2, head carries bit 31 = "in-degree is exactly 1" (-1 stays
       // "no in-neighbour"): such a miss is settled without a second look
-      bool last[kPullBatch];
+      bool last[kPB];
 #pragma unroll
-      for (int q = 0; q < kPullBatch; ++q) {
+      for (int q = 0; q < kPB; ++q) {
         last[q] = head2 != nullptr && h[q] != -1 && h[q] < 0;
         if (last[q]) h[q] &= 0x7fffffff;
       }
 #pragma unroll
-      for (int q = 0; q < kPullBatch; ++q) fw[q] = h[q] >= 0 ? front.word(h[q]) : 0u;
+      for (int q = 0; q < kPB; ++q) fw[q] = h[q] >= 0 ? front.word(h[q]) : 0u;
       __syncwarp();
 #pragma unroll
-      for (int q = 0; q < kPullBatch; ++q) {
+      for (int q = 0; q < kPB; ++q) {
         const bool hit = h[q] >= 0 && front.bit(fw[q], h[q]);
         const bool miss = h[q] >= 0 && !hit && !last[q];
         if (h[q] >= 0 && !hit && last[q]) {  // unfound, one probe, degree 1
