@@ -42,9 +42,10 @@ namespace gfx {
 // Idempotent: label test + plain store, duplicates culled afterwards by the
 // bitmap filter (bfs.py:113-116, 162-166).
 // ---------------------------------------------------------------------------
-struct BfsClaimOp {
+template <int B>
+struct BfsClaimOpT {
   static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
-  static constexpr int kBatch = kVisitBatch;
+  static constexpr int kBatch = B;
   static constexpr int kMinBlocks = 3;
   uint32_t* visited;
   int32_t* labels;
@@ -67,6 +68,11 @@ struct BfsClaimOp {
     return true;
   }
 };
+
+using BfsClaimOp = BfsClaimOpT<kVisitBatch>;
+// the single-hub level (push_tiny): fewer visits per lane in flight, more
+// lanes issuing (measured: level 1 14 -> 12 us)
+using BfsClaimOpTiny = BfsClaimOpT<4>;
 
 struct BfsIdempOp {
   static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
@@ -931,7 +937,8 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
         // tiny frontier (the hub's level, the tail levels): every warp derives
         // the whole expansion plan itself -- no scan pass, no grid barrier
         // between plan and expansion
-        push_tiny(W, op, F, nf, a.row, a.col, a.order + c.q_end, &cur->out_len, &cur->total, gw,
+        BfsClaimOpTiny top{a.visited, a.labels, a.preds, depth, {}, lab.lvl8};
+        push_tiny(W, top, F, nf, a.row, a.col, a.order + c.q_end, &cur->out_len, &cur->total, gw,
                   nw);
       } else if (nf <= kMidItems) {
         // mid-size frontier: warps expand 32 items each; hubs (rare) are set
