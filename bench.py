@@ -49,6 +49,7 @@ def parse_args():
     ap.add_argument("--no-s27", action="store_true", help="skip the single-GPU scale-27 extra")
     ap.add_argument("--partitioned", action="store_true",
                     help="use the partitioned multi-GPU engine even at N=1 (default: N>1)")
+    ap.add_argument("--write-ref-cache", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--python-loop", action="store_true",
                     help="partitioned engine: drive the levels from Python (dist.bfs_partitioned) "
                          "instead of the native loop (gfx_dbfs_run)")
@@ -295,12 +296,9 @@ def run_ours(args, dist: Dist):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": f"bfs_do_rmat_s{args.scale}_ef{args.edge_factor}_src{args.source}",
-                   "scale": args.scale, "edge_factor": args.edge_factor, "seed": 0,
-                   "source": args.source, "direction": args.direction, "do_a": 1e-3,
-                   "do_b": 0.2, "n": n, "m": dg.num_edges, "E_r": e_r,
-                   "reached": st.reached, "parallelism": f"replicas{dist.world}" if dist.world > 1 else "1gpu",
-                   "l2": "inputs larger than L2 (CSR 2.2 GB vs 126 MB L2); per-BFS state re-initialised each step",
+        "config": workload_config(args, n, dg.num_edges, e_r, st.reached),
+        "run": {"parallelism": f"replicas{dist.world}" if dist.world > 1 else "1gpu",
+                   "l2": "per-BFS state re-initialised each step",
                    "graph_build_s": round(build_s, 3),
                    "stats_post_pass": "off in timed steps (E_r from a warm-up run)",
                    "level_loop": "device-resident cooperative kernel, K launches enqueued back to back",
@@ -370,14 +368,12 @@ def run_partitioned(args, dist: Dist):
         "n_gpus": P, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic",
-        "config": {"workload": f"bfs_do_rmat_s{args.scale}_ef{args.edge_factor}_src{args.source}",
-                   "scale": args.scale, "edge_factor": args.edge_factor, "seed": 0,
-                   "source": args.source, "direction": args.direction, "n": n, "m": m, "E_r": e_r,
-                   "parallelism": f"1d-cyclic-partition{P}",
+        "config": workload_config(args, n, m, e_r, run["reached"]),
+        "run": {"parallelism": f"1d-cyclic-partition{P}",
                    "exchange": "NCCL all_to_all(pair counts) + send/recv(dst,src pairs) push / "
                                "all_gather(frontier bitmaps) pull / allreduce(level counters)",
                    "level_loop": loop,
-                   "l2": "inputs larger than L2; per-BFS state re-initialised each step",
+                   "l2": "per-BFS state re-initialised each step",
                    "graph_build_s": round(build_s, 3)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": None,
@@ -453,6 +449,7 @@ def _partitioned_run(args, dist, scale: int, steps: int, warmup: int, with_1gpu:
         st = step()
     reached, deg = eng.reached_degree_sum()
     e_r = int(dist.sum(float(deg)))
+    reached = int(dist.sum(float(reached)))
     dist.barrier()
     torch.cuda.synchronize()
     l0 = _native.launch_count()
@@ -491,7 +488,8 @@ def _partitioned_run(args, dist, scale: int, steps: int, warmup: int, with_1gpu:
         ncomm.close()
     del eng, comm, lrow, lcol
     torch.cuda.empty_cache()
-    return {"st": st, "t_ms": t_ms, "e_r": e_r, "n": n, "m": m, "launches": launches,
+    return {"st": st, "t_ms": t_ms, "e_r": e_r, "reached": reached, "n": n, "m": m,
+            "launches": launches,
             "build_s": build_s, "one_gpu": one_gpu, "loop": loop, "e2e": e2e}
 
 
@@ -732,54 +730,179 @@ def cpu_baseline(args, dg, e_r):
 
 
 # ---------------------------------------------------------------------------
-# reference arm: the reference's CPU algorithm (oracle port) on host cores
+# reference arm: the UNMODIFIED reference (baseline/_ref) on the host cores
 # ---------------------------------------------------------------------------
-def run_reference(args, dist: Dist):
-    if dist.world > 1 and dist.rank != 0:
-        return
+REF_DIR = ROOT / "baseline" / "_ref"
+REF_BUDGET_S = float(os.environ.get("GFX_REF_BUDGET_S", "150"))
+
+
+def workload_config(args, n: int, m: int, e_r: int, reached: int) -> dict:
+    """The workload both arms report, key for key (same_config)."""
+    return {"workload": f"bfs_do_rmat_s{args.scale}_ef{args.edge_factor}_src{args.source}",
+            "scale": args.scale, "edge_factor": args.edge_factor, "seed": 0,
+            "source": args.source, "direction": args.direction, "do_a": 1e-3, "do_b": 0.2,
+            "n": int(n), "m": int(m), "E_r": int(e_r), "reached": int(reached),
+            "l2": "inputs larger than L2 (CSR 2.2 GB vs 126 MB L2)"}
+
+
+def write_reference_cache(args, path: str) -> None:
+    """Child process of the reference arm: build the input with the GPU
+    builder (input construction is untimed, reference bench.py:1-7) and write
+    it in the reference's own GFXCSR v1 format (io.py:121-159)."""
     import torch
 
-    from oracle import graphfx_port as port
     from paper_1701_01170_b200.generators import rmat_device_graph
+    from paper_1701_01170_b200.io import save_csr_cache_device
 
-    # input generation only (untimed, reference bench.py:1-7): the bit-exact
-    # GPU builder, downloaded to the reference's int64 host layout
-    torch.cuda.set_device(dist.local)
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
     dg = rmat_device_graph(args.scale, args.edge_factor, 0)
-    row, col = _host_graph(dg)
-    del dg
-    torch.cuda.empty_cache()
+    save_csr_cache_device(dg, path)
+
+
+def _sha(a) -> str:
+    import hashlib
+
     import numpy as np
 
-    deg = np.diff(row)
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
-    def one():
-        labels, _, _, _ = port.bfs(row, col, args.source, direction=args.direction,
-                                   rev=(row, col, None))
-        return labels
 
-    for _ in range(args.warmup):
-        labels = one()
-    e_r = int(deg[labels != port.UNVISITED].sum())
+def run_reference(args, dist: Dist):
+    """Times ``graphfx.bfs(g, source, direction, num_threads=cores)`` from the
+    pip-installed reference in baseline/_ref through its public API.  The input
+    is made by a CHILD process (GPU builder -> cache file) so this process
+    never loads libgfx; it is read with the reference's own
+    ``load_csr_cache`` and checked against the SHA-256 digests of the
+    reference-built CSR (tests/golden/rmat_s<S>.json).  Each step is one full
+    BFS; the timed steps stop once REF_BUDGET_S seconds are spent (at least
+    one), so the run ends in minutes -- ``steps`` reports how many ran."""
+    if dist.world > 1 and dist.rank != 0:
+        return
+    if not (REF_DIR / "graphfx" / "__init__.py").exists():
+        return run_reference_port(args, dist)
+    import numpy as np
+
+    shm = Path("/dev/shm") if Path("/dev/shm").is_dir() else Path("/tmp")
+    cache = shm / f"gfx_ref_rmat{args.scale}_{os.getpid()}.gfxcsr"
     t0 = time.perf_counter()
+    env = dict(os.environ)
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_WORLD_SIZE", "GROUP_RANK"):
+        env.pop(k, None)
+    subprocess.run([sys.executable, str(ROOT / "bench.py"), "--write-ref-cache", str(cache),
+                    "--scale", str(args.scale), "--edge-factor", str(args.edge_factor)],
+                   check=True, env=env, stdout=sys.stderr)
+    sys.path.insert(0, str(REF_DIR))
+    import graphfx
+
+    try:
+        g = graphfx.load_csr_cache(str(cache))
+    finally:
+        cache.unlink(missing_ok=True)
+    input_s = time.perf_counter() - t0
+    golden = ROOT / "tests" / "golden" / f"rmat_s{args.scale}.json"
+    verified = None
+    if golden.exists():
+        rec = json.loads(golden.read_text())
+        verified = (_sha(g.row_offsets) == rec["row_sha"] and _sha(g.column_indices) == rec["col_sha"])
+        if not verified:
+            raise RuntimeError("reference-arm input differs from the reference-built CSR digests")
+    cores = os.cpu_count() or 1
+    kw = dict(direction=args.direction, num_threads=cores)
+    t_pre = time.perf_counter()
+    g.csc()  # the reference's own preprocessing (bfs.py:72-74), untimed as in its bench
+    pre_s = time.perf_counter() - t_pre
+    r = None
+    for _ in range(max(1, min(args.warmup, 1))):
+        r = graphfx.bfs(g, args.source, **kw)
+    reached_mask = r.labels != graphfx.UNVISITED
+    deg = np.diff(g.row_offsets)
+    e_r = int(deg[reached_mask].sum())
+    reached = int(reached_mask.sum())
+    times = []
+    t_end = time.perf_counter() + REF_BUDGET_S
     for _ in range(args.steps):
-        one()
-    dt = (time.perf_counter() - t0) / args.steps
+        t = time.perf_counter()
+        graphfx.bfs(g, args.source, **kw)
+        times.append(time.perf_counter() - t)
+        if time.perf_counter() > t_end:
+            break
+    dt = sum(times) / len(times)
     v = e_r / dt / 1e9
+    so = [p for p in _mapped_objects() if "paper_1701_01170_b200" in p or "libgfx" in p]
     out = {"metric": "BFS GTEPS on R-MAT scale-24 ef16 (direction-optimized, source 0)",
-           "value": round(v, 6), "unit": "GTEPS", "n_gpus": dist.world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
-           "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-           "impl": "reference",
-           "config": {"workload": f"bfs_do_rmat_s{args.scale}_ef{args.edge_factor}_src{args.source}",
-                      "scale": args.scale, "edge_factor": args.edge_factor, "source": args.source,
-                      "direction": args.direction, "E_r": e_r},
-           "cpu_baseline": {"value": round(v, 6), "unit": "GTEPS", "cores": 1, "kind": "port",
-                            "sample": "full DO-BFS per step, oracle/graphfx_port.py (numpy "
-                                      "restatement of reference bfs.py), 1 thread"},
+           "value": round(v, 6), "unit": "GTEPS", "n_gpus": dist.world, "steps": len(times),
+           "steps_requested": args.steps, "warmup": 1, "ms_per_step": round(dt * 1e3, 3),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+           "data": "synthetic", "impl": "reference",
+           "config": workload_config(args, g.num_vertices, g.num_edges, e_r, reached),
+           "reference": {"package": f"graphfx {getattr(graphfx, '__version__', '?')} from "
+                                    f"{Path(graphfx.__file__).parent}",
+                         "call": f"graphfx.bfs(g, {args.source}, direction='{args.direction}', "
+                                 f"num_threads={cores})",
+                         "input": "child process: GPU builder -> GFXCSR v1 cache -> "
+                                  "graphfx.load_csr_cache",
+                         "input_sha_verified": verified, "input_s": round(input_s, 1),
+                         "csc_preprocess_s": round(pre_s, 1),
+                         "step_seconds": [round(x, 3) for x in times],
+                         "libgfx_mapped": so},
+           "cpu_baseline": {"value": round(v, 6), "unit": "GTEPS", "cores": cores,
+                            "kind": "reference",
+                            "sample": f"{len(times)} full DO-BFS runs of the reference package "
+                                      f"(1 Python thread + {cores}-thread gather pool)"},
            "e2e": {"value": round(v, 6), "unit": "GTEPS", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     emit(out)
+
+
+def _mapped_objects() -> list[str]:
+    try:
+        with open("/proc/self/maps") as f:
+            return sorted({ln.split()[-1] for ln in f if ln.rstrip().endswith(".so")})
+    except OSError:
+        return []
+
+
+def run_reference_port(args, dist: Dist):
+    """Fallback when baseline/_ref is absent: the oracle port (numpy
+    restatement of reference bfs.py), 1 thread, on a cache written by a child."""
+    import numpy as np
+
+    from oracle import graphfx_port as port
+
+    shm = Path("/dev/shm") if Path("/dev/shm").is_dir() else Path("/tmp")
+    cache = shm / f"gfx_ref_rmat{args.scale}_{os.getpid()}.gfxcsr"
+    subprocess.run([sys.executable, str(ROOT / "bench.py"), "--write-ref-cache", str(cache),
+                    "--scale", str(args.scale), "--edge-factor", str(args.edge_factor)],
+                   check=True, stdout=sys.stderr)
+    from paper_1701_01170_b200.io import load_csr_cache
+
+    g = load_csr_cache(cache)
+    cache.unlink(missing_ok=True)
+    row, col = g.row_offsets, g.column_indices
+    labels, _, _, _ = port.bfs(row, col, args.source, direction=args.direction,
+                               rev=(row, col, None))
+    mask = labels != port.UNVISITED
+    e_r = int(np.diff(row)[mask].sum())
+    times = []
+    t_end = time.perf_counter() + REF_BUDGET_S
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        port.bfs(row, col, args.source, direction=args.direction, rev=(row, col, None))
+        times.append(time.perf_counter() - t)
+        if time.perf_counter() > t_end:
+            break
+    dt = sum(times) / len(times)
+    v = e_r / dt / 1e9
+    emit({"metric": "BFS GTEPS on R-MAT scale-24 ef16 (direction-optimized, source 0)",
+          "value": round(v, 6), "unit": "GTEPS", "n_gpus": dist.world, "steps": len(times),
+          "warmup": 1, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
+          "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+          "impl": "reference",
+          "config": workload_config(args, len(row) - 1, len(col), e_r, int(mask.sum())),
+          "cpu_baseline": {"value": round(v, 6), "unit": "GTEPS", "cores": 1, "kind": "port",
+                           "sample": "full DO-BFS per step, oracle/graphfx_port.py, 1 thread"},
+          "e2e": {"value": round(v, 6), "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                  "d2h_bytes_per_step": 0}})
 
 
 _JSON_OUT = None
@@ -800,6 +923,8 @@ def main():
     sys.stdout.flush()
     _JSON_OUT = os.fdopen(os.dup(1), "w")
     os.dup2(2, 1)
+    if args.write_ref_cache:
+        return write_reference_cache(args, args.write_ref_cache)
     dist = Dist()
     if args.impl == "reference":
         run_reference(args, dist)

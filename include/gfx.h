@@ -189,21 +189,37 @@ GFX_API int gfx_segmented_intersect(gfx_graph* g, const int32_t* u_d, const int3
                             int64_t num_pairs, int32_t* counts_d, int64_t* total);
 
 /* ---- generic advance / filter with the closed device-functor registry ---
- * (reference operators.py:218-266, 360-384; SURVEY 8(b) functor table) */
+ * (reference operators.py:218-266, 360-384; SURVEY 8(b) functor table).
+ * Registry functors run fused inside the load-balanced expansion; arbitrary
+ * Python callables run staged on device tensors through the building blocks
+ * further below (gfx_scan_offsets / gfx_gather / gfx_select_i64 ...). */
 #define GFX_FN_NONE 0
-#define GFX_FN_BFS_CLAIM 1   /* bfs.py:118-121 */
-#define GFX_FN_BFS_IDEMP 2   /* bfs.py:113-116 */
-#define GFX_FN_SSSP_RELAX 3  /* sssp.py:95-103 */
-#define GFX_FN_TC_ORIENT 4   /* tc.py:57-59 */
-#define GFX_FN_LABEL_EQ 5    /* cond / vertex_cond labels[x] == value */
-#define GFX_FN_LABEL_NE 6    /* cond / vertex_cond labels[x] != value */
-#define GFX_FN_SET_LABEL 7   /* compute: labels[v] = value */
-#define GFX_FN_ADD_I64 8     /* compute: acc[v] += value (atomic_add, operators.py:127-128) */
+#define GFX_FN_BFS_CLAIM 1     /* bfs.py:118-121 compare_and_swap claim + preds[d] = s */
+#define GFX_FN_BFS_IDEMP 2     /* bfs.py:113-116 labels[d] == UNVISITED; _set_depth */
+#define GFX_FN_SSSP_RELAX 3    /* sssp.py:95-103 atomic_min winners + set_pred */
+#define GFX_FN_TC_ORIENT 4     /* tc.py:57-59 */
+#define GFX_FN_LABEL_EQ 5      /* cond / vertex_cond labels[x] == value */
+#define GFX_FN_LABEL_NE 6      /* cond / vertex_cond labels[x] != value */
+#define GFX_FN_SET_LABEL 7     /* compute: labels[v] = value */
+#define GFX_FN_ADD_I64 8       /* compute: acc[v] += value (atomic_add, operators.py:127-128) */
+#define GFX_FN_BFS_PULL 9      /* bfs.py:142-145 pull cond labels[s] == value-1; _set_depth */
+#define GFX_FN_BC_CLAIM 10     /* bc.py:80-84 compare_and_swap(labels, d, UNVISITED, depth) */
+#define GFX_FN_BC_SIGMA 11     /* bc.py:87-92 labels[d] == value; sigma[d] += sigma[s] */
+#define GFX_FN_BC_DELTA 12     /* bc.py:104-109 labels[d] == value;
+                                  delta[s] += sigma[s]/sigma[d]*(1+delta[d]) */
+#define GFX_FN_PR_SCATTER 13   /* pagerank.py:71-75 rank_next[d] += scalar*rank[s]/outdeg[s] */
+#define GFX_FN_PR_MOVED 14     /* pagerank.py:81-85 vertex_cond |rank_next-rank| >= scalar */
+#define GFX_FN_CC_SAME_COMP 15 /* cc.py:55-58 edge vertex_cond comp[src(e)] != comp[col[e]] */
+#define GFX_FN_SSSP_STAMP 16   /* sssp.py:112-115 vertex_cond stamps[v] == value */
+#define GFX_FN_COUNT 17
 
 typedef struct gfx_functor_args {
-  int32_t* labels_d;   /* int32 labels / distances */
+  int32_t* labels_d;   /* int32 labels / distances / comp / stamps */
   int32_t* preds_d;    /* int32 preds (may be NULL) */
   int64_t value;       /* depth / compared value */
+  double* f0_d;        /* BC sigma / PR rank */
+  double* f1_d;        /* BC delta / PR rank_next */
+  double scalar;       /* PR damping (scatter) / epsilon (moved) */
 } gfx_functor_args;
 
 #define GFX_KIND_V2V 0
@@ -217,15 +233,98 @@ typedef struct gfx_functor_args {
 GFX_API int gfx_advance(gfx_graph* g, const int32_t* fin_d, int64_t nin, int kind,
                 int functor_id, const gfx_functor_args* args, int32_t* fout_d,
                 int64_t fout_cap, int64_t* nout, int64_t* edges);
+/* advance_filter_fused (operators.py:392-456): ONE load-balanced expansion
+ * that evaluates the registry cond, the registry vertex_cond on the image and
+ * culls re-occurrences against a bitmap over the output domain (n or m), so
+ * every survivor is emitted once and no middle frontier exists. */
+GFX_API int gfx_advance_fused(gfx_graph* g, const int32_t* fin_d, int64_t nin, int kind,
+                              int cond_id, const gfx_functor_args* cond_args, int vcond_id,
+                              const gfx_functor_args* vcond_args, int32_t* fout_d,
+                              int64_t fout_cap, int64_t* nout, int64_t* edges);
+/* pull_expand with a registry functor (operators.py:269-307, direction.py:73-89):
+ * for each unvisited u in fin_d (in order), probe its in-neighbours s in
+ * reverse-adjacency order and stop at the first cond-true triple; for
+ * GFX_FN_BFS_PULL the hit commits labels[u] = value, preds[u] = s.  The input
+ * is split stably into active_d (a hit) and rest_d (no hit); *edges gets the
+ * probes made (the early-exit count S(U)). */
+GFX_API int gfx_pull_advance(gfx_graph* g, const int32_t* fin_d, int64_t nin, int functor_id,
+                             const gfx_functor_args* args, int32_t* active_d, int64_t* nactive,
+                             int32_t* rest_d, int64_t* nrest, int64_t* edges);
 /* Filter: keep items satisfying vertex functor, then (EXACT) dedup to the
  * sorted unique set of survivors (np.unique semantics) or (INEXACT) cull. */
 GFX_API int gfx_filter(gfx_graph* g, const int32_t* fin_d, int64_t nin, int mode,
                int functor_id, const gfx_functor_args* args, int64_t domain,
                int32_t* fout_d, int64_t* nout);
+/* mask_d[i] = registry vertex_cond(fin_d[i]) (INEXACT filtering runs the
+ * culling stages over the survivors) */
+GFX_API int gfx_vertex_mask(gfx_graph* g, const int32_t* fin_d, int64_t nin, int functor_id,
+                            const gfx_functor_args* args, uint8_t* mask_d);
 /* compute (operators.py:528-533): apply a registry functor to every item,
  * multiplicity included (acc_d: int64 array for GFX_FN_ADD_I64) */
 GFX_API int gfx_compute(gfx_graph* g, const int32_t* fin_d, int64_t nin, int functor_id,
                         const gfx_functor_args* args, int64_t* acc_d);
+
+/* ---- building blocks of the staged operator path (Python callables as
+ * functors, evaluated on device tensors between these calls) ------------- */
+/* compute_scan_offsets (load_balance.py:94-113): scan_d int64[nin+1] is the
+ * exclusive prefix sum of the expansion degrees of fin_d (vertex ids, or edge
+ * ids whose head col[e] expands when edge_input); reverse: in-degrees. */
+GFX_API int gfx_scan_offsets(gfx_graph* g, const int32_t* fin_d, int64_t nin, int edge_input,
+                             int reverse, int64_t* scan_d, int64_t* total);
+/* _gather (operators.py:161-197): every expansion slot k in slot order.  Item
+ * i owns slots [scan[i], scan[i+1]); its vertex v expands slot j = row[v] +
+ * k - scan[i]: a_d[k] = v, b_d[k] = col[j], e_d[k] = j.  reverse: the reverse
+ * adjacency (gfx_graph_build_csc), e_d[k] = the forward slot of the in-edge.
+ * rep_d[k] = i (nullable). */
+GFX_API int gfx_gather(gfx_graph* g, const int32_t* fin_d, int64_t nin, int edge_input,
+                       int reverse, const int64_t* scan_d, int64_t total, int64_t* a_d,
+                       int64_t* b_d, int64_t* e_d, int32_t* rep_d);
+/* CsrGraph.csc (graph.py:113-126) on the device: rrow_d int64[n+1], rcol_d
+ * int32[m] (sources, ascending within a row) and reid_d int64[m] (forward
+ * slot of each in-edge), from a stable radix sort of the column ids; the
+ * result is attached to the graph as its reverse adjacency. */
+GFX_API int gfx_graph_build_csc(gfx_graph* g, int64_t* rrow_d, int32_t* rcol_d, int64_t* reid_d);
+/* stable stream compaction: out_d = in_d[flags_d != invert] (order kept) */
+GFX_API int gfx_select_i64(gfx_ctx* ctx, const int64_t* in_d, const uint8_t* flags_d, int64_t n,
+                           int invert, int64_t* out_d, int64_t* nout);
+/* StatusBitmap.test_and_set (frontier.py:70-94): fresh_d[i] = bit ids[i]
+ * clear before the call (reads precede writes), then every bit is set */
+GFX_API int gfx_bitmap_test_and_set(gfx_ctx* ctx, uint32_t* words_d, const int64_t* ids_d,
+                                    int64_t k, uint8_t* fresh_d);
+/* generate_unvisited_frontier (frontier.py:97-100): ascending ids with
+ * labels[v] == sentinel (dtype 0 int32, 1 int64) */
+GFX_API int gfx_unvisited(gfx_ctx* ctx, int dtype, const void* labels_d, int64_t n,
+                          int64_t sentinel, int64_t* out_d, int64_t* nout);
+/* hits_d[rep_d[k]] = 1 for every k with mask_d[k] (pull_expand hit marking) */
+GFX_API int gfx_mark_items(gfx_ctx* ctx, const uint8_t* mask_d, const int32_t* rep_d, int64_t k,
+                           uint8_t* hits_d);
+/* INEXACT culling (operators.py:315-357), reproduced exactly: keep_d[i] = 0
+ * for items the reference heuristics drop.  Bitmask: an item is kept iff no
+ * earlier batch of bitmask_batch items held its id; history tables: within
+ * each batch an item is dropped when the previous item of the batch hashing
+ * to its slot (id mod table) carried the same id.  Pass table 0 to skip a
+ * stage.  Stages run in the reference order, each over the survivors of the
+ * previous one, so the caller compacts between stages (stage = 0, 1, 2). */
+GFX_API int gfx_cull_stage(gfx_ctx* ctx, const int64_t* items_d, int64_t n, int stage,
+                           int64_t domain, int64_t table_or_batch, int64_t batch,
+                           uint8_t* keep_d);
+
+/* ---- batched atomic helpers (operators.py:111-153) on device arrays -----
+ * dtype: 0 int32, 1 int64, 2 float32, 3 float64.  idx_d int64[k]. */
+/* scatter-min; won_d[i] = vals[i] < pre[idx[i]] && vals[i] == post[idx[i]] */
+GFX_API int gfx_atomic_min(gfx_ctx* ctx, int dtype, void* arr_d, const int64_t* idx_d,
+                           const void* vals_d, int64_t k, uint8_t* won_d, void* pre_d);
+/* scatter-add (np.add.at); vals_d NULL adds the scalar */
+GFX_API int gfx_atomic_add(gfx_ctx* ctx, int dtype, void* arr_d, const int64_t* idx_d,
+                           const void* vals_d, double scalar, int64_t k);
+/* first-claim-wins conditional store: among entries with arr[idx] ==
+ * expected (pre-call state) the earliest occurrence of each index wins and
+ * stores vals[i] (or the scalar when vals_d is NULL); pos_d: int64 scratch
+ * over the array (n entries) */
+GFX_API int gfx_compare_and_swap(gfx_ctx* ctx, int dtype, void* arr_d, const int64_t* idx_d,
+                                 int64_t k, int64_t expected, const void* vals_d, int64_t scalar,
+                                 uint8_t* won_d, int64_t* pos_d);
+
 /* intersection elements per pair, in pair order, ascending within a pair
  * (IntersectResult.intersections); offsets_d = exclusive scan of counts */
 GFX_API int gfx_segmented_intersect_list(gfx_graph* g, const int32_t* u_d, const int32_t* v_d,

@@ -355,3 +355,45 @@ def tc(row, col):
         if len(a) and len(b):
             counts[i] = len(np.intersect1d(a, b, assume_unique=True))
     return int(counts.sum()), counts, osrc, odst
+
+
+# ---------------------------------------------------------------------------
+# INEXACT filter culling: operators.py:315-357
+# ---------------------------------------------------------------------------
+def cull_inexact(items, use_bitmask=True, team_table_size=256, local_table_size=64,
+                 bitmask_batch=1024, local_batch=32, domain_size=None):
+    """operators.py:344-357 (_apply_culling): bitmask over the domain where a
+    batch reads the seen bits before marking them (:315-322), then the
+    direct-mapped team and local history tables (:325-341), each stage over
+    the previous stage's survivors."""
+    items = np.asarray(items, dtype=np.int64)
+    if len(items) == 0:
+        return items
+    if use_bitmask:
+        seen = np.zeros(domain_size or int(items.max()) + 1, dtype=bool)
+        keep = np.ones(len(items), dtype=bool)
+        for lo in range(0, len(items), bitmask_batch):
+            chunk = items[lo:lo + bitmask_batch]
+            keep[lo:lo + bitmask_batch] = ~seen[chunk]
+            seen[chunk] = True
+        items = items[keep]
+
+    def history(items, table, batch):
+        keep = np.ones(len(items), dtype=bool)
+        for lo in range(0, len(items), batch):
+            chunk = items[lo:lo + batch]
+            slots = chunk % table
+            order = np.argsort(slots, kind="stable")
+            s, v = slots[order], chunk[order]
+            dup = np.zeros(len(chunk), dtype=bool)
+            dup[1:] = (s[1:] == s[:-1]) & (v[1:] == v[:-1])
+            sub = np.ones(len(chunk), dtype=bool)
+            sub[order] = ~dup
+            keep[lo:lo + batch] = sub
+        return items[keep]
+
+    if team_table_size:
+        items = history(items, team_table_size, team_table_size)
+    if local_table_size:
+        items = history(items, local_table_size, local_batch)
+    return items

@@ -23,7 +23,8 @@ FILTER_EXACT, FILTER_INEXACT = 0, 1
 LOOP_HOST, LOOP_DEVICE = 0, 1
 
 (FN_NONE, FN_BFS_CLAIM, FN_BFS_IDEMP, FN_SSSP_RELAX, FN_TC_ORIENT, FN_LABEL_EQ, FN_LABEL_NE,
- FN_SET_LABEL, FN_ADD_I64) = range(9)
+ FN_SET_LABEL, FN_ADD_I64, FN_BFS_PULL, FN_BC_CLAIM, FN_BC_SIGMA, FN_BC_DELTA, FN_PR_SCATTER,
+ FN_PR_MOVED, FN_CC_SAME_COMP, FN_SSSP_STAMP) = range(17)
 KIND_V2V, KIND_V2E, KIND_E2V, KIND_E2E = range(4)
 
 
@@ -57,7 +58,8 @@ class DbfsComm(Structure):
 
 
 class FunctorArgs(Structure):
-    _fields_ = [("labels_d", c_void_p), ("preds_d", c_void_p), ("value", c_int64)]
+    _fields_ = [("labels_d", c_void_p), ("preds_d", c_void_p), ("value", c_int64),
+                ("f0_d", c_void_p), ("f1_d", c_void_p), ("scalar", c_double)]
 
 
 # name -> (restype, argtypes); every function listed here is declared in gfx.h
@@ -96,6 +98,33 @@ _SIGS = {
                                         POINTER(c_int64)]),
     "gfx_advance": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, POINTER(FunctorArgs),
                             c_void_p, c_int64, POINTER(c_int64), POINTER(c_int64)]),
+    "gfx_advance_fused": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, POINTER(FunctorArgs),
+                                  c_int, POINTER(FunctorArgs), c_void_p, c_int64,
+                                  POINTER(c_int64), POINTER(c_int64)]),
+    "gfx_pull_advance": (c_int, [c_void_p, c_void_p, c_int64, c_int, POINTER(FunctorArgs),
+                                 c_void_p, POINTER(c_int64), c_void_p, POINTER(c_int64),
+                                 POINTER(c_int64)]),
+    "gfx_vertex_mask": (c_int, [c_void_p, c_void_p, c_int64, c_int, POINTER(FunctorArgs),
+                                c_void_p]),
+    "gfx_scan_offsets": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_void_p,
+                                 POINTER(c_int64)]),
+    "gfx_gather": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_void_p, c_int64,
+                           c_void_p, c_void_p, c_void_p, c_void_p]),
+    "gfx_graph_build_csc": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "gfx_select_i64": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int, c_void_p,
+                               POINTER(c_int64)]),
+    "gfx_mark_items": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
+    "gfx_bitmap_test_and_set": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
+    "gfx_unvisited": (c_int, [c_void_p, c_int, c_void_p, c_int64, c_int64, c_void_p,
+                              POINTER(c_int64)]),
+    "gfx_cull_stage": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int64, c_int64, c_int64,
+                               c_void_p]),
+    "gfx_atomic_min": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
+                               c_void_p]),
+    "gfx_atomic_add": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_double,
+                               c_int64]),
+    "gfx_compare_and_swap": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_int64, c_int64,
+                                     c_void_p, c_int64, c_void_p, c_void_p]),
     "gfx_filter": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, POINTER(FunctorArgs),
                            c_int64, c_void_p, POINTER(c_int64)]),
     "gfx_compute": (c_int, [c_void_p, c_void_p, c_int64, c_int, POINTER(FunctorArgs), c_void_p]),

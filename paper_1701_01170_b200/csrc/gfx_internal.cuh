@@ -89,6 +89,7 @@ struct gfx_graph {
   const int32_t* w = nullptr;
   const int64_t* rrow = nullptr;  // reverse adjacency (== row/col if undirected)
   const int32_t* rcol = nullptr;
+  const int64_t* reid = nullptr;  // forward slot of each reverse slot (gfx_graph_build_csc)
   int flags = 0;
   int64_t max_deg = 0;
   int64_t nnz_vertices = 0;       // vertices with out-degree > 0

@@ -218,6 +218,7 @@ class DeviceGraph:
                      _native.ptr(row), _native.ptr(col), _native.ptr(w),
                      _native.GRAPH_UNDIRECTED if undirected else 0, ctypes.byref(h))
         self.handle = h
+        self._csc_dev = None
         if not undirected and rrow is not None:
             _native.call("gfx_graph_set_reverse", h, _native.ptr(rrow), _native.ptr(rcol))
         self.max_degree = int(_native.load_library().gfx_graph_max_degree(h))
@@ -291,6 +292,7 @@ class DeviceGraph:
                              "DeviceGraph instead")
         self.row.copy_(row_h, non_blocking=True)
         self.col.copy_(col_h, non_blocking=True)
+        self._csc_dev = None  # stale reverse edge ids (the handle's reid)
         _native.call("gfx_graph_refresh", self.handle)
 
     def refresh_weights(self, w) -> None:
@@ -312,7 +314,27 @@ class DeviceGraph:
             _native.call("gfx_graph_set_reverse", h, _native.ptr(self.rrow),
                          _native.ptr(self.rcol))
         self.handle = h
+        self._csc_dev = None
         _native.load_library().gfx_graph_destroy(old)
+
+    def ensure_csc(self):
+        """Reverse adjacency with edge ids on the device (CsrGraph.csc,
+        graph.py:113-126): (rrow int64[n+1], rcol int32[m], reid int64[m]),
+        built once by a stable radix sort of the column ids and attached to
+        the handle (pull operators with callable functors need reid)."""
+        import torch
+
+        if getattr(self, "_csc_dev", None) is None:
+            dev = self.row.device
+            rrow = torch.empty(self.num_vertices + 1, dtype=torch.int64, device=dev)
+            rcol = torch.empty(max(self.num_edges, 1), dtype=torch.int32, device=dev)
+            reid = torch.empty(max(self.num_edges, 1), dtype=torch.int64, device=dev)
+            _native.call("gfx_graph_build_csc", self.handle, _native.ptr(rrow), _native.ptr(rcol),
+                         _native.ptr(reid))
+            self._csc_dev = (rrow, rcol, reid)
+            if not self.undirected:
+                self.rrow, self.rcol = rrow, rcol
+        return self._csc_dev
 
     def degrees(self):
         return self.row[1:] - self.row[:-1]

@@ -91,6 +91,11 @@ def test_filter_exact_is_sorted_unique():
     labels = torch.from_numpy((np.arange(500) % 3).astype(np.int32)).cuda()
     fs = gfx.FunctorSet(vertex_cond=gfx.functors.label_eq(labels, 1))
     out = gfx.filter_frontier(gfx.Frontier.from_items(items), gfx.FilterMode.INEXACT, fs)
+    # INEXACT: the reference culling heuristics exactly (input order kept)
+    from oracle import graphfx_port as port
+
+    assert out.to_array().tolist() == port.cull_inexact(items[items % 3 == 1]).tolist()
+    out = gfx.filter_frontier(gfx.Frontier.from_items(items), gfx.FilterMode.EXACT, fs)
     assert out.to_array().tolist() == np.unique(items[items % 3 == 1]).tolist()
 
 
