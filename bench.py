@@ -407,6 +407,7 @@ def _partitioned_run(args, dist, scale: int, steps: int, warmup: int, with_1gpu:
 
     P, r = dist.world, dist.rank
     torch.cuda.empty_cache()
+    ref_labels = None
     t_build = time.perf_counter()
     dg = rmat_device_graph(scale, args.edge_factor, 0)
     n, m = dg.num_vertices, dg.num_edges
@@ -420,7 +421,8 @@ def _partitioned_run(args, dist, scale: int, steps: int, warmup: int, with_1gpu:
             st1 = bfs_device(dg, args.source, direction=args.direction, labels=lab, preds=prd)[2]
         ms1 = bfs_batch(dg, [args.source] * 5, direction=args.direction, labels=lab, preds=prd) / 5
         one_gpu = {"gteps": round(st1.edges_reached / (ms1 * 1e-3) / 1e9, 2), "ms": round(ms1, 4)}
-        del lab, prd
+        ref_labels = lab  # kept: the partitioned labels are checked against it below
+        del prd
     lrow, lcol = partition_graph(dg, P, r)
     del dg
     torch.cuda.empty_cache()
@@ -463,6 +465,11 @@ def _partitioned_run(args, dist, scale: int, steps: int, warmup: int, with_1gpu:
     launches = _native.launch_count() - l0
     dist.barrier()
     t_ms = dist.max(ev0.elapsed_time(ev1))
+    if with_1gpu:
+        match = _labels_match(eng, ref_labels if r == 0 else None, P, r, n)
+        if one_gpu is not None:
+            one_gpu["labels_equal_partitioned"] = match
+        ref_labels = None
     # end to end with the graph resident: the source goes up, every rank's
     # labels + preds come back to pinned host memory, each step
     lab_h = torch.empty(eng.nl, dtype=torch.int32, pin_memory=True)
@@ -491,6 +498,30 @@ def _partitioned_run(args, dist, scale: int, steps: int, warmup: int, with_1gpu:
     return {"st": st, "t_ms": t_ms, "e_r": e_r, "reached": reached, "n": n, "m": m,
             "launches": launches,
             "build_s": build_s, "one_gpu": one_gpu, "loop": loop, "e2e": e2e}
+
+
+def _labels_match(eng, ref_labels, P: int, r: int, n: int):
+    """labels(P) == labels(1): every rank's owned labels
+    (cyclic: local l is global l*P + r) gathered to rank 0 and compared with
+    the single-GPU labels of the same graph."""
+    import torch
+
+    nlmax = (n + P - 1) // P
+    buf = torch.full((nlmax,), -2, dtype=torch.int32, device=eng.device)
+    buf[: eng.nl] = eng.labels[: eng.nl]
+    parts = [buf]
+    if P > 1:
+        import torch.distributed as tdist
+
+        parts = [torch.empty_like(buf) for _ in range(P)]
+        tdist.all_gather(parts, buf)
+    if r != 0:
+        return None
+    ok = True
+    for q in range(P):
+        want = ref_labels[q::P]
+        ok = ok and bool(torch.equal(parts[q][: want.numel()], want))
+    return ok
 
 
 def extras(args, dg, labels, preds, dist, peak):

@@ -401,6 +401,34 @@ GFX_API int gfx_dbfs_commit(gfx_dbfs* db, int64_t nf_local);
  * trace; stats the totals (edges_traversed = push slots, bytes_alg,
  * device_ms = CUDA-event time of the whole BFS on this rank). */
 typedef struct gfx_nccl gfx_nccl;
+/* ---- partitioned near/far SSSP (reference sssp.py:41-121,
+ * near_far.py:20-85) --------------------------------------------------------
+ * Same 1D cyclic partition as the BFS engine.  Per iteration the host calls
+ * relax (expand the local near queue; owned targets relaxed in place, remote
+ * ones bucketed as (d, dist<<32|pred) messages of 2 words, send_counts in
+ * words), exchanges counts then messages (all_to_all), apply (owners relax
+ * the received offers), split (touched -> near / far at the GLOBAL
+ * threshold; stats[0..3] = near, far, slots, touched, copied to stats[4..7]
+ * for the allreduce).  When the global near count is 0 and far is not,
+ * every rank calls refar(threshold + delta, 1, far_local).  Nothing
+ * synchronises the host inside relax / apply / split / refar. */
+typedef struct gfx_dsssp gfx_dsssp;
+GFX_API int gfx_dist_partition_weights(gfx_graph* g, int P, int r, const int64_t* lrow_d,
+                                       int32_t* lw_d);
+GFX_API int gfx_dsssp_create(gfx_ctx* ctx, int64_t n, int P, int r, const int64_t* lrow_d,
+                             const int32_t* lcol_d, const int32_t* lw_d, int64_t n_local,
+                             int64_t m_local, gfx_dsssp** out);
+GFX_API int gfx_dsssp_destroy(gfx_dsssp* ds);
+GFX_API int gfx_dsssp_bind(gfx_dsssp* ds, void* send_d, int64_t send_cap_words, void* recv_d,
+                           int64_t recv_cap_words, int64_t* send_counts_d, int64_t* stats_d);
+GFX_API int gfx_dsssp_reset(gfx_dsssp* ds, int64_t source, int64_t* near_local);
+GFX_API int gfx_dsssp_relax(gfx_dsssp* ds);
+GFX_API int gfx_dsssp_apply(gfx_dsssp* ds, int64_t nrecv_words);
+GFX_API int gfx_dsssp_split(gfx_dsssp* ds, double threshold);
+GFX_API int gfx_dsssp_refar(gfx_dsssp* ds, double threshold, int split, int64_t far_local);
+/* local distances (INT32_MAX unreached) and global preds of the owned vertices */
+GFX_API int gfx_dsssp_result(gfx_dsssp* ds, int32_t* dist_d, int32_t* preds_d);
+
 /* resolve NCCL from the library already loaded in the process (path: its
  * file, e.g. torch's nvidia/nccl/lib/libnccl.so.2; NULL: by soname) */
 GFX_API int gfx_nccl_load(const char* path);

@@ -150,6 +150,18 @@ _SIGS = {
     "gfx_dbfs_pull_prepare": (c_int, [c_void_p]),
     "gfx_dbfs_pull": (c_int, [c_void_p, c_int32]),
     "gfx_dbfs_commit": (c_int, [c_void_p, c_int64]),
+    "gfx_dist_partition_weights": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p]),
+    "gfx_dsssp_create": (c_int, [c_void_p, c_int64, c_int, c_int, c_void_p, c_void_p, c_void_p,
+                                 c_int64, c_int64, POINTER(c_void_p)]),
+    "gfx_dsssp_destroy": (c_int, [c_void_p]),
+    "gfx_dsssp_bind": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_void_p,
+                               c_void_p]),
+    "gfx_dsssp_reset": (c_int, [c_void_p, c_int64, POINTER(c_int64)]),
+    "gfx_dsssp_relax": (c_int, [c_void_p]),
+    "gfx_dsssp_apply": (c_int, [c_void_p, c_int64]),
+    "gfx_dsssp_split": (c_int, [c_void_p, c_double]),
+    "gfx_dsssp_refar": (c_int, [c_void_p, c_double, c_int, c_int64]),
+    "gfx_dsssp_result": (c_int, [c_void_p, c_void_p, c_void_p]),
     "gfx_nccl_load": (c_int, [c_char_p]),
     "gfx_nccl_unique_id": (c_int, [c_void_p]),
     "gfx_nccl_comm_create": (c_int, [c_void_p, c_int, c_int, c_void_p, POINTER(c_void_p)]),

@@ -16,6 +16,7 @@
 // bit-identical; heavier rows use a warp reduction (rel <= 1e-5, north_star).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <vector>
 
 #include "gfx_device.cuh"
@@ -129,9 +130,10 @@ __global__ void __launch_bounds__(256)
 // Push forms, used on undirected graphs for a level whose neighbour level
 // has fewer slots than the level itself (the load-balanced expansion then
 // splits hubs across warps).  Forward: sigma values are path counts --
-// integers held exactly in fp64 -- so the atomic sums are exact in any
-// order.  Backward: the atomic fp64 sums are order-dependent in the last
-// bits only (north_star tolerance rel <= 1e-5).
+// integers held exactly in fp64 (< 2^53) -- so the atomic sums are exact in
+// any order and the result is deterministic.  Backward: the atomic fp64
+// sums are order-dependent in the last bits, so the delta push is OFF by
+// default (GFX_BC_DELTA_PUSH=1 turns it on) and every delta is gathered.
 struct SigmaPushOp {
   static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
   static constexpr int kBatch = kVisitBatch;
@@ -211,6 +213,11 @@ extern "C" int gfx_bc(gfx_graph* g, const int64_t* sources, int64_t num_sources,
   GFX_TRY(scratch_t(g, "q_rowbase", n + 1, &rowbase));
   GFX_TRY(scratch_t(g, "q_part", part_capacity(g->m, g->n), &part));
   Counters* pc = g->counters + 2;  // push plans (C[2], C[3])
+  // the backward push adds fp64 terms with atomics (order-dependent last
+  // bits): off by default so BC values are bit-reproducible run to run;
+  // GFX_BC_DELTA_PUSH=1 re-enables it (diagnostic)
+  const char* dp = std::getenv("GFX_BC_DELTA_PUSH");
+  const bool delta_push = dp && dp[0] == '1';
   int64_t iterations = 0, edges = 0;
   std::vector<int64_t> off;
   GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
@@ -250,7 +257,7 @@ extern "C" int gfx_bc(gfx_graph* g, const int64_t* sources, int64_t num_sources,
     for (int64_t d = L - 2; d >= 1; --d) {
       const int64_t cnt = off[d + 1] - off[d];
       if (cnt <= 0) continue;
-      if (undirected && d + 1 < (int64_t)slots.size() && slots[d + 1] < slots[d] &&
+      if (delta_push && undirected && d + 1 < (int64_t)slots.size() && slots[d + 1] < slots[d] &&
           off[d + 2] > off[d + 1]) {
         GFX_TRY(push_from(d + 1, DeltaPushOp{labels, sigma, delta, (int32_t)d, {}}));
         continue;

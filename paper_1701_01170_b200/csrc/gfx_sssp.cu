@@ -27,6 +27,7 @@
 #include "gfx_device.cuh"
 #include "gfx_expand.cuh"
 #include "gfx_internal.cuh"
+#include "gfx_sssp.cuh"
 
 namespace gfx {
 
@@ -103,133 +104,6 @@ __global__ void k_sssp_seed(unsigned long long* dp, uint32_t* dist, int32_t src,
   dp[src] = 0xFFFFFFFFull;  // dist 0, pred -1
   dist[src] = 0u;
   near[0] = src;
-}
-
-// Block-staged appends for the near / far piles: each CTA collects its
-// items in shared memory (block-local atomics) and appends them to the
-// global pile with ONE atomicAdd per flush, instead of two same-address
-// global atomics per warp and tile.
-constexpr int kPileStage = 2048;
-struct PileStage {
-  int32_t nv[kPileStage];
-  int32_t fv[kPileStage], fk[kPileStage];
-  int nn, nfar;
-  unsigned long long base;
-};
-
-__device__ __forceinline__ void pile_flush(PileStage& S, int32_t* __restrict__ near,
-                                           unsigned long long* __restrict__ near_len,
-                                           int32_t* __restrict__ far, int32_t* __restrict__ far_key,
-                                           unsigned long long* __restrict__ far_len) {
-  __syncthreads();
-  if (threadIdx.x == 0) S.base = S.nn ? atomicAdd(near_len, (unsigned long long)S.nn) : 0ull;
-  __syncthreads();
-  for (int i = threadIdx.x; i < S.nn; i += blockDim.x) near[S.base + i] = S.nv[i];
-  __syncthreads();
-  if (threadIdx.x == 0) S.base = S.nfar ? atomicAdd(far_len, (unsigned long long)S.nfar) : 0ull;
-  __syncthreads();
-  for (int i = threadIdx.x; i < S.nfar; i += blockDim.x) {
-    far[S.base + i] = S.fv[i];
-    far_key[S.base + i] = S.fk[i];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) S.nn = S.nfar = 0;
-  __syncthreads();
-}
-
-// split the improved vertices against the threshold (near_far.py:40-57)
-__global__ void __launch_bounds__(256)
-    k_sssp_split(const int32_t* __restrict__ touched, const unsigned long long* __restrict__ n_d,
-                 const uint32_t* __restrict__ dist, uint32_t* __restrict__ mark, double threshold,
-                 int32_t* __restrict__ near, unsigned long long* __restrict__ near_len,
-                 int32_t* __restrict__ far, int32_t* __restrict__ far_key,
-                 unsigned long long* __restrict__ far_len) {
-  __shared__ PileStage S;
-  const int64_t n = (int64_t)*n_d;
-  if (threadIdx.x == 0) S.nn = S.nfar = 0;
-  __syncthreads();
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n;
-       base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = base + threadIdx.x;
-    if (i < n) {
-      const int32_t v = touched[i];
-      const int32_t key = (int32_t)dist[v];
-      atomicAnd(&mark[v >> 5], ~(1u << (v & 31)));  // re-arm for the next iteration
-      if ((double)key < threshold) {
-        S.nv[atomicAdd(&S.nn, 1)] = v;
-      } else {
-        const int at = atomicAdd(&S.nfar, 1);
-        S.fv[at] = v;
-        S.fk[at] = key;
-      }
-    }
-    __syncthreads();
-    if (S.nn > kPileStage - (int)blockDim.x || S.nfar > kPileStage - (int)blockDim.x)
-      pile_flush(S, near, near_len, far, far_key, far_len);
-  }
-  pile_flush(S, near, near_len, far, far_key, far_len);
-}
-
-// advance_bucket (near_far.py:68-85): drop stale far entries, split the rest
-// against the new threshold.  With split == false only the stale drop runs
-// (capacity compaction; everything fresh stays far).
-__global__ void __launch_bounds__(256)
-    k_sssp_refar(const int32_t* __restrict__ far, const int32_t* __restrict__ far_key, int64_t n,
-                 const uint32_t* __restrict__ dist, double threshold, int split,
-                 int32_t* __restrict__ near, unsigned long long* __restrict__ near_len,
-                 int32_t* __restrict__ far2, int32_t* __restrict__ far2_key,
-                 unsigned long long* __restrict__ far2_len) {
-  __shared__ PileStage S;
-  if (threadIdx.x == 0) S.nn = S.nfar = 0;
-  __syncthreads();
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n;
-       base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = base + threadIdx.x;
-    if (i < n) {
-      const int32_t v = far[i];
-      const int32_t key = far_key[i];
-      if ((int32_t)dist[v] == key) {  // fresh
-        if (split && (double)key < threshold) {
-          S.nv[atomicAdd(&S.nn, 1)] = v;
-        } else {
-          const int at = atomicAdd(&S.nfar, 1);
-          S.fv[at] = v;
-          S.fk[at] = key;
-        }
-      }
-    }
-    __syncthreads();
-    if (S.nn > kPileStage - (int)blockDim.x || S.nfar > kPileStage - (int)blockDim.x)
-      pile_flush(S, near, near_len, far2, far2_key, far2_len);
-  }
-  pile_flush(S, near, near_len, far2, far2_key, far2_len);
-}
-
-// (dist | pred) words -> the two int32 outputs; two vertices per thread with
-// 16-byte loads and 8-byte stores when the outputs are 8-byte aligned
-__global__ void k_sssp_unpack(const unsigned long long* __restrict__ dp, int64_t n,
-                              int32_t* __restrict__ dist, int32_t* __restrict__ preds, int vec) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t done = 0;
-  if (vec) {
-    const int64_t pairs = n >> 1;
-    for (int64_t p = t0; p < pairs; p += stride) {
-      const ulonglong2 x = reinterpret_cast<const ulonglong2*>(dp)[p];
-      const uint32_t d0 = (uint32_t)(x.x >> 32), d1 = (uint32_t)(x.y >> 32);
-      reinterpret_cast<int2*>(dist)[p] =
-          make_int2(d0 == 0xFFFFFFFFu ? GFX_UNVISITED : (int32_t)d0,
-                    d1 == 0xFFFFFFFFu ? GFX_UNVISITED : (int32_t)d1);
-      reinterpret_cast<int2*>(preds)[p] = make_int2((int32_t)(uint32_t)x.x, (int32_t)(uint32_t)x.y);
-    }
-    done = pairs << 1;
-  }
-  for (int64_t v = done + t0; v < n; v += stride) {
-    const unsigned long long x = dp[v];
-    const uint32_t d = (uint32_t)(x >> 32);
-    dist[v] = d == 0xFFFFFFFFu ? GFX_UNVISITED : (int32_t)d;
-    preds[v] = (int32_t)(uint32_t)x;
-  }
 }
 
 int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t* preds,

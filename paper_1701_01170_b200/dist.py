@@ -410,3 +410,158 @@ def gather_labels(engines, n: int):
         labels[e.r::P] = lab
         preds[e.r::P] = prd
     return labels, preds
+
+
+# ---------------------------------------------------------------------------
+# partitioned near/far SSSP (reference sssp.py:41-121, near_far.py)
+# ---------------------------------------------------------------------------
+def partition_weights(dg, lrow, P: int, r: int):
+    """Rank r's weights aligned with its local rows (gfx_dist_partition_weights)."""
+    import torch
+
+    ml = int(lrow[-1].item()) if lrow.numel() else 0
+    lw = torch.empty(max(ml, 1), dtype=torch.int32, device=lrow.device)
+    _native.call("gfx_dist_partition_weights", dg.handle, P, r, _native.ptr(lrow), _native.ptr(lw))
+    return lw[:ml]
+
+
+class SsspEngine:
+    """Rank r's partitioned-SSSP engine (gfx_dsssp) and the exchange buffers
+    it binds.  Messages are (d, dist << 32 | pred) -- 2 int64 words -- so the
+    send / recv tensors and send_counts are in words, which is what the
+    ProcessComm / VirtualComm all_to_all already moves."""
+
+    def __init__(self, lrow, lcol, lw, n: int, P: int, r: int):
+        import torch
+
+        self.P, self.r, self.n = P, r, int(n)
+        self.device = lrow.device
+        self.lrow, self.lcol, self.lw = lrow, lcol, lw
+        self.nl = lrow.numel() - 1
+        ml = lcol.numel()
+        ctx = _native.Context.get(lrow.device.index)
+        torch.cuda.synchronize(self.device)
+        h = ctypes.c_void_p()
+        _native.call("gfx_dsssp_create", ctx.handle, self.n, P, r, _native.ptr(lrow),
+                     _native.ptr(lcol), _native.ptr(lw), self.nl, ml, ctypes.byref(h))
+        self.handle = h
+        dev = self.device
+        send_words = 2 * (min(ml, self.n) + 64)
+        recv_words = 2 * (max(P - 1, 1) * self.nl + 64)
+        self.send = torch.empty(send_words, dtype=torch.int64, device=dev)
+        self.recv = torch.empty(recv_words, dtype=torch.int64, device=dev)
+        self.counts = torch.zeros(2 * P, dtype=torch.int64, device=dev)
+        self.send_counts, self.recv_counts = self.counts[:P], self.counts[P:]
+        self.stats = torch.zeros(8, dtype=torch.int64, device=dev)
+        _native.call("gfx_dsssp_bind", h, _native.ptr(self.send), send_words,
+                     _native.ptr(self.recv), recv_words, _native.ptr(self.send_counts),
+                     _native.ptr(self.stats))
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and _native._lib is not None:
+            _native._lib.gfx_dsssp_destroy(h)
+            self.handle = None
+
+    def reset(self, source: int) -> int:
+        k = ctypes.c_int64()
+        _native.call("gfx_dsssp_reset", self.handle, int(source), ctypes.byref(k))
+        return k.value
+
+    def relax(self) -> None:
+        _native.call("gfx_dsssp_relax", self.handle)
+
+    def apply(self, nrecv_words: int) -> None:
+        _native.call("gfx_dsssp_apply", self.handle, int(nrecv_words))
+
+    def split(self, threshold: float) -> None:
+        _native.call("gfx_dsssp_split", self.handle, float(threshold))
+
+    def refar(self, threshold: float, split: bool, far_local: int) -> None:
+        _native.call("gfx_dsssp_refar", self.handle, float(threshold), int(bool(split)),
+                     int(far_local))
+
+    def result(self):
+        """(local int32 distances, global int32 preds) of the owned vertices."""
+        import torch
+
+        dist = torch.empty(max(self.nl, 1), dtype=torch.int32, device=self.device)
+        preds = torch.empty(max(self.nl, 1), dtype=torch.int32, device=self.device)
+        _native.call("gfx_dsssp_result", self.handle, _native.ptr(dist), _native.ptr(preds))
+        return dist[: self.nl], preds[: self.nl]
+
+
+@dataclass
+class DistSsspStats:
+    iterations: int = 0
+    bucket_advances: int = 0
+    relaxed_slots: int = 0
+    messages: int = 0
+    per_iteration: list = field(default_factory=list)
+
+
+def sssp_partitioned(comm, n: int, source: int, delta: float | None) -> DistSsspStats:
+    """One near/far SSSP over the engines attached to ``comm`` (all ranks call
+    this collectively; results stay in the engines).  ``delta`` None or <= 0:
+    no splitting (everything near), as the reference's never-splitting
+    default on R-MAT."""
+    import math
+
+    if not 0 <= source < n:
+        raise ValueError(f"source {source} out of range")
+    d = float(delta) if delta is not None and delta > 0 else math.inf
+    engines = comm.engines
+    for e in engines:
+        e.reset(source)
+    st = DistSsspStats()
+    threshold = d
+    near_g, far_g = 1, 0
+    far_loc = [0] * len(engines)
+    while near_g > 0 or far_g > 0:
+        if near_g == 0:
+            # advance_bucket on every rank (near_far.py:63-85)
+            threshold += d
+            for e, fl in zip(engines, far_loc):
+                e.refar(threshold, True, fl)
+            loc, glob = comm.allreduce_stats()
+            near_g, far_g = glob[0], glob[1]
+            far_loc = [lv[1] for lv in loc]
+            st.bucket_advances += 1
+            continue
+        st.iterations += 1
+        for e in engines:
+            e.relax()
+        sc, rc = comm.exchange_counts()
+        recv = comm.exchange_pairs(sc, rc)
+        for e, nr in zip(engines, recv):
+            e.apply(nr)
+        for e in engines:
+            e.split(threshold)
+        loc, glob = comm.allreduce_stats()
+        near_g, far_g = glob[0], glob[1]
+        far_loc = [lv[1] for lv in loc]
+        st.relaxed_slots += glob[2]
+        st.messages += sum(sum(c) for c in sc) // 2
+        st.per_iteration.append({"iteration": st.iterations, "near_out": near_g, "far": far_g,
+                                 "slots": glob[2], "touched": glob[3]})
+        # capacity guard: drop stale far entries on ranks whose pile grew past nl
+        for i, e in enumerate(engines):
+            if far_loc[i] > max(e.nl, 1):
+                e.refar(threshold, False, far_loc[i])
+                far_loc[i] = int(e.stats[1].item())
+    return st
+
+
+def gather_sssp(engines, n: int):
+    """Global int32 distances / preds from virtual-rank SSSP engines."""
+    import torch
+
+    P = len(engines)
+    dev = engines[0].device
+    dist = torch.empty(n, dtype=torch.int32, device=dev)
+    preds = torch.empty(n, dtype=torch.int32, device=dev)
+    for e in engines:
+        d, p = e.result()
+        dist[e.r::P] = d
+        preds[e.r::P] = p
+    return dist, preds

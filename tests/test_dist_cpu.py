@@ -131,3 +131,80 @@ def test_gloo_two_processes():
     for direction, (labels, tr) in out.items():
         assert np.array_equal(labels, want), direction
     assert out["auto"][1] == _rows(trace)
+
+
+def _sssp_worker(rank, world, port_, q):
+    import torch.distributed as dist
+
+    from _dist_cpu import CpuSsspEngine
+    from paper_1701_01170_b200.dist import ProcessComm, sssp_partitioned
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        row, col = port.rmat_csr(10, 16, 0)
+        w = port.assign_random_weights(row, col, 1, 64, 0)
+        n = len(row) - 1
+        eng = CpuSsspEngine(row, col, w, n, world, rank)
+        out = {}
+        for delta in (None, 8, 32):
+            st = sssp_partitioned(ProcessComm(eng), n, 0, delta)
+            lab = torch.from_numpy(eng.dist.copy())
+            L = torch.tensor([len(lab)])
+            lens = [torch.zeros_like(L) for _ in range(world)]
+            dist.all_gather(lens, L)
+            mx = int(max(x.item() for x in lens))
+            pad = torch.full((mx,), -7, dtype=torch.int64)
+            pad[: len(lab)] = lab
+            allp = [torch.zeros_like(pad) for _ in range(world)]
+            dist.all_gather(allp, pad)
+            if rank == 0:
+                g = np.full(n, -1, dtype=np.int64)
+                for r in range(world):
+                    g[r::world] = allp[r].numpy()[: int(lens[r].item())]
+                out[delta] = (g, st.iterations, st.bucket_advances)
+        if rank == 0:
+            q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_two_processes_sssp():
+    """Partitioned near/far SSSP orchestration (dist.sssp_partitioned) across
+    two real gloo processes: distances equal Dijkstra (C oracle) for several
+    deltas; small deltas advance the bucket."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_ = _free_port()
+    procs = [ctx.Process(target=_sssp_worker, args=(r, 2, port_, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    row, col = port.rmat_csr(10, 16, 0)
+    w = port.assign_random_weights(row, col, 1, 64, 0)
+    want = c_oracle.dijkstra(row, col, w, 0)
+    for delta, (dist_, iters, adv) in out.items():
+        assert np.array_equal(dist_, want), delta
+    assert out[8][2] > 0
+
+
+def test_virtual_ranks_sssp_cpu_engine():
+    from _dist_cpu import CpuSsspEngine
+    from paper_1701_01170_b200.dist import VirtualComm, sssp_partitioned
+
+    row, col = port.rmat_csr(9, 16, 0)
+    w = port.assign_random_weights(row, col, 1, 64, 0)
+    n = len(row) - 1
+    want = c_oracle.dijkstra(row, col, w, 0)
+    for P in (1, 3, 4):
+        engines = [CpuSsspEngine(row, col, w, n, P, r) for r in range(P)]
+        sssp_partitioned(VirtualComm(engines), n, 0, 16)
+        got = np.full(n, -1, dtype=np.int64)
+        for e in engines:
+            got[e.r::P] = e.dist
+        assert np.array_equal(got, want), P

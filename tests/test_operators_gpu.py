@@ -154,9 +154,29 @@ def test_segmented_intersect_kats():
         assert res.per_pair_counts.tolist() == want and res.total == sum(want)
 
 
-def test_python_callables_rejected():
+def test_callables_run_on_device_tensors_and_mixing_is_rejected():
+    """Callables see int64 CUDA tensors (the staged path); a callable that
+    indexes host data fails loudly instead of falling back to the CPU; a
+    FunctorSet mixing registry functors and callables is rejected."""
+    import torch
+
     import paper_1701_01170_b200 as gfx
 
+    seen = {}
+
+    def cond(s, d, e, _):
+        seen["dev"] = (s.device.type, d.device.type, e.device.type, s.dtype)
+        return d > 0
+
+    out = gfx.advance(_k(3), gfx.Frontier.from_items([0]), functors=gfx.FunctorSet(cond=cond))
+    assert sorted(out.to_array().tolist()) == [1, 2]
+    assert seen["dev"] == ("cuda", "cuda", "cuda", torch.int64)
+    host = np.array([True, False, True])
+    with pytest.raises(Exception):
+        gfx.advance(_k(3), gfx.Frontier.from_items([0]),
+                    functors=gfx.FunctorSet(cond=lambda s, d, e, _: host[d]))
+    labels = torch.zeros(3, dtype=torch.int32, device="cuda")
     with pytest.raises(TypeError):
         gfx.advance(_k(3), gfx.Frontier.from_items([0]),
-                    functors=gfx.FunctorSet(cond=lambda s, d, e, _: d > 0))
+                    functors=gfx.FunctorSet(cond=gfx.functors.label_eq(labels, 0),
+                                            apply=lambda s, d, e, _: None))
