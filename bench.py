@@ -245,7 +245,9 @@ def run_ours(args, dist: Dist):
     dist.barrier()
     local_ms = ev0.elapsed_time(ev1)
     t_ms = dist.max(local_ms)
-    # the same K steps through the per-call API (one host round trip each)
+    # the same K steps through the per-call API (one host round trip each),
+    # with the RunStats post-pass back on as every public call has it
+    ctx.set_stats(1)
     t_call0 = time.perf_counter()
     for _ in range(args.steps):
         step(args.direction)
@@ -302,7 +304,10 @@ def run_ours(args, dist: Dist):
                    "graph_build_s": round(build_s, 3),
                    "stats_post_pass": "off in timed steps (E_r from a warm-up run)",
                    "level_loop": "device-resident cooperative kernel, K launches enqueued back to back",
-                   "per_call_ms": round(per_call_ms, 4)},
+                   "per_call_ms": round(per_call_ms, 4),
+                   "per_call_gteps": round(e_r / (per_call_ms * 1e-3) / 1e9, 2),
+                   "per_call_what": "public bfs_device call: one host round trip per BFS "
+                                    "and the RunStats degree post-pass (stats on)"},
         "roofline": roofline, "gpu_launches": int(launches), "clocks": clocks,
     }
 
@@ -432,7 +437,7 @@ def _partitioned_run(args, dist, scale: int, steps: int, warmup: int, with_1gpu:
     if not args.python_loop:
         err = None
         try:
-            ncomm = NativeComm(eng)
+            ncomm = NativeComm(eng, single_rank_nccl=(P == 1))
         except Exception as exc:  # noqa: BLE001 -- agreed on below, reported in the line
             err = repr(exc)
         if dist.sum(0.0 if err is None else 1.0) == 0:
@@ -556,11 +561,16 @@ def extras(args, dg, labels, preds, dist, peak):
             # included), mean of k calls
             times = [sssp_device(dgw, args.source, delta=delta)[2].device_ms for _ in range(k)]
             ms = sum(times) / len(times)
+            # work-optimal lower bound: every reached vertex
+            # settled once, 28 B per vertex + 8 B per slot of E_r
+            lb = 28 * st.reached + 8 * st.edges_reached
             res[f"sssp_delta{delta or 'default'}"] = {
                 "gteps": round(st.edges_reached / (ms * 1e-3) / 1e9, 2), "ms": round(ms, 4),
                 "relaxed_slots": st.work_slots, "work_inflation": round(st.work_slots / max(st.edges_reached, 1), 3),
                 "bytes_alg": st.bytes_alg,
-                "frac_of_hbm": round(st.bytes_alg / (ms * 1e-3) / 1e9 / peak, 4)}
+                "frac_of_hbm": round(st.bytes_alg / (ms * 1e-3) / 1e9 / peak, 4),
+                "bytes_lower_bound": lb,
+                "frac_of_hbm_lower_bound": round(lb / (ms * 1e-3) / 1e9 / peak, 4)}
         del dgw
     except Exception as exc:  # report, do not hide
         res["sssp_error"] = repr(exc)
@@ -644,11 +654,23 @@ def secondary(args, dg, peak):
                                 "frac_of_hbm": round(st.bytes_alg / (ms * 1e-3) / 1e9 / peak, 4)}
     small = max(args.scale - 2, 10)
     dg2 = rmat_device_graph(small, args.edge_factor, 0)
+    from paper_1701_01170_b200.primitives.bfs import bfs_device
+
+    st_b = bfs_device(dg2, args.source, direction="push")[2]
+    v_r, e_r2 = st_b.reached, st_b.edges_reached
     st, ms = timed(lambda: bc_device(dg2, [args.source])[1])
+    b = 2 * (28 * v_r + 4 * e_r2) + 16 * v_r  # 2 x BFS-push bytes + 16 V_r
     out[f"bc_s{small}"] = {"ms": round(ms, 3), "gteps_x2": round(
-        2 * st.edges_traversed / (ms * 1e-3) / 1e9, 2)}
+        2 * st.edges_traversed / (ms * 1e-3) / 1e9, 2), "bytes_alg": b,
+        "frac_of_hbm": round(b / (ms * 1e-3) / 1e9 / peak, 4)}
+    total, _, osrc, odst, _ = tc_device(dg2)
+    dplus = torch.bincount(osrc.long(), minlength=dg2.num_vertices)
+    wedge = int((dplus[osrc.long()] + dplus[odst.long()]).sum().item())
+    b = 4 * wedge + 8 * int(osrc.numel())  # 4 sum(deg+u + deg+v) + 8 |E+|
+    del osrc, odst, dplus
     st, ms = timed(lambda: tc_device(dg2)[4])
-    out[f"tc_s{small}"] = {"ms": round(ms, 3)}
+    out[f"tc_s{small}"] = {"ms": round(ms, 3), "triangles": int(total), "bytes_alg": b,
+                           "frac_of_hbm": round(b / (ms * 1e-3) / 1e9 / peak, 4)}
     del dg2
     torch.cuda.empty_cache()
     return out

@@ -827,7 +827,7 @@ int gfx_dbfs_run_comm(gfx_dbfs* db, const gfx_dbfs_comm* comm, int64_t source, i
     if (dec == GFX_DIR_PUSH) {
       GFX_TRY(gfx_dbfs_push_expand(db, (int32_t)depth));
       int64_t nrecv = 0;
-      if (P > 1) {
+      if (comm) {
         GFX_REQUIRE(comm->exchange_counts(comm->user) == 0, "exchange_counts failed");
         GFX_CK(cudaMemcpyAsync(pin, db->send_counts, 2 * P * 8, cudaMemcpyDeviceToHost, st));
         GFX_CK(cudaStreamSynchronize(st));
@@ -844,14 +844,14 @@ int gfx_dbfs_run_comm(gfx_dbfs* db, const gfx_dbfs_comm* comm, int64_t source, i
       GFX_TRY(gfx_dbfs_push_claim(db, nrecv, (int32_t)depth));
     } else {
       GFX_TRY(gfx_dbfs_pull_prepare(db));
-      if (P > 1)
+      if (comm)
         GFX_REQUIRE(comm->allgather_frontier(comm->user) == 0, "allgather_frontier failed");
       else
         GFX_CK(cudaMemcpyAsync(db->gathered, db->front_local, db->wmax * 4,
                                cudaMemcpyDeviceToDevice, st));
       GFX_TRY(gfx_dbfs_pull(db, (int32_t)depth));
     }
-    if (P > 1) GFX_REQUIRE(comm->allreduce_stats(comm->user) == 0, "allreduce_stats failed");
+    if (comm) GFX_REQUIRE(comm->allreduce_stats(comm->user) == 0, "allreduce_stats failed");
     GFX_CK(cudaMemcpyAsync(pin, db->stats, 8 * 8, cudaMemcpyDeviceToHost, st));
     GFX_CK(cudaStreamSynchronize(st));
     const int64_t local_out = pin[0], nout = pin[4];
@@ -900,7 +900,9 @@ int gfx_dbfs_run(gfx_dbfs* db, gfx_nccl* comm, int64_t source, int direction, do
                  double do_b, int mu_edge_based, gfx_iter_rec* recs, int64_t rec_cap,
                  gfx_stats* stats) {
   GFX_REQUIRE(db, "gfx_dbfs_run: null engine");
-  if (db->P == 1)
+  // P = 1 without a communicator: the collectives are identities and are
+  // skipped; with one (a 1-rank NCCL communicator) they run through NCCL
+  if (db->P == 1 && !comm)
     return gfx_dbfs_run_comm(db, nullptr, source, direction, do_a, do_b, mu_edge_based, recs,
                              rec_cap, stats);
   GFX_REQUIRE(comm && comm->comm && comm->nranks == db->P && comm->rank == db->r,

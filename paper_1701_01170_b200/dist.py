@@ -300,19 +300,31 @@ class NativeComm:
     native level loop.  Created collectively: rank 0 draws the unique id and
     the torch.distributed group broadcasts it.  ``None`` handle at P = 1."""
 
-    def __init__(self, engine, group=None):
+    def __init__(self, engine, group=None, single_rank_nccl: bool = False):
         import torch
-        import torch.distributed as dist
 
         self.handle = None
         P, r = engine.P, engine.r
-        if P == 1:
+        if P == 1 and not single_rank_nccl:
             return
         path = _nccl_library_path()
+        if path is None:
+            import torch.cuda.nccl  # noqa: F401 -- maps torch's libnccl into the process
+
+            torch.cuda.nccl.version()
+            path = _nccl_library_path()
         _native.call("gfx_nccl_load", path.encode() if path else None)
         uid = (ctypes.c_uint8 * 128)()
         if r == 0:
             _native.call("gfx_nccl_unique_id", uid)
+        if P == 1:  # a 1-rank communicator: every NCCL call of the loop executes
+            ctx = _native.Context.get(engine.device.index)
+            h = ctypes.c_void_p()
+            _native.call("gfx_nccl_comm_create", ctx.handle, 1, 0, uid, ctypes.byref(h))
+            self.handle = h
+            return
+        import torch.distributed as dist
+
         dev = engine.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
         t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
         dist.broadcast(t, src=0, group=group)

@@ -83,6 +83,17 @@ def rmat_device_graph(scale: int, edge_factor: int = 16, seed: int = 0, *, weigh
     dg = DeviceGraph.from_tensors(row, col, None, undirected=make_undirected)
     if weights is not None:
         lo, hi = weights
+        span = int(hi) - int(lo) + 1
+        if span < 1 or span & (span - 1):
+            # numpy's bounded integers() rejects draws for ranges that are not a
+            # power of two (Lemire), a sequential stream the GPU builder does not
+            # reproduce: draw them with the reference algorithm over the
+            # downloaded CSR (input construction, untimed) and upload
+            from .graph import assign_random_weights
+
+            host = assign_random_weights(dg.to_host(), int(lo), int(hi), weight_seed)
+            w = DeviceGraph._weights_tensor(host.edge_weights, dev)
+            return DeviceGraph.from_tensors(row, col, w, undirected=make_undirected)
         w = torch.empty(max(m, 1), dtype=torch.int32, device=dev)[:m]
         wsh, wsl, wih, wil = pcg64_state(weight_seed)
         _native.call("gfx_assign_weights", dg.handle, int(lo), int(hi), wsh, wsl, wih, wil,

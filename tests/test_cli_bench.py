@@ -5,6 +5,7 @@ import json
 import subprocess
 import sys
 
+import numpy as np
 import pytest
 
 from conftest import ROOT
@@ -98,6 +99,22 @@ def test_cli_runs(tmp_path):
     cache = ROOT / "tests" / "golden" / "cache_rmat8_w.gfxcsr"
     p = run_cli("sssp", "--graph", str(cache), "--iters", "1", "--warmup", "0", "--output", "json")
     assert p.returncode == 0, p.stderr
+    # a weight range that is not a power of two (numpy's rejection
+    # sampler) works like the reference CLI
+    p = run_cli("sssp", "--graph", "rmat:6,4", "--weight-range", "1,100", "--iters", "1",
+                "--warmup", "0", "--output", "json")
+    assert p.returncode == 0, p.stderr
+
+
+@pytest.mark.gpu
+def test_weights_non_power_of_two_range_match_reference_rng():
+    import paper_1701_01170_b200 as gfx
+    from paper_1701_01170_b200.generators import rmat_device_graph
+
+    dg = rmat_device_graph(8, 8, 3, weights=(1, 100), weight_seed=5)
+    host = gfx.coo_to_csr(gfx.generate_rmat(8, 8, seed=3), make_undirected=True)
+    want = gfx.assign_random_weights(host, 1, 100, seed=5).edge_weights
+    assert np.array_equal(dg.w.cpu().numpy().astype(np.int64), want)
 
 
 @pytest.mark.gpu

@@ -114,6 +114,31 @@ def test_rmat_native_loop_single_rank(scale):
     assert st.edges_push == rec["bfs_edges_traversed"]
 
 
+@pytest.mark.parametrize("scale", [16, 22])
+def test_native_loop_through_single_rank_nccl(scale):
+    """The native level loop with a REAL 1-rank NCCL communicator: every
+    collective of the protocol (count send/recv, pair send/recv, frontier
+    all-gather, counter all-reduce) executes through NCCL on the device;
+    labels and trace equal the reference's."""
+    from paper_1701_01170_b200._results import labels_to_host
+    from paper_1701_01170_b200.dist import NativeComm, bfs_partitioned_native, gather_labels
+    from paper_1701_01170_b200.generators import rmat_device_graph
+
+    rec, _ = rmat_golden(scale)
+    dg = rmat_device_graph(scale, 16, 0)
+    (eng,) = _engines(dg, 1)
+    comm = NativeComm(eng, single_rank_nccl=True)
+    assert comm.handle is not None
+    for direction in ("auto", "push"):
+        st = bfs_partitioned_native(eng, comm, dg.num_vertices, dg.num_edges, 0,
+                                    direction=direction)
+        lab, _ = gather_labels([eng], dg.num_vertices)
+        assert sha(labels_to_host(lab)) == rec["bfs_sha"], direction
+        if direction == "auto":
+            assert _rows(st.direction_trace) == [list(x) for x in rec["bfs_auto_trace"]]
+    comm.close()
+
+
 class _StagedComm:
     """Test-only: ProcessComm's protocol with each collective staged through
     host memory so gloo can carry it -- two real processes share the one
