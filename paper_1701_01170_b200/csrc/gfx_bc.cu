@@ -192,6 +192,7 @@ using namespace gfx;
 
 extern "C" int gfx_bc(gfx_graph* g, const int64_t* sources, int64_t num_sources, double* bc_d,
                       gfx_stats* stats) {
+  GFX_NVTX("gfx_bc");
   GFX_REQUIRE(g && bc_d && (num_sources == 0 || sources), "gfx_bc: null argument");
   for (int64_t i = 0; i < num_sources; ++i)
     GFX_REQUIRE(sources[i] >= 0 && sources[i] < g->n, "source %lld out of range",

@@ -53,6 +53,7 @@ struct BfsClaimOpT {
   int32_t depth;
   uint32_t wv[kBatch];
   uint8_t* lvl8 = nullptr;  // optional: deferred labels (depth bytes, see LabelOut)
+  uint32_t* fbits = nullptr;  // optional: the new frontier as a bitmap too (pre-zeroed)
   __device__ int32_t src_value(int32_t) const { return 0; }
   __device__ void prefetch(const int32_t* d) {
 #pragma unroll
@@ -65,6 +66,7 @@ struct BfsClaimOpT {
     if (lvl8) lvl8[d] = (uint8_t)depth;
     else labels[d] = depth;
     preds[d] = s;
+    if (fbits) atomicOr(&fbits[d >> 5], bit);  // no return value: a fire-and-forget RED
     return true;
   }
 };
@@ -346,7 +348,7 @@ int bfs_level_stats(gfx_graph* g, const int32_t* labels, int64_t depth, gfx_iter
 }
 
 struct BfsBuffers {
-  uint32_t *visited, *front0, *front1;
+  uint32_t *visited, *front0, *front1, *front2;
   int32_t *order, *part, *raw;
   int64_t *scan, *rowbase;
 };
@@ -356,6 +358,7 @@ static int bfs_buffers(gfx_graph* g, bool idemp, BfsBuffers* b) {
   GFX_TRY(scratch_t(g, "bfs_visited", W, &b->visited));
   GFX_TRY(scratch_t(g, "bfs_front0", W, &b->front0));
   GFX_TRY(scratch_t(g, "bfs_front1", W, &b->front1));
+  GFX_TRY(scratch_t(g, "bfs_front2", W, &b->front2));
   GFX_TRY(scratch_t(g, "q_order", n + 1, &b->order));
   GFX_TRY(scratch_t(g, "q_scan", n + 2, &b->scan));
   GFX_TRY(scratch_t(g, "q_rowbase", n + 1, &b->rowbase));
@@ -617,7 +620,10 @@ struct PBfsArgs {
   const int32_t* head;
   const uint32_t* nz_in;
   uint32_t* visited;
-  uint32_t* front[2];
+  // three rotating frontier bitmaps: at every level front[f] is the
+  // frontier, front[f+1] (zeroed) receives the next one, and front[f+2] --
+  // last read one level ago -- is zeroed in passing for the level after
+  uint32_t* front[3];
   int32_t* order;
   int64_t* scan;
   int64_t* rowbase;
@@ -810,8 +816,38 @@ __device__ __forceinline__ void push_mid(WarpSmem& W, Op& o, const int32_t* __re
 // store instruction writes 512 contiguous bytes.
 __device__ __forceinline__ void materialize_labels(const PBfsArgs& a, int64_t gw, int64_t nw) {
   const int lane = threadIdx.x & 31;
+  // 16 vertices per lane and step: one 16-byte depth load, half a visited
+  // word, four 16-byte label stores (64 contiguous bytes); two steps in
+  // flight per lane -> 1024 vertices per warp step
+  const int64_t n16 = a.vec_ok ? (a.n & ~(int64_t)1023) : 0;
+  for (int64_t base = gw * 1024; base < n16; base += nw * 1024) {
+    uint4 d16[2];
+    uint32_t vb[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int64_t v = base + 512 * k + 16 * lane;
+      d16[k] = *reinterpret_cast<const uint4*>(a.lvl8 + v);
+      vb[k] = a.visited[v >> 5] >> (v & 16);
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int64_t v = base + 512 * k + 16 * lane;
+      const uint32_t dw[4] = {d16[k].x, d16[k].y, d16[k].z, d16[k].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t bits = (vb[k] >> (4 * j)) & 0xFu, d4 = dw[j];
+        int4 lab;
+        lab.x = (bits & 1u) ? (int32_t)(d4 & 0xFF) : GFX_UNVISITED;
+        lab.y = (bits & 2u) ? (int32_t)((d4 >> 8) & 0xFF) : GFX_UNVISITED;
+        lab.z = (bits & 4u) ? (int32_t)((d4 >> 16) & 0xFF) : GFX_UNVISITED;
+        lab.w = (bits & 8u) ? (int32_t)(d4 >> 24) : GFX_UNVISITED;
+        *reinterpret_cast<int4*>(a.labels + v + 4 * j) = lab;
+      }
+    }
+  }
+  // remainder (and unaligned outputs): the 4-per-lane form below
   const int64_t nfull = a.vec_ok ? (a.n & ~(int64_t)3) : 0;
-  for (int64_t base = gw * 1024; base < a.n; base += nw * 1024) {
+  for (int64_t base = n16 + gw * 1024; base < a.n; base += nw * 1024) {
     uint32_t vw[8], d4[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -864,7 +900,19 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
   } else {
     for (int64_t i = gtid; i < a.n; i += nthr) a.preds[i] = -1;
   }
-  for (int64_t i = gtid; i < a.words; i += nthr) a.visited[i] = 0u;
+  // visited and the three frontier bitmaps start clear; the source's word
+  // is written with its bit in the same pass (one barrier for the whole init)
+  {
+    const int64_t sw = a.source >> 5;
+    const uint32_t sbit = 1u << (a.source & 31);
+    for (int64_t i = gtid; i < a.words; i += nthr) {
+      const uint32_t x = i == sw ? sbit : 0u;
+      a.visited[i] = x;
+      a.front[0][i] = x;
+      a.front[1][i] = 0u;
+      a.front[2][i] = 0u;
+    }
+  }
   for (int64_t i = gtid; i < 3 * (int64_t)(sizeof(Counters) / 8); i += nthr)
     reinterpret_cast<unsigned long long*>(a.C)[i] = 0ull;
   if (threadIdx.x == 0) {
@@ -879,10 +927,8 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
     c.fsel = 0;
     c.direct = 0;
   }
-  grid.sync();
   if (leader) {
     a.lvl8[a.source] = 0;
-    a.visited[a.source >> 5] = 1u << (a.source & 31);
     a.order[0] = a.source;
   }
   grid.sync();
@@ -917,7 +963,18 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
     if (blockIdx.x == 0 && threadIdx.x < (int)(sizeof(Counters) / 8))
       reinterpret_cast<unsigned long long*>(&a.C[(c.depth + 1) % 3])[threadIdx.x] = 0ull;
     uint32_t* fcur = a.front[c.fsel];
-    uint32_t* fnext = a.front[c.fsel ^ 1];
+    uint32_t* fnext = a.front[(c.fsel + 1) % 3];
+    {
+      // the bitmap the NEXT level writes was last read one level ago: zero it
+      // in passing (no barrier -- nothing reads it during this level)
+      uint32_t* fclr = a.front[(c.fsel + 2) % 3];
+      if (a.direction != GFX_DIR_PUSH)
+        for (int64_t i = gtid; i < a.words; i += nthr) fclr[i] = 0u;
+    }
+    // a direction-optimising run keeps the frontier as a bitmap at every
+    // level: push levels also set the new frontier's bits (fbits), so a pull
+    // level never converts a queue
+    uint32_t* fbits = a.direction != GFX_DIR_PUSH ? fnext : nullptr;
     long long level_edges = 0, nout = 0, work = 0, cands = 0, bytes = 0;
 
     if (c.mode == GFX_DIR_PUSH) {
@@ -932,12 +989,12 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
         __syncthreads();
       }
       const int32_t* F = a.order + c.q_off;
-      BfsClaimOp op{a.visited, a.labels, a.preds, depth, {}, lab.lvl8};
+      BfsClaimOp op{a.visited, a.labels, a.preds, depth, {}, lab.lvl8, fbits};
       if (nf <= 32) {
         // tiny frontier (the hub's level, the tail levels): every warp derives
         // the whole expansion plan itself -- no scan pass, no grid barrier
         // between plan and expansion
-        BfsClaimOpTiny top{a.visited, a.labels, a.preds, depth, {}, lab.lvl8};
+        BfsClaimOpTiny top{a.visited, a.labels, a.preds, depth, {}, lab.lvl8, fbits};
         push_tiny(W, top, F, nf, a.row, a.col, a.order + c.q_end, &cur->out_len, &cur->total, gw,
                   nw);
       } else if (nf <= kMidItems) {
@@ -982,25 +1039,25 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
       if (threadIdx.x == 0) {
         c.q_off = c.q_end;
         c.q_end += nout;
+        c.fsel = (c.fsel + 1) % 3;
       }
     } else {
-      if (c.queue_form) {
-        for (int64_t i = gtid; i < a.words; i += nthr) fcur[i] = 0u;
-        grid.sync();
-        queue_to_bitmap(a.order + c.q_off, nf, fcur, gtid, nthr);
-        grid.sync();
-      }
       // dense levels (unvisited non-isolated vertices above n/8): 8
       // candidates per lane in flight and a dynamic tail; sparse levels: 4
-      // in flight and the static deal
-      if ((c.n_u - (a.n - a.nnz)) * 8 > a.n)
+      // in flight and the static deal.  When at most n/64 candidates remain
+      // the found vertices are also queued (cheap then), so a push level
+      // after this one needs no bitmap-to-queue sweep.
+      const long long ncand = c.n_u - (a.n - a.nnz);
+      const bool qsmall = ncand <= (a.n >> 6);
+      if (ncand * 8 > a.n)
         pull_groups<BitmapFront, 8>(a.words, a.nz_in, a.visited, BitmapFront{fcur}, fnext, a.head,
                                     a.rrow, a.rcol, a.directed, lab, a.preds, depth, cur, gw, nw,
                                     PS, a.head + a.n + 1, &cur->aux2);
       else
         pull_groups<BitmapFront, 4>(a.words, a.nz_in, a.visited, BitmapFront{fcur}, fnext, a.head,
                                     a.rrow, a.rcol, a.directed, lab, a.preds, depth, cur, gw, nw,
-                                    PS, a.head + a.n + 1, nullptr);
+                                    PS, a.head + a.n + 1, nullptr,
+                                    qsmall ? a.order + c.q_end : nullptr, &cur->aux3);
       grid.sync();
       nout = (long long)ld_ctr(&cur->out_len);
       work = (long long)ld_ctr(&cur->aux0);
@@ -1008,8 +1065,12 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
       level_edges = a.directed ? (long long)ld_ctr(&cur->edges) : -1;
       bytes = 12 * cands + 4 * work + 8 * nout;
       if (threadIdx.x == 0) {
-        c.fsel ^= 1;
-        c.queue_form = 0;
+        c.fsel = (c.fsel + 1) % 3;
+        c.queue_form = qsmall ? 1 : 0;
+        if (qsmall) {
+          c.q_off = c.q_end;
+          c.q_end += nout;
+        }
       }
     }
     if (leader && c.nrec < a.rec_cap) {
@@ -1089,6 +1150,7 @@ static int pbfs_setup(gfx_graph* g, int64_t source, int direction, double do_a, 
   a.visited = B.visited;
   a.front[0] = B.front0;
   a.front[1] = B.front1;
+  a.front[2] = B.front2;
   a.order = B.order;
   a.scan = B.scan;
   a.rowbase = B.rowbase;
@@ -1213,6 +1275,7 @@ extern "C" int gfx_bfs(gfx_graph* g, int64_t source, int direction, int idempote
                        int filter_mode, double do_a, double do_b, int mu_edge_based, int loop,
                        int32_t* labels_d, int32_t* preds_d, gfx_iter_rec* recs, int64_t rec_cap,
                        gfx_stats* stats) {
+  GFX_NVTX("gfx_bfs");
   GFX_REQUIRE(g, "gfx_bfs: null graph");
   GFX_REQUIRE(source >= 0 && source < g->n, "source %lld out of range", (long long)source);
   GFX_REQUIRE(direction == GFX_DIR_PUSH || direction == GFX_DIR_PULL || direction == GFX_DIR_AUTO,
@@ -1235,6 +1298,7 @@ extern "C" int gfx_bfs(gfx_graph* g, int64_t source, int direction, int idempote
 extern "C" int gfx_bfs_batch(gfx_graph* g, const int64_t* sources, int64_t count,
                              int direction, double do_a, double do_b, int mu_edge_based,
                              int32_t* labels_d, int32_t* preds_d, float* ms) {
+  GFX_NVTX("gfx_bfs_batch");
   GFX_REQUIRE(g && sources && count > 0 && labels_d && preds_d && ms,
               "gfx_bfs_batch: bad argument");
   for (int64_t k = 0; k < count; ++k)

@@ -171,6 +171,7 @@ int iota_frontier(gfx_graph* g, int32_t** out) {
 using namespace gfx;
 
 extern "C" int gfx_cc(gfx_graph* g, int32_t* comp_d, int64_t* num_components, gfx_stats* stats) {
+  GFX_NVTX("gfx_cc");
   GFX_REQUIRE(g && comp_d && num_components, "gfx_cc: null argument");
   GFX_REQUIRE(g->flags & GFX_GRAPH_UNDIRECTED, "cc expects an undirected graph");
   gfx_ctx* ctx = g->ctx;

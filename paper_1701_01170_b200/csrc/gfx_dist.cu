@@ -790,6 +790,7 @@ extern "C" {
 int gfx_dbfs_run_comm(gfx_dbfs* db, const gfx_dbfs_comm* comm, int64_t source, int direction,
                       double do_a, double do_b, int mu_edge_based, gfx_iter_rec* recs,
                       int64_t rec_cap, gfx_stats* stats) {
+  GFX_NVTX("gfx_dbfs_run_comm");
   GFX_REQUIRE(db && stats && db->stats, "gfx_dbfs_run: unbound engine");
   GFX_REQUIRE(direction == GFX_DIR_PUSH || direction == GFX_DIR_PULL || direction == GFX_DIR_AUTO,
               "bad direction %d", direction);

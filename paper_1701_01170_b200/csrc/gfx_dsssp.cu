@@ -367,6 +367,7 @@ int gfx_dsssp_reset(gfx_dsssp* ds, int64_t source, int64_t* near_local) {
 }
 
 int gfx_dsssp_relax(gfx_dsssp* ds) {
+  GFX_NVTX("gfx_dsssp_relax");
   GFX_REQUIRE(ds && ds->send, "gfx_dsssp_relax: engine not bound");
   gfx_ctx* ctx = ds->ctx;
   GFX_CK(cudaSetDevice(ctx->device));
@@ -394,6 +395,7 @@ int gfx_dsssp_relax(gfx_dsssp* ds) {
 }
 
 int gfx_dsssp_apply(gfx_dsssp* ds, int64_t nrecv_words) {
+  GFX_NVTX("gfx_dsssp_apply");
   GFX_REQUIRE(ds && ds->recv, "gfx_dsssp_apply: engine not bound");
   GFX_REQUIRE(nrecv_words >= 0 && nrecv_words % 2 == 0 && nrecv_words <= ds->recv_cap,
               "bad received word count %lld", (long long)nrecv_words);
@@ -409,6 +411,7 @@ int gfx_dsssp_apply(gfx_dsssp* ds, int64_t nrecv_words) {
 }
 
 int gfx_dsssp_split(gfx_dsssp* ds, double threshold) {
+  GFX_NVTX("gfx_dsssp_split");
   GFX_REQUIRE(ds && ds->stats, "gfx_dsssp_split: engine not bound");
   gfx_ctx* ctx = ds->ctx;
   GFX_CK(cudaSetDevice(ctx->device));
@@ -426,6 +429,7 @@ int gfx_dsssp_split(gfx_dsssp* ds, double threshold) {
 // advance_bucket (split = 1) or the stale-drop compaction (split = 0); far_local
 // is the host's copy of this rank's far count (from the allreduced stats)
 int gfx_dsssp_refar(gfx_dsssp* ds, double threshold, int split, int64_t far_local) {
+  GFX_NVTX("gfx_dsssp_refar");
   GFX_REQUIRE(ds && ds->stats, "gfx_dsssp_refar: engine not bound");
   gfx_ctx* ctx = ds->ctx;
   GFX_CK(cudaSetDevice(ctx->device));

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../../include/gfx.h"
+#include <nvtx3/nvToolsExt.h>
 
 namespace gfx {
 
@@ -25,6 +26,14 @@ int cuda_status(cudaError_t e, const char* what, const char* file, int line);
     cudaError_t _e = (call);                                                    \
     if (_e != cudaSuccess) return ::gfx::cuda_status(_e, #call, __FILE__, __LINE__); \
   } while (0)
+
+// NVTX range over a C-ABI entry point (header-only NVTX v3: a no-op unless a
+// profiler injects itself, e.g. nsys / ncu --nvtx)
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+};
+#define GFX_NVTX(name) ::gfx::NvtxScope gfx_nvtx_scope_(name)
 
 // every kernel launch goes through GFX_LAUNCH so gfx_launch_count() is exact
 void count_launch();

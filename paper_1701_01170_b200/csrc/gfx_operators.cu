@@ -429,6 +429,7 @@ extern "C" {
 int gfx_advance(gfx_graph* g, const int32_t* fin_d, int64_t nin, int kind, int functor_id,
                 const gfx_functor_args* args, int32_t* fout_d, int64_t fout_cap, int64_t* nout,
                 int64_t* edges) {
+  GFX_NVTX("gfx_advance");
   GFX_REQUIRE(g && nout && (nin == 0 || (fin_d && fout_d)), "gfx_advance: null argument");
   GFX_REQUIRE(kind >= GFX_KIND_V2V && kind <= GFX_KIND_E2E, "unknown advance kind %d", kind);
   GFX_REQUIRE(is_advance_fn(functor_id), "functor %d is not an advance functor of the registry",
@@ -449,6 +450,7 @@ int gfx_advance_fused(gfx_graph* g, const int32_t* fin_d, int64_t nin, int kind,
                       const gfx_functor_args* cond_args, int vcond_id,
                       const gfx_functor_args* vcond_args, int32_t* fout_d, int64_t fout_cap,
                       int64_t* nout, int64_t* edges) {
+  GFX_NVTX("gfx_advance_fused");
   GFX_REQUIRE(g && nout && (nin == 0 || (fin_d && fout_d)), "gfx_advance_fused: null argument");
   GFX_REQUIRE(kind >= GFX_KIND_V2V && kind <= GFX_KIND_E2E, "unknown advance kind %d", kind);
   GFX_REQUIRE(is_advance_fn(cond_id) && cond_id != GFX_FN_SSSP_RELAX,
@@ -477,6 +479,7 @@ int gfx_advance_fused(gfx_graph* g, const int32_t* fin_d, int64_t nin, int kind,
 int gfx_pull_advance(gfx_graph* g, const int32_t* fin_d, int64_t nin, int functor_id,
                      const gfx_functor_args* args, int32_t* active_d, int64_t* nactive,
                      int32_t* rest_d, int64_t* nrest, int64_t* edges) {
+  GFX_NVTX("gfx_pull_advance");
   GFX_REQUIRE(g && nactive && nrest && (nin == 0 || (fin_d && active_d && rest_d)),
               "gfx_pull_advance: null argument");
   GFX_REQUIRE(functor_id == GFX_FN_BFS_PULL, "functor %d is not a pull functor of the registry",
@@ -514,6 +517,7 @@ int gfx_pull_advance(gfx_graph* g, const int32_t* fin_d, int64_t nin, int functo
 
 int gfx_filter(gfx_graph* g, const int32_t* fin_d, int64_t nin, int mode, int functor_id,
                const gfx_functor_args* args, int64_t domain, int32_t* fout_d, int64_t* nout) {
+  GFX_NVTX("gfx_filter");
   GFX_REQUIRE(g && nout && (nin == 0 || (fin_d && fout_d)), "gfx_filter: null argument");
   GFX_REQUIRE(mode == GFX_FILTER_EXACT || mode == GFX_FILTER_INEXACT, "unknown filter mode %d", mode);
   GFX_REQUIRE(is_vertex_fn(functor_id), "functor %d is not a filter functor of the registry",
@@ -571,6 +575,7 @@ int gfx_vertex_mask(gfx_graph* g, const int32_t* fin_d, int64_t nin, int functor
 
 int gfx_compute(gfx_graph* g, const int32_t* fin_d, int64_t nin, int functor_id,
                 const gfx_functor_args* args, int64_t* acc_d) {
+  GFX_NVTX("gfx_compute");
   GFX_REQUIRE(g && (nin == 0 || fin_d), "gfx_compute: null argument");
   GFX_REQUIRE(functor_id == GFX_FN_SET_LABEL || functor_id == GFX_FN_ADD_I64,
               "functor %d is not a compute functor of the registry", functor_id);

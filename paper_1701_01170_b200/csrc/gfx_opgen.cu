@@ -256,6 +256,7 @@ int gfx_scan_offsets(gfx_graph* g, const int32_t* fin_d, int64_t nin, int edge_i
 int gfx_gather(gfx_graph* g, const int32_t* fin_d, int64_t nin, int edge_input, int reverse,
                const int64_t* scan_d, int64_t total, int64_t* a_d, int64_t* b_d, int64_t* e_d,
                int32_t* rep_d) {
+  GFX_NVTX("gfx_gather");
   GFX_REQUIRE(g && (total == 0 || (fin_d && scan_d && a_d && b_d && e_d)),
               "gfx_gather: null argument");
   GFX_REQUIRE(!reverse || (g->rrow && g->rcol && g->reid),
@@ -272,6 +273,7 @@ int gfx_gather(gfx_graph* g, const int32_t* fin_d, int64_t nin, int edge_input, 
 }
 
 int gfx_graph_build_csc(gfx_graph* g, int64_t* rrow_d, int32_t* rcol_d, int64_t* reid_d) {
+  GFX_NVTX("gfx_graph_build_csc");
   GFX_REQUIRE(g && rrow_d && (g->m == 0 || (rcol_d && reid_d)), "gfx_graph_build_csc: null argument");
   gfx_ctx* ctx = g->ctx;
   GFX_CK(cudaSetDevice(ctx->device));

@@ -184,6 +184,7 @@ using namespace gfx;
 
 extern "C" int gfx_pagerank(gfx_graph* g, double damping, double epsilon, int64_t max_iters,
                             double* rank_d, gfx_stats* stats) {
+  GFX_NVTX("gfx_pagerank");
   GFX_REQUIRE(g && rank_d, "gfx_pagerank: null argument");
   GFX_REQUIRE(damping > 0.0 && damping < 1.0, "damping must be in (0, 1)");
   GFX_REQUIRE(epsilon >= 0.0, "epsilon must be >= 0");

@@ -63,7 +63,10 @@ __device__ __forceinline__ void pull_groups(
     const int32_t* __restrict__ rcol, int count_in_edges, const LabelOut labels,
     int32_t* __restrict__ preds, int32_t depth, Counters* __restrict__ ctr, int64_t gw,
     int64_t nwarps, PullSmem& P, const int32_t* __restrict__ head2 = nullptr,
-    unsigned long long* __restrict__ grab = nullptr) {
+    unsigned long long* __restrict__ grab = nullptr, int32_t* __restrict__ qout = nullptr,
+    unsigned long long* __restrict__ qlen = nullptr) {
+  // qout (optional): the found vertices are also appended to a queue, one
+  // reservation per 1024-vertex group (*qlen counts them)
   const int lane = threadIdx.x & 31;
   unsigned long long found_cnt = 0, in_edges = 0, probes = 0, cands = 0;
   // groups are dealt out statically for all but the last ~1.5 rounds; the
@@ -225,10 +228,27 @@ __device__ __forceinline__ void pull_groups(
       }
     }
     __syncwarp();
-    if (w < words) {
-      const uint32_t nb = P.newbits[lane];
-      next[w] = nb;
-      if (nb) visited[w] = vis | nb;
+    {
+      const uint32_t nb = w < words ? P.newbits[lane] : 0u;
+      if (w < words) {
+        next[w] = nb;
+        if (nb) visited[w] = vis | nb;
+      }
+      if (qout) {
+        int qt;
+        const int qo = warp_excl_scan(__popc(nb), lane, &qt);
+        if (qt) {
+          unsigned long long qb = 0;
+          if (lane == 0) qb = atomicAdd(qlen, (unsigned long long)qt);
+          qb = __shfl_sync(0xffffffffu, qb, 0) + qo;
+          uint32_t x = nb;
+          while (x) {
+            const int b = __ffs(x) - 1;
+            x &= x - 1;
+            qout[qb++] = (int32_t)(w * 32 + b);
+          }
+        }
+      }
     }
     __syncwarp();
     grp = (grab && dyn_next) ? nstatic + (int64_t)__shfl_sync(0xffffffffu, nxt, 0) : grp + nwarps;

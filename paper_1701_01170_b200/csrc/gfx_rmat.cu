@@ -205,6 +205,7 @@ extern "C" int gfx_rmat_keys(gfx_ctx* ctx, int scale, int edge_factor, const dou
                              uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
                              uint64_t inc_lo, int make_undirected, uint64_t* keys_d,
                              int64_t* num_keys) {
+  GFX_NVTX("gfx_rmat_keys");
   GFX_REQUIRE(ctx && cum3 && keys_d && num_keys, "gfx_rmat_keys: null argument");
   GFX_REQUIRE(scale >= 1 && scale <= 30, "gfx_rmat_keys: scale must be in [1, 30]");
   GFX_REQUIRE(edge_factor >= 1, "gfx_rmat_keys: edge_factor must be >= 1");
@@ -264,6 +265,7 @@ extern "C" int gfx_rmat_keys(gfx_ctx* ctx, int scale, int edge_factor, const dou
 
 extern "C" int gfx_keys_to_csr(gfx_ctx* ctx, const uint64_t* keys_d, int64_t num_keys, int scale,
                                int64_t* row_d, int32_t* col_d) {
+  GFX_NVTX("gfx_keys_to_csr");
   GFX_REQUIRE(ctx && keys_d && row_d && (num_keys == 0 || col_d), "gfx_keys_to_csr: null argument");
   GFX_CK(cudaSetDevice(ctx->device));
   const int64_t n = 1ll << scale;
@@ -279,6 +281,7 @@ extern "C" int gfx_keys_to_csr(gfx_ctx* ctx, const uint64_t* keys_d, int64_t num
 extern "C" int gfx_assign_weights(gfx_graph* g, int64_t lo, int64_t hi, uint64_t state_hi,
                                   uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
                                   int32_t* w_d) {
+  GFX_NVTX("gfx_assign_weights");
   GFX_REQUIRE(g && w_d, "gfx_assign_weights: null argument");
   GFX_REQUIRE(lo >= 1 && lo <= hi, "need 1 <= lo <= hi");
   GFX_REQUIRE(g->flags & GFX_GRAPH_UNDIRECTED,

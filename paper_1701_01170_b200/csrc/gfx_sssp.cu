@@ -19,14 +19,19 @@
 //   far / far_key     far pile with enqueue keys, capacity 2n (compacted when
 //                     it would overflow: after dropping stale entries each
 //                     vertex appears at most once)
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <string>
+#include <vector>
 
 #include "gfx_device.cuh"
 #include "gfx_expand.cuh"
 #include "gfx_internal.cuh"
+#include "gfx_scan.cuh"
 #include "gfx_sssp.cuh"
 
 namespace gfx {
@@ -106,6 +111,209 @@ __global__ void k_sssp_seed(unsigned long long* dp, uint32_t* dist, int32_t src,
   near[0] = src;
 }
 
+// ---------------------------------------------------------------------------
+// Device-resident loop: ONE cooperative launch runs the whole near/far SSSP.
+// Every CTA keeps an identical copy of the loop state (near / far counts,
+// threshold, queue selectors); the phases of an iteration -- fused degree
+// scan, load-balanced relax expansion, near/far split -- and the bucket
+// advances (stale drop + re-split) are separated by grid barriers instead of
+// kernel boundaries and a host round trip per iteration.  Same kernels'
+// bodies as the host-driven loop below (expand_tasks, sssp_split_phase,
+// sssp_refar_phase), same results.
+// ---------------------------------------------------------------------------
+namespace cg = cooperative_groups;
+
+struct PSsspArgs {
+  int64_t n, words;
+  const int64_t* row;
+  const int32_t* col;
+  const void* wgt;  // int32 weights or their compact uint8 copy
+  unsigned long long* dp;
+  uint32_t* dist;
+  uint32_t* mark;
+  int32_t* nearq[2];
+  int32_t* touched;
+  int32_t* far[2];
+  int32_t* fkey[2];
+  int64_t* scan;
+  int64_t* rowbase;
+  int32_t* part;
+  unsigned long long* status;
+  Counters* C;  // 3 rotating blocks
+  int32_t* out_dist;
+  int32_t* out_preds;
+  int vec;
+  double delta;
+  int32_t source;
+  gfx_iter_rec* recs;
+  int64_t rec_cap;
+  long long* summary;
+};
+
+struct PSCtl {
+  long long nnear, nfar, it, ph, slots, bytes, nrec, nadv;
+  int q, f;
+  double th;
+  unsigned long long t0;
+};
+
+__device__ __forceinline__ unsigned long long sssp_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <class WT>
+__global__ void __launch_bounds__(256, 3) k_sssp_persistent(PSsspArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  WarpSmem& W = warp_smem(smem_raw);
+  __shared__ ScanSmem ss;
+  __shared__ PileStage S;
+  __shared__ PSCtl c;
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int64_t gw = gtid >> 5, nw = nthr >> 5;
+  const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+  const WT* wgt = static_cast<const WT*>(a.wgt);
+  // ---- init: (dist | pred) and the distance mirror at "unreached" (the
+  // source's words written with its values in the same pass), marks clear
+  for (int64_t v = gtid; v < a.n; v += nthr) {
+    const bool src = v == a.source;
+    a.dp[v] = src ? 0xFFFFFFFFull : ~0ull;  // dist 0, pred -1
+    a.dist[v] = src ? 0u : 0xFFFFFFFFu;
+  }
+  for (int64_t i = gtid; i <= a.words; i += nthr) a.mark[i] = 0u;
+  for (int64_t i = gtid; i < 3 * (int64_t)(sizeof(Counters) / 8); i += nthr)
+    reinterpret_cast<unsigned long long*>(a.C)[i] = 0ull;
+  if (leader) a.nearq[0][0] = a.source;
+  if (threadIdx.x == 0) {
+    c.nnear = 1;
+    c.nfar = c.it = c.ph = c.slots = c.bytes = c.nrec = c.nadv = 0;
+    c.q = c.f = 0;
+    c.th = a.delta;
+  }
+  grid.sync();
+  for (;;) {
+    Counters* cur = &a.C[c.ph % 3];
+    if (blockIdx.x == 0 && threadIdx.x < (int)(sizeof(Counters) / 8))
+      reinterpret_cast<unsigned long long*>(&a.C[(c.ph + 1) % 3])[threadIdx.x] = 0ull;
+    if (c.nnear == 0) {
+      if (c.nfar == 0) break;
+      // advance_bucket (near_far.py:63-85): threshold += delta, drop stale
+      // far entries, re-split the rest
+      const double th = c.th + a.delta;
+      sssp_refar_phase(S, a.far[c.f], a.fkey[c.f], c.nfar, a.dist, th, 1, a.nearq[c.q],
+                       &cur->out_len, a.far[c.f ^ 1], a.fkey[c.f ^ 1], &cur->aux1);
+      grid.sync();
+      if (threadIdx.x == 0) {
+        c.bytes += 8 * c.nfar;
+        c.th = th;
+        c.nnear = (long long)ld_volatile_u64(&cur->out_len);
+        c.nfar = (long long)ld_volatile_u64(&cur->aux1);
+        c.f ^= 1;
+        c.ph += 1;
+        c.nadv += 1;
+      }
+      __syncthreads();
+      continue;
+    }
+    if (threadIdx.x == 0) {
+      c.it += 1;
+      c.t0 = sssp_gtime();
+    }
+    __syncthreads();
+    const int32_t* F = a.nearq[c.q];
+    const int64_t nf = c.nnear;
+    const int64_t stiles = (nf + kScanTileItems - 1) / kScanTileItems;
+    for (int64_t t = blockIdx.x; t < stiles; t += gridDim.x)
+      scan_tile(t, stiles, F, nf, a.row, a.scan, a.rowbase, a.part, a.status, (unsigned)c.ph + 1u,
+                cur, ss);
+    grid.sync();
+    {
+      SsspRelaxOp<WT> op{a.dp, a.dist, a.mark, {}};
+      expand_tasks(W, op, F, nf, a.scan, a.rowbase, a.part,
+                   (int64_t)ld_volatile_u64(&cur->ntiles), (int64_t)ld_volatile_u64(&cur->total),
+                   a.col, wgt, a.touched, &cur->out_len, gw, nw);
+    }
+    for (int64_t i = gtid; i < stiles; i += nthr) a.status[i] = 0ull;
+    grid.sync();
+    const int64_t ntouched = (int64_t)ld_volatile_u64(&cur->out_len);
+    sssp_split_phase(S, a.touched, ntouched, a.dist, a.mark, c.th, a.nearq[c.q ^ 1], &cur->aux0,
+                     a.far[c.f] + c.nfar, a.fkey[c.f] + c.nfar, &cur->aux1);
+    grid.sync();
+    const long long slots = (long long)ld_volatile_u64(&cur->total);
+    const long long bytes = 20 * nf + 8 * slots + 8 * ntouched;
+    if (leader && c.nrec < a.rec_cap) {
+      gfx_iter_rec r{};
+      r.iteration = c.it;
+      r.frontier_in = nf;
+      r.frontier_out = ntouched;
+      r.edges = slots;
+      r.work = slots;
+      r.bytes_alg = bytes;
+      r.n_u = c.nfar + (long long)ld_volatile_u64(&cur->aux1);
+      r.ms = (float)((sssp_gtime() - c.t0) * 1e-6);
+      a.recs[c.nrec] = r;
+    }
+    if (threadIdx.x == 0) {
+      c.nrec += 1;
+      c.slots += slots;
+      c.bytes += bytes;
+      c.nnear = (long long)ld_volatile_u64(&cur->aux0);
+      c.nfar += (long long)ld_volatile_u64(&cur->aux1);
+      c.q ^= 1;
+      c.ph += 1;
+    }
+    __syncthreads();
+    if (c.nfar > a.n) {
+      // capacity guard: drop stale far entries (each vertex then appears once)
+      Counters* g2 = &a.C[c.ph % 3];
+      if (blockIdx.x == 0 && threadIdx.x < (int)(sizeof(Counters) / 8))
+        reinterpret_cast<unsigned long long*>(&a.C[(c.ph + 1) % 3])[threadIdx.x] = 0ull;
+      sssp_refar_phase(S, a.far[c.f], a.fkey[c.f], c.nfar, a.dist, c.th, 0, a.nearq[c.q],
+                       &g2->aux2, a.far[c.f ^ 1], a.fkey[c.f ^ 1], &g2->aux1);
+      grid.sync();
+      if (threadIdx.x == 0) {
+        c.nfar = (long long)ld_volatile_u64(&g2->aux1);
+        c.f ^= 1;
+        c.ph += 1;
+      }
+      __syncthreads();
+    }
+  }
+  sssp_unpack_phase(a.dp, a.n, a.out_dist, a.out_preds, a.vec, gtid, nthr);
+  if (leader) {
+    a.summary[0] = c.it;
+    a.summary[1] = c.slots;
+    a.summary[2] = c.bytes;
+    a.summary[3] = c.nrec < a.rec_cap ? c.nrec : a.rec_cap;
+    a.summary[4] = c.nadv;
+  }
+}
+
+template <class WT>
+static int launch_sssp_persistent(gfx_ctx* ctx, PSsspArgs& a) {
+  static int per_sm = 0;
+  const int smem = expand_smem_bytes();
+  if (per_sm == 0) {
+    GFX_CK(cudaFuncSetAttribute(k_sssp_persistent<WT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem));
+    GFX_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sssp_persistent<WT>, 256,
+                                                         smem));
+    if (per_sm < 1) {
+      set_error("k_sssp_persistent cannot be resident");
+      return GFX_ECUDA;
+    }
+  }
+  void* kargs[] = {&a};
+  GFX_CK(cudaLaunchCooperativeKernel((const void*)k_sssp_persistent<WT>,
+                                     dim3(per_sm * ctx->sm_count), dim3(256), kargs, smem,
+                                     ctx->stream));
+  count_launch();
+  return GFX_OK;
+}
+
 int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t* preds,
              gfx_iter_rec* recs, int64_t rec_cap, gfx_stats* st) {
   gfx_ctx* ctx = g->ctx;
@@ -139,6 +347,67 @@ int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t*
   const int grid = ctx->sm_count * 8;
 
   l2_window(ctx, dist32, (dist_words + g->words + 1) * sizeof(uint32_t), true);
+  const char* loop_env = getenv("GFX_SSSP_LOOP");
+  if (!(loop_env && std::string(loop_env) == "host")) {
+    PSsspArgs a{};
+    a.n = n;
+    a.words = g->words;
+    a.row = g->row;
+    a.col = g->col;
+    a.wgt = w8 ? static_cast<const void*>(w8) : static_cast<const void*>(g->w);
+    a.dp = dp;
+    a.dist = dist32;
+    a.mark = mark;
+    a.nearq[0] = nearA;
+    a.nearq[1] = nearB;
+    a.touched = touched;
+    a.far[0] = far;
+    a.far[1] = far2;
+    a.fkey[0] = fkey;
+    a.fkey[1] = fkey2;
+    a.scan = scan;
+    a.rowbase = rowbase;
+    a.part = part;
+    const int64_t stiles_max = std::max<int64_t>(1, (n + kScanTileItems - 1) / kScanTileItems);
+    GFX_TRY(scratch_t(g, "psssp_status", stiles_max + 1, &a.status));
+    GFX_CK(cudaMemsetAsync(a.status, 0, (stiles_max + 1) * 8, ctx->stream));
+    a.C = C;
+    a.out_dist = dist;
+    a.out_preds = preds;
+    a.vec = ((reinterpret_cast<uintptr_t>(dist) | reinterpret_cast<uintptr_t>(preds) |
+              reinterpret_cast<uintptr_t>(dp)) & 15) == 0 ? 1 : 0;
+    a.delta = delta;
+    a.source = (int32_t)source;
+    const int64_t cap = 1 << 16;
+    GFX_TRY(scratch_t(g, "psssp_recs", cap, &a.recs));
+    a.rec_cap = cap;
+    GFX_TRY(scratch_t(g, "psssp_summary", 8, &a.summary));
+    GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
+    if (w8) GFX_TRY(launch_sssp_persistent<uint8_t>(ctx, a));
+    else GFX_TRY(launch_sssp_persistent<int32_t>(ctx, a));
+    GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));
+    long long summary[8];
+    GFX_CK(cudaMemcpyAsync(summary, a.summary, 5 * sizeof(long long), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+    GFX_CK(cudaStreamSynchronize(ctx->stream));
+    l2_window(ctx, nullptr, 0, false);
+    float ms = 0.f;
+    GFX_CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    const int64_t nrec = std::min<int64_t>(summary[3], recs ? rec_cap : 0);
+    if (nrec > 0)
+      GFX_CK(cudaMemcpy(recs, a.recs, nrec * sizeof(gfx_iter_rec), cudaMemcpyDeviceToHost));
+    if (st) {
+      *st = gfx_stats{};
+      st->iterations = summary[0];
+      st->edges_traversed = summary[1];
+      st->work_slots = summary[1];
+      st->bytes_alg = summary[2];
+      st->device_ms = ms;
+      st->num_records = nrec;
+      GFX_TRY(reached_stats(g, dist, &st->reached, &st->edges_reached));
+    }
+    return GFX_OK;
+  }
   GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
   GFX_CK(cudaMemsetAsync(dp, 0xFF, n * sizeof(unsigned long long), ctx->stream));
   GFX_CK(cudaMemsetAsync(dist32, 0xFF, n * sizeof(uint32_t), ctx->stream));
@@ -256,6 +525,7 @@ using namespace gfx;
 
 extern "C" int gfx_sssp(gfx_graph* g, int64_t source, double delta, int32_t* dist_d,
                         int32_t* preds_d, gfx_iter_rec* recs, int64_t rec_cap, gfx_stats* stats) {
+  GFX_NVTX("gfx_sssp");
   GFX_REQUIRE(g, "gfx_sssp: null graph");
   GFX_REQUIRE(source >= 0 && source < g->n, "source %lld out of range", (long long)source);
   GFX_REQUIRE(g->w != nullptr,

@@ -1,6 +1,9 @@
-// Near/far pile kernels shared by the single-GPU SSSP (gfx_sssp.cu) and the
+// Near/far pile phases shared by the single-GPU SSSP (gfx_sssp.cu: the
+// host-driven loop's kernels and the device-resident persistent loop) and the
 // partitioned SSSP engine (gfx_dsssp.cu).  Reference near_far.py:20-85.
-// `static` so each translation unit keeps its own copy (no -rdc).
+// Kernels are `static` so each translation unit keeps its own copy (no -rdc);
+// the phase bodies are device functions so the persistent loop runs them
+// between grid barriers.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -23,9 +26,10 @@ struct PileStage {
 };
 
 static __device__ __forceinline__ void pile_flush(PileStage& S, int32_t* __restrict__ near,
-                                           unsigned long long* __restrict__ near_len,
-                                           int32_t* __restrict__ far, int32_t* __restrict__ far_key,
-                                           unsigned long long* __restrict__ far_len) {
+                                                  unsigned long long* __restrict__ near_len,
+                                                  int32_t* __restrict__ far,
+                                                  int32_t* __restrict__ far_key,
+                                                  unsigned long long* __restrict__ far_len) {
   __syncthreads();
   if (threadIdx.x == 0) S.base = S.nn ? atomicAdd(near_len, (unsigned long long)S.nn) : 0ull;
   __syncthreads();
@@ -42,15 +46,13 @@ static __device__ __forceinline__ void pile_flush(PileStage& S, int32_t* __restr
   __syncthreads();
 }
 
-// split the improved vertices against the threshold (near_far.py:40-57)
-static __global__ void __launch_bounds__(256)
-    k_sssp_split(const int32_t* __restrict__ touched, const unsigned long long* __restrict__ n_d,
-                 const uint32_t* __restrict__ dist, uint32_t* __restrict__ mark, double threshold,
-                 int32_t* __restrict__ near, unsigned long long* __restrict__ near_len,
-                 int32_t* __restrict__ far, int32_t* __restrict__ far_key,
-                 unsigned long long* __restrict__ far_len) {
-  __shared__ PileStage S;
-  const int64_t n = (int64_t)*n_d;
+// split the improved vertices touched[0..n) against the threshold
+// (near_far.py:40-57); every CTA of the grid calls it (block-uniform loop)
+static __device__ __forceinline__ void sssp_split_phase(
+    PileStage& S, const int32_t* __restrict__ touched, int64_t n, const uint32_t* __restrict__ dist,
+    uint32_t* __restrict__ mark, double threshold, int32_t* __restrict__ near,
+    unsigned long long* __restrict__ near_len, int32_t* __restrict__ far,
+    int32_t* __restrict__ far_key, unsigned long long* __restrict__ far_len) {
   if (threadIdx.x == 0) S.nn = S.nfar = 0;
   __syncthreads();
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n;
@@ -75,16 +77,25 @@ static __global__ void __launch_bounds__(256)
   pile_flush(S, near, near_len, far, far_key, far_len);
 }
 
+static __global__ void __launch_bounds__(256)
+    k_sssp_split(const int32_t* __restrict__ touched, const unsigned long long* __restrict__ n_d,
+                 const uint32_t* __restrict__ dist, uint32_t* __restrict__ mark, double threshold,
+                 int32_t* __restrict__ near, unsigned long long* __restrict__ near_len,
+                 int32_t* __restrict__ far, int32_t* __restrict__ far_key,
+                 unsigned long long* __restrict__ far_len) {
+  __shared__ PileStage S;
+  sssp_split_phase(S, touched, (int64_t)*n_d, dist, mark, threshold, near, near_len, far, far_key,
+                   far_len);
+}
+
 // advance_bucket (near_far.py:68-85): drop stale far entries, split the rest
 // against the new threshold.  With split == false only the stale drop runs
 // (capacity compaction; everything fresh stays far).
-static __global__ void __launch_bounds__(256)
-    k_sssp_refar(const int32_t* __restrict__ far, const int32_t* __restrict__ far_key, int64_t n,
-                 const uint32_t* __restrict__ dist, double threshold, int split,
-                 int32_t* __restrict__ near, unsigned long long* __restrict__ near_len,
-                 int32_t* __restrict__ far2, int32_t* __restrict__ far2_key,
-                 unsigned long long* __restrict__ far2_len) {
-  __shared__ PileStage S;
+static __device__ __forceinline__ void sssp_refar_phase(
+    PileStage& S, const int32_t* __restrict__ far, const int32_t* __restrict__ far_key, int64_t n,
+    const uint32_t* __restrict__ dist, double threshold, int split, int32_t* __restrict__ near,
+    unsigned long long* __restrict__ near_len, int32_t* __restrict__ far2,
+    int32_t* __restrict__ far2_key, unsigned long long* __restrict__ far2_len) {
   if (threadIdx.x == 0) S.nn = S.nfar = 0;
   __syncthreads();
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n;
@@ -110,12 +121,23 @@ static __global__ void __launch_bounds__(256)
   pile_flush(S, near, near_len, far2, far2_key, far2_len);
 }
 
+static __global__ void __launch_bounds__(256)
+    k_sssp_refar(const int32_t* __restrict__ far, const int32_t* __restrict__ far_key, int64_t n,
+                 const uint32_t* __restrict__ dist, double threshold, int split,
+                 int32_t* __restrict__ near, unsigned long long* __restrict__ near_len,
+                 int32_t* __restrict__ far2, int32_t* __restrict__ far2_key,
+                 unsigned long long* __restrict__ far2_len) {
+  __shared__ PileStage S;
+  sssp_refar_phase(S, far, far_key, n, dist, threshold, split, near, near_len, far2, far2_key,
+                   far2_len);
+}
+
 // (dist | pred) words -> the two int32 outputs; two vertices per thread with
 // 16-byte loads and 8-byte stores when the outputs are 8-byte aligned
-static __global__ void k_sssp_unpack(const unsigned long long* __restrict__ dp, int64_t n,
-                              int32_t* __restrict__ dist, int32_t* __restrict__ preds, int vec) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+static __device__ __forceinline__ void sssp_unpack_phase(const unsigned long long* __restrict__ dp,
+                                                         int64_t n, int32_t* __restrict__ dist,
+                                                         int32_t* __restrict__ preds, int vec,
+                                                         int64_t t0, int64_t stride) {
   int64_t done = 0;
   if (vec) {
     const int64_t pairs = n >> 1;
@@ -135,6 +157,13 @@ static __global__ void k_sssp_unpack(const unsigned long long* __restrict__ dp, 
     dist[v] = d == 0xFFFFFFFFu ? GFX_UNVISITED : (int32_t)d;
     preds[v] = (int32_t)(uint32_t)x;
   }
+}
+
+static __global__ void k_sssp_unpack(const unsigned long long* __restrict__ dp, int64_t n,
+                                     int32_t* __restrict__ dist, int32_t* __restrict__ preds,
+                                     int vec) {
+  sssp_unpack_phase(dp, n, dist, preds, vec, blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
+                    (int64_t)gridDim.x * blockDim.x);
 }
 
 }  // namespace gfx

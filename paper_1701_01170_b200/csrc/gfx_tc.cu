@@ -510,6 +510,7 @@ static int build_reverse(gfx_graph* g, int64_t mo) {
 using namespace gfx;
 
 extern "C" int gfx_tc_orient(gfx_graph* g, int64_t* m_oriented) {
+  GFX_NVTX("gfx_tc_orient");
   GFX_REQUIRE(g && m_oriented, "gfx_tc_orient: null argument");
   GFX_REQUIRE(g->flags & GFX_GRAPH_UNDIRECTED, "tc expects a canonical undirected graph");
   gfx_ctx* ctx = g->ctx;
@@ -549,6 +550,7 @@ extern "C" int gfx_tc_orient(gfx_graph* g, int64_t* m_oriented) {
 
 extern "C" int gfx_tc_count(gfx_graph* g, int32_t* osrc_d, int32_t* odst_d, int32_t* counts_d,
                             int64_t* total, gfx_stats* stats) {
+  GFX_NVTX("gfx_tc_count");
   GFX_REQUIRE(g && total, "gfx_tc_count: null argument");
   GFX_REQUIRE(g->m_oriented >= 0, "gfx_tc_count: call gfx_tc_orient first");
   gfx_ctx* ctx = g->ctx;
@@ -676,6 +678,7 @@ extern "C" int gfx_tc_count(gfx_graph* g, int32_t* osrc_d, int32_t* odst_d, int3
 
 extern "C" int gfx_segmented_intersect(gfx_graph* g, const int32_t* u_d, const int32_t* v_d,
                                        int64_t num_pairs, int32_t* counts_d, int64_t* total) {
+  GFX_NVTX("gfx_segmented_intersect");
   GFX_REQUIRE(g && total && (num_pairs == 0 || (u_d && v_d && counts_d)),
               "gfx_segmented_intersect: null argument");
   GFX_CK(cudaSetDevice(g->ctx->device));

