@@ -553,7 +553,7 @@ def extras(args, dg, labels, preds, dist, peak):
         from paper_1701_01170_b200.generators import rmat_device_graph
 
         dgw = rmat_device_graph(args.scale, args.edge_factor, 0, weights=(1, 64), weight_seed=0)
-        for delta in (32, None):
+        for delta in (32, None, 4):
             for _ in range(2):
                 st = sssp_device(dgw, args.source, delta=delta)[2]
             # device time of the primitive as the library measures it (CUDA
@@ -677,22 +677,30 @@ def secondary(args, dg, peak):
 
 
 def e2e(args, dg, dist, e_r):
-    """End to end with host buffers, every step: the CSR is uploaded from
-    pinned host memory into the resident device graph (DeviceGraph.reload_,
-    C ABI gfx_graph_refresh recomputes the graph constants), the BFS runs
+    """End to end with host buffers, every step: the graph crosses PCIe from
+    pinned host memory into the resident device graph, the BFS runs
     (gfx_bfs), and the reference-layout int64 labels and preds are read back
-    into pinned host memory.  Step k's read-back runs on its own stream and
-    overlaps step k+1's upload (the two PCIe directions are independent);
-    the upload of step k+1 waits for BFS k.  Also reported: the same public
-    BFS call with the graph already resident (per-query host traffic only)."""
+    into pinned host memory.  The graph's host image is the packed CSR
+    (io.PackedCsr: int64 row offsets + the column ids as zigzag deltas in a
+    StreamVByte layout, ~1.9 instead of 4 bytes per slot), decoded on the
+    device (gfx_csr_unpack) before gfx_graph_refresh recomputes the graph
+    constants; the same loop with plain int32 columns is reported beside it.
+    Step k's read-back runs on its own stream and overlaps step k+1's upload
+    (the two PCIe directions are independent); the upload of step k+1 waits
+    for BFS k.  Also reported: the same public BFS call with the graph
+    already resident (per-query host traffic only)."""
     import torch
 
+    from paper_1701_01170_b200 import _native
     from paper_1701_01170_b200._native import UNVISITED32
     from paper_1701_01170_b200.graph import UNVISITED
+    from paper_1701_01170_b200.io import pack_csr_device
     from paper_1701_01170_b200.primitives.bfs import bfs_device
 
+    col_ref = dg.col.clone()
     row_h = dg.row.cpu().pin_memory()
     col_h = dg.col.cpu().pin_memory()
+    packed = pack_csr_device(dg)
     n = dg.num_vertices
     labels = torch.empty(n, dtype=torch.int32, device="cuda")
     preds = torch.empty(n, dtype=torch.int32, device="cuda")
@@ -713,15 +721,29 @@ def e2e(args, dg, dist, e_r):
         return ev
 
     def run(k_steps, upload):
-        pending = []
         for k in range(k_steps):
-            if upload:
+            if upload == "packed":
                 with torch.cuda.stream(up):
                     up.wait_stream(comp)  # BFS k-1 is done with the graph buffers
+                    st = getattr(dg, "_pack_stage", None)
+                    if st is None:
+                        dg._pack_stage = st = tuple(torch.empty_like(t, device="cuda") for t in
+                                                    (packed.ctrl, packed.data, packed.boff))
+                    dg.row.copy_(packed.row, non_blocking=True)
+                    for dst, src in zip(st, (packed.ctrl, packed.data, packed.boff)):
+                        dst.copy_(src, non_blocking=True)
+                comp.wait_stream(up)
+                ctrl, data, boff = dg._pack_stage
+                _native.call("gfx_csr_unpack", dg.ctx.handle, _native.ptr(ctrl),
+                             _native.ptr(data), _native.ptr(boff), dg.num_edges,
+                             _native.ptr(dg.col), 0)
+                _native.call("gfx_graph_refresh", dg.handle)
+            elif upload == "plain":
+                with torch.cuda.stream(up):
+                    up.wait_stream(comp)
                     dg.row.copy_(row_h, non_blocking=True)
                     dg.col.copy_(col_h, non_blocking=True)
                 comp.wait_stream(up)
-                from paper_1701_01170_b200 import _native
                 _native.call("gfx_graph_refresh", dg.handle)
             bfs_device(dg, args.source, direction=args.direction, labels=labels, preds=preds)
             ev = widen(k)
@@ -732,29 +754,39 @@ def e2e(args, dg, dist, e_r):
                 hp.copy_(wide[k % 2][1], non_blocking=True)
         torch.cuda.synchronize()
 
-    run(1, True)
-    dist.barrier()
-    torch.cuda.synchronize()
     k = max(2, min(args.steps, 5))
-    t0 = time.perf_counter()
-    run(k, True)
-    dt = dist.max((time.perf_counter() - t0) / k)
     total = dist.sum(float(e_r))
-    # check the last read-back against the device result (cheap sanity)
-    assert int(host[(k - 1) % 2][0][args.source]) == 0
-    h2d = row_h.numel() * 8 + col_h.numel() * 4
     d2h = n * 8 * 2
+    out = {}
+    for mode in ("plain", "packed"):
+        run(1, mode)
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        run(k, mode)
+        dt = dist.max((time.perf_counter() - t0) / k)
+        # the decoded graph is the graph; the last read-back is the device result
+        assert torch.equal(dg.col, col_ref), mode
+        assert int(host[(k - 1) % 2][0][args.source]) == 0
+        out[mode] = (dt, (row_h.numel() * 8 + col_h.numel() * 4) if mode == "plain"
+                     else packed.nbytes)
+    del col_ref
     t0 = time.perf_counter()
-    run(k, False)
+    run(k, None)
     dt_res = dist.max((time.perf_counter() - t0) / k)
     resident = {"value": round(total / dt_res / 1e9, 3), "unit": "GTEPS",
                 "h2d_bytes_per_step": 8, "d2h_bytes_per_step": d2h,
                 "ms_per_step": round(dt_res * 1e3, 3)}
+    dt, h2d = out["packed"]
+    dtp, h2dp = out["plain"]
     return {"value": round(total / dt / 1e9, 3), "unit": "GTEPS", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": round(dt * 1e3, 3), "steps": k,
-            "what": "per step: CSR upload from pinned host into the resident device graph "
-                    "(gfx_graph_refresh) + DO-BFS + int64 labels/preds read back to pinned host "
+            "what": "per step: the packed CSR (int64 rows + delta-coded columns) uploaded from "
+                    "pinned host, decoded into the resident device graph (gfx_csr_unpack, "
+                    "gfx_graph_refresh) + DO-BFS + int64 labels/preds read back to pinned host "
                     "(read-back overlapped with the next upload)",
+            "plain_int32_columns": {"value": round(total / dtp / 1e9, 3), "unit": "GTEPS",
+                                    "h2d_bytes_per_step": h2dp, "ms_per_step": round(dtp * 1e3, 3)},
             "graph_resident": resident}
 
 

@@ -295,6 +295,34 @@ class DeviceGraph:
         self._csc_dev = None  # stale reverse edge ids (the handle's reid)
         _native.call("gfx_graph_refresh", self.handle)
 
+    def reload_packed_(self, packed) -> None:
+        """``reload_`` from a ``io.PackedCsr``: the packed column streams
+        (about half the bytes of int32 columns) cross PCIe into device staging
+        buffers kept on this graph, are decoded in place into ``col`` on the
+        device (gfx_csr_unpack), then the graph constants are refreshed."""
+        import torch
+
+        if packed.num_vertices != self.num_vertices or packed.num_edges != self.num_edges:
+            raise ValueError("reload_packed_: shape differs from the resident graph")
+        if not self.undirected:
+            raise ValueError("reload_packed_: undirected graphs only")
+        st = getattr(self, "_pack_stage", None)
+        if st is None or st[1].numel() < packed.data.numel():
+            dev = self.row.device
+            st = (torch.empty(packed.ctrl.numel(), dtype=torch.uint8, device=dev),
+                  torch.empty(packed.data.numel(), dtype=torch.uint8, device=dev),
+                  torch.empty(packed.boff.numel(), dtype=torch.int64, device=dev))
+            self._pack_stage = st
+        ctrl, data, boff = st
+        self.row.copy_(packed.row, non_blocking=True)
+        ctrl[: packed.ctrl.numel()].copy_(packed.ctrl, non_blocking=True)
+        data[: packed.data.numel()].copy_(packed.data, non_blocking=True)
+        boff[: packed.boff.numel()].copy_(packed.boff, non_blocking=True)
+        _native.call("gfx_csr_unpack", self.ctx.handle, _native.ptr(ctrl), _native.ptr(data),
+                     _native.ptr(boff), self.num_edges, _native.ptr(self.col), 0)
+        self._csc_dev = None
+        _native.call("gfx_graph_refresh", self.handle)
+
     def refresh_weights(self, w) -> None:
         """Re-upload weights if the host graph's weight array was replaced."""
         if self.host is None or w is self._w_src:

@@ -18,6 +18,11 @@ from ..stats import RunStats
 
 @dataclass
 class CcResult:
+    """``component[v]`` is the SMALLEST vertex id of v's component (canonical
+    min-id labels).  The reference's labels are other representatives of the
+    same partition (its hooking order decides them, cc.py:62-72); map them
+    with ``label[v] = min{u : comp[u] == comp[v]}`` to compare."""
+
     component: np.ndarray
     num_components: int
     stats: RunStats
