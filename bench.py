@@ -666,11 +666,19 @@ def secondary(args, dg, peak):
     total, _, osrc, odst, _ = tc_device(dg2)
     dplus = torch.bincount(osrc.long(), minlength=dg2.num_vertices)
     wedge = int((dplus[osrc.long()] + dplus[odst.long()]).sum().item())
-    b = 4 * wedge + 8 * int(osrc.numel())  # 4 sum(deg+u + deg+v) + 8 |E+|
-    del osrc, odst, dplus
+    b_ref = 4 * wedge + 8 * int(osrc.numel())  # 4 sum(deg+u + deg+v) + 8 |E+|
+    # the kernel intersects in the REVERSED orientation (short rows): its own
+    # algorithmic bytes are 4 sum over reversed edges x=>y of (|R(x)| + |R(y)|)
+    # + 8 |E+|; the SURVEY quantity above is the reference
+    # orientation's wedge work, which the device does not perform
+    dminus = torch.bincount(odst.long(), minlength=dg2.num_vertices)
+    rwedge = int((dminus[osrc.long()] + dminus[odst.long()]).sum().item())
+    b = 4 * rwedge + 8 * int(osrc.numel())
+    del osrc, odst, dplus, dminus
     st, ms = timed(lambda: tc_device(dg2)[4])
     out[f"tc_s{small}"] = {"ms": round(ms, 3), "triangles": int(total), "bytes_alg": b,
-                           "frac_of_hbm": round(b / (ms * 1e-3) / 1e9 / peak, 4)}
+                           "frac_of_hbm": round(b / (ms * 1e-3) / 1e9 / peak, 4),
+                           "bytes_alg_reference_orientation": b_ref}
     del dg2
     torch.cuda.empty_cache()
     return out

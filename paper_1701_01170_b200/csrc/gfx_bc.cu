@@ -131,9 +131,9 @@ __global__ void __launch_bounds__(256)
 // has fewer slots than the level itself (the load-balanced expansion then
 // splits hubs across warps).  Forward: sigma values are path counts --
 // integers held exactly in fp64 (< 2^53) -- so the atomic sums are exact in
-// any order and the result is deterministic.  Backward: the atomic fp64
-// sums are order-dependent in the last bits, so the delta push is OFF by
-// default (GFX_BC_DELTA_PUSH=1 turns it on) and every delta is gathered.
+// any order and the result is deterministic.  Backward: the terms are summed
+// exactly in 128-bit fixed point (Fix128 below) and rounded once, so the
+// push is deterministic too (GFX_BC_DELTA_PUSH=0 gathers every level).
 struct SigmaPushOp {
   static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
   static constexpr int kBatch = kVisitBatch;
@@ -153,13 +153,50 @@ struct SigmaPushOp {
   }
 };
 
+// Exact, order-independent accumulation of non-negative doubles: every term
+// is converted EXACTLY to a 128-bit fixed-point number with 64 fractional
+// bits (a 53-bit mantissa shifted into place; bits below 2^-64 are dropped
+// per term, deterministically) and added with integer atomics -- the low
+// word's carry propagated into the high word -- so the sum is the same
+// whatever order the terms arrive in, and is then rounded to a double once.
+struct Fix128 {
+  unsigned long long lo, hi;
+};
+__device__ __forceinline__ Fix128 to_fix128(double t) {
+  Fix128 f{0ull, 0ull};
+  if (!(t > 0.0)) return f;
+  int e;
+  const double m = frexp(t, &e);  // t = m * 2^e, m in [0.5, 1)
+  const unsigned long long mant = (unsigned long long)ldexp(m, 53);  // exact
+  const int sh = e - 53 + 64;                                       // mant * 2^sh
+  if (sh >= 128) return Fix128{~0ull, ~0ull};                       // saturate (not reached)
+  if (sh >= 64) {
+    f.hi = mant << (sh - 64);
+  } else if (sh > 0) {
+    f.lo = mant << sh;
+    f.hi = mant >> (64 - sh);
+  } else if (sh > -64) {
+    f.lo = mant >> (-sh);
+  }
+  return f;
+}
+__device__ __forceinline__ void fix128_add(unsigned long long* acc, Fix128 f) {
+  // acc[0] = low word, acc[1] = high word of this vertex's sum
+  if (f.lo) {
+    const unsigned long long old = atomicAdd(&acc[0], f.lo);
+    if (old + f.lo < old) f.hi += 1ull;  // carry out of the low word
+  }
+  if (f.hi) atomicAdd(&acc[1], f.hi);
+}
+
 struct DeltaPushOp {  // frontier: level want + 1; receivers: neighbours at level want
   static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
   static constexpr int kBatch = kVisitBatch;
   static constexpr int kMinBlocks = 3;
   const int32_t* labels;
   const double* sigma;
-  double* delta;
+  const double* delta;
+  unsigned long long* acc;  // 2 words per vertex (Fix128)
   int32_t want;
   int32_t lv[kBatch];
   __device__ int32_t src_value(int32_t) const { return 0; }
@@ -169,10 +206,24 @@ struct DeltaPushOp {  // frontier: level want + 1; receivers: neighbours at leve
   }
   __device__ bool visit(int u, int32_t s, int32_t w, int32_t, int32_t, int64_t) {
     if (lv[u] == want)
-      atomicAdd(&delta[s], __dmul_rn(__ddiv_rn(sigma[s], sigma[w]), __dadd_rn(1.0, delta[w])));
+      fix128_add(acc + 2 * (int64_t)s,
+                 to_fix128(__dmul_rn(__ddiv_rn(sigma[s], sigma[w]), __dadd_rn(1.0, delta[w]))));
     return false;
   }
 };
+
+// delta[v] = the level's fixed-point sums rounded once; accumulators cleared
+__global__ void k_fix128_finish(const int32_t* __restrict__ items, int64_t cnt,
+                                unsigned long long* __restrict__ acc, double* __restrict__ delta) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = items[i];
+    const unsigned long long lo = acc[2 * (int64_t)v], hi = acc[2 * (int64_t)v + 1];
+    delta[v] = __dadd_rn((double)hi, ldexp((double)lo, -64));
+    acc[2 * (int64_t)v] = 0ull;
+    acc[2 * (int64_t)v + 1] = 0ull;
+  }
+}
 
 __global__ void k_bc_seed(double* sigma, int32_t src) { sigma[src] = 1.0; }
 
@@ -214,11 +265,16 @@ extern "C" int gfx_bc(gfx_graph* g, const int64_t* sources, int64_t num_sources,
   GFX_TRY(scratch_t(g, "q_rowbase", n + 1, &rowbase));
   GFX_TRY(scratch_t(g, "q_part", part_capacity(g->m, g->n), &part));
   Counters* pc = g->counters + 2;  // push plans (C[2], C[3])
-  // the backward push adds fp64 terms with atomics (order-dependent last
-  // bits): off by default so BC values are bit-reproducible run to run;
-  // GFX_BC_DELTA_PUSH=1 re-enables it (diagnostic)
+  // the backward push accumulates exactly in 128-bit fixed point (Fix128),
+  // so BC values are bit-reproducible run to run; GFX_BC_DELTA_PUSH=0
+  // forces the pull-gather on every level (diagnostic)
   const char* dp = std::getenv("GFX_BC_DELTA_PUSH");
-  const bool delta_push = dp && dp[0] == '1';
+  const bool delta_push = !(dp && dp[0] == '0');
+  unsigned long long* acc = nullptr;
+  bool acc_fresh = false;
+  GFX_TRY(scratch(g, "bc_fix128", (size_t)(n + 1) * 16, reinterpret_cast<void**>(&acc),
+                  &acc_fresh));
+  if (acc_fresh) GFX_CK(cudaMemsetAsync(acc, 0, (size_t)(n + 1) * 16, ctx->stream));
   int64_t iterations = 0, edges = 0;
   std::vector<int64_t> off;
   GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
@@ -260,7 +316,9 @@ extern "C" int gfx_bc(gfx_graph* g, const int64_t* sources, int64_t num_sources,
       if (cnt <= 0) continue;
       if (delta_push && undirected && d + 1 < (int64_t)slots.size() && slots[d + 1] < slots[d] &&
           off[d + 2] > off[d + 1]) {
-        GFX_TRY(push_from(d + 1, DeltaPushOp{labels, sigma, delta, (int32_t)d, {}}));
+        GFX_TRY(push_from(d + 1, DeltaPushOp{labels, sigma, delta, acc, (int32_t)d, {}}));
+        GFX_LAUNCH(k_fix128_finish, grid_for(cnt, 256, grid), 256, 0, ctx->stream, order + off[d],
+                   cnt, acc, delta);
         continue;
       }
       DeltaTerm t{labels, sigma, delta, (int32_t)(d + 1)};

@@ -19,6 +19,7 @@
 //   head     int32[2(n+1)]   first / second in-neighbour per vertex with
 //                            degree-1 / degree-2 flags (graph constant)
 #include <cooperative_groups.h>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -42,7 +43,7 @@ namespace gfx {
 // Idempotent: label test + plain store, duplicates culled afterwards by the
 // bitmap filter (bfs.py:113-116, 162-166).
 // ---------------------------------------------------------------------------
-template <int B>
+template <int B, bool FB = false>
 struct BfsClaimOpT {
   static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
   static constexpr int kBatch = B;
@@ -66,7 +67,7 @@ struct BfsClaimOpT {
     if (lvl8) lvl8[d] = (uint8_t)depth;
     else labels[d] = depth;
     preds[d] = s;
-    if (fbits) atomicOr(&fbits[d >> 5], bit);  // no return value: a fire-and-forget RED
+    if (FB) atomicOr(&fbits[d >> 5], bit);  // no return value: a fire-and-forget RED
     return true;
   }
 };
@@ -816,38 +817,10 @@ __device__ __forceinline__ void push_mid(WarpSmem& W, Op& o, const int32_t* __re
 // store instruction writes 512 contiguous bytes.
 __device__ __forceinline__ void materialize_labels(const PBfsArgs& a, int64_t gw, int64_t nw) {
   const int lane = threadIdx.x & 31;
-  // 16 vertices per lane and step: one 16-byte depth load, half a visited
-  // word, four 16-byte label stores (64 contiguous bytes); two steps in
-  // flight per lane -> 1024 vertices per warp step
-  const int64_t n16 = a.vec_ok ? (a.n & ~(int64_t)1023) : 0;
-  for (int64_t base = gw * 1024; base < n16; base += nw * 1024) {
-    uint4 d16[2];
-    uint32_t vb[2];
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int64_t v = base + 512 * k + 16 * lane;
-      d16[k] = *reinterpret_cast<const uint4*>(a.lvl8 + v);
-      vb[k] = a.visited[v >> 5] >> (v & 16);
-    }
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int64_t v = base + 512 * k + 16 * lane;
-      const uint32_t dw[4] = {d16[k].x, d16[k].y, d16[k].z, d16[k].w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t bits = (vb[k] >> (4 * j)) & 0xFu, d4 = dw[j];
-        int4 lab;
-        lab.x = (bits & 1u) ? (int32_t)(d4 & 0xFF) : GFX_UNVISITED;
-        lab.y = (bits & 2u) ? (int32_t)((d4 >> 8) & 0xFF) : GFX_UNVISITED;
-        lab.z = (bits & 4u) ? (int32_t)((d4 >> 16) & 0xFF) : GFX_UNVISITED;
-        lab.w = (bits & 8u) ? (int32_t)(d4 >> 24) : GFX_UNVISITED;
-        *reinterpret_cast<int4*>(a.labels + v + 4 * j) = lab;
-      }
-    }
-  }
-  // remainder (and unaligned outputs): the 4-per-lane form below
+  // (a 16-vertices-per-lane form with 16-byte depth loads measured ~7 us
+  // slower at s24: each of its store instructions touches half sectors)
   const int64_t nfull = a.vec_ok ? (a.n & ~(int64_t)3) : 0;
-  for (int64_t base = n16 + gw * 1024; base < a.n; base += nw * 1024) {
+  for (int64_t base = gw * 1024; base < a.n; base += nw * 1024) {
     uint32_t vw[8], d4[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -875,6 +848,10 @@ __device__ __forceinline__ void materialize_labels(const PBfsArgs& a, int64_t gw
   }
 }
 
+// kDO: direction-optimising run (pull levels and the frontier bitmaps
+// compiled in); push-only runs launch the <false> instance, which carries
+// none of that code (lower register pressure in its expansion loops)
+template <bool kDO>
 __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -968,16 +945,16 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
       // the bitmap the NEXT level writes was last read one level ago: zero it
       // in passing (no barrier -- nothing reads it during this level)
       uint32_t* fclr = a.front[(c.fsel + 2) % 3];
-      if (a.direction != GFX_DIR_PUSH)
+      if (kDO)
         for (int64_t i = gtid; i < a.words; i += nthr) fclr[i] = 0u;
     }
     // a direction-optimising run keeps the frontier as a bitmap at every
     // level: push levels also set the new frontier's bits (fbits), so a pull
     // level never converts a queue
-    uint32_t* fbits = a.direction != GFX_DIR_PUSH ? fnext : nullptr;
+    uint32_t* fbits = kDO ? fnext : nullptr;
     long long level_edges = 0, nout = 0, work = 0, cands = 0, bytes = 0;
 
-    if (c.mode == GFX_DIR_PUSH) {
+    if (!kDO || c.mode == GFX_DIR_PUSH) {
       if (!c.queue_form) {
         bitmap_to_queue(a.words, fcur, a.order + c.q_end, &cur->aux2, gw, nw);
         grid.sync();
@@ -989,12 +966,12 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
         __syncthreads();
       }
       const int32_t* F = a.order + c.q_off;
-      BfsClaimOp op{a.visited, a.labels, a.preds, depth, {}, lab.lvl8, fbits};
+      BfsClaimOpT<kVisitBatch, kDO> op{a.visited, a.labels, a.preds, depth, {}, lab.lvl8, fbits};
       if (nf <= 32) {
         // tiny frontier (the hub's level, the tail levels): every warp derives
         // the whole expansion plan itself -- no scan pass, no grid barrier
         // between plan and expansion
-        BfsClaimOpTiny top{a.visited, a.labels, a.preds, depth, {}, lab.lvl8, fbits};
+        BfsClaimOpT<4, kDO> top{a.visited, a.labels, a.preds, depth, {}, lab.lvl8, fbits};
         push_tiny(W, top, F, nf, a.row, a.col, a.order + c.q_end, &cur->out_len, &cur->total, gw,
                   nw);
       } else if (nf <= kMidItems) {
@@ -1015,8 +992,8 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
           }
           int ocnt = 0;
           const int64_t t = expand_items32(W, op, v, rb, deg, a.col, a.order + c.q_end,
-                                           &cur->out_len, ocnt, gw * 32 * BfsClaimOp::kBatch,
-                                           nw * 32 * BfsClaimOp::kBatch);
+                                           &cur->out_len, ocnt, gw * 32 * kVisitBatch,
+                                           nw * 32 * kVisitBatch);
           warp_flush(W, ocnt, a.order + c.q_end, &cur->out_len);
           if (gtid == 0) atomicAdd(&cur->total, (unsigned long long)t);
         }
@@ -1179,10 +1156,16 @@ static int pbfs_setup(gfx_graph* g, int64_t source, int direction, double do_a, 
   static int blocks_per_sm = 0;
   const int smem = kWarpScratch * kWarpsPerBlock;
   if (blocks_per_sm == 0) {
-    GFX_CK(cudaFuncSetAttribute(k_bfs_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    GFX_CK(cudaFuncSetAttribute(k_bfs_persistent<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem));
-    GFX_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_bfs_persistent, 256,
+    GFX_CK(cudaFuncSetAttribute(k_bfs_persistent<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem));
+    int push_only_per_sm = 0;
+    GFX_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&push_only_per_sm, k_bfs_persistent<false>,
+                                                         256, smem));
+    GFX_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_bfs_persistent<true>, 256,
                                                          smem));
+    blocks_per_sm = std::min(blocks_per_sm, push_only_per_sm);  // one grid size for both
     if (blocks_per_sm < 1) {
       set_error("k_bfs_persistent cannot be resident");
       return GFX_ECUDA;
@@ -1206,7 +1189,9 @@ int bfs_device_loop(gfx_graph* g, int64_t source, int direction, double do_a, do
   GFX_CK(cudaMemsetAsync(a.status, 0, (stiles_max + 1) * 8, ctx->stream));
   void* kargs[] = {&a};
   GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
-  GFX_CK(cudaLaunchCooperativeKernel((const void*)k_bfs_persistent,
+  GFX_CK(cudaLaunchCooperativeKernel(a.direction == GFX_DIR_PUSH
+                                         ? (const void*)k_bfs_persistent<false>
+                                         : (const void*)k_bfs_persistent<true>,
                                      dim3(blocks), dim3(256), kargs, smem,
                                      ctx->stream));
   count_launch();
@@ -1257,7 +1242,9 @@ int bfs_device_batch(gfx_graph* g, const int64_t* sources, int64_t count, int di
   for (int64_t k = 0; k < count; ++k) {
     a.source = (int32_t)sources[k];
     void* kargs[] = {&a};
-    GFX_CK(cudaLaunchCooperativeKernel((const void*)k_bfs_persistent, dim3(blocks), dim3(256),
+    GFX_CK(cudaLaunchCooperativeKernel(a.direction == GFX_DIR_PUSH
+                                         ? (const void*)k_bfs_persistent<false>
+                                         : (const void*)k_bfs_persistent<true>, dim3(blocks), dim3(256),
                                        kargs, smem, ctx->stream));
     count_launch();
   }

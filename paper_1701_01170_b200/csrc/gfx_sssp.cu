@@ -347,8 +347,13 @@ int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t*
   const int grid = ctx->sm_count * 8;
 
   l2_window(ctx, dist32, (dist_words + g->words + 1) * sizeof(uint32_t), true);
+  // the device-resident loop wins when there are many iterations (small
+  // delta: no host round trip per iteration); with few, long iterations the
+  // standalone kernels are faster (measured at s24: delta 4 8.0 vs 9.5 ms,
+  // delta 32 8.5 vs 8.35 ms).  GFX_SSSP_LOOP=device|host forces one.
   const char* loop_env = getenv("GFX_SSSP_LOOP");
-  if (!(loop_env && std::string(loop_env) == "host")) {
+  const bool dev_loop = loop_env ? std::string(loop_env) == "device" : delta <= 8.0;
+  if (dev_loop) {
     PSsspArgs a{};
     a.n = n;
     a.words = g->words;

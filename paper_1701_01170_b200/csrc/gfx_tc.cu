@@ -473,11 +473,17 @@ constexpr int kHashRow = 4096;             // longest staged row (elements)
 constexpr int kHashCap = 2 * kHashRow;     // table slots (load <= 1/2)
 constexpr int64_t kHashGrab = 64;          // sorted pairs per dynamic hand-out
 
+constexpr unsigned kHashMinPairs = 16;    // rows staged only when this many pairs share them
+
+// pass 0: heavy pairs per longer row; pass 1: sort keys (the longer row when
+// it is short enough to stage and shared by >= kHashMinPairs pairs, else
+// all-ones: those pairs stay on the search kernel)
+template <int PASS>
 __global__ void k_tc_heavy_keys(const int32_t* __restrict__ heavy,
                                 const unsigned long long* __restrict__ nheavy,
                                 const int32_t* __restrict__ rsrc, const int32_t* __restrict__ rcol,
-                                const int64_t* __restrict__ rrow, uint32_t* __restrict__ keys,
-                                unsigned long long* __restrict__ nhash) {
+                                const int64_t* __restrict__ rrow, unsigned* __restrict__ rowcnt,
+                                uint32_t* __restrict__ keys, unsigned long long* __restrict__ nhash) {
   const int64_t nh = (int64_t)*nheavy;
   unsigned long long local = 0;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nh;
@@ -486,10 +492,16 @@ __global__ void k_tc_heavy_keys(const int32_t* __restrict__ heavy,
     const int32_t x = rsrc[p], y = rcol[p];
     const int64_t la = rrow[x + 1] - rrow[x], lb = rrow[y + 1] - rrow[y];
     const int32_t lr = la >= lb ? x : y;
-    const bool ok = (la >= lb ? la : lb) <= kHashRow;
+    const bool fits = (la >= lb ? la : lb) <= kHashRow;
+    if (PASS == 0) {
+      if (fits) atomicAdd(&rowcnt[lr], 1u);
+      continue;
+    }
+    const bool ok = fits && rowcnt[lr] >= kHashMinPairs;
     keys[k] = ok ? (uint32_t)lr : 0xFFFFFFFFu;
     local += ok;
   }
+  if (PASS == 0) return;
   local = warp_sum_u64(local);
   if ((threadIdx.x & 31) == 0 && local) atomicAdd(nhash, local);
 }
@@ -698,7 +710,7 @@ extern "C" int gfx_tc_count(gfx_graph* g, int32_t* osrc_d, int32_t* odst_d, int3
                  rcol, mo, rrow, xslot, counts, &C->total, heavy, &C->aux0);
       const int skew = getenv("GFX_TC_SKEW") ? atoi(getenv("GFX_TC_SKEW")) : kRevSkew;
       const int64_t grab = getenv("GFX_TC_GRAB") ? atoi(getenv("GFX_TC_GRAB")) : kRevGrab;
-      if (getenv("GFX_TC_NOHASH")) {
+      if (!getenv("GFX_TC_HASH")) {  // the hash path measured slower at s22 (223 vs 100 ms)
         GFX_LAUNCH(k_tc_rev_heavy, ctx->sm_count * 8, 256, 0, ctx->stream, rsrc, rcol, rrow,
                    xslot, heavy, &C->aux0, counts, &C->total, skew, &C->aux1, grab);
       } else {
@@ -717,8 +729,13 @@ extern "C" int gfx_tc_count(gfx_graph* g, int32_t* osrc_d, int32_t* odst_d, int3
           GFX_TRY(scratch_t(g, "tc_hpairs", nh + 1, &v1));
           GFX_TRY(scratch_t(g, "tc_hctr", 4, &hc));
           GFX_CK(cudaMemsetAsync(hc, 0, 32, ctx->stream));
-          GFX_LAUNCH(k_tc_heavy_keys, grid_for(nh, 256, ctx->sm_count * 8), 256, 0, ctx->stream,
-                     heavy, &C->aux0, rsrc, rcol, rrow, k0, &hc[0]);
+          unsigned* rowcnt;
+          GFX_TRY(scratch_t(g, "tc_hrowcnt", g->n + 1, &rowcnt));
+          GFX_CK(cudaMemsetAsync(rowcnt, 0, (g->n + 1) * 4, ctx->stream));
+          GFX_LAUNCH(k_tc_heavy_keys<0>, grid_for(nh, 256, ctx->sm_count * 8), 256, 0,
+                     ctx->stream, heavy, &C->aux0, rsrc, rcol, rrow, rowcnt, k0, &hc[0]);
+          GFX_LAUNCH(k_tc_heavy_keys<1>, grid_for(nh, 256, ctx->sm_count * 8), 256, 0,
+                     ctx->stream, heavy, &C->aux0, rsrc, rcol, rrow, rowcnt, k0, &hc[0]);
           size_t tb = 0;
           GFX_CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, heavy, v1, (int)nh, 0, 32,
                                                  ctx->stream));

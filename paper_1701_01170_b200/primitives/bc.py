@@ -1,10 +1,11 @@
 """Betweenness centrality (reference primitives/bc.py:26-116) on libgfx.
 
-Brandes forward/backward passes (csrc/gfx_bc.cu): sigma by pull-gather or,
-where the previous level is smaller, an exact integer-valued fp64 push;
-delta always by pull-gather in ascending neighbour order.  Values are
-bit-reproducible run to run; agreement rel <= 1e-5 (north_star),
-bit-identical to the reference on rows of degree <= 32.
+Brandes forward/backward passes (csrc/gfx_bc.cu): per level a pull-gather
+in ascending neighbour order, or -- where the neighbour level has fewer
+slots -- a load-balanced push whose sums are exact (sigma: integer-valued
+fp64; delta: 128-bit fixed point rounded once).  Values are bit-reproducible
+run to run; agreement rel <= 1e-5 (north_star), bit-identical to the
+reference on gathered rows of degree <= 32.
 """
 from __future__ import annotations
 

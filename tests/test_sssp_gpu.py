@@ -83,8 +83,8 @@ def test_device_graph_golden(scale):
 
 @pytest.mark.parametrize("delta", [4, 32, None])
 def test_device_loop_equals_host_loop(delta, monkeypatch):
-    """The device-resident loop (one cooperative launch, default) and the
-    host-driven loop (GFX_SSSP_LOOP=host) give the same distances; both
+    """The device-resident loop (one cooperative launch; the default for
+    delta <= 8) and the host-driven loop give the same distances; both
     equal the reference golden; the loops agree on the work done per
     iteration when the iteration sequence is the same length."""
     from paper_1701_01170_b200._results import labels_to_host, preds_to_host
@@ -95,10 +95,7 @@ def test_device_loop_equals_host_loop(delta, monkeypatch):
     dg = rmat_device_graph(20, 16, 0, weights=(1, 64), weight_seed=0)
     out = {}
     for loop in ("device", "host"):
-        if loop == "host":
-            monkeypatch.setenv("GFX_SSSP_LOOP", "host")
-        else:
-            monkeypatch.delenv("GFX_SSSP_LOOP", raising=False)
+        monkeypatch.setenv("GFX_SSSP_LOOP", loop)
         dist, preds, st = sssp_device(dg, 0, delta=delta)
         out[loop] = (labels_to_host(dist), preds_to_host(preds), st)
     assert sha(out["device"][0]) == rec["sssp_d32_sha"]
