@@ -705,7 +705,7 @@ def e2e(args, dg, dist, e_r):
     from paper_1701_01170_b200.io import pack_csr_device
     from paper_1701_01170_b200.primitives.bfs import bfs_device
 
-    col_ref = dg.col.clone()
+    col_ref, row_ref = dg.col.clone(), dg.row.clone()
     row_h = dg.row.cpu().pin_memory()
     col_h = dg.col.cpu().pin_memory()
     packed = pack_csr_device(dg)
@@ -733,19 +733,9 @@ def e2e(args, dg, dist, e_r):
             if upload == "packed":
                 with torch.cuda.stream(up):
                     up.wait_stream(comp)  # BFS k-1 is done with the graph buffers
-                    st = getattr(dg, "_pack_stage", None)
-                    if st is None:
-                        dg._pack_stage = st = tuple(torch.empty_like(t, device="cuda") for t in
-                                                    (packed.ctrl, packed.data, packed.boff))
-                    dg.row.copy_(packed.row, non_blocking=True)
-                    for dst, src in zip(st, (packed.ctrl, packed.data, packed.boff)):
-                        dst.copy_(src, non_blocking=True)
+                    dg.upload_packed_(packed)
                 comp.wait_stream(up)
-                ctrl, data, boff = dg._pack_stage
-                _native.call("gfx_csr_unpack", dg.ctx.handle, _native.ptr(ctrl),
-                             _native.ptr(data), _native.ptr(boff), dg.num_edges,
-                             _native.ptr(dg.col), 0)
-                _native.call("gfx_graph_refresh", dg.handle)
+                dg.decode_packed_()
             elif upload == "plain":
                 with torch.cuda.stream(up):
                     up.wait_stream(comp)
@@ -774,11 +764,11 @@ def e2e(args, dg, dist, e_r):
         run(k, mode)
         dt = dist.max((time.perf_counter() - t0) / k)
         # the decoded graph is the graph; the last read-back is the device result
-        assert torch.equal(dg.col, col_ref), mode
+        assert torch.equal(dg.col, col_ref) and torch.equal(dg.row, row_ref), mode
         assert int(host[(k - 1) % 2][0][args.source]) == 0
         out[mode] = (dt, (row_h.numel() * 8 + col_h.numel() * 4) if mode == "plain"
                      else packed.nbytes)
-    del col_ref
+    del col_ref, row_ref
     t0 = time.perf_counter()
     run(k, None)
     dt_res = dist.max((time.perf_counter() - t0) / k)
@@ -789,8 +779,8 @@ def e2e(args, dg, dist, e_r):
     dtp, h2dp = out["plain"]
     return {"value": round(total / dt / 1e9, 3), "unit": "GTEPS", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": round(dt * 1e3, 3), "steps": k,
-            "what": "per step: the packed CSR (int64 rows + delta-coded columns) uploaded from "
-                    "pinned host, decoded into the resident device graph (gfx_csr_unpack, "
+            "what": "per step: the packed CSR (delta-coded row offsets and columns) uploaded "
+                    "from pinned host, decoded into the resident device graph (gfx_csr_unpack, "
                     "gfx_graph_refresh) + DO-BFS + int64 labels/preds read back to pinned host "
                     "(read-back overlapped with the next upload)",
             "plain_int32_columns": {"value": round(total / dtp / 1e9, 3), "unit": "GTEPS",

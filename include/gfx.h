@@ -337,15 +337,17 @@ GFX_API int gfx_segmented_intersect_list(gfx_graph* g, const int32_t* u_d, const
  * deltas to the previous slot in a StreamVByte-like layout: ctrl_d holds a
  * 2-bit length code per slot ((m+3)/4 bytes), data_d the 1..4 low bytes of
  * each delta, boff_d[b] the data offset of slot block b (1024 slots per
- * block, (m+1023)/1024 + 1 entries).  pack_size fills boff_d and returns the
- * data size; unpack decodes into col_d (int32[m]); sync = 0 leaves the work
- * enqueued on the ctx stream. */
-GFX_API int gfx_csr_pack_size(gfx_ctx* ctx, const int32_t* col_d, int64_t m, int64_t* boff_d,
-                              int64_t* data_bytes);
-GFX_API int gfx_csr_pack(gfx_ctx* ctx, const int32_t* col_d, int64_t m, const int64_t* boff_d,
-                         uint8_t* ctrl_d, uint8_t* data_d);
+ * block, (m+1023)/1024 + 1 entries).  vals_d: int32 column ids (elem_bytes
+ * 4) or int64 row offsets (elem_bytes 8; differences = degrees < 2^31).
+ * pack_size fills boff_d and returns the data size; unpack decodes into
+ * vals_d; sync = 0 leaves the work enqueued on the ctx stream. */
+GFX_API int gfx_csr_pack_size(gfx_ctx* ctx, const void* vals_d, int elem_bytes, int64_t m,
+                              int64_t* boff_d, int64_t* data_bytes);
+GFX_API int gfx_csr_pack(gfx_ctx* ctx, const void* vals_d, int elem_bytes, int64_t m,
+                         const int64_t* boff_d, uint8_t* ctrl_d, uint8_t* data_d);
 GFX_API int gfx_csr_unpack(gfx_ctx* ctx, const uint8_t* ctrl_d, const uint8_t* data_d,
-                           const int64_t* boff_d, int64_t m, int32_t* col_d, int sync);
+                           const int64_t* boff_d, int64_t m, void* vals_d, int elem_bytes,
+                           int sync);
 
 /* ---- bit-exact R-MAT + canonical CSR builder ----------------------------
  * (reference generators.py:22-52, graph.py:158-203, graph.py:227-246)

@@ -130,9 +130,10 @@ _SIGS = {
     "gfx_compute": (c_int, [c_void_p, c_void_p, c_int64, c_int, POINTER(FunctorArgs), c_void_p]),
     "gfx_segmented_intersect_list": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
                                              c_void_p]),
-    "gfx_csr_pack_size": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, POINTER(c_int64)]),
-    "gfx_csr_pack": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
-    "gfx_csr_unpack": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
+    "gfx_csr_pack_size": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_void_p,
+                                  POINTER(c_int64)]),
+    "gfx_csr_pack": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_void_p, c_void_p, c_void_p]),
+    "gfx_csr_unpack": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int,
                                c_int]),
     "gfx_rmat_keys": (c_int, [c_void_p, c_int, c_int, POINTER(c_double), c_uint64, c_uint64,
                               c_uint64, c_uint64, c_int, c_void_p, POINTER(c_int64)]),

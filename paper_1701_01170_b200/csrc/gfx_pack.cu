@@ -24,14 +24,18 @@ __device__ __forceinline__ uint32_t zz_len(uint32_t z) {
   return 1u + (z >= (1u << 8)) + (z >= (1u << 16)) + (z >= (1u << 24));
 }
 
-__device__ __forceinline__ uint32_t zz_delta(const int32_t* __restrict__ col, int64_t j) {
-  const int32_t prev = j ? col[j - 1] : 0;
-  const int32_t d = col[j] - prev;
+// zigzag of the difference to the previous element (int32 column ids, or
+// int64 row offsets whose differences -- the degrees -- fit 32 bits)
+template <class T>
+__device__ __forceinline__ uint32_t zz_delta(const T* __restrict__ col, int64_t j) {
+  const T prev = j ? col[j - 1] : T(0);
+  const int32_t d = (int32_t)(col[j] - prev);
   return ((uint32_t)d << 1) ^ (uint32_t)(d >> 31);
 }
 
 // pass 1: data bytes per block (warp per block)
-__global__ void k_pack_sizes(const int32_t* __restrict__ col, int64_t m,
+template <class T>
+__global__ void k_pack_sizes(const T* __restrict__ col, int64_t m,
                              int64_t* __restrict__ bsize) {
   const int lane = threadIdx.x & 31;
   const int64_t nb = (m + kPackBlock - 1) / kPackBlock;
@@ -47,7 +51,8 @@ __global__ void k_pack_sizes(const int32_t* __restrict__ col, int64_t m,
 
 // pass 2: control and data streams (warp per block; lanes take 32 slots at a
 // time, a warp scan of the lengths places each value's bytes)
-__global__ void k_pack_write(const int32_t* __restrict__ col, int64_t m,
+template <class T>
+__global__ void k_pack_write(const T* __restrict__ col, int64_t m,
                              const int64_t* __restrict__ boff, uint8_t* __restrict__ ctrl,
                              uint8_t* __restrict__ data) {
   const int lane = threadIdx.x & 31;
@@ -78,9 +83,9 @@ __global__ void k_pack_write(const int32_t* __restrict__ col, int64_t m,
 }
 
 // decode: warp per block -> zigzag deltas decoded to int32 differences
+template <class T>
 __global__ void k_unpack_deltas(const uint8_t* __restrict__ ctrl, const uint8_t* __restrict__ data,
-                                const int64_t* __restrict__ boff, int64_t m,
-                                int32_t* __restrict__ out) {
+                                const int64_t* __restrict__ boff, int64_t m, T* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int64_t nb = (m + kPackBlock - 1) / kPackBlock;
   for (int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; b < nb;
@@ -99,7 +104,7 @@ __global__ void k_unpack_deltas(const uint8_t* __restrict__ ctrl, const uint8_t*
         if (len > 1) z |= (uint32_t)p[1] << 8;
         if (len > 2) z |= (uint32_t)p[2] << 16;
         if (len > 3) z |= (uint32_t)p[3] << 24;
-        out[j] = (int32_t)((z >> 1) ^ (0u - (z & 1u)));
+        out[j] = (T)(int32_t)((z >> 1) ^ (0u - (z & 1u)));
       }
       pos += tot;
     }
@@ -110,20 +115,14 @@ __global__ void k_unpack_deltas(const uint8_t* __restrict__ ctrl, const uint8_t*
 
 using namespace gfx;
 
-extern "C" {
-
-int gfx_csr_pack_size(gfx_ctx* ctx, const int32_t* col_d, int64_t m, int64_t* boff_d,
-                      int64_t* data_bytes) {
-  GFX_NVTX("gfx_csr_pack_size");
-  GFX_REQUIRE(ctx && data_bytes && (m == 0 || (col_d && boff_d)), "gfx_csr_pack_size: null argument");
-  GFX_CK(cudaSetDevice(ctx->device));
+template <class T>
+static int pack_size_t(gfx_ctx* ctx, const T* col_d, int64_t m, int64_t* boff_d,
+                       int64_t* data_bytes) {
   const int64_t nb = (m + kPackBlock - 1) / kPackBlock;
-  *data_bytes = 0;
-  if (m == 0) return GFX_OK;
   int64_t* bsize;
   GFX_CK(cudaMallocAsync(&bsize, (nb + 1) * 8, ctx->stream));
   GFX_CK(cudaMemsetAsync(bsize + nb, 0, 8, ctx->stream));
-  GFX_LAUNCH(k_pack_sizes, grid_for(nb * 32, 256, ctx->sm_count * 16), 256, 0, ctx->stream,
+  GFX_LAUNCH(k_pack_sizes<T>, grid_for(nb * 32, 256, ctx->sm_count * 16), 256, 0, ctx->stream,
              col_d, m, bsize);
   size_t tb = 0;
   GFX_CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, bsize, boff_d, nb + 1, ctx->stream));
@@ -140,34 +139,14 @@ int gfx_csr_pack_size(gfx_ctx* ctx, const int32_t* col_d, int64_t m, int64_t* bo
   return GFX_OK;
 }
 
-int gfx_csr_pack(gfx_ctx* ctx, const int32_t* col_d, int64_t m, const int64_t* boff_d,
-                 uint8_t* ctrl_d, uint8_t* data_d) {
-  GFX_NVTX("gfx_csr_pack");
-  GFX_REQUIRE(ctx && (m == 0 || (col_d && boff_d && ctrl_d && data_d)), "gfx_csr_pack: null argument");
-  GFX_CK(cudaSetDevice(ctx->device));
-  if (m == 0) return GFX_OK;
+template <class T>
+static int unpack_t(gfx_ctx* ctx, const uint8_t* ctrl_d, const uint8_t* data_d,
+                    const int64_t* boff_d, int64_t m, T* col_d) {
   const int64_t nb = (m + kPackBlock - 1) / kPackBlock;
-  GFX_CK(cudaMemsetAsync(ctrl_d, 0, (m + 3) / 4, ctx->stream));
-  GFX_LAUNCH(k_pack_write, grid_for(nb * 32, 256, ctx->sm_count * 16), 256, 0, ctx->stream, col_d,
-             m, boff_d, ctrl_d, data_d);
-  GFX_CK(cudaGetLastError());
-  GFX_CK(cudaStreamSynchronize(ctx->stream));
-  return GFX_OK;
-}
-
-int gfx_csr_unpack(gfx_ctx* ctx, const uint8_t* ctrl_d, const uint8_t* data_d,
-                   const int64_t* boff_d, int64_t m, int32_t* col_d, int sync) {
-  GFX_NVTX("gfx_csr_unpack");
-  GFX_REQUIRE(ctx && (m == 0 || (ctrl_d && data_d && boff_d && col_d)),
-              "gfx_csr_unpack: null argument");
-  GFX_REQUIRE(m < (int64_t)INT32_MAX * 2, "gfx_csr_unpack: too many slots for one scan");
-  GFX_CK(cudaSetDevice(ctx->device));
-  if (m == 0) return GFX_OK;
-  const int64_t nb = (m + kPackBlock - 1) / kPackBlock;
-  GFX_LAUNCH(k_unpack_deltas, grid_for(nb * 32, 256, ctx->sm_count * 16), 256, 0, ctx->stream,
+  GFX_LAUNCH(k_unpack_deltas<T>, grid_for(nb * 32, 256, ctx->sm_count * 16), 256, 0, ctx->stream,
              ctrl_d, data_d, boff_d, m, col_d);
-  // prefix sum of the differences restores the ids (int32 wrap-around is
-  // harmless: every partial sum is a real column id)
+  // prefix sum of the differences restores the values (for int32 columns the
+  // wrap-around is harmless: every partial sum is a real column id)
   size_t tb = 0;
   GFX_CK(cub::DeviceScan::InclusiveSum(nullptr, tb, col_d, col_d, m, ctx->stream));
   void* tmp;
@@ -175,6 +154,54 @@ int gfx_csr_unpack(gfx_ctx* ctx, const uint8_t* ctrl_d, const uint8_t* data_d,
   GFX_CK(cub::DeviceScan::InclusiveSum(tmp, tb, col_d, col_d, m, ctx->stream));
   count_launch();
   GFX_CK(cudaFreeAsync(tmp, ctx->stream));
+  return GFX_OK;
+}
+
+extern "C" {
+
+int gfx_csr_pack_size(gfx_ctx* ctx, const void* vals_d, int elem_bytes, int64_t m, int64_t* boff_d,
+                      int64_t* data_bytes) {
+  GFX_NVTX("gfx_csr_pack_size");
+  GFX_REQUIRE(ctx && data_bytes && (m == 0 || (vals_d && boff_d)), "gfx_csr_pack_size: null argument");
+  GFX_REQUIRE(elem_bytes == 4 || elem_bytes == 8, "elem_bytes must be 4 (int32) or 8 (int64)");
+  GFX_CK(cudaSetDevice(ctx->device));
+  *data_bytes = 0;
+  if (m == 0) return GFX_OK;
+  return elem_bytes == 4
+             ? pack_size_t(ctx, static_cast<const int32_t*>(vals_d), m, boff_d, data_bytes)
+             : pack_size_t(ctx, static_cast<const int64_t*>(vals_d), m, boff_d, data_bytes);
+}
+
+int gfx_csr_pack(gfx_ctx* ctx, const void* vals_d, int elem_bytes, int64_t m,
+                 const int64_t* boff_d, uint8_t* ctrl_d, uint8_t* data_d) {
+  GFX_NVTX("gfx_csr_pack");
+  GFX_REQUIRE(ctx && (m == 0 || (vals_d && boff_d && ctrl_d && data_d)), "gfx_csr_pack: null argument");
+  GFX_REQUIRE(elem_bytes == 4 || elem_bytes == 8, "elem_bytes must be 4 (int32) or 8 (int64)");
+  GFX_CK(cudaSetDevice(ctx->device));
+  if (m == 0) return GFX_OK;
+  const int64_t nb = (m + kPackBlock - 1) / kPackBlock;
+  GFX_CK(cudaMemsetAsync(ctrl_d, 0, (m + 3) / 4, ctx->stream));
+  if (elem_bytes == 4)
+    GFX_LAUNCH(k_pack_write<int32_t>, grid_for(nb * 32, 256, ctx->sm_count * 16), 256, 0,
+               ctx->stream, static_cast<const int32_t*>(vals_d), m, boff_d, ctrl_d, data_d);
+  else
+    GFX_LAUNCH(k_pack_write<int64_t>, grid_for(nb * 32, 256, ctx->sm_count * 16), 256, 0,
+               ctx->stream, static_cast<const int64_t*>(vals_d), m, boff_d, ctrl_d, data_d);
+  GFX_CK(cudaGetLastError());
+  GFX_CK(cudaStreamSynchronize(ctx->stream));
+  return GFX_OK;
+}
+
+int gfx_csr_unpack(gfx_ctx* ctx, const uint8_t* ctrl_d, const uint8_t* data_d,
+                   const int64_t* boff_d, int64_t m, void* vals_d, int elem_bytes, int sync) {
+  GFX_NVTX("gfx_csr_unpack");
+  GFX_REQUIRE(ctx && (m == 0 || (ctrl_d && data_d && boff_d && vals_d)),
+              "gfx_csr_unpack: null argument");
+  GFX_REQUIRE(elem_bytes == 4 || elem_bytes == 8, "elem_bytes must be 4 (int32) or 8 (int64)");
+  GFX_CK(cudaSetDevice(ctx->device));
+  if (m == 0) return GFX_OK;
+  if (elem_bytes == 4) GFX_TRY(unpack_t(ctx, ctrl_d, data_d, boff_d, m, static_cast<int32_t*>(vals_d)));
+  else GFX_TRY(unpack_t(ctx, ctrl_d, data_d, boff_d, m, static_cast<int64_t*>(vals_d)));
   GFX_CK(cudaGetLastError());
   if (sync) GFX_CK(cudaStreamSynchronize(ctx->stream));
   return GFX_OK;

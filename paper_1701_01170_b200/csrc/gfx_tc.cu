@@ -462,139 +462,6 @@ __global__ void __launch_bounds__(256)
   if (lane == 0 && local) atomicAdd(total, local);
 }
 
-// Heavy pairs grouped by their LONGER row (sorted by that row's id): a CTA
-// stages the row once into a shared-memory hash table -- element z -> its
-// global reversed slot -- and its warps take the group's pairs, lanes walking
-// the SHORTER row (coalesced) and probing the table (one or two shared
-// loads) instead of binary-searching the longer row in global memory per
-// element.  The long row is read once per group instead of log2(len) times
-// per probe.  Rows longer than kHashRow stay on the binary-search kernel.
-constexpr int kHashRow = 4096;             // longest staged row (elements)
-constexpr int kHashCap = 2 * kHashRow;     // table slots (load <= 1/2)
-constexpr int64_t kHashGrab = 64;          // sorted pairs per dynamic hand-out
-
-constexpr unsigned kHashMinPairs = 16;    // rows staged only when this many pairs share them
-
-// pass 0: heavy pairs per longer row; pass 1: sort keys (the longer row when
-// it is short enough to stage and shared by >= kHashMinPairs pairs, else
-// all-ones: those pairs stay on the search kernel)
-template <int PASS>
-__global__ void k_tc_heavy_keys(const int32_t* __restrict__ heavy,
-                                const unsigned long long* __restrict__ nheavy,
-                                const int32_t* __restrict__ rsrc, const int32_t* __restrict__ rcol,
-                                const int64_t* __restrict__ rrow, unsigned* __restrict__ rowcnt,
-                                uint32_t* __restrict__ keys, unsigned long long* __restrict__ nhash) {
-  const int64_t nh = (int64_t)*nheavy;
-  unsigned long long local = 0;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nh;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = heavy[k];
-    const int32_t x = rsrc[p], y = rcol[p];
-    const int64_t la = rrow[x + 1] - rrow[x], lb = rrow[y + 1] - rrow[y];
-    const int32_t lr = la >= lb ? x : y;
-    const bool fits = (la >= lb ? la : lb) <= kHashRow;
-    if (PASS == 0) {
-      if (fits) atomicAdd(&rowcnt[lr], 1u);
-      continue;
-    }
-    const bool ok = fits && rowcnt[lr] >= kHashMinPairs;
-    keys[k] = ok ? (uint32_t)lr : 0xFFFFFFFFu;
-    local += ok;
-  }
-  if (PASS == 0) return;
-  local = warp_sum_u64(local);
-  if ((threadIdx.x & 31) == 0 && local) atomicAdd(nhash, local);
-}
-
-__device__ __forceinline__ uint32_t tc_hash(int32_t z, uint32_t mask) {
-  return ((uint32_t)z * 2654435761u) >> 7 & mask;
-}
-
-__global__ void __launch_bounds__(256)
-    k_tc_heavy_hash(const uint32_t* __restrict__ skeys, const int32_t* __restrict__ spairs,
-                    int64_t nhash, const int32_t* __restrict__ rsrc,
-                    const int32_t* __restrict__ rcol, const int64_t* __restrict__ rrow,
-                    const int32_t* __restrict__ xslot, int32_t* __restrict__ counts,
-                    unsigned long long* __restrict__ total, unsigned long long* __restrict__ grab) {
-  extern __shared__ __align__(16) int32_t hsm[];  // kHashCap keys, then kHashCap slots
-  int32_t* tz = hsm;
-  int32_t* tpos = hsm + kHashCap;
-  __shared__ int64_t chunk0, run_end;
-  __shared__ int32_t staged;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nwarps = blockDim.x >> 5;
-  unsigned long long local = 0;
-  if (threadIdx.x == 0) staged = -1;
-  for (;;) {
-    if (threadIdx.x == 0) chunk0 = (int64_t)atomicAdd(grab, (unsigned long long)kHashGrab);
-    __syncthreads();
-    const int64_t c0 = chunk0;
-    if (c0 >= nhash) break;
-    const int64_t c1 = min(c0 + kHashGrab, nhash);
-    for (int64_t i = c0; i < c1;) {
-      const uint32_t key = skeys[i];
-      if (threadIdx.x == 0) {  // end of this row's run inside the chunk
-        int64_t lo = i, hi = c1;
-        while (lo < hi) {
-          const int64_t mid = (lo + hi) >> 1;
-          if (skeys[mid] <= key) lo = mid + 1; else hi = mid;
-        }
-        run_end = lo;
-      }
-      const int32_t r = (int32_t)key;
-      const int64_t rb = rrow[r], re = rrow[r + 1];
-      uint32_t cap = 64;
-      while (cap < 2 * (uint32_t)(re - rb)) cap <<= 1;
-      const uint32_t mask = cap - 1;
-      if (staged != r) {  // stage row r (block-uniform: staged is shared)
-        __syncthreads();
-        for (uint32_t t = threadIdx.x; t < cap; t += blockDim.x) tz[t] = -1;
-        __syncthreads();
-        for (int64_t j = rb + threadIdx.x; j < re; j += blockDim.x) {
-          const int32_t z = rcol[j];
-          uint32_t h = tc_hash(z, mask);
-          while (atomicCAS(&tz[h], -1, z) != -1) h = (h + 1) & mask;
-          tpos[h] = (int32_t)j;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) staged = r;
-      }
-      __syncthreads();
-      const int64_t e = run_end;
-      for (int64_t k = i + warp; k < e; k += nwarps) {
-        const int64_t p = spairs[k];
-        const int32_t x = rsrc[p], y = rcol[p];
-        // the other row is walked; credit goes to the slot of z in y's row
-        const bool staged_is_y = y == r;
-        const int32_t o = staged_is_y ? x : y;
-        const int64_t ob = rrow[o], oe = rrow[o + 1];
-        for (int64_t t = ob + lane; t < oe; t += 32) {
-          const int32_t z = rcol[t];
-          uint32_t h = tc_hash(z, mask);
-          int32_t hit = -1;
-          for (;;) {
-            const int32_t v = tz[h];
-            if (v == z) {
-              hit = tpos[h];
-              break;
-            }
-            if (v == -1) break;
-            h = (h + 1) & mask;
-          }
-          if (hit >= 0) {
-            atomicAdd(&counts[xslot[staged_is_y ? hit : t]], 1);
-            ++local;
-          }
-        }
-      }
-      __syncthreads();
-      i = e;
-    }
-  }
-  local = warp_sum_u64(local);
-  if (lane == 0 && local) atomicAdd(total, local);
-}
-
 // reversed CSR of the oriented graph + slot map (graph constant, cached)
 static int build_reverse(gfx_graph* g, int64_t mo) {
   gfx_ctx* ctx = g->ctx;
@@ -710,63 +577,8 @@ extern "C" int gfx_tc_count(gfx_graph* g, int32_t* osrc_d, int32_t* odst_d, int3
                  rcol, mo, rrow, xslot, counts, &C->total, heavy, &C->aux0);
       const int skew = getenv("GFX_TC_SKEW") ? atoi(getenv("GFX_TC_SKEW")) : kRevSkew;
       const int64_t grab = getenv("GFX_TC_GRAB") ? atoi(getenv("GFX_TC_GRAB")) : kRevGrab;
-      if (!getenv("GFX_TC_HASH")) {  // the hash path measured slower at s22 (223 vs 100 ms)
-        GFX_LAUNCH(k_tc_rev_heavy, ctx->sm_count * 8, 256, 0, ctx->stream, rsrc, rcol, rrow,
-                   xslot, heavy, &C->aux0, counts, &C->total, skew, &C->aux1, grab);
-      } else {
-        // heavy pairs sorted by their longer row: rows up to kHashRow through
-        // the shared-memory hash kernel, the rest through the search kernel
-        auto* pinc = static_cast<Counters*>(ctx->pinned);
-        GFX_CK(cudaMemcpyAsync(pinc, C, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
-        GFX_CK(cudaStreamSynchronize(ctx->stream));
-        const int64_t nh = (int64_t)pinc->aux0;
-        if (nh > 0) {
-          uint32_t *k0, *k1;
-          int32_t* v1;
-          unsigned long long* hc;
-          GFX_TRY(scratch_t(g, "tc_hkeys0", nh + 1, &k0));
-          GFX_TRY(scratch_t(g, "tc_hkeys1", nh + 1, &k1));
-          GFX_TRY(scratch_t(g, "tc_hpairs", nh + 1, &v1));
-          GFX_TRY(scratch_t(g, "tc_hctr", 4, &hc));
-          GFX_CK(cudaMemsetAsync(hc, 0, 32, ctx->stream));
-          unsigned* rowcnt;
-          GFX_TRY(scratch_t(g, "tc_hrowcnt", g->n + 1, &rowcnt));
-          GFX_CK(cudaMemsetAsync(rowcnt, 0, (g->n + 1) * 4, ctx->stream));
-          GFX_LAUNCH(k_tc_heavy_keys<0>, grid_for(nh, 256, ctx->sm_count * 8), 256, 0,
-                     ctx->stream, heavy, &C->aux0, rsrc, rcol, rrow, rowcnt, k0, &hc[0]);
-          GFX_LAUNCH(k_tc_heavy_keys<1>, grid_for(nh, 256, ctx->sm_count * 8), 256, 0,
-                     ctx->stream, heavy, &C->aux0, rsrc, rcol, rrow, rowcnt, k0, &hc[0]);
-          size_t tb = 0;
-          GFX_CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, heavy, v1, (int)nh, 0, 32,
-                                                 ctx->stream));
-          void* tmp = nullptr;
-          GFX_TRY(scratch(g, "tc_hsort_tmp", tb + 16, &tmp));
-          GFX_CK(cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, heavy, v1, (int)nh, 0, 32,
-                                                 ctx->stream));
-          count_launch();
-          unsigned long long nhash = 0;
-          GFX_CK(cudaMemcpyAsync(&pinc->aux2, &hc[0], 8, cudaMemcpyDeviceToHost, ctx->stream));
-          GFX_CK(cudaStreamSynchronize(ctx->stream));
-          nhash = pinc->aux2;
-          static bool attr = false;
-          const int hsmem = 2 * kHashCap * (int)sizeof(int32_t);
-          if (!attr) {
-            GFX_CK(cudaFuncSetAttribute(k_tc_heavy_hash,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem));
-            attr = true;
-          }
-          if (nhash > 0)
-            GFX_LAUNCH(k_tc_heavy_hash, ctx->sm_count * 3, 256, hsmem, ctx->stream, k1, v1,
-                       (int64_t)nhash, rsrc, rcol, rrow, xslot, counts, &C->total, &hc[1]);
-          const unsigned long long rest = (unsigned long long)nh - nhash;
-          if (rest > 0) {
-            GFX_CK(cudaMemcpyAsync(&hc[2], &rest, 8, cudaMemcpyHostToDevice, ctx->stream));
-            GFX_LAUNCH(k_tc_rev_heavy, ctx->sm_count * 8, 256, 0, ctx->stream, rsrc, rcol, rrow,
-                       xslot, v1 + nhash, &hc[2], counts, &C->total, skew, &hc[3], grab);
-          }
-          GFX_CK(cudaStreamSynchronize(ctx->stream));
-        }
-      }
+      GFX_LAUNCH(k_tc_rev_heavy, ctx->sm_count * 8, 256, 0, ctx->stream, rsrc, rcol, rrow, xslot,
+                 heavy, &C->aux0, counts, &C->total, skew, &C->aux1, grab);
     }
     GFX_CK(cudaGetLastError());
     GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));

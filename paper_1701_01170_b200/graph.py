@@ -296,30 +296,39 @@ class DeviceGraph:
         _native.call("gfx_graph_refresh", self.handle)
 
     def reload_packed_(self, packed) -> None:
-        """``reload_`` from a ``io.PackedCsr``: the packed column streams
-        (about half the bytes of int32 columns) cross PCIe into device staging
-        buffers kept on this graph, are decoded in place into ``col`` on the
-        device (gfx_csr_unpack), then the graph constants are refreshed."""
-        import torch
-
+        """``reload_`` from a ``io.PackedCsr``: the packed row and column
+        streams (about half the bytes of int64 rows + int32 columns) cross
+        PCIe into device staging buffers kept on this graph, are decoded into
+        ``row`` / ``col`` on the device (gfx_csr_unpack), then the graph
+        constants are refreshed.  Stream-ordered on torch's current stream."""
         if packed.num_vertices != self.num_vertices or packed.num_edges != self.num_edges:
             raise ValueError("reload_packed_: shape differs from the resident graph")
         if not self.undirected:
             raise ValueError("reload_packed_: undirected graphs only")
+        self.upload_packed_(packed)
+        self.decode_packed_()
+
+    def upload_packed_(self, packed) -> None:
+        """Copy the packed streams into the graph's device staging buffers
+        (asynchronous on the current stream)."""
+        import torch
+
         st = getattr(self, "_pack_stage", None)
-        if st is None or st[1].numel() < packed.data.numel():
+        parts = packed.row + packed.col
+        if st is None or any(d.numel() < h.numel() for d, h in zip(st, parts)):
             dev = self.row.device
-            st = (torch.empty(packed.ctrl.numel(), dtype=torch.uint8, device=dev),
-                  torch.empty(packed.data.numel(), dtype=torch.uint8, device=dev),
-                  torch.empty(packed.boff.numel(), dtype=torch.int64, device=dev))
+            st = tuple(torch.empty(h.numel(), dtype=h.dtype, device=dev) for h in parts)
             self._pack_stage = st
-        ctrl, data, boff = st
-        self.row.copy_(packed.row, non_blocking=True)
-        ctrl[: packed.ctrl.numel()].copy_(packed.ctrl, non_blocking=True)
-        data[: packed.data.numel()].copy_(packed.data, non_blocking=True)
-        boff[: packed.boff.numel()].copy_(packed.boff, non_blocking=True)
-        _native.call("gfx_csr_unpack", self.ctx.handle, _native.ptr(ctrl), _native.ptr(data),
-                     _native.ptr(boff), self.num_edges, _native.ptr(self.col), 0)
+        for d, h in zip(st, parts):
+            d[: h.numel()].copy_(h, non_blocking=True)
+
+    def decode_packed_(self) -> None:
+        """Decode the staged streams into row / col and refresh the graph."""
+        rc, rd, rb, cc, cd, cb = self._pack_stage
+        _native.call("gfx_csr_unpack", self.ctx.handle, _native.ptr(rc), _native.ptr(rd),
+                     _native.ptr(rb), self.num_vertices + 1, _native.ptr(self.row), 8, 0)
+        _native.call("gfx_csr_unpack", self.ctx.handle, _native.ptr(cc), _native.ptr(cd),
+                     _native.ptr(cb), self.num_edges, _native.ptr(self.col), 4, 0)
         self._csc_dev = None
         _native.call("gfx_graph_refresh", self.handle)
 

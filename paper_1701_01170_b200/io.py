@@ -237,44 +237,49 @@ def save_csr_cache_device(dg: DeviceGraph, path: str | Path, compact: bool = Fal
 # packed columns for PCIe-bound uploads (csrc/gfx_pack.cu)
 # ---------------------------------------------------------------------------
 class PackedCsr:
-    """Host (pinned) image of an undirected device CSR with its columns packed
-    as zigzag deltas in a StreamVByte-like layout (~1.9 bytes per slot on
-    R-MAT ef16 instead of 4): ``row`` int64[n+1], ``ctrl`` uint8, ``data``
-    uint8, ``boff`` int64 block offsets.  ``DeviceGraph.reload_packed_``
-    uploads it into a resident graph and decodes it on the device."""
+    """Host (pinned) image of an undirected device CSR with BOTH arrays packed
+    as zigzag differences in a StreamVByte-like layout (csrc/gfx_pack.cu):
+    the int64 row offsets (differences = degrees, ~1 byte per vertex) and the
+    int32 column ids (~1.9 bytes per slot on R-MAT ef16 instead of 4).  Each
+    packed array is (ctrl, data, boff) uint8 / uint8 / int64 pinned tensors.
+    ``DeviceGraph.reload_packed_`` uploads it into a resident graph and
+    decodes it on the device."""
 
-    def __init__(self, n, m, row, ctrl, data, boff):
+    def __init__(self, n, m, row, col):
         self.num_vertices, self.num_edges = int(n), int(m)
-        self.row, self.ctrl, self.data, self.boff = row, ctrl, data, boff
+        self.row, self.col = row, col  # (ctrl, data, boff) each
 
     @property
     def nbytes(self) -> int:
-        return sum(t.numel() * t.element_size() for t in (self.row, self.ctrl, self.data,
-                                                            self.boff))
+        return sum(t.numel() * t.element_size() for part in (self.row, self.col) for t in part)
 
 
-def pack_csr_device(dg: DeviceGraph) -> PackedCsr:
-    """Pack a device graph's columns on the device and download the packed
-    streams (plus the row offsets) into pinned host memory."""
+def _pack_device(ctx, vals, elem_bytes: int):
     import torch
 
     from . import _native
 
-    n, m = dg.num_vertices, dg.num_edges
-    dev = dg.row.device
-    nb = (m + 1023) // 1024
-    boff = torch.empty(nb + 1, dtype=torch.int64, device=dev)
+    count = vals.numel()
+    dev = vals.device
+    boff = torch.empty((count + 1023) // 1024 + 1, dtype=torch.int64, device=dev)
     nbytes = ctypes.c_int64()
-    _native.call("gfx_csr_pack_size", dg.ctx.handle, _native.ptr(dg.col), m, _native.ptr(boff),
-                 ctypes.byref(nbytes))
-    ctrl = torch.empty(max((m + 3) // 4, 1), dtype=torch.uint8, device=dev)
+    _native.call("gfx_csr_pack_size", ctx.handle, _native.ptr(vals), elem_bytes, count,
+                 _native.ptr(boff), ctypes.byref(nbytes))
+    ctrl = torch.empty(max((count + 3) // 4, 1), dtype=torch.uint8, device=dev)
     data = torch.empty(max(nbytes.value, 1), dtype=torch.uint8, device=dev)
-    _native.call("gfx_csr_pack", dg.ctx.handle, _native.ptr(dg.col), m, _native.ptr(boff),
-                 _native.ptr(ctrl), _native.ptr(data))
+    _native.call("gfx_csr_pack", ctx.handle, _native.ptr(vals), elem_bytes, count,
+                 _native.ptr(boff), _native.ptr(ctrl), _native.ptr(data))
 
     def pinned(t):
         h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
         h.copy_(t)
         return h
 
-    return PackedCsr(n, m, pinned(dg.row), pinned(ctrl), pinned(data), pinned(boff))
+    return tuple(pinned(t) for t in (ctrl, data, boff))
+
+
+def pack_csr_device(dg: DeviceGraph) -> PackedCsr:
+    """Pack a device graph's row offsets and columns on the device and
+    download the packed streams into pinned host memory."""
+    return PackedCsr(dg.num_vertices, dg.num_edges, _pack_device(dg.ctx, dg.row, 8),
+                     _pack_device(dg.ctx, dg.col[: dg.num_edges], 4))

@@ -8,7 +8,7 @@ echo "launch list rc $?"
 bash tools/gpu_ncu_bfs.sh
 echo "bfs ncu rc $?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sssp_persistent -c 1 \
-  -o gpurun_out/sssp_full python tools/prof_run.py --prim sssp --scale 24 --runs 1 --delta 32 \
+  -o gpurun_out/sssp_full python tools/prof_run.py --prim sssp --scale 24 --runs 1 --delta 4 \
   > gpurun_out/ncu_sssp.log 2>&1
 python tools/ncu_summary.py gpurun_out/sssp_full.ncu-rep > gpurun_out/ncu_sssp_summary.txt 2>&1
 python tools/ncu_lines.py gpurun_out/sssp_full.ncu-rep 40 > gpurun_out/ncu_sssp_lines.txt 2>&1
