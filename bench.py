@@ -364,6 +364,11 @@ def run_partitioned(args, dist: Dist):
                           for t in r27["st"].direction_trace]}
         except Exception as exc:  # noqa: BLE001 -- report, keep the headline line
             extra["s27_error"] = repr(exc)
+    if not args.no_extras:
+        try:
+            extra["sssp_partitioned"] = _partitioned_sssp(args, dist)
+        except Exception as exc:  # noqa: BLE001 -- report, keep the headline line
+            extra["sssp_partitioned_error"] = repr(exc)
     peak, peak_kind = measured_peak_gbs()
     ms = t_ms / args.steps
     achieved = st.bytes_alg / (ms * 1e-3) / 1e9 / P
@@ -503,6 +508,65 @@ def _partitioned_run(args, dist, scale: int, steps: int, warmup: int, with_1gpu:
     return {"st": st, "t_ms": t_ms, "e_r": e_r, "reached": reached, "n": n, "m": m,
             "launches": launches,
             "build_s": build_s, "one_gpu": one_gpu, "loop": loop, "e2e": e2e}
+
+
+def _partitioned_sssp(args, dist, delta: int = 32, steps: int = 3):
+    """Partitioned near/far SSSP (SURVEY 8(e) row e, dist.sssp_partitioned) on
+    the bench graph with weights 1..64: each rank holds its 1D-cyclic share,
+    offers cross ranks through all_to_all; CUDA events, max over ranks.  The
+    distances are checked against the single-GPU SSSP on rank 0."""
+    import torch
+
+    from paper_1701_01170_b200.dist import (ProcessComm, SsspEngine, partition_graph,
+                                            partition_weights, sssp_partitioned)
+    from paper_1701_01170_b200.generators import rmat_device_graph
+    from paper_1701_01170_b200.primitives.sssp import sssp_device
+
+    P, r = dist.world, dist.rank
+    torch.cuda.empty_cache()
+    dgw = rmat_device_graph(args.scale, args.edge_factor, 0, weights=(1, 64), weight_seed=0)
+    n = dgw.num_vertices
+    ref = None
+    if r == 0:
+        d1, _, st1 = sssp_device(dgw, args.source, delta=delta)
+        ref, e_r = d1, st1.edges_reached
+    else:
+        e_r = 0
+    e_r = int(dist.sum(float(e_r)))
+    lrow, lcol = partition_graph(dgw, P, r)
+    lw = partition_weights(dgw, lrow, P, r)
+    eng = SsspEngine(lrow, lcol, lw, n, P, r)
+    comm = ProcessComm(eng)
+    st = sssp_partitioned(comm, n, args.source, delta)  # warm-up
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(steps):
+        st = sssp_partitioned(comm, n, args.source, delta)
+    ev1.record()
+    torch.cuda.synchronize()
+    ms = dist.max(ev0.elapsed_time(ev1)) / steps
+    dl, _ = eng.result()
+    nlmax = (n + P - 1) // P
+    buf = torch.full((nlmax,), -2, dtype=torch.int32, device=eng.device)
+    buf[: eng.nl] = dl
+    parts = [buf]
+    if P > 1:
+        import torch.distributed as tdist
+
+        parts = [torch.empty_like(buf) for _ in range(P)]
+        tdist.all_gather(parts, buf)
+    ok = None
+    if r == 0:
+        ok = all(bool(torch.equal(parts[q][: len(range(q, n, P))], ref[q::P])) for q in range(P))
+    del eng, comm, lrow, lcol, lw, dgw
+    torch.cuda.empty_cache()
+    return {"gteps": round(e_r / (ms * 1e-3) / 1e9, 2), "ms": round(ms, 3), "delta": delta,
+            "n_gpus": P, "iterations": st.iterations, "bucket_advances": st.bucket_advances,
+            "relaxed_slots": st.relaxed_slots, "messages": st.messages,
+            "dist_equal_single_gpu": ok,
+            "what": "host-driven level loop over torch.distributed (NCCL) collectives"}
 
 
 def _labels_match(eng, ref_labels, P: int, r: int, n: int):

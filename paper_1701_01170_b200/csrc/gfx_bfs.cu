@@ -1156,6 +1156,12 @@ static int pbfs_setup(gfx_graph* g, int64_t source, int direction, double do_a, 
   static int blocks_per_sm = 0;
   const int smem = kWarpScratch * kWarpsPerBlock;
   if (blocks_per_sm == 0) {
+    if (const char* cv = getenv("GFX_BFS_CARVEOUT")) {  // L1 / shared split (percent shared)
+      GFX_CK(cudaFuncSetAttribute(k_bfs_persistent<true>,
+                                  cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv)));
+      GFX_CK(cudaFuncSetAttribute(k_bfs_persistent<false>,
+                                  cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv)));
+    }
     GFX_CK(cudaFuncSetAttribute(k_bfs_persistent<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem));
     GFX_CK(cudaFuncSetAttribute(k_bfs_persistent<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
