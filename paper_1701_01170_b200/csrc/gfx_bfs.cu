@@ -653,10 +653,6 @@ struct PCtl {
   unsigned long long t0;
 };
 
-__device__ __forceinline__ unsigned long long ld_ctr(const unsigned long long* p) {
-  return ld_volatile_u64(p);
-}
-
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -678,6 +674,57 @@ __device__ __noinline__ void device_decide(long long n, long long m, long long n
     *mode = depth > 1 ? GFX_DIR_PULL : GFX_DIR_PUSH;
   else
     *mode = GFX_DIR_PUSH;
+}
+
+// Per-CTA aggregation of the level counters and queue reservations.  All
+// counters of a level share one 64-byte line, so per-warp atomics on them
+// serialise in one L2 slice (~3500 warps per level); the persistent loop
+// sums per CTA in shared memory and issues one atomic per CTA instead, and
+// one thread per CTA reads the counters back after a grid barrier.
+struct CtaAgg {
+  unsigned long long ctr[8];  // shared mirror of Counters (summed, then flushed)
+  unsigned long long rd[8];   // Counters as read after the last grid barrier
+  unsigned long long base;
+  int woff[kWarpsPerBlock + 1];
+};
+static_assert(sizeof(Counters) == 8 * sizeof(unsigned long long), "Counters layout");
+
+// every thread of the CTA: add the CTA's sums to the global counters and
+// clear them (callers separate this from the next use by a barrier)
+__device__ __forceinline__ void cta_flush_ctrs(CtaAgg& g, Counters* cur) {
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    const unsigned long long v = g.ctr[threadIdx.x];
+    if (v) atomicAdd(reinterpret_cast<unsigned long long*>(cur) + threadIdx.x, v);
+    g.ctr[threadIdx.x] = 0ull;
+  }
+}
+
+// every thread of the CTA: read the 8 counters once per CTA into g.rd
+__device__ __forceinline__ void cta_read_ctrs(CtaAgg& g, const Counters* cur) {
+  if (threadIdx.x < 8)
+    g.rd[threadIdx.x] =
+        ld_volatile_u64(reinterpret_cast<const unsigned long long*>(cur) + threadIdx.x);
+  __syncthreads();
+}
+
+// every thread of the CTA: append every warp's staged output (ocnt entries
+// in W.obuf) to the queue with ONE reservation per CTA
+__device__ __forceinline__ void cta_flush(WarpSmem& W, int& ocnt, int32_t* __restrict__ out,
+                                          unsigned long long* __restrict__ out_len, CtaAgg& g) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) g.woff[wid + 1] = ocnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    g.woff[0] = 0;
+    for (int k = 1; k <= kWarpsPerBlock; ++k) g.woff[k] += g.woff[k - 1];
+    const int tot = g.woff[kWarpsPerBlock];
+    g.base = tot ? atomicAdd(out_len, (unsigned long long)tot) : 0ull;
+  }
+  __syncthreads();
+  const unsigned long long b = g.base + g.woff[wid];
+  for (int j = lane; j < ocnt; j += 32) out[b + j] = W.obuf[j];
+  ocnt = 0;
 }
 
 // Expansion of at most 32 items held one per lane (v, row base, degree; 0
@@ -750,7 +797,7 @@ __device__ __forceinline__ void push_tiny(WarpSmem& W, Op& o, const int32_t* __r
                                           int32_t* __restrict__ out,
                                           unsigned long long* __restrict__ out_len,
                                           unsigned long long* __restrict__ total_out, int64_t gw,
-                                          int64_t nw) {
+                                          int64_t nw, CtaAgg& agg) {
   const int lane = threadIdx.x & 31;
   int32_t v = 0;
   int64_t rb = 0, deg = 0;
@@ -762,7 +809,7 @@ __device__ __forceinline__ void push_tiny(WarpSmem& W, Op& o, const int32_t* __r
   int ocnt = 0;
   const int64_t total = expand_items32(W, o, v, rb, deg, col, out, out_len, ocnt,
                                        gw * 32 * Op::kBatch, nw * 32 * Op::kBatch);
-  warp_flush(W, ocnt, out, out_len);
+  cta_flush(W, ocnt, out, out_len, agg);
   if (gw == 0 && lane == 0) *total_out = (unsigned long long)total;
 }
 
@@ -778,10 +825,9 @@ __device__ __forceinline__ void push_mid(WarpSmem& W, Op& o, const int32_t* __re
                                          const int32_t* __restrict__ col,
                                          int32_t* __restrict__ out,
                                          unsigned long long* __restrict__ out_len,
-                                         unsigned long long* __restrict__ total_out,
                                          int32_t* __restrict__ heavy,
                                          unsigned long long* __restrict__ nheavy, int64_t gw,
-                                         int64_t nw) {
+                                         int64_t nw, CtaAgg& agg) {
   const int lane = threadIdx.x & 31;
   int ocnt = 0;
   unsigned long long tot = 0;
@@ -805,8 +851,8 @@ __device__ __forceinline__ void push_mid(WarpSmem& W, Op& o, const int32_t* __re
     tot += (unsigned long long)expand_items32(W, o, v, rb, hv ? 0 : deg, col, out, out_len, ocnt,
                                               0, 32 * Op::kBatch);
   }
-  warp_flush(W, ocnt, out, out_len);
-  if (lane == 0 && tot) atomicAdd(total_out, tot);
+  cta_flush(W, ocnt, out, out_len, agg);
+  if (lane == 0 && tot) atomicAdd(&agg.ctr[2], tot);  // Counters::total, flushed by the caller
 }
 
 // Deferred labels: write labels[v] = depth byte of v if visited, else
@@ -848,6 +894,26 @@ __device__ __forceinline__ void materialize_labels(const PBfsArgs& a, int64_t gw
   }
 }
 
+// Diagnostic timeline (compiled in only with -DGFX_BFS_TIMELINE, see
+// tools/bfs_timeline.sh): per grid barrier and CTA, the globaltimer when the
+// CTA arrives and when it leaves; bfs_device_loop prints the spread.
+#ifdef GFX_BFS_TIMELINE
+constexpr int kTlSlots = 96, kTlCtas = 1024;
+__device__ unsigned long long g_tl[kTlSlots * 2 * kTlCtas + kTlCtas];
+#define GSYNC()                                                                          \
+  do {                                                                                   \
+    __syncthreads();                                                                     \
+    if (threadIdx.x == 0 && tl_slot < kTlSlots)                                          \
+      g_tl[(tl_slot * 2) * kTlCtas + blockIdx.x] = globaltimer();                        \
+    grid.sync();                                                                         \
+    if (threadIdx.x == 0 && tl_slot < kTlSlots)                                          \
+      g_tl[(tl_slot * 2 + 1) * kTlCtas + blockIdx.x] = globaltimer();                    \
+    ++tl_slot;                                                                           \
+  } while (0)
+#else
+#define GSYNC() grid.sync()
+#endif
+
 // kDO: direction-optimising run (pull levels and the frontier bitmaps
 // compiled in); push-only runs launch the <false> instance, which carries
 // none of that code (lower register pressure in its expansion loops)
@@ -859,11 +925,16 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
   PullSmem& PS = *reinterpret_cast<PullSmem*>(smem_raw + (threadIdx.x >> 5) * kWarpScratch);
   __shared__ ScanSmem ss;
   __shared__ PCtl c;
+  __shared__ CtaAgg agg;
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   const int64_t gw = gtid >> 5, nw = nthr >> 5;
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
   const unsigned long long t_start = leader ? globaltimer() : 0ull;
+#ifdef GFX_BFS_TIMELINE
+  int tl_slot = 0;
+  if (threadIdx.x == 0) g_tl[kTlSlots * 2 * kTlCtas + blockIdx.x] = globaltimer();
+#endif
 
   // ---- initialise outputs and state.  Labels are deferred: levels record
   // depths in the L2-resident byte array lvl8 and materialize_labels writes
@@ -892,6 +963,7 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
   }
   for (int64_t i = gtid; i < 3 * (int64_t)(sizeof(Counters) / 8); i += nthr)
     reinterpret_cast<unsigned long long*>(a.C)[i] = 0ull;
+  if (threadIdx.x < 8) agg.ctr[threadIdx.x] = 0ull;
   if (threadIdx.x == 0) {
     c.nf = 1;
     c.n_u = a.n;
@@ -908,7 +980,7 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
     a.lvl8[a.source] = 0;
     a.order[0] = a.source;
   }
-  grid.sync();
+  GSYNC();
   const unsigned long long t_init = leader ? globaltimer() : 0ull;
 
   for (;;) {
@@ -929,7 +1001,7 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
     if (!c.direct && c.depth == 255) {
       // depth bytes exhausted: write the labels so far, label directly from here on
       materialize_labels(a, gw, nw);
-      grid.sync();
+      GSYNC();
       if (threadIdx.x == 0) c.direct = 1;
       __syncthreads();
     }
@@ -957,7 +1029,7 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
     if (!kDO || c.mode == GFX_DIR_PUSH) {
       if (!c.queue_form) {
         bitmap_to_queue(a.words, fcur, a.order + c.q_end, &cur->aux2, gw, nw);
-        grid.sync();
+        GSYNC();
         if (threadIdx.x == 0) {
           c.q_off = c.q_end;
           c.q_end += nf;
@@ -973,14 +1045,16 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
         // between plan and expansion
         BfsClaimOpT<4, kDO> top{a.visited, a.labels, a.preds, depth, {}, lab.lvl8, fbits};
         push_tiny(W, top, F, nf, a.row, a.col, a.order + c.q_end, &cur->out_len, &cur->total, gw,
-                  nw);
+                  nw, agg);
       } else if (nf <= kMidItems) {
         // mid-size frontier: warps expand 32 items each; hubs (rare) are set
         // aside and expanded cooperatively after one barrier
-        push_mid(W, op, F, nf, a.row, a.col, a.order + c.q_end, &cur->out_len, &cur->total,
-                 a.part, &cur->aux3, gw, nw);
-        grid.sync();
-        const int64_t nh = (int64_t)ld_ctr(&cur->aux3);
+        push_mid(W, op, F, nf, a.row, a.col, a.order + c.q_end, &cur->out_len, a.part,
+                 &cur->aux3, gw, nw, agg);
+        cta_flush_ctrs(agg, cur);
+        GSYNC();
+        cta_read_ctrs(agg, cur);
+        const int64_t nh = (int64_t)agg.rd[7];
         for (int64_t h0 = 0; h0 < nh; h0 += 32) {  // heavy items, 32 at a time
           const int lane = threadIdx.x & 31;
           int32_t v = 0;
@@ -1002,15 +1076,17 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
         const unsigned ep = a.epoch_base + (unsigned)c.depth;
         for (int64_t t = blockIdx.x; t < stiles; t += gridDim.x)
           scan_tile(t, stiles, F, nf, a.row, a.scan, a.rowbase, a.part, a.status, ep, cur, ss);
-        grid.sync();
-        expand_tasks(W, op, F, nf, a.scan, a.rowbase, a.part, (int64_t)ld_ctr(&cur->ntiles),
-                     (int64_t)ld_ctr(&cur->total), a.col, nullptr, a.order + c.q_end,
+        GSYNC();
+        cta_read_ctrs(agg, cur);
+        expand_tasks(W, op, F, nf, a.scan, a.rowbase, a.part, (int64_t)agg.rd[3],
+                     (int64_t)agg.rd[2], a.col, nullptr, a.order + c.q_end,
                      &cur->out_len, gw, nw);
         for (int64_t i = gtid; i < stiles; i += nthr) a.status[i] = 0ull;
       }
-      grid.sync();
-      level_edges = (long long)ld_ctr(&cur->total);
-      nout = (long long)ld_ctr(&cur->out_len);
+      GSYNC();
+      cta_read_ctrs(agg, cur);
+      level_edges = (long long)agg.rd[2];
+      nout = (long long)agg.rd[0];
       work = level_edges;
       bytes = 20 * nf + 4 * level_edges + 8 * nout;
       if (threadIdx.x == 0) {
@@ -1026,20 +1102,23 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
       // after this one needs no bitmap-to-queue sweep.
       const long long ncand = c.n_u - (a.n - a.nnz);
       const bool qsmall = ncand <= (a.n >> 6);
+      Counters* actr = reinterpret_cast<Counters*>(agg.ctr);  // summed per CTA
       if (ncand * 8 > a.n)
         pull_groups<BitmapFront, 8>(a.words, a.nz_in, a.visited, BitmapFront{fcur}, fnext, a.head,
-                                    a.rrow, a.rcol, a.directed, lab, a.preds, depth, cur, gw, nw,
+                                    a.rrow, a.rcol, a.directed, lab, a.preds, depth, actr, gw, nw,
                                     PS, a.head + a.n + 1, &cur->aux2);
       else
         pull_groups<BitmapFront, 4>(a.words, a.nz_in, a.visited, BitmapFront{fcur}, fnext, a.head,
-                                    a.rrow, a.rcol, a.directed, lab, a.preds, depth, cur, gw, nw,
+                                    a.rrow, a.rcol, a.directed, lab, a.preds, depth, actr, gw, nw,
                                     PS, a.head + a.n + 1, nullptr,
                                     qsmall ? a.order + c.q_end : nullptr, &cur->aux3);
-      grid.sync();
-      nout = (long long)ld_ctr(&cur->out_len);
-      work = (long long)ld_ctr(&cur->aux0);
-      cands = (long long)ld_ctr(&cur->aux1);
-      level_edges = a.directed ? (long long)ld_ctr(&cur->edges) : -1;
+      cta_flush_ctrs(agg, cur);
+      GSYNC();
+      cta_read_ctrs(agg, cur);
+      nout = (long long)agg.rd[0];
+      work = (long long)agg.rd[4];
+      cands = (long long)agg.rd[5];
+      level_edges = a.directed ? (long long)agg.rd[1] : -1;
       bytes = 12 * cands + 4 * work + 8 * nout;
       if (threadIdx.x == 0) {
         c.fsel = (c.fsel + 1) % 3;
@@ -1080,6 +1159,9 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
     if (c.nf == 0) break;
   }
   if (!c.direct) materialize_labels(a, gw, nw);
+#ifdef GFX_BFS_TIMELINE
+  GSYNC();  // the end of the label pass
+#endif
   if (leader) {
     a.summary[0] = c.depth;
     a.summary[1] = c.edges_total;
@@ -1208,6 +1290,34 @@ int bfs_device_loop(gfx_graph* g, int64_t source, int direction, double do_a, do
   GFX_CK(cudaStreamSynchronize(ctx->stream));
   float ms = 0.f;
   GFX_CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+#ifdef GFX_BFS_TIMELINE
+  {
+    std::vector<unsigned long long> tl((size_t)kTlSlots * 2 * kTlCtas + kTlCtas);
+    GFX_CK(cudaMemcpyFromSymbol(tl.data(), g_tl, tl.size() * 8));
+    const unsigned long long* st0 = tl.data() + (size_t)kTlSlots * 2 * kTlCtas;
+    const unsigned long long t0 = *std::min_element(st0, st0 + blocks);
+    fprintf(stderr, "timeline: %d CTAs, start spread %.2f us\n", blocks,
+            (*std::max_element(st0, st0 + blocks) - t0) * 1e-3);
+    for (int s = 0; s < kTlSlots; ++s) {
+      std::vector<unsigned long long> arr(tl.begin() + (size_t)(2 * s) * kTlCtas,
+                                          tl.begin() + (size_t)(2 * s) * kTlCtas + blocks);
+      std::vector<unsigned long long> lev(tl.begin() + (size_t)(2 * s + 1) * kTlCtas,
+                                          tl.begin() + (size_t)(2 * s + 1) * kTlCtas + blocks);
+      if (arr[0] < t0) break;
+      std::sort(arr.begin(), arr.end());
+      std::sort(lev.begin(), lev.end());
+      fprintf(stderr,
+              "sync %2d arrive min %8.2f med %8.2f p90 %8.2f max %8.2f | leave min %8.2f max %8.2f"
+              " | barrier %6.2f us\n",
+              s, (arr.front() - t0) * 1e-3, (arr[blocks / 2] - t0) * 1e-3,
+              (arr[blocks * 9 / 10] - t0) * 1e-3, (arr.back() - t0) * 1e-3,
+              (lev.front() - t0) * 1e-3, (lev.back() - t0) * 1e-3,
+              ((double)lev.front() - (double)arr.back()) * 1e-3);
+    }
+    std::vector<unsigned long long> zero(tl.size(), 0ull);
+    GFX_CK(cudaMemcpyToSymbol(g_tl, zero.data(), zero.size() * 8));
+  }
+#endif
   std::vector<gfx_iter_rec> lrecs((size_t)summary[7]);
   if (!lrecs.empty())
     GFX_CK(cudaMemcpy(lrecs.data(), a.recs, lrecs.size() * sizeof(gfx_iter_rec),

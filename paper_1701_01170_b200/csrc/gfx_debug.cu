@@ -106,9 +106,20 @@ __global__ void k_gridsync_bench(int variant, int iters, unsigned* flags, unsign
                                  unsigned* sink) {
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   unsigned acc = 0;
+  __shared__ unsigned sh[4];
+  volatile unsigned* ctr = gen + 8;  // four level counters on one line
   for (int i = 0; i < iters; ++i) {
-    if (variant == 0) grid.sync();
-    else flag_barrier(flags, gen, (unsigned)i + 1);
+    if (variant == 1) flag_barrier(flags, gen, (unsigned)i + 1);
+    else grid.sync();
+    if (variant == 2) {  // every thread reads the counters (the level-end pattern)
+      acc += ctr[0] + ctr[1] + ctr[2] + ctr[3];
+    } else if (variant == 3) {  // thread 0 reads them, the block shares them
+      if (threadIdx.x == 0)
+        for (int k = 0; k < 4; ++k) sh[k] = ctr[k];
+      __syncthreads();
+      acc += sh[0] + sh[1] + sh[2] + sh[3];
+      __syncthreads();
+    }
     acc += flags[(blockIdx.x * 7 + i) % gridDim.x * 32];
   }
   if (acc == 0xdeadbeef) sink[0] = acc;

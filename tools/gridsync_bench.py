@@ -9,9 +9,9 @@ from paper_1701_01170_b200 import _native  # noqa: E402
 
 ctx = _native.Context(0)
 for blocks, threads in ((444, 256), (296, 256), (148, 768), (148, 256), (148, 512)):
-    for variant in (0, 1):
+    for variant in (0, 1, 2, 3):
         us = ctypes.c_float()
         _native.call("gfx_debug_gridsync", ctx.handle, variant, blocks, threads, 2000,
                      ctypes.byref(us))
-        print(f"blocks {blocks:4d} x {threads:4d}  {'cg' if variant == 0 else 'flag'}  "
+        print(f"blocks {blocks:4d} x {threads:4d}  {('cg', 'flag', 'cg+ctr-all', 'cg+ctr-t0')[variant]}  "
               f"{us.value:.3f} us/sync")
