@@ -480,9 +480,15 @@ GFX_API int gfx_dbfs_run_comm(gfx_dbfs* db, const gfx_dbfs_comm* comm, int64_t s
  * One LB expansion of F_d with functor variant 0 (stream only), 1 (stream +
  * visited probe) or 2 (full claim); visited = {labels < depth}. */
 /* Diagnostics: microseconds per grid-wide barrier (variant 0: cooperative
- * groups grid sync, 1: flag barrier) for a cooperative grid of blocks x threads. */
+ * groups grid sync, 1: flag barrier, 2: grid sync + every thread reads four
+ * counters on one line, 3: grid sync + one read per CTA) for a cooperative
+ * grid of blocks x threads. */
 GFX_API int gfx_debug_gridsync(gfx_ctx* ctx, int variant, int blocks, int threads, int iters,
                                float* us_per_sync);
+/* Diagnostic: ns per same-address atomic (variant 0 returned, 1 RED, 2 own
+ * line per warp), one atomic per warp per iteration over blocks x 256. */
+GFX_API int gfx_debug_atomics(gfx_ctx* ctx, int variant, int blocks, int iters,
+                              double* ns_per_atomic);
 /* Diagnostics: clock cycles per dependent load, chasing next = buf[next]
  * (uint32 words, device buffer prepared by the caller) from `start`. */
 GFX_API int gfx_debug_chase(gfx_ctx* ctx, const uint32_t* buf_d, int iters, uint32_t start,

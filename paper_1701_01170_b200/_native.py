@@ -176,6 +176,7 @@ _SIGS = {
     "gfx_dbfs_run_comm": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_double, c_double, c_int,
                                   POINTER(IterRec), c_int64, POINTER(Stats)]),
     "gfx_debug_gridsync": (c_int, [c_void_p, c_int, c_int, c_int, c_int, POINTER(c_float)]),
+    "gfx_debug_atomics": (c_int, [c_void_p, c_int, c_int, c_int, POINTER(c_double)]),
     "gfx_debug_chase": (c_int, [c_void_p, c_void_p, c_int, ctypes.c_uint32, POINTER(c_double)]),
     "gfx_debug_expand": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_int32,
                                  POINTER(c_float), POINTER(c_int64)]),

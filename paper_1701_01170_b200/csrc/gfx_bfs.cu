@@ -910,8 +910,21 @@ __device__ unsigned long long g_tl[kTlSlots * 2 * kTlCtas + kTlCtas];
       g_tl[(tl_slot * 2 + 1) * kTlCtas + blockIdx.x] = globaltimer();                    \
     ++tl_slot;                                                                           \
   } while (0)
+// GSTAMP(): the time every thread of the CTA has passed this point
+constexpr int kTlStamps = 96;
+__device__ unsigned long long g_tls[kTlStamps * kTlCtas];
+#define GSTAMP()                                                                         \
+  do {                                                                                   \
+    __syncthreads();                                                                     \
+    if (threadIdx.x == 0 && tl_stamp < kTlStamps)                                        \
+      g_tls[tl_stamp * kTlCtas + blockIdx.x] = globaltimer();                            \
+    ++tl_stamp;                                                                          \
+  } while (0)
 #else
 #define GSYNC() grid.sync()
+#define GSTAMP() \
+  do {           \
+  } while (0)
 #endif
 
 // kDO: direction-optimising run (pull levels and the frontier bitmaps
@@ -932,7 +945,7 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
   const unsigned long long t_start = leader ? globaltimer() : 0ull;
 #ifdef GFX_BFS_TIMELINE
-  int tl_slot = 0;
+  int tl_slot = 0, tl_stamp = 0;
   if (threadIdx.x == 0) g_tl[kTlSlots * 2 * kTlCtas + blockIdx.x] = globaltimer();
 #endif
 
@@ -1005,6 +1018,7 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
       if (threadIdx.x == 0) c.direct = 1;
       __syncthreads();
     }
+    GSTAMP();  // level start (decision taken)
     const LabelOut lab{a.labels, c.direct ? nullptr : a.lvl8};
     const int32_t depth = (int32_t)c.depth;
     const int64_t nf = c.nf;
@@ -1023,6 +1037,7 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
     // a direction-optimising run keeps the frontier as a bitmap at every
     // level: push levels also set the new frontier's bits (fbits), so a pull
     // level never converts a queue
+    GSTAMP();  // bitmap zeroing done
     uint32_t* fbits = kDO ? fnext : nullptr;
     long long level_edges = 0, nout = 0, work = 0, cands = 0, bytes = 0;
 
@@ -1083,6 +1098,7 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
                      &cur->out_len, gw, nw);
         for (int64_t i = gtid; i < stiles; i += nthr) a.status[i] = 0ull;
       }
+      GSTAMP();  // push body done
       GSYNC();
       cta_read_ctrs(agg, cur);
       level_edges = (long long)agg.rd[2];
@@ -1112,6 +1128,7 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
                                     a.rrow, a.rcol, a.directed, lab, a.preds, depth, actr, gw, nw,
                                     PS, a.head + a.n + 1, nullptr,
                                     qsmall ? a.order + c.q_end : nullptr, &cur->aux3);
+      GSTAMP();  // pull body done
       cta_flush_ctrs(agg, cur);
       GSYNC();
       cta_read_ctrs(agg, cur);
@@ -1314,8 +1331,41 @@ int bfs_device_loop(gfx_graph* g, int64_t source, int direction, double do_a, do
               (lev.front() - t0) * 1e-3, (lev.back() - t0) * 1e-3,
               ((double)lev.front() - (double)arr.back()) * 1e-3);
     }
+    std::vector<unsigned long long> ts((size_t)kTlStamps * kTlCtas);
+    GFX_CK(cudaMemcpyFromSymbol(ts.data(), g_tls, ts.size() * 8));
+    for (int k = 0; k < kTlStamps; ++k) {
+      std::vector<unsigned long long> v(ts.begin() + (size_t)k * kTlCtas,
+                                        ts.begin() + (size_t)k * kTlCtas + blocks);
+      if (v[0] < t0) break;
+      std::vector<int> ids(blocks);
+      for (int b = 0; b < blocks; ++b) ids[b] = b;
+      std::sort(ids.begin(), ids.end(), [&](int x, int y) { return v[x] > v[y]; });
+      std::sort(v.begin(), v.end());
+      fprintf(stderr, "stamp %2d min %8.2f med %8.2f p90 %8.2f max %8.2f | slowest CTAs", k,
+              (v.front() - t0) * 1e-3, (v[blocks / 2] - t0) * 1e-3,
+              (v[blocks * 9 / 10] - t0) * 1e-3, (v.back() - t0) * 1e-3);
+      for (int b = 0; b < 6; ++b) fprintf(stderr, " %d", ids[b]);
+      fprintf(stderr, "\n");
+    }
+    {
+      static unsigned long long ph[64][8];
+      GFX_CK(cudaMemcpyFromSymbol(ph, g_pull_ph, sizeof(ph)));
+      const int nwarps = blocks * kWarpsPerBlock;
+      for (int d = 0; d < 64; ++d)
+        if (ph[d][5])
+          fprintf(stderr,
+                  "pull depth %d per warp (us @1.965GHz): words+list %.2f head %.2f rebuild %.2f "
+                  "misses %.2f stores %.2f | groups/warp %.2f misses/group %.1f\n",
+                  d, ph[d][0] / 1965.0 / nwarps, ph[d][1] / 1965.0 / nwarps,
+                  ph[d][2] / 1965.0 / nwarps, ph[d][3] / 1965.0 / nwarps,
+                  ph[d][4] / 1965.0 / nwarps, (double)ph[d][5] / nwarps,
+                  (double)ph[d][6] / ph[d][5]);
+      memset(ph, 0, sizeof(ph));
+      GFX_CK(cudaMemcpyToSymbol(g_pull_ph, ph, sizeof(ph)));
+    }
     std::vector<unsigned long long> zero(tl.size(), 0ull);
     GFX_CK(cudaMemcpyToSymbol(g_tl, zero.data(), zero.size() * 8));
+    GFX_CK(cudaMemcpyToSymbol(g_tls, zero.data(), ts.size() * 8));
   }
 #endif
   std::vector<gfx_iter_rec> lrecs((size_t)summary[7]);

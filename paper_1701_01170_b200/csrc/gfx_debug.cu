@@ -125,6 +125,22 @@ __global__ void k_gridsync_bench(int variant, int iters, unsigned* flags, unsign
   if (acc == 0xdeadbeef) sink[0] = acc;
 }
 
+// same-address atomic throughput: every warp's lane 0 adds `iters` times to
+// one counter (variant 0, with return value), to one counter without using
+// the result (variant 1: RED), or to its own 128-byte line (variant 2)
+__global__ void k_atomic_bench(int variant, int iters, unsigned long long* ctr,
+                               unsigned long long* sink) {
+  if ((threadIdx.x & 31) != 0) return;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  unsigned long long acc = 0;
+  for (int i = 0; i < iters; ++i) {
+    if (variant == 0) acc += atomicAdd(ctr, 1ull);
+    else if (variant == 1) atomicAdd(ctr, 1ull);
+    else acc += atomicAdd(ctr + 16 * (wid & 1023), 1ull);
+  }
+  if (acc == 0xdeadbeefull) sink[0] = acc;
+}
+
 // dependent-load latency: one thread chases next = buf[next] through a
 // random cyclic permutation of `span` words (stride-randomised), timing
 // `iters` hops with clock64
@@ -183,6 +199,26 @@ extern "C" int gfx_debug_gridsync(gfx_ctx* ctx, int variant, int blocks, int thr
   float ms = 0.f;
   GFX_CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   *us_per_sync = ms * 1000.f / iters;
+  GFX_CK(cudaFree(buf));
+  return GFX_OK;
+}
+
+// ns per atomic over `blocks` x 256 threads (one atomic per warp per iteration)
+extern "C" int gfx_debug_atomics(gfx_ctx* ctx, int variant, int blocks, int iters,
+                                 double* ns_per_atomic) {
+  GFX_REQUIRE(ctx && ns_per_atomic && blocks > 0 && iters > 0, "gfx_debug_atomics: bad argument");
+  GFX_CK(cudaSetDevice(ctx->device));
+  unsigned long long* buf = nullptr;
+  GFX_CK(cudaMalloc(&buf, (1024 * 16 + 16) * 8));
+  GFX_CK(cudaMemsetAsync(buf, 0, (1024 * 16 + 16) * 8, ctx->stream));
+  k_atomic_bench<<<blocks, 256, 0, ctx->stream>>>(variant, 1, buf, buf + 1024 * 16);
+  GFX_CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  k_atomic_bench<<<blocks, 256, 0, ctx->stream>>>(variant, iters, buf, buf + 1024 * 16);
+  GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  GFX_CK(cudaEventSynchronize(ctx->ev1));
+  float ms = 0.f;
+  GFX_CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  *ns_per_atomic = ms * 1e6 / ((double)blocks * 8 * iters);
   GFX_CK(cudaFree(buf));
   return GFX_OK;
 }

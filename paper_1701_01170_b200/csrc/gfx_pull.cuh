@@ -30,6 +30,23 @@ struct LabelOut {
 
 constexpr int kPullBatch = 8;  // candidates per lane in flight
 
+// Diagnostic (-DGFX_BFS_TIMELINE only): SM cycles per pull phase summed over
+// warps, per depth: [0] bitmap words + candidate list, [1] head probes,
+// [2] found-bit rebuild, [3] misses, [4] stores, [5] groups, [6] misses count
+#ifdef GFX_BFS_TIMELINE
+static __device__ unsigned long long g_pull_ph[64][8];
+#define PULL_T(k)                                   \
+  do {                                              \
+    const long long t_ = clock64();                 \
+    ph[k] += (unsigned long long)(t_ - t_last);     \
+    t_last = t_;                                    \
+  } while (0)
+#else
+#define PULL_T(k) \
+  do {            \
+  } while (0)
+#endif
+
 // per-warp scratch of the pull phase (aliases the expansion's WarpSmem)
 struct PullSmem {
   int32_t cand[1024];    // compacted candidate vertices of the warp's 32 words
@@ -77,6 +94,10 @@ __device__ __forceinline__ void pull_groups(
   // (every warp's first group is static: the dynamic range starts after them)
   const int64_t nstatic = grab ? max(ngroups / nwarps - 1, (int64_t)1) * nwarps : ngroups;
   unsigned long long nxt = 0;
+#ifdef GFX_BFS_TIMELINE
+  unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long t_last = clock64();
+#endif
   for (int64_t grp = gw; grp < ngroups;) {
     const bool dyn_next = grp + nwarps >= nstatic;
     if (grab && dyn_next && lane == 0) nxt = atomicAdd(grab, 1ull);
@@ -103,6 +124,10 @@ __device__ __forceinline__ void pull_groups(
       }
     }
     __syncwarp();
+    PULL_T(0);
+#ifdef GFX_BFS_TIMELINE
+    ph[5] += 1;
+#endif
     cands += (unsigned long long)(lane == 0 ? total : 0);
     // phase 1: first probe of every candidate from the dense head array;
     // misses are compacted in place to the front of the list
@@ -150,6 +175,10 @@ __device__ __forceinline__ void pull_groups(
       }
     }
     __syncwarp();
+    PULL_T(1);
+#ifdef GFX_BFS_TIMELINE
+    ph[6] += nmiss;
+#endif
     // each lane rebuilds its word's found bits: its candidates are entries
     // [off, off + popc(cand)) of the list, whose hit bits are consecutive in
     // hitmask; deposit them onto the candidate bit positions (no shared
@@ -171,6 +200,7 @@ __device__ __forceinline__ void pull_groups(
       P.newbits[lane] = nb;
     }
     __syncwarp();
+    PULL_T(2);
     // phase 2: misses, one per lane, scanning on from the second in-neighbour
     // with four column loads in flight (early-exit count stays exact)
     for (int base = 0; base < nmiss; base += 32) {
@@ -228,6 +258,7 @@ __device__ __forceinline__ void pull_groups(
       }
     }
     __syncwarp();
+    PULL_T(3);
     {
       const uint32_t nb = w < words ? P.newbits[lane] : 0u;
       if (w < words) {
@@ -251,8 +282,13 @@ __device__ __forceinline__ void pull_groups(
       }
     }
     __syncwarp();
+    PULL_T(4);
     grp = (grab && dyn_next) ? nstatic + (int64_t)__shfl_sync(0xffffffffu, nxt, 0) : grp + nwarps;
   }
+#ifdef GFX_BFS_TIMELINE
+  if (lane == 0)
+    for (int k = 0; k < 7; ++k) atomicAdd(&g_pull_ph[depth & 63][k], ph[k]);
+#endif
   found_cnt = warp_sum_u64(found_cnt);
   in_edges = warp_sum_u64(in_edges);
   probes = warp_sum_u64(probes);
