@@ -201,15 +201,61 @@ __device__ __forceinline__ void pull_groups(
     }
     __syncwarp();
     PULL_T(2);
-    // phase 2: misses, one per lane, scanning on from the second in-neighbour
-    // with four column loads in flight (early-exit count stays exact)
+    // phase 2a (head2 given): the second in-neighbour of every miss from the
+    // dense head2 array (bit 31 = "in-degree is exactly 2"), up to
+    // kPB2 misses per lane in flight; most misses settle here without their
+    // row bounds, the rest are compacted in place for phase 2b
+    // (dense levels only: on sparse ones misses are rare and the extra
+    // pass only costs registers -- measured +2 us on the s24 level 3)
+    const bool two = head2 != nullptr && !count_in_edges;
+    if (two && kPB >= 8) {
+      constexpr int kPB2 = 4;
+      int nrest = 0;
+      for (int base = 0; base < nmiss; base += 32 * kPB2) {
+        int32_t uu[kPB2], h2[kPB2];
+        uint32_t fw[kPB2];
+#pragma unroll
+        for (int q = 0; q < kPB2; ++q) {
+          const int k = base + q * 32 + lane;
+          uu[q] = k < nmiss ? P.cand[k] : -1;
+          h2[q] = uu[q] >= 0 ? head2[uu[q]] : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < kPB2; ++q)
+          fw[q] = uu[q] >= 0 ? front.word(h2[q] & 0x7fffffff) : 0u;
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < kPB2; ++q) {
+          const int32_t s2 = h2[q] & 0x7fffffff;
+          const bool hit = uu[q] >= 0 && front.bit(fw[q], s2);
+          const bool rest = uu[q] >= 0 && !hit && h2[q] >= 0;
+          if (hit) {
+            labels.set(uu[q], depth);
+            preds[uu[q]] = s2;
+            atomicOr(&P.newbits[(uu[q] >> 5) - grp * 32], 1u << (uu[q] & 31));
+            ++found_cnt;
+            probes += 2;
+          } else if (uu[q] >= 0 && !rest) {  // in-degree 2, unfound
+            probes += 2;
+            in_edges += 2;
+          }
+          const unsigned rm = __ballot_sync(0xffffffffu, rest);
+          if (rest) P.cand[nrest + __popc(rm & ((1u << lane) - 1))] = uu[q];
+          nrest += __popc(rm);
+        }
+      }
+      __syncwarp();
+      nmiss = nrest;
+    }
+    // phase 2b: misses, one per lane, scanning on from the second (third
+    // after phase 2a) in-neighbour with four column loads in flight
+    // (early-exit count stays exact)
     for (int base = 0; base < nmiss; base += 32) {
       const int k = base + lane;
       if (k >= nmiss) continue;
       const int32_t uu = P.cand[k];
-      if (head2 != nullptr && !count_in_edges) {
-        // second in-neighbour from the dense head2 array (bit 31 = "in-degree
-        // is exactly 2"): most misses settle here without the row bounds
+      if (two && kPB < 8) {
+        // second in-neighbour inline (see phase 2a)
         int32_t h2 = head2[uu];
         const bool deg2 = h2 < 0;
         h2 &= 0x7fffffff;
@@ -230,7 +276,7 @@ __device__ __forceinline__ void pull_groups(
       const int64_t b = rrow[uu], e = rrow[uu + 1];
       bool found = false;
       int32_t par = -1;
-      int64_t p = b + ((head2 != nullptr && !count_in_edges) ? 2 : 1);
+      int64_t p = b + (two ? 2 : 1);
       while (p < e && !found) {
         int32_t sv[4];
         uint32_t wv[4];
