@@ -85,6 +85,9 @@ __device__ __forceinline__ void pull_groups(
   // qout (optional): the found vertices are also appended to a queue, one
   // reservation per 1024-vertex group (*qlen counts them)
   const int lane = threadIdx.x & 31;
+  // head / head2 are streamed once per level: no L1 allocation (the L1
+  // keeps the frontier words the probes hit), evict-first in L2
+  const unsigned long long pol = l2_evict_first_policy();
   unsigned long long found_cnt = 0, in_edges = 0, probes = 0, cands = 0;
   // groups are dealt out statically for all but the last ~1.5 rounds; the
   // rest are handed out dynamically when `grab` (a zeroed counter) is given
@@ -139,7 +142,7 @@ __device__ __forceinline__ void pull_groups(
       for (int q = 0; q < kPB; ++q) {
         const int k = base + q * 32 + lane;
         u[q] = k < total ? P.cand[k] : -1;
-        h[q] = u[q] >= 0 ? head[u[q]] : -1;
+        h[q] = u[q] >= 0 ? ld_stream_i32(head + u[q], pol) : -1;
       }
       // with head2, head carries bit 31 = "in-degree is exactly 1" (-1 stays
       // "no in-neighbour"): such a miss is settled without a second look
@@ -218,7 +221,7 @@ __device__ __forceinline__ void pull_groups(
         for (int q = 0; q < kPB2; ++q) {
           const int k = base + q * 32 + lane;
           uu[q] = k < nmiss ? P.cand[k] : -1;
-          h2[q] = uu[q] >= 0 ? head2[uu[q]] : 0;
+          h2[q] = uu[q] >= 0 ? ld_stream_i32(head2 + uu[q], pol) : 0;
         }
 #pragma unroll
         for (int q = 0; q < kPB2; ++q)
@@ -256,7 +259,7 @@ __device__ __forceinline__ void pull_groups(
       const int32_t uu = P.cand[k];
       if (two && kPB < 8) {
         // second in-neighbour inline (see phase 2a)
-        int32_t h2 = head2[uu];
+        int32_t h2 = ld_stream_i32(head2 + uu, pol);
         const bool deg2 = h2 < 0;
         h2 &= 0x7fffffff;
         if (front.bit(front.word(h2), h2)) {
