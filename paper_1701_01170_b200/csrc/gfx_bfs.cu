@@ -1118,6 +1118,10 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
       // after this one needs no bitmap-to-queue sweep.
       const long long ncand = c.n_u - (a.n - a.nnz);
       const bool qsmall = ncand <= (a.n >> 6);
+      // the first sparse pull level also writes every label (the deferred
+      // labels' final pass, overlapped with the latency-bound sweep); later
+      // levels label directly
+      const bool fold = qsmall && !c.direct;
       Counters* actr = reinterpret_cast<Counters*>(agg.ctr);  // summed per CTA
       if (ncand * 8 > a.n)
         pull_groups<BitmapFront, 8>(a.words, a.nz_in, a.visited, BitmapFront{fcur}, fnext, a.head,
@@ -1128,6 +1132,11 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
                                     a.rrow, a.rcol, a.directed, lab, a.preds, depth, actr, gw, nw,
                                     PS, a.head + a.n + 1, nullptr,
                                     qsmall ? a.order + c.q_end : nullptr, &cur->aux3);
+      // a sparse pull level deals its 1024-vertex groups statically, exactly
+      // as materialize_labels walks them, and only the owning warp writes a
+      // group's visited words and depth bytes: each warp labels its own
+      // groups right after pulling them, with no barrier in between
+      if (fold) materialize_labels(a, gw, nw);
       GSTAMP();  // pull body done
       cta_flush_ctrs(agg, cur);
       GSYNC();
@@ -1140,6 +1149,7 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
       if (threadIdx.x == 0) {
         c.fsel = (c.fsel + 1) % 3;
         c.queue_form = qsmall ? 1 : 0;
+        if (fold) c.direct = 1;
         if (qsmall) {
           c.q_off = c.q_end;
           c.q_end += nout;
