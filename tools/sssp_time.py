@@ -1,4 +1,4 @@
-"""SSSP device ms at s24 (delta 32 and default), min of 3 after warm-up: for
+"""SSSP device ms at s24 (delta 4, 32 and default), min of 3 after warm-up: for
 A/B sweeps of compile-time tunables (GFX_LIB_PATH=<variant .so>)."""
 import os
 import sys
@@ -11,7 +11,7 @@ from paper_1701_01170_b200.primitives.sssp import sssp_device  # noqa: E402
 
 dg = rmat_device_graph(24, 16, 0, weights=(1, 64), weight_seed=0)
 out = []
-for d in (32, None):
+for d in (4, 32, None):
     sssp_device(dg, 0, delta=d)
     out.append(round(min(sssp_device(dg, 0, delta=d)[2].device_ms for _ in range(3)), 3))
 print(*out)
