@@ -30,16 +30,41 @@ __global__ void __launch_bounds__(kPrBlock)
   __shared__ double s_warp[kPrBlock / 32];
   double dang = 0.0;
   unsigned long long work = 0;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t deg = row[v + 1] - row[v];
-    double c = 0.0;
-    if (active[v]) {
-      work += (unsigned long long)deg;
-      if (deg == 0) dang = __dadd_rn(dang, rank[v]);
-      else c = __ddiv_rn(__dmul_rn(damping, rank[v]), (double)deg);
+  // kPrCu vertices per thread in flight (independent loads), each thread's
+  // dangling terms still added in increasing v within the thread
+  constexpr int kPrCu = 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < n;
+       v0 += kPrCu * stride) {
+    int64_t r0[kPrCu], r1[kPrCu];
+    double rk[kPrCu];
+    uint8_t act[kPrCu];
+#pragma unroll
+    for (int k = 0; k < kPrCu; ++k) {
+      const int64_t v = v0 + k * stride;
+      r0[k] = r1[k] = 0;
+      rk[k] = 0.0;
+      act[k] = 0;
+      if (v < n) {
+        r0[k] = row[v];
+        r1[k] = row[v + 1];
+        rk[k] = rank[v];
+        act[k] = active[v];
+      }
     }
-    contrib[v] = c;
+#pragma unroll
+    for (int k = 0; k < kPrCu; ++k) {
+      const int64_t v = v0 + k * stride;
+      if (v >= n) break;
+      const int64_t deg = r1[k] - r0[k];
+      double c = 0.0;
+      if (act[k]) {
+        work += (unsigned long long)deg;
+        if (deg == 0) dang = __dadd_rn(dang, rk[k]);
+        else c = __ddiv_rn(__dmul_rn(damping, rk[k]), (double)deg);
+      }
+      contrib[v] = c;
+    }
   }
   dang = warp_sum_f64(dang);
   work = warp_sum_u64(work);
