@@ -680,56 +680,6 @@ __device__ __noinline__ void device_decide(long long n, long long m, long long n
     *mode = GFX_DIR_PUSH;
 }
 
-// Per-CTA aggregation of the level counters and queue reservations.  All
-// counters of a level share one 64-byte line, so per-warp atomics on them
-// serialise in one L2 slice (~3500 warps per level); the persistent loop
-// sums per CTA in shared memory and issues one atomic per CTA instead, and
-// one thread per CTA reads the counters back after a grid barrier.
-struct CtaAgg {
-  unsigned long long ctr[8];  // shared mirror of Counters (summed, then flushed)
-  unsigned long long rd[8];   // Counters as read after the last grid barrier
-  unsigned long long base;
-  int woff[kWarpsPerBlock + 1];
-};
-static_assert(sizeof(Counters) == 8 * sizeof(unsigned long long), "Counters layout");
-
-// every thread of the CTA: add the CTA's sums to the global counters and
-// clear them (callers separate this from the next use by a barrier)
-__device__ __forceinline__ void cta_flush_ctrs(CtaAgg& g, Counters* cur) {
-  __syncthreads();
-  if (threadIdx.x < 8) {
-    const unsigned long long v = g.ctr[threadIdx.x];
-    if (v) atomicAdd(reinterpret_cast<unsigned long long*>(cur) + threadIdx.x, v);
-    g.ctr[threadIdx.x] = 0ull;
-  }
-}
-
-// every thread of the CTA: read the 8 counters once per CTA into g.rd
-__device__ __forceinline__ void cta_read_ctrs(CtaAgg& g, const Counters* cur) {
-  if (threadIdx.x < 8)
-    g.rd[threadIdx.x] =
-        ld_volatile_u64(reinterpret_cast<const unsigned long long*>(cur) + threadIdx.x);
-  __syncthreads();
-}
-
-// every thread of the CTA: append every warp's staged output (ocnt entries
-// in W.obuf) to the queue with ONE reservation per CTA
-__device__ __forceinline__ void cta_flush(WarpSmem& W, int& ocnt, int32_t* __restrict__ out,
-                                          unsigned long long* __restrict__ out_len, CtaAgg& g) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (lane == 0) g.woff[wid + 1] = ocnt;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    g.woff[0] = 0;
-    for (int k = 1; k <= kWarpsPerBlock; ++k) g.woff[k] += g.woff[k - 1];
-    const int tot = g.woff[kWarpsPerBlock];
-    g.base = tot ? atomicAdd(out_len, (unsigned long long)tot) : 0ull;
-  }
-  __syncthreads();
-  const unsigned long long b = g.base + g.woff[wid];
-  for (int j = lane; j < ocnt; j += 32) out[b + j] = W.obuf[j];
-  ocnt = 0;
-}
 
 // Expansion of at most 32 items held one per lane (v, row base, degree; 0
 // for empty lanes) without any scan pass: the degrees are scanned with

@@ -168,9 +168,14 @@ __global__ void __launch_bounds__(256, 3) k_sssp_persistent(PSsspArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WarpSmem& W = warp_smem(smem_raw);
+  // the split / re-split phases' pile staging aliases the expansion's warp
+  // slices (the phases are separated by grid barriers): 24 KB less shared
+  // memory per CTA, i.e. that much more L1 for the distance probes
+  static_assert(sizeof(PileStage) <= sizeof(WarpSmem) * kWarpsPerBlock, "pile stage must fit");
+  PileStage& S = *reinterpret_cast<PileStage*>(smem_raw);
   __shared__ ScanSmem ss;
-  __shared__ PileStage S;
   __shared__ PSCtl c;
+  __shared__ CtaAgg agg;  // counters read back once per CTA (gfx_expand.cuh)
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   const int64_t gw = gtid >> 5, nw = nthr >> 5;
@@ -230,19 +235,21 @@ __global__ void __launch_bounds__(256, 3) k_sssp_persistent(PSsspArgs a) {
       scan_tile(t, stiles, F, nf, a.row, a.scan, a.rowbase, a.part, a.status, (unsigned)c.ph + 1u,
                 cur, ss);
     grid.sync();
+    cta_read_ctrs(agg, cur);
     {
       SsspRelaxOp<WT> op{a.dp, a.dist, a.mark, {}};
-      expand_tasks(W, op, F, nf, a.scan, a.rowbase, a.part,
-                   (int64_t)ld_volatile_u64(&cur->ntiles), (int64_t)ld_volatile_u64(&cur->total),
-                   a.col, wgt, a.touched, &cur->out_len, gw, nw);
+      expand_tasks(W, op, F, nf, a.scan, a.rowbase, a.part, (int64_t)agg.rd[3],
+                   (int64_t)agg.rd[2], a.col, wgt, a.touched, &cur->out_len, gw, nw, &agg);
     }
     for (int64_t i = gtid; i < stiles; i += nthr) a.status[i] = 0ull;
     grid.sync();
-    const int64_t ntouched = (int64_t)ld_volatile_u64(&cur->out_len);
+    cta_read_ctrs(agg, cur);
+    const int64_t ntouched = (int64_t)agg.rd[0];
     sssp_split_phase(S, a.touched, ntouched, a.dist, a.mark, c.th, a.nearq[c.q ^ 1], &cur->aux0,
                      a.far[c.f] + c.nfar, a.fkey[c.f] + c.nfar, &cur->aux1);
     grid.sync();
-    const long long slots = (long long)ld_volatile_u64(&cur->total);
+    cta_read_ctrs(agg, cur);
+    const long long slots = (long long)agg.rd[2];
     const long long bytes = 20 * nf + 8 * slots + 8 * ntouched;
     if (leader && c.nrec < a.rec_cap) {
       gfx_iter_rec r{};
@@ -252,7 +259,7 @@ __global__ void __launch_bounds__(256, 3) k_sssp_persistent(PSsspArgs a) {
       r.edges = slots;
       r.work = slots;
       r.bytes_alg = bytes;
-      r.n_u = c.nfar + (long long)ld_volatile_u64(&cur->aux1);
+      r.n_u = c.nfar + (long long)agg.rd[5];
       r.ms = (float)((sssp_gtime() - c.t0) * 1e-6);
       a.recs[c.nrec] = r;
     }
@@ -260,8 +267,8 @@ __global__ void __launch_bounds__(256, 3) k_sssp_persistent(PSsspArgs a) {
       c.nrec += 1;
       c.slots += slots;
       c.bytes += bytes;
-      c.nnear = (long long)ld_volatile_u64(&cur->aux0);
-      c.nfar += (long long)ld_volatile_u64(&cur->aux1);
+      c.nnear = (long long)agg.rd[4];
+      c.nfar += (long long)agg.rd[5];
       c.q ^= 1;
       c.ph += 1;
     }
