@@ -476,6 +476,31 @@ GFX_API int gfx_dbfs_run_comm(gfx_dbfs* db, const gfx_dbfs_comm* comm, int64_t s
                               int direction, double do_a, double do_b, int mu_edge_based,
                               gfx_iter_rec* recs, int64_t rec_cap, gfx_stats* stats);
 
+/* ---- device-resident partitioned BFS (SURVEY 8(e) low-latency path) -----
+ * Replaces the host-driven level loop of the partitioned BFS (gfx_dbfs_run:
+ * one host-launched collective per level) with ONE cooperative launch per
+ * rank; ranks exchange frontier slices, (dst, src) claim pairs and level
+ * counters through peer memory and device flags.  Same partition (owner(v) =
+ * v mod P, local id v / P), same results as gfx_dbfs_run / the reference
+ * bfs (primitives/bfs.py:42-159, direction.py:52-70).
+ * Virtual ranks: all P ranks run inside one launch on this GPU (CTA b runs
+ * rank b mod P) -- the complete multi-rank protocol on one device.
+ * lrow / lcol / n_local / m_local: P entries (gfx_dist_partition output). */
+typedef struct gfx_pdbfs gfx_pdbfs;
+GFX_API int gfx_pdbfs_create_virtual(gfx_ctx* ctx, int64_t n, int64_t m, int P,
+                                     const int64_t* const* lrow, const int32_t* const* lcol,
+                                     const int64_t* n_local, const int64_t* m_local,
+                                     gfx_pdbfs** out);
+GFX_API int gfx_pdbfs_destroy(gfx_pdbfs* e);
+/* One BFS; labels_d[q] / preds_d[q] (optional, int32 device, n_local[q]
+ * entries) receive rank q's labels (local ids) and preds (global ids). */
+GFX_API int gfx_pdbfs_run(gfx_pdbfs* e, int64_t source, int direction, double do_a, double do_b,
+                          int mu_edge_based, int32_t* const* labels_d, int32_t* const* preds_d,
+                          gfx_iter_rec* recs, int64_t rec_cap, gfx_stats* stats);
+/* count BFS runs back to back (one cooperative launch each); device ms. */
+GFX_API int gfx_pdbfs_batch(gfx_pdbfs* e, int64_t source, int64_t count, int direction,
+                            double do_a, double do_b, int mu_edge_based, float* ms);
+
 /* ---- kernel experiments (tools/expand_lab.py; not a product path) -------
  * One LB expansion of F_d with functor variant 0 (stream only), 1 (stream +
  * visited probe) or 2 (full claim); visited = {labels < depth}. */

@@ -175,6 +175,13 @@ _SIGS = {
                              POINTER(IterRec), c_int64, POINTER(Stats)]),
     "gfx_dbfs_run_comm": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_double, c_double, c_int,
                                   POINTER(IterRec), c_int64, POINTER(Stats)]),
+    "gfx_pdbfs_create_virtual": (c_int, [c_void_p, c_int64, c_int64, c_int, c_void_p, c_void_p,
+                                         c_void_p, c_void_p, POINTER(c_void_p)]),
+    "gfx_pdbfs_destroy": (c_int, [c_void_p]),
+    "gfx_pdbfs_run": (c_int, [c_void_p, c_int64, c_int, c_double, c_double, c_int, c_void_p,
+                              c_void_p, POINTER(IterRec), c_int64, POINTER(Stats)]),
+    "gfx_pdbfs_batch": (c_int, [c_void_p, c_int64, c_int64, c_int, c_double, c_double, c_int,
+                                POINTER(c_float)]),
     "gfx_debug_gridsync": (c_int, [c_void_p, c_int, c_int, c_int, c_int, POINTER(c_float)]),
     "gfx_debug_atomics": (c_int, [c_void_p, c_int, c_int, c_int, POINTER(c_double)]),
     "gfx_debug_chase": (c_int, [c_void_p, c_void_p, c_int, ctypes.c_uint32, POINTER(c_double)]),

@@ -425,6 +425,88 @@ def gather_labels(engines, n: int):
 
 
 # ---------------------------------------------------------------------------
+# device-resident partitioned BFS (csrc/gfx_pdbfs.cu): one cooperative launch
+# per rank, exchanges through peer memory and device flags
+# ---------------------------------------------------------------------------
+_DIR_CODES = {PUSH: 0, PULL: 1, "auto": 2}
+
+
+class VirtualRanksBfs:
+    """P ranks of the device-resident partitioned BFS inside ONE launch on one
+    GPU (CTA b runs rank b mod P): the complete multi-rank protocol -- sliced
+    frontier copies, peer inbox stores, counter tables -- on a single device.
+    ``run`` returns global int32 labels / preds (reassembled from the ranks'
+    local arrays) and the per-level records."""
+
+    def __init__(self, dg, P: int):
+        import torch
+
+        self.P, self.n, self.m = int(P), dg.num_vertices, dg.num_edges
+        self.device = dg.row.device
+        parts = [partition_graph(dg, self.P, r) for r in range(self.P)]
+        self._keep = parts  # the ranks' CSRs (the engine borrows them)
+        ctx = _native.Context.get(self.device.index)
+        torch.cuda.synchronize(self.device)
+        lrow = (ctypes.c_void_p * self.P)(*[_native.ptr(p[0]) for p in parts])
+        lcol = (ctypes.c_void_p * self.P)(*[_native.ptr(p[1]) for p in parts])
+        self.nl = [p[0].numel() - 1 for p in parts]
+        nl = (ctypes.c_int64 * self.P)(*self.nl)
+        ml = (ctypes.c_int64 * self.P)(*[p[1].numel() for p in parts])
+        h = ctypes.c_void_p()
+        _native.call("gfx_pdbfs_create_virtual", ctx.handle, self.n, self.m, self.P, lrow, lcol,
+                     nl, ml, ctypes.byref(h))
+        self.handle = h
+        self.labels = [torch.empty(max(k, 1), dtype=torch.int32, device=self.device)
+                       for k in self.nl]
+        self.preds = [torch.empty_like(t) for t in self.labels]
+
+    def close(self):
+        h = getattr(self, "handle", None)
+        if h:
+            self.handle = None
+            _native.call("gfx_pdbfs_destroy", h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown: the library may be gone
+            pass
+
+    def run(self, source: int, direction: str = "auto", do_a: float = 0.001, do_b: float = 0.2,
+            mu_edge_based: bool = False, rec_cap: int = 4096):
+        import torch
+
+        recs = (_native.IterRec * rec_cap)()
+        st = _native.Stats()
+        lab = (ctypes.c_void_p * self.P)(*[_native.ptr(t) for t in self.labels])
+        prd = (ctypes.c_void_p * self.P)(*[_native.ptr(t) for t in self.preds])
+        _native.call("gfx_pdbfs_run", self.handle, int(source), _DIR_CODES[direction],
+                     float(do_a), float(do_b), int(bool(mu_edge_based)), lab, prd, recs, rec_cap,
+                     ctypes.byref(st))
+        labels = torch.empty(self.n, dtype=torch.int32, device=self.device)
+        preds = torch.empty(self.n, dtype=torch.int32, device=self.device)
+        for r in range(self.P):
+            labels[r::self.P] = self.labels[r][: self.nl[r]]
+            preds[r::self.P] = self.preds[r][: self.nl[r]]
+        levels = [dict(iteration=recs[i].iteration, mode="pull" if recs[i].decision == 1 else "push",
+                       mode_before=PULL if recs[i].mode_before == 1 else PUSH,
+                       decision=PULL if recs[i].decision == 1 else PUSH,
+                       n_f=recs[i].frontier_in, n_u=recs[i].n_u, m_f=recs[i].m_f,
+                       m_u=recs[i].m_u, frontier_in=recs[i].frontier_in,
+                       frontier_out=recs[i].frontier_out, edges=recs[i].edges, ms=recs[i].ms)
+                  for i in range(st.num_records)]
+        return labels, preds, st, levels
+
+    def batch_ms(self, source: int, count: int, direction: str = "auto", do_a: float = 0.001,
+                 do_b: float = 0.2) -> float:
+        """count BFS back to back on the device; device ms for all of them."""
+        ms = ctypes.c_float()
+        _native.call("gfx_pdbfs_batch", self.handle, int(source), int(count),
+                     _DIR_CODES[direction], float(do_a), float(do_b), 0, ctypes.byref(ms))
+        return ms.value
+
+
+# ---------------------------------------------------------------------------
 # partitioned near/far SSSP (SURVEY 8(e); reference sssp.py:41-121, near_far.py)
 # ---------------------------------------------------------------------------
 def partition_weights(dg, lrow, P: int, r: int):
