@@ -399,6 +399,134 @@ __device__ __forceinline__ void expand_tasks(WarpSmem& W, Op& o, const int32_t* 
   else warp_flush(W, ocnt, out, out_len);
 }
 
+// Expansion of at most 32 items held one per lane (v, row base, degree; 0
+// for empty lanes) without any scan pass: the degrees are scanned with
+// shuffles, the exclusive offsets parked in the warp's shared memory, and
+// the slots [c0, c0 + 32 * Op::kBatch) for c0 = chunk0, chunk0 + stride, ...
+// expanded by this warp; a slot's item comes from a binary search over the
+// <= 32 offsets.  Returns the item set's slot count.  Output and claims as
+// expand_tasks (staged in the warp buffer, ocnt carried by the caller).
+template <class Op>
+__device__ __forceinline__ int64_t expand_items32(WarpSmem& W, Op& o, int32_t v, int64_t rb,
+                                                  int64_t deg, const int32_t* __restrict__ col,
+                                                  int32_t* __restrict__ out,
+                                                  unsigned long long* __restrict__ out_len,
+                                                  int& ocnt, int64_t chunk0, int64_t stride) {
+  constexpr int B = Op::kBatch;
+  const int lane = threadIdx.x & 31;
+  int64_t* ex = reinterpret_cast<int64_t*>(W.owner);  // exclusive offsets
+  int64_t incl = deg;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += y;
+  }
+  const int64_t total = __shfl_sync(0xffffffffu, incl, 31);
+  __syncwarp();
+  ex[lane] = incl - deg;
+  W.delta[lane] = rb - (incl - deg);
+  W.src[lane] = v;
+  __syncwarp();
+  const unsigned long long pol = l2_evict_first_policy();
+  for (int64_t c0 = chunk0; c0 < total; c0 += stride) {
+    int32_t d[B];
+    int it[B];
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      const int64_t sl = c0 + q * 32 + lane;
+      d[q] = -1;
+      it[q] = 0;
+      if (sl < total) {
+        int lo = 0, hi = 31;  // last item with ex[item] <= sl (empty items repeat offsets)
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (ex[mid] <= sl) lo = mid; else hi = mid - 1;
+        }
+        it[q] = lo;
+        d[q] = ld_stream_i32(col + W.delta[lo] + sl, pol);
+      }
+    }
+    o.prefetch(d);
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      const bool emit = d[q] >= 0 && o.visit(q, d[q], W.src[it[q]], 1, 0, 0);
+      const unsigned em = __ballot_sync(0xffffffffu, emit);
+      if (emit) W.obuf[ocnt + __popc(em & ((1u << lane) - 1))] = d[q];
+      ocnt += __popc(em);
+    }
+    if (ocnt > kOutCap - 32 * B) warp_flush(W, ocnt, out, out_len);
+  }
+  __syncwarp();
+  return total;
+}
+
+// A frontier of <= 32 items: every warp derives the whole plan and takes
+// its own slot chunks (the hub's level, the last levels).
+template <class Op>
+__device__ __forceinline__ void push_tiny(WarpSmem& W, Op& o, const int32_t* __restrict__ F,
+                                          int64_t nf, const int64_t* __restrict__ row,
+                                          const int32_t* __restrict__ col,
+                                          int32_t* __restrict__ out,
+                                          unsigned long long* __restrict__ out_len,
+                                          unsigned long long* __restrict__ total_out, int64_t gw,
+                                          int64_t nw, CtaAgg& agg) {
+  const int lane = threadIdx.x & 31;
+  int32_t v = 0;
+  int64_t rb = 0, deg = 0;
+  if (lane < nf) {
+    v = F[lane];
+    rb = row[v];
+    deg = row[v + 1] - rb;
+  }
+  int ocnt = 0;
+  const int64_t total = expand_items32(W, o, v, rb, deg, col, out, out_len, ocnt,
+                                       gw * 32 * Op::kBatch, nw * 32 * Op::kBatch);
+  cta_flush(W, ocnt, out, out_len, agg);
+  if (gw == 0 && lane == 0) *total_out = (unsigned long long)total;
+}
+
+// A frontier of up to kMidItems items: each warp expands 32 consecutive
+// items by itself (no scan pass, no plan barrier); items with more than
+// kHeavyDeg slots are set aside in `heavy` (count in *nheavy) for a second,
+// cooperative pass after the caller's barrier.
+constexpr int64_t kMidItems = 1 << 16;
+constexpr int64_t kHeavyDeg = 1024;
+template <class Op>
+__device__ __forceinline__ void push_mid(WarpSmem& W, Op& o, const int32_t* __restrict__ F,
+                                         int64_t nf, const int64_t* __restrict__ row,
+                                         const int32_t* __restrict__ col,
+                                         int32_t* __restrict__ out,
+                                         unsigned long long* __restrict__ out_len,
+                                         int32_t* __restrict__ heavy,
+                                         unsigned long long* __restrict__ nheavy, int64_t gw,
+                                         int64_t nw, CtaAgg& agg) {
+  const int lane = threadIdx.x & 31;
+  int ocnt = 0;
+  unsigned long long tot = 0;
+  for (int64_t base = gw * 32; base < nf; base += nw * 32) {
+    const int64_t i = base + lane;
+    int32_t v = 0;
+    int64_t rb = 0, deg = 0;
+    if (i < nf) {
+      v = F[i];
+      rb = row[v];
+      deg = row[v + 1] - rb;
+    }
+    const bool hv = deg > kHeavyDeg;
+    const unsigned hm = __ballot_sync(0xffffffffu, hv);
+    if (hm) {
+      unsigned long long at = 0;
+      if (lane == __ffs(hm) - 1) at = atomicAdd(nheavy, (unsigned long long)__popc(hm));
+      at = __shfl_sync(0xffffffffu, at, __ffs(hm) - 1);
+      if (hv) heavy[at + __popc(hm & ((1u << lane) - 1))] = i;
+    }
+    tot += (unsigned long long)expand_items32(W, o, v, rb, hv ? 0 : deg, col, out, out_len, ocnt,
+                                              0, 32 * Op::kBatch);
+  }
+  cta_flush(W, ocnt, out, out_len, agg);
+  if (lane == 0 && tot) atomicAdd(&agg.ctr[2], tot);  // Counters::total, flushed by the caller
+}
+
 template <class Op>
 __global__ void __launch_bounds__(kExpandBlock, Op::kMinBlocks)
     k_lb_expand(const int32_t* __restrict__ F, const unsigned long long* __restrict__ nf_d,

@@ -58,7 +58,8 @@ struct PdRank {
   const int32_t* head2;
   const uint32_t* nz;    // local rows with degree > 0
   uint32_t* visited;     // local ids
-  int32_t* labels;       // local ids, int32 (UNVISITED / depth)
+  int32_t* labels;       // local ids, int32 (UNVISITED / depth), written at the end
+  uint8_t* lvl8;         // local ids: depth bytes while labels are deferred
   int32_t* preds;        // local ids -> global parent, -1
   int32_t* order;        // local queue, every level's frontier concatenated
   int32_t* emit;         // push output before the owner split (global ids)
@@ -81,6 +82,7 @@ struct PdRank {
 
 struct PdArgs {
   const PdRank* rk;  // device array [P]
+  PdRank self;       // the executing rank's entry (real ranks): kernel-parameter operands
   int P, sh, me_real;
   int64_t n, m, wmax, inbox_cap, nnz;
   int32_t source;
@@ -94,7 +96,7 @@ struct PdArgs {
 
 struct PdCtl {
   long long nf, nf_loc, n_u, q_off, q_end, depth, reached, edges_total, switches, nrec;
-  int mode_state, queue_form, mode, fsel;
+  int mode_state, queue_form, mode, fsel, direct;
   double mf, mu;
   unsigned long long t0;
   unsigned epoch;
@@ -144,12 +146,35 @@ struct SlicedFront {
   }
 };
 
+// deferred labels of a rank: labels[l] = depth byte if visited, else
+// UNVISITED; four vertices per thread (16-byte label stores when aligned)
+__device__ __forceinline__ void pd_materialize(const PdRank& R, int64_t gtid, int64_t nthr) {
+  const bool vec = ((reinterpret_cast<uintptr_t>(R.labels) | reinterpret_cast<uintptr_t>(R.lvl8)) &
+                    15) == 0;
+  for (int64_t v = gtid * 4; v < R.nl; v += nthr * 4) {
+    const uint32_t bits = (R.visited[v >> 5] >> (v & 31)) & 0xFu;
+    if (vec && v + 3 < R.nl) {
+      const uint32_t d4 = *reinterpret_cast<const uint32_t*>(R.lvl8 + v);
+      int4 lab;
+      lab.x = (bits & 1u) ? (int32_t)(d4 & 0xFF) : GFX_UNVISITED;
+      lab.y = (bits & 2u) ? (int32_t)((d4 >> 8) & 0xFF) : GFX_UNVISITED;
+      lab.z = (bits & 4u) ? (int32_t)((d4 >> 16) & 0xFF) : GFX_UNVISITED;
+      lab.w = (bits & 8u) ? (int32_t)(d4 >> 24) : GFX_UNVISITED;
+      *reinterpret_cast<int4*>(R.labels + v) = lab;
+    } else {
+      for (int j = 0; j < 4 && v + j < R.nl; ++j)
+        R.labels[v + j] = ((bits >> j) & 1u) ? (int32_t)R.lvl8[v + j] : GFX_UNVISITED;
+    }
+  }
+}
+
 // push claim: owned targets claimed in place (label, pred, next-frontier
 // bit) and emitted; remote targets de-duplicated through `sent` and emitted
 // with their source remembered (the owner split follows the expansion)
-struct PdClaimOp {
+template <int B>
+struct PdClaimOpT {
   static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
-  static constexpr int kBatch = kVisitBatch;
+  static constexpr int kBatch = B;
   static constexpr int kMinBlocks = 3;
   uint32_t* visited;
   uint32_t* sent;
@@ -160,6 +185,7 @@ struct PdClaimOp {
   int32_t depth;
   int P, r, sh;
   uint32_t wv[kBatch];
+  uint8_t* lvl8 = nullptr;  // deferred labels (depth bytes)
   __device__ __forceinline__ int owner(int32_t d) const { return sh >= 0 ? (d & (P - 1)) : d % P; }
   __device__ __forceinline__ int32_t local(int32_t d) const { return sh >= 0 ? (d >> sh) : d / P; }
   __device__ int32_t src_value(int32_t) const { return 0; }
@@ -178,7 +204,8 @@ struct PdClaimOp {
       const uint32_t bit = 1u << (l & 31);
       if (wv[u] & bit) return false;
       if (atomicOr(&visited[l >> 5], bit) & bit) return false;
-      labels[l] = depth;
+      if (lvl8) lvl8[l] = (uint8_t)depth;
+      else labels[l] = depth;
       preds[l] = sg;
       atomicOr(&fnext[l >> 5], bit);
       return true;
@@ -218,7 +245,9 @@ struct PdSync {
   }
 };
 
-template <bool kVirt>
+// kMulti: P > 1 (the exchange code compiled in); the P = 1 instance carries
+// none of it (lower register pressure in its pull and expansion loops)
+template <bool kVirt, bool kMulti>
 __global__ void __launch_bounds__(256, 3) k_pdbfs(PdArgs a) {
   cg::grid_group grid = cg::this_grid();
   PdSync<kVirt> sync{grid};
@@ -228,7 +257,7 @@ __global__ void __launch_bounds__(256, 3) k_pdbfs(PdArgs a) {
   __shared__ ScanSmem ss;
   __shared__ PdCtl c;
   __shared__ CtaAgg agg;
-  const int P = a.P;
+  const int P = kMulti ? a.P : 1;
   const int me = kVirt ? (int)(blockIdx.x % P) : a.me_real;
   const int64_t rcta = kVirt ? blockIdx.x / P : blockIdx.x;
   const int64_t nrcta = kVirt ? gridDim.x / P : gridDim.x;
@@ -243,16 +272,16 @@ __global__ void __launch_bounds__(256, 3) k_pdbfs(PdArgs a) {
   }
   if (threadIdx.x < 8) agg.ctr[threadIdx.x] = 0ull;
   __syncthreads();
-  const PdRank& R = c.R;
+  // virtual ranks: the CTA's rank entry in shared memory; a real rank reads
+  // its own entry from the kernel parameters (constant-bank operands, no
+  // registers held)
+  const PdRank& R = kVirt ? c.R : a.self;
   const int32_t src_owner = a.sh >= 0 ? (a.source & (P - 1)) : a.source % P;
   const int32_t src_local = a.sh >= 0 ? (a.source >> a.sh) : a.source / P;
   const int64_t wl = R.wl, wmax = a.wmax;
 
   // ---- init (rank-local state; the exchange block: own copy only)
-  for (int64_t l = gtid; l < R.nl; l += nthr) {
-    R.labels[l] = GFX_UNVISITED;
-    R.preds[l] = -1;
-  }
+  for (int64_t l = gtid; l < R.nl; l += nthr) R.preds[l] = -1;  // labels: deferred
   for (int64_t w = gtid; w < wl; w += nthr) R.visited[w] = 0u;
   for (int64_t w = gtid; w < (a.n + 31) / 32; w += nthr) R.sent[w] = 0u;
   for (int64_t w = gtid; w < 3 * P * wmax; w += nthr) {
@@ -271,7 +300,7 @@ __global__ void __launch_bounds__(256, 3) k_pdbfs(PdArgs a) {
     // the source's level probes it); its owner also queues it
     R.gfront[0][(int64_t)src_owner * wmax + (src_local >> 5)] = 1u << (src_local & 31);
     if (me == src_owner) {
-      R.labels[src_local] = 0;
+      R.lvl8[src_local] = 0;
       R.visited[src_local >> 5] = 1u << (src_local & 31);
       R.order[0] = src_local;
     }
@@ -286,6 +315,7 @@ __global__ void __launch_bounds__(256, 3) k_pdbfs(PdArgs a) {
     c.mode_state = GFX_DIR_PUSH;
     c.queue_form = 1;
     c.fsel = 0;
+    c.direct = 0;
   }
   sync.rank();
 
@@ -304,6 +334,14 @@ __global__ void __launch_bounds__(256, 3) k_pdbfs(PdArgs a) {
       c.t0 = pd_gtime();
     }
     __syncthreads();
+    if (!c.direct && c.depth == 255) {
+      // depth bytes exhausted: labels so far written, labelled directly from here
+      pd_materialize(R, gtid, nthr);
+      sync.rank();
+      if (threadIdx.x == 0) c.direct = 1;
+      __syncthreads();
+    }
+    uint8_t* const lvl8 = c.direct ? nullptr : R.lvl8;
     const int32_t depth = (int32_t)c.depth;
     const int par = (int)(c.depth & 1);
     Counters* cur = &R.C[c.depth % 3];
@@ -331,7 +369,7 @@ __global__ void __launch_bounds__(256, 3) k_pdbfs(PdArgs a) {
           const int off = warp_excl_scan(__popc(x), lane, &tot);
           if (tot == 0) continue;
           unsigned long long b = 0;
-          if (lane == 0) b = atomicAdd(&cur->aux3, (unsigned long long)tot);
+          if (lane == 0) b = atomicAdd(&cur->aux0, (unsigned long long)tot);
           b = __shfl_sync(0xffffffffu, b, 0) + off;
           while (x) {
             const int k = __ffs(x) - 1;
@@ -349,23 +387,55 @@ __global__ void __launch_bounds__(256, 3) k_pdbfs(PdArgs a) {
       }
       const int32_t* F = R.order + c.q_off;
       const int64_t nf = c.nf_loc;
-      PdClaimOp op{R.visited, R.sent, R.sent_src, R.labels, R.preds, fnext_me, depth, P, me, a.sh,
-                   {}};
+      PdClaimOpT<kVisitBatch> op{R.visited, R.sent, R.sent_src, R.labels, R.preds, fnext_me,
+                                 depth, P, me, a.sh, {}, lvl8};
       // P = 1: the owned winners go straight into the queue (global = local)
       int32_t* out = P == 1 ? R.order + c.q_end : R.emit;
-      const int64_t stiles = (nf + kScanTileItems - 1) / kScanTileItems;
-      const unsigned ep = a.epoch_base + (unsigned)c.depth;
-      for (int64_t t = rcta; t < stiles; t += nrcta)
-        scan_tile(t, stiles, F, nf, R.row, R.scan, R.rowbase, R.part, R.status, ep, cur, ss);
-      sync.rank();
-      cta_read_ctrs(agg, cur);
-      expand_tasks(W, op, F, nf, R.scan, R.rowbase, R.part, (int64_t)agg.rd[3],
-                   (int64_t)agg.rd[2], R.col, nullptr, out, &cur->out_len, gw, nw, &agg);
-      for (int64_t i = gtid; i < stiles; i += nthr) R.status[i] = 0ull;
+      // expansion by frontier size, as the single-GPU loop: <= 32 items with
+      // no plan pass, <= 64K items 32 per warp (hubs after one barrier),
+      // else the fused degree scan + load-balanced tiles.  Chosen on the
+      // GLOBAL frontier size: every rank takes the same path, so the barrier
+      // sequence is identical on every rank (virtual ranks share one grid)
+      if (c.nf <= 32) {
+        PdClaimOpT<4> top{R.visited, R.sent, R.sent_src, R.labels, R.preds, fnext_me, depth, P, me,
+                          a.sh, {}, lvl8};
+        push_tiny(W, top, F, nf, R.row, R.col, out, &cur->out_len, &cur->total, gw, nw, agg);
+      } else if (c.nf <= kMidItems) {
+        push_mid(W, op, F, nf, R.row, R.col, out, &cur->out_len, R.part, &cur->aux3, gw, nw, agg);
+        cta_flush_ctrs(agg, cur);
+        sync.rank();
+        cta_read_ctrs(agg, cur);
+        const int64_t nh = (int64_t)agg.rd[7];
+        for (int64_t h0 = 0; h0 < nh; h0 += 32) {  // heavy items, 32 at a time
+          const int lane = threadIdx.x & 31;
+          int32_t v = 0;
+          int64_t rb = 0, deg = 0;
+          if (h0 + lane < nh) {
+            v = F[R.part[h0 + lane]];
+            rb = R.row[v];
+            deg = R.row[v + 1] - rb;
+          }
+          int ocnt = 0;
+          const int64_t t = expand_items32(W, op, v, rb, deg, R.col, out, &cur->out_len, ocnt,
+                                           gw * 32 * kVisitBatch, nw * 32 * kVisitBatch);
+          warp_flush(W, ocnt, out, &cur->out_len);
+          if (gtid == 0) atomicAdd(&cur->total, (unsigned long long)t);
+        }
+      } else {
+        const int64_t stiles = (nf + kScanTileItems - 1) / kScanTileItems;
+        const unsigned ep = a.epoch_base + (unsigned)c.depth;
+        for (int64_t t = rcta; t < stiles; t += nrcta)
+          scan_tile(t, stiles, F, nf, R.row, R.scan, R.rowbase, R.part, R.status, ep, cur, ss);
+        sync.rank();
+        cta_read_ctrs(agg, cur);
+        expand_tasks(W, op, F, nf, R.scan, R.rowbase, R.part, (int64_t)agg.rd[3],
+                     (int64_t)agg.rd[2], R.col, nullptr, out, &cur->out_len, gw, nw, &agg);
+        for (int64_t i = gtid; i < stiles; i += nthr) R.status[i] = 0ull;
+      }
       sync.rank();
       cta_read_ctrs(agg, cur);
       slots_loc = (long long)agg.rd[2];
-      if (P == 1) {
+      if constexpr (!kMulti) {
         nout_loc = (long long)agg.rd[0];
       } else {
         // owner split: owned winners -> queue (local ids), remote
@@ -419,7 +489,8 @@ __global__ void __launch_bounds__(256, 3) k_pdbfs(PdArgs a) {
               const uint32_t bit = 1u << (l & 31);
               if (!(atomicOr(&R.visited[l >> 5], bit) & bit)) {
                 won = true;
-                R.labels[l] = depth;
+                if (lvl8) lvl8[l] = (uint8_t)depth;
+                else R.labels[l] = depth;
                 R.preds[l] = s;
                 atomicOr(&fnext_me[l >> 5], bit);
               }
@@ -448,11 +519,11 @@ __global__ void __launch_bounds__(256, 3) k_pdbfs(PdArgs a) {
       const SlicedFront front{fcur, wmax, P, a.sh};
       if (ncand * 8 > a.n)
         pull_groups<SlicedFront, 8>(wl, R.nz, R.visited, front, fnext_me, R.head, R.row, R.col, 0,
-                                    LabelOut{R.labels, nullptr}, R.preds, depth, actr, gw, nw, PS,
+                                    LabelOut{R.labels, lvl8}, R.preds, depth, actr, gw, nw, PS,
                                     R.head2, &cur->aux2);
       else
         pull_groups<SlicedFront, 4>(wl, R.nz, R.visited, front, fnext_me, R.head, R.row, R.col, 0,
-                                    LabelOut{R.labels, nullptr}, R.preds, depth, actr, gw, nw, PS,
+                                    LabelOut{R.labels, lvl8}, R.preds, depth, actr, gw, nw, PS,
                                     R.head2, nullptr, qsmall ? R.order + c.q_end : nullptr,
                                     &cur->aux3);
       cta_flush_ctrs(agg, cur);
@@ -472,7 +543,7 @@ __global__ void __launch_bounds__(256, 3) k_pdbfs(PdArgs a) {
     // ---- end of level: the rank's next-frontier slice and level counters
     // to every rank, then the global sums
     long long g_nout = nout_loc, g_slots = slots_loc, g_probes = probes_loc, g_cands = cands_loc;
-    if (P > 1) {
+    if constexpr (kMulti) {
       for (int q = 0; q < P; ++q) {
         if (q == me) continue;
         uint32_t* dst = a.rk[q].gfront[(c.fsel + 1) % 3] + me * wmax;
@@ -528,6 +599,7 @@ __global__ void __launch_bounds__(256, 3) k_pdbfs(PdArgs a) {
     __syncthreads();
     if (c.nf == 0) break;
   }
+  if (!c.direct) pd_materialize(R, gtid, nthr);
   if (leader) {
     a.summary[0] = c.depth;
     a.summary[1] = c.edges_total;
@@ -615,6 +687,7 @@ int pd_setup_rank(gfx_pdbfs* e, int q, const int64_t* lrow, const int32_t* lcol,
   R.head2 = heads + nl + 1;
   GFX_TRY(pd_alloc_t(o, R.wl + 1, &R.visited));
   GFX_TRY(pd_alloc_t(o, nl + 1, &R.labels));
+  GFX_TRY(pd_alloc_t(o, (size_t)nl + 16, &R.lvl8));
   GFX_TRY(pd_alloc_t(o, nl + 1, &R.preds));
   GFX_TRY(pd_alloc_t(o, nl + 2, &R.order));
   GFX_TRY(pd_alloc_t(o, (size_t)e->n + 1, &R.emit));
@@ -642,10 +715,15 @@ int pd_setup_rank(gfx_pdbfs* e, int q, const int64_t* lrow, const int32_t* lcol,
   return GFX_OK;
 }
 
+const void* pd_kernel(const gfx_pdbfs* e) {
+  if (e->P == 1) return (const void*)k_pdbfs<false, false>;
+  return e->virt ? (const void*)k_pdbfs<true, true> : (const void*)k_pdbfs<false, true>;
+}
+
 int pd_grid(gfx_pdbfs* e) {
   const int smem = kWarpScratch * kWarpsPerBlock;
   int per_sm = 0;
-  const void* fn = e->virt ? (const void*)k_pdbfs<true> : (const void*)k_pdbfs<false>;
+  const void* fn = pd_kernel(e);
   GFX_CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   GFX_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem));
   GFX_REQUIRE(per_sm >= 1, "k_pdbfs cannot be resident");
@@ -681,6 +759,7 @@ int pd_launch(gfx_pdbfs* e, int64_t source, int direction, double do_a, double d
     while ((1 << a.sh) < e->P) ++a.sh;
   }
   a.me_real = e->me;
+  a.self = e->rk[e->virt ? 0 : e->me];
   a.n = e->n;
   a.m = e->m;
   a.wmax = e->wmax;
@@ -698,8 +777,8 @@ int pd_launch(gfx_pdbfs* e, int64_t source, int direction, double do_a, double d
   a.epoch_base = e->epoch;
   e->epoch += 4096;
   void* kargs[] = {&a};
-  GFX_CK(cudaLaunchCooperativeKernel(e->virt ? (const void*)k_pdbfs<true> : (const void*)k_pdbfs<false>,
-                                     dim3(e->grid), dim3(256), kargs, e->smem, e->ctx->stream));
+  GFX_CK(cudaLaunchCooperativeKernel(pd_kernel(e), dim3(e->grid), dim3(256), kargs, e->smem,
+                                     e->ctx->stream));
   count_launch();
   return GFX_OK;
 }
