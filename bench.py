@@ -52,7 +52,10 @@ def parse_args():
     ap.add_argument("--write-ref-cache", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--python-loop", action="store_true",
                     help="partitioned engine: drive the levels from Python (dist.bfs_partitioned) "
-                         "instead of the native loop (gfx_dbfs_run)")
+                         "instead of the native loop (gfx_dbfs_run); implies --host-loop")
+    ap.add_argument("--host-loop", action="store_true",
+                    help="partitioned engine: the host-driven level loop with NCCL collectives "
+                         "(gfx_dbfs_run) instead of the device-resident kernel (gfx_pdbfs)")
     return ap.parse_args()
 
 
@@ -369,6 +372,11 @@ def run_partitioned(args, dist: Dist):
             extra["sssp_partitioned"] = _partitioned_sssp(args, dist)
         except Exception as exc:  # noqa: BLE001 -- report, keep the headline line
             extra["sssp_partitioned_error"] = repr(exc)
+    if P == 1 and not args.no_extras and not (args.host_loop or args.python_loop):
+        try:
+            extra["virtual_ranks"] = _virtual_ranks(args)
+        except Exception as exc:  # noqa: BLE001 -- report, keep the headline line
+            extra["virtual_ranks_error"] = repr(exc)
     peak, peak_kind = measured_peak_gbs()
     ms = t_ms / args.steps
     achieved = st.bytes_alg / (ms * 1e-3) / 1e9 / P
@@ -380,8 +388,12 @@ def run_partitioned(args, dist: Dist):
         "data": "synthetic",
         "config": workload_config(args, n, m, e_r, run["reached"]),
         "run": {"parallelism": f"1d-cyclic-partition{P}",
-                   "exchange": "NCCL all_to_all(pair counts) + send/recv(dst,src pairs) push / "
-                               "all_gather(frontier bitmaps) pull / allreduce(level counters)",
+                   "exchange": ("NCCL all_to_all(pair counts) + send/recv(dst,src pairs) push / "
+                                "all_gather(frontier bitmaps) pull / allreduce(level counters)")
+                   if (args.host_loop or args.python_loop) else
+                   ("peer stores over CUDA-IPC mappings: (dst,src) pairs into the owner's inbox "
+                    "(push), frontier-bitmap slices and level counters to every rank, "
+                    "release/acquire flag barriers"),
                    "level_loop": loop,
                    "l2": "per-BFS state re-initialised each step",
                    "graph_build_s": round(build_s, 3)},
@@ -408,6 +420,8 @@ def run_partitioned(args, dist: Dist):
 def _partitioned_run(args, dist, scale: int, steps: int, warmup: int, with_1gpu: bool = False):
     """Build R-MAT ``scale`` on every rank, keep this rank's partition, and
     time ``steps`` partitioned BFS (CUDA events, max over ranks)."""
+    if not (args.host_loop or args.python_loop):
+        return _partitioned_run_device(args, dist, scale, steps, warmup, with_1gpu)
     import torch
 
     from paper_1701_01170_b200 import _native
@@ -508,6 +522,135 @@ def _partitioned_run(args, dist, scale: int, steps: int, warmup: int, with_1gpu:
     return {"st": st, "t_ms": t_ms, "e_r": e_r, "reached": reached, "n": n, "m": m,
             "launches": launches,
             "build_s": build_s, "one_gpu": one_gpu, "loop": loop, "e2e": e2e}
+
+
+class _DevStats:
+    """DistBfsStats-shaped view of the device-resident engine's records."""
+
+    def __init__(self, levels, st):
+        self.iterations = st.iterations
+        self.direction_trace = [dict(iteration=lv["iteration"], decision=lv["decision"],
+                                     n_f=lv["n_f"]) for lv in levels]
+        self.bytes_alg = sum(lv["bytes_alg"] for lv in levels)
+        self.device_ms = st.device_ms
+
+
+def _one_gpu_reference(args, dg):
+    import torch
+
+    from paper_1701_01170_b200.primitives.bfs import bfs_batch, bfs_device
+
+    n = dg.num_vertices
+    lab = torch.empty(n, dtype=torch.int32, device=dg.row.device)
+    prd = torch.empty(n, dtype=torch.int32, device=dg.row.device)
+    for _ in range(3):
+        st1 = bfs_device(dg, args.source, direction=args.direction, labels=lab, preds=prd)[2]
+    ms1 = bfs_batch(dg, [args.source] * 5, direction=args.direction, labels=lab, preds=prd) / 5
+    return {"gteps": round(st1.edges_reached / (ms1 * 1e-3) / 1e9, 2), "ms": round(ms1, 4)}, lab
+
+
+def _partitioned_run_device(args, dist, scale: int, steps: int, warmup: int,
+                            with_1gpu: bool = False):
+    """The device-resident partitioned BFS (csrc/gfx_pdbfs.cu): one cooperative
+    launch per rank and BFS; frontier slices, claim pairs and level counters
+    go to the peers through CUDA-IPC mappings (NVLink) and device flag
+    barriers -- no host round trip and no host-launched collective per level.
+    ``steps`` BFS launched back to back, timed with CUDA events (max over
+    ranks)."""
+    import torch
+
+    from paper_1701_01170_b200 import _native
+    from paper_1701_01170_b200.dist import DeviceResidentRank
+    from paper_1701_01170_b200.generators import rmat_device_graph
+
+    P, r = dist.world, dist.rank
+    torch.cuda.empty_cache()
+    t_build = time.perf_counter()
+    dg = rmat_device_graph(scale, args.edge_factor, 0)
+    n, m = dg.num_vertices, dg.num_edges
+    one_gpu, ref_labels = None, None
+    if with_1gpu and r == 0:
+        one_gpu, ref_labels = _one_gpu_reference(args, dg)
+    eng = DeviceResidentRank(dg, P, r, group=None)
+    del dg
+    torch.cuda.empty_cache()
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t_build
+    for _ in range(warmup):
+        lab, prd, st, levels = eng.run(args.source, direction=args.direction)
+    deg = (eng.lrow[1:] - eng.lrow[:-1])
+    hit = lab != 2147483647
+    e_r = int(dist.sum(float(deg[hit].sum().item())))
+    reached = int(dist.sum(float(hit.sum().item())))
+    dist.barrier()
+    torch.cuda.synchronize()
+    l0 = _native.launch_count()
+    local_ms = eng.batch_ms(args.source, steps, direction=args.direction)
+    launches = _native.launch_count() - l0
+    dist.barrier()
+    t_ms = dist.max(local_ms)
+    # the timed launches leave the labels in the engine: the last run's result
+    lab, prd, st, levels = eng.run(args.source, direction=args.direction)
+    if with_1gpu:
+        match = _labels_match(eng, ref_labels if r == 0 else None, P, r, n)
+        if one_gpu is not None:
+            one_gpu["labels_equal_partitioned"] = match
+        ref_labels = None
+    # end to end with the graph resident: per step the source goes up and this
+    # rank's int32 labels + preds come back to pinned host memory
+    lab_h = torch.empty(eng.nl, dtype=torch.int32, pin_memory=True)
+    prd_h = torch.empty(eng.nl, dtype=torch.int32, pin_memory=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        lab, prd, _, _ = eng.run(args.source, direction=args.direction)
+        lab_h.copy_(lab, non_blocking=True)
+        prd_h.copy_(prd, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    dist.barrier()
+    e2e_ms = dist.max((time.perf_counter() - t0) * 1e3)
+    e2e = {"ms": e2e_ms, "d2h_bytes_per_step": int(dist.sum(float(8 * eng.nl))),
+           "h2d_bytes_per_step": 8 * P}
+    stats = _DevStats(levels, st)
+    eng.close()
+    del eng
+    torch.cuda.empty_cache()
+    return {"st": stats, "t_ms": t_ms, "e_r": e_r, "reached": reached, "n": n, "m": m,
+            "launches": launches, "build_s": build_s, "one_gpu": one_gpu,
+            "loop": "device-resident (gfx_pdbfs: one cooperative launch per rank, peer-memory "
+                    "exchange, device flag barriers)",
+            "e2e": e2e}
+
+
+def _virtual_ranks(args, Ps=(2, 4, 8), steps: int = 10):
+    """The device-resident partitioned BFS with P virtual ranks in ONE launch on
+    this GPU (dist.VirtualRanksBfs): the whole multi-rank protocol -- inbox
+    stores, sliced frontier copies, counter tables, exchange barriers -- with
+    every rank sharing one GPU's SMs and HBM.  Labels checked against the
+    single-GPU BFS."""
+    import torch
+
+    from paper_1701_01170_b200.dist import VirtualRanksBfs
+    from paper_1701_01170_b200.generators import rmat_device_graph
+    from paper_1701_01170_b200.primitives.bfs import bfs_device
+
+    dg = rmat_device_graph(args.scale, args.edge_factor, 0)
+    ref = bfs_device(dg, args.source, direction=args.direction)[0]
+    out = {"what": "P ranks of the partitioned BFS in one launch on ONE GPU (CTA b runs rank "
+                   "b mod P); ms per BFS over back-to-back launches"}
+    for P in Ps:
+        eng = VirtualRanksBfs(dg, P)
+        lab, _, st, levels = eng.run(args.source, direction=args.direction)
+        ok = bool(torch.equal(lab, ref))
+        eng.batch_ms(args.source, 2, direction=args.direction)
+        ms = eng.batch_ms(args.source, steps, direction=args.direction) / steps
+        out[f"P{P}"] = {"ms": round(ms, 4), "labels_equal_1gpu": ok,
+                        "levels_ms": [round(lv["ms"], 4) for lv in levels]}
+        eng.close()
+        del eng
+        torch.cuda.empty_cache()
+    return out
 
 
 def _partitioned_sssp(args, dist, delta: int = 32, steps: int = 3):

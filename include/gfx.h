@@ -492,6 +492,19 @@ GFX_API int gfx_pdbfs_create_virtual(gfx_ctx* ctx, int64_t n, int64_t m, int P,
                                      const int64_t* n_local, const int64_t* m_local,
                                      gfx_pdbfs** out);
 GFX_API int gfx_pdbfs_destroy(gfx_pdbfs* e);
+/* Real ranks, one process per GPU: rank r's engine over its partition.  Its
+ * exchange block is shared through CUDA IPC: gfx_pdbfs_export writes 5
+ * cudaIpcMemHandle_t (320 bytes); the caller all-gathers them (P x 320
+ * bytes, rank-major) and the sum over ranks of gfx_pdbfs_local_nnz
+ * (vertices with degree > 0), and every rank calls gfx_pdbfs_import before
+ * its first run (at P = 1: with its own handles and count). */
+GFX_API int gfx_pdbfs_create_rank(gfx_ctx* ctx, int64_t n, int64_t m, int P, int r,
+                                  const int64_t* lrow, const int32_t* lcol, int64_t n_local,
+                                  int64_t m_local, gfx_pdbfs** out);
+GFX_API int gfx_pdbfs_local_nnz(gfx_pdbfs* e, int64_t* nnz);
+GFX_API int gfx_pdbfs_export(gfx_pdbfs* e, void* handles);
+GFX_API int gfx_pdbfs_import(gfx_pdbfs* e, const void* all_handles, int64_t nnz_global);
+
 /* One BFS; labels_d[q] / preds_d[q] (optional, int32 device, n_local[q]
  * entries) receive rank q's labels (local ids) and preds (global ids). */
 GFX_API int gfx_pdbfs_run(gfx_pdbfs* e, int64_t source, int direction, double do_a, double do_b,

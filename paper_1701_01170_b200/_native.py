@@ -178,6 +178,11 @@ _SIGS = {
     "gfx_pdbfs_create_virtual": (c_int, [c_void_p, c_int64, c_int64, c_int, c_void_p, c_void_p,
                                          c_void_p, c_void_p, POINTER(c_void_p)]),
     "gfx_pdbfs_destroy": (c_int, [c_void_p]),
+    "gfx_pdbfs_create_rank": (c_int, [c_void_p, c_int64, c_int64, c_int, c_int, c_void_p,
+                                      c_void_p, c_int64, c_int64, POINTER(c_void_p)]),
+    "gfx_pdbfs_local_nnz": (c_int, [c_void_p, POINTER(c_int64)]),
+    "gfx_pdbfs_export": (c_int, [c_void_p, c_void_p]),
+    "gfx_pdbfs_import": (c_int, [c_void_p, c_void_p, c_int64]),
     "gfx_pdbfs_run": (c_int, [c_void_p, c_int64, c_int, c_double, c_double, c_int, c_void_p,
                               c_void_p, POINTER(IterRec), c_int64, POINTER(Stats)]),
     "gfx_pdbfs_batch": (c_int, [c_void_p, c_int64, c_int64, c_int, c_double, c_double, c_int,

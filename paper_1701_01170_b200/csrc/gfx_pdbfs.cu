@@ -826,6 +826,96 @@ int gfx_pdbfs_create_virtual(gfx_ctx* ctx, int64_t n, int64_t m, int P,
   return GFX_OK;
 }
 
+// Real ranks (one process per GPU).  Rank r allocates its own buffers; its
+// exchange block (frontier copies, inbox, inbox counts, counter table,
+// barrier flags) is exported as CUDA-IPC handles, all-gathered by the caller
+// (torch.distributed) and imported by every peer, after which peers store
+// into it directly over NVLink.
+constexpr int kPdHandles = 5;
+
+int gfx_pdbfs_create_rank(gfx_ctx* ctx, int64_t n, int64_t m, int P, int r, const int64_t* lrow,
+                          const int32_t* lcol, int64_t n_local, int64_t m_local,
+                          gfx_pdbfs** out) {
+  GFX_NVTX("gfx_pdbfs_create_rank");
+  GFX_REQUIRE(ctx && lrow && out, "gfx_pdbfs_create_rank: null argument");
+  GFX_REQUIRE(P >= 1 && P <= kPdMaxRanks && r >= 0 && r < P, "bad partition P=%d r=%d", P, r);
+  GFX_REQUIRE(n > 0 && n < (int64_t)INT32_MAX, "n=%lld out of range", (long long)n);
+  GFX_REQUIRE(n_local == (n > r ? (n - r + P - 1) / P : 0), "n_local does not match the partition");
+  GFX_CK(cudaSetDevice(ctx->device));
+  auto* e = new gfx_pdbfs();
+  e->ctx = ctx;
+  e->P = P;
+  e->me = r;
+  e->virt = 0;
+  e->n = n;
+  e->m = m;
+  const int64_t nmax = (n + P - 1) / P;
+  e->wmax = (nmax + 31) / 32;
+  e->inbox_cap = nmax + 1;
+  e->own.resize(1);
+  e->rk.assign(P, PdRank{});
+  int st = pd_setup_rank(e, r, lrow, lcol, n_local, m_local, e->own[0], e->rk[r]);
+  if (st == GFX_OK) {
+    e->nnz = e->rk[r].nnz;  // the global count arrives with gfx_pdbfs_import
+    st = pd_finish_create(e);
+  }
+  if (st == GFX_OK) st = pd_upload_table(e);
+  if (st != GFX_OK) {
+    gfx_pdbfs_destroy(e);
+    return st;
+  }
+  GFX_CK(cudaStreamSynchronize(ctx->stream));
+  *out = e;
+  return GFX_OK;
+}
+
+// vertices of this rank with degree > 0 (the caller sums them over ranks)
+int gfx_pdbfs_local_nnz(gfx_pdbfs* e, int64_t* nnz) {
+  GFX_REQUIRE(e && nnz, "gfx_pdbfs_local_nnz: null argument");
+  *nnz = e->rk[e->virt ? 0 : e->me].nnz;
+  return GFX_OK;
+}
+
+// kPdHandles cudaIpcMemHandle_t (64 bytes each) of this rank's exchange block
+int gfx_pdbfs_export(gfx_pdbfs* e, void* handles) {
+  GFX_REQUIRE(e && handles && !e->virt, "gfx_pdbfs_export: real-rank engine required");
+  const PdRank& R = e->rk[e->me];
+  void* bases[kPdHandles] = {R.gfront[0], R.inbox, R.inbox_cnt, R.ctab, R.flags};
+  auto* h = static_cast<cudaIpcMemHandle_t*>(handles);
+  for (int k = 0; k < kPdHandles; ++k) GFX_CK(cudaIpcGetMemHandle(&h[k], bases[k]));
+  return GFX_OK;
+}
+
+// all ranks' handles (P x kPdHandles, rank-major): map every peer's
+// exchange block and publish the rank table to the device
+int gfx_pdbfs_import(gfx_pdbfs* e, const void* all_handles, int64_t nnz_global) {
+  GFX_REQUIRE(e && all_handles && !e->virt, "gfx_pdbfs_import: real-rank engine required");
+  GFX_REQUIRE(nnz_global >= e->rk[e->me].nnz && nnz_global <= e->n, "bad nnz_global %lld",
+              (long long)nnz_global);
+  e->nnz = nnz_global;
+  GFX_CK(cudaSetDevice(e->ctx->device));
+  const auto* h = static_cast<const cudaIpcMemHandle_t*>(all_handles);
+  for (int q = 0; q < e->P; ++q) {
+    if (q == e->me) continue;
+    void* p[kPdHandles];
+    for (int k = 0; k < kPdHandles; ++k) {
+      GFX_CK(cudaIpcOpenMemHandle(&p[k], h[q * kPdHandles + k], cudaIpcMemLazyEnablePeerAccess));
+      e->ipc_opened.push_back(p[k]);
+    }
+    PdRank& Q = e->rk[q];
+    std::memset(&Q, 0, sizeof(Q));
+    auto* gf = static_cast<uint32_t*>(p[0]);
+    for (int k = 0; k < 3; ++k) Q.gfront[k] = gf + (size_t)k * e->P * e->wmax;
+    Q.inbox = static_cast<unsigned long long*>(p[1]);
+    Q.inbox_cnt = static_cast<unsigned long long*>(p[2]);
+    Q.ctab = static_cast<long long*>(p[3]);
+    Q.flags = static_cast<unsigned*>(p[4]);
+  }
+  GFX_TRY(pd_upload_table(e));
+  GFX_CK(cudaStreamSynchronize(e->ctx->stream));
+  return GFX_OK;
+}
+
 int gfx_pdbfs_destroy(gfx_pdbfs* e) {
   if (!e) return GFX_OK;
   cudaSetDevice(e->ctx->device);

@@ -506,6 +506,83 @@ class VirtualRanksBfs:
         return ms.value
 
 
+class DeviceResidentRank:
+    """This process's rank of the device-resident partitioned BFS
+    (csrc/gfx_pdbfs.cu) -- one process per GPU.  Creation is collective over
+    ``group`` (torch.distributed): the ranks all-gather their CUDA-IPC
+    exchange handles and degree counts, then every rank maps its peers'
+    frontier copies, inboxes, counter tables and barrier flags.  ``run`` is
+    collective too (all ranks launch; the kernels meet at device barriers)."""
+
+    def __init__(self, dg, P: int, r: int, group=None):
+        import torch
+        import torch.distributed as tdist
+
+        self.P, self.r, self.n, self.m = int(P), int(r), dg.num_vertices, dg.num_edges
+        self.device = dg.row.device
+        self.lrow, self.lcol = partition_graph(dg, self.P, self.r)
+        self.nl = self.lrow.numel() - 1
+        ctx = _native.Context.get(self.device.index)
+        torch.cuda.synchronize(self.device)
+        h = ctypes.c_void_p()
+        _native.call("gfx_pdbfs_create_rank", ctx.handle, self.n, self.m, self.P, self.r,
+                     _native.ptr(self.lrow), _native.ptr(self.lcol), self.nl, self.lcol.numel(),
+                     ctypes.byref(h))
+        self.handle = h
+        nnz = ctypes.c_int64()
+        _native.call("gfx_pdbfs_local_nnz", h, ctypes.byref(nnz))
+        mine = ctypes.create_string_buffer(320)
+        _native.call("gfx_pdbfs_export", h, mine)
+        if self.P > 1:
+            gathered = [None] * self.P
+            tdist.all_gather_object(gathered, (mine.raw, int(nnz.value)), group=group)
+        else:
+            gathered = [(mine.raw, int(nnz.value))]
+        blob = ctypes.create_string_buffer(b"".join(g[0] for g in gathered), 320 * self.P)
+        _native.call("gfx_pdbfs_import", h, blob, sum(g[1] for g in gathered))
+        self.labels = torch.empty(max(self.nl, 1), dtype=torch.int32, device=self.device)
+        self.preds = torch.empty_like(self.labels)
+
+    def close(self):
+        h = getattr(self, "handle", None)
+        if h:
+            self.handle = None
+            _native.call("gfx_pdbfs_destroy", h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown: the library may be gone
+            pass
+
+    def run(self, source: int, direction: str = "auto", do_a: float = 0.001, do_b: float = 0.2,
+            rec_cap: int = 4096):
+        """One BFS (collective); returns this rank's (labels, preds) over its
+        local ids (preds are global ids), the stats and the level records."""
+        recs = (_native.IterRec * rec_cap)()
+        st = _native.Stats()
+        lab = (ctypes.c_void_p * 1)(_native.ptr(self.labels))
+        prd = (ctypes.c_void_p * 1)(_native.ptr(self.preds))
+        _native.call("gfx_pdbfs_run", self.handle, int(source), _DIR_CODES[direction],
+                     float(do_a), float(do_b), 0, lab, prd, recs, rec_cap, ctypes.byref(st))
+        levels = [dict(iteration=recs[i].iteration, mode="pull" if recs[i].decision == 1 else "push",
+                       mode_before=PULL if recs[i].mode_before == 1 else PUSH,
+                       decision=PULL if recs[i].decision == 1 else PUSH,
+                       n_f=recs[i].frontier_in, n_u=recs[i].n_u, m_f=recs[i].m_f,
+                       m_u=recs[i].m_u, frontier_in=recs[i].frontier_in,
+                       frontier_out=recs[i].frontier_out, edges=recs[i].edges, ms=recs[i].ms,
+                       bytes_alg=recs[i].bytes_alg)
+                  for i in range(st.num_records)]
+        return self.labels[: self.nl], self.preds[: self.nl], st, levels
+
+    def batch_ms(self, source: int, count: int, direction: str = "auto", do_a: float = 0.001,
+                 do_b: float = 0.2) -> float:
+        ms = ctypes.c_float()
+        _native.call("gfx_pdbfs_batch", self.handle, int(source), int(count),
+                     _DIR_CODES[direction], float(do_a), float(do_b), 0, ctypes.byref(ms))
+        return ms.value
+
+
 # ---------------------------------------------------------------------------
 # partitioned near/far SSSP (SURVEY 8(e); reference sssp.py:41-121, near_far.py)
 # ---------------------------------------------------------------------------

@@ -81,3 +81,20 @@ def test_push_only_virtual_ranks(P):
     assert st.edges_traversed == rec["bfs_edges_traversed"]
     # per-level discovered counts equal the reference's level sizes
     assert [lv["frontier_out"] for lv in levels] == [int(x) for x in rec["bfs_levels"][1:]] + [0]
+
+
+@pytest.mark.parametrize("P,scale", [(2, 12), (3, 16)])
+def test_real_ranks_processes_share_one_gpu(P, scale):
+    """Real-rank mode: P processes on the one GPU, each its own cooperative
+    launch; CUDA-IPC-mapped peer buffers and release/acquire flag barriers
+    (the code path one process per GPU runs over NVLink).  The gathered
+    labels equal the single-GPU BFS."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    r = subprocess.run([sys.executable, str(root / "tools" / "pd_procs_one_gpu.py"), str(scale),
+                        str(P)], capture_output=True, text=True, timeout=300, cwd=root)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "labels equal: True" in r.stdout, r.stdout[-2000:]
