@@ -514,6 +514,34 @@ GFX_API int gfx_pdbfs_run(gfx_pdbfs* e, int64_t source, int direction, double do
 GFX_API int gfx_pdbfs_batch(gfx_pdbfs* e, int64_t source, int64_t count, int direction,
                             double do_a, double do_b, int mu_edge_based, float* ms);
 
+/* ---- device-resident partitioned near/far SSSP (gfx_pdsssp.cu) ----------
+ * The low-latency form of the partitioned SSSP (gfx_dsssp: host-driven, one
+ * host-launched collective per step): one cooperative launch per rank;
+ * (d, dist << 32 | pred) offers stored into the owners' inboxes, level
+ * counters into every rank's table, flag barriers.  Reference sssp.py:41-121,
+ * near_far.py:20-85.  lw: the ranks' weights aligned with their local rows
+ * (gfx_dist_partition_weights).  Virtual ranks: all P inside one launch on
+ * this GPU; real ranks: one process per GPU, exchange block shared through
+ * CUDA IPC (export: 4 handles, 256 bytes; import: P x 256 bytes). */
+typedef struct gfx_pdsssp gfx_pdsssp;
+GFX_API int gfx_pdsssp_create_virtual(gfx_ctx* ctx, int64_t n, int P, const int64_t* const* lrow,
+                                      const int32_t* const* lcol, const int32_t* const* lw,
+                                      const int64_t* n_local, const int64_t* m_local,
+                                      gfx_pdsssp** out);
+GFX_API int gfx_pdsssp_create_rank(gfx_ctx* ctx, int64_t n, int P, int r, const int64_t* lrow,
+                                   const int32_t* lcol, const int32_t* lw, int64_t n_local,
+                                   int64_t m_local, gfx_pdsssp** out);
+GFX_API int gfx_pdsssp_export(gfx_pdsssp* e, void* handles);
+GFX_API int gfx_pdsssp_import(gfx_pdsssp* e, const void* all_handles);
+GFX_API int gfx_pdsssp_destroy(gfx_pdsssp* e);
+/* delta <= 0: one bucket (infinite width).  dist_d[k] / preds_d[k]: rank k's
+ * (virtual) or this rank's (real: k = 0) int32 outputs over local ids. */
+GFX_API int gfx_pdsssp_run(gfx_pdsssp* e, int64_t source, double delta, int32_t* const* dist_d,
+                           int32_t* const* preds_d, gfx_iter_rec* recs, int64_t rec_cap,
+                           gfx_stats* stats);
+GFX_API int gfx_pdsssp_batch(gfx_pdsssp* e, int64_t source, int64_t count, double delta,
+                             float* ms);
+
 /* ---- kernel experiments (tools/expand_lab.py; not a product path) -------
  * One LB expansion of F_d with functor variant 0 (stream only), 1 (stream +
  * visited probe) or 2 (full claim); visited = {labels < depth}. */

@@ -187,6 +187,16 @@ _SIGS = {
                               c_void_p, POINTER(IterRec), c_int64, POINTER(Stats)]),
     "gfx_pdbfs_batch": (c_int, [c_void_p, c_int64, c_int64, c_int, c_double, c_double, c_int,
                                 POINTER(c_float)]),
+    "gfx_pdsssp_create_virtual": (c_int, [c_void_p, c_int64, c_int, c_void_p, c_void_p, c_void_p,
+                                          c_void_p, c_void_p, POINTER(c_void_p)]),
+    "gfx_pdsssp_create_rank": (c_int, [c_void_p, c_int64, c_int, c_int, c_void_p, c_void_p,
+                                       c_void_p, c_int64, c_int64, POINTER(c_void_p)]),
+    "gfx_pdsssp_export": (c_int, [c_void_p, c_void_p]),
+    "gfx_pdsssp_import": (c_int, [c_void_p, c_void_p]),
+    "gfx_pdsssp_destroy": (c_int, [c_void_p]),
+    "gfx_pdsssp_run": (c_int, [c_void_p, c_int64, c_double, c_void_p, c_void_p, POINTER(IterRec),
+                               c_int64, POINTER(Stats)]),
+    "gfx_pdsssp_batch": (c_int, [c_void_p, c_int64, c_int64, c_double, POINTER(c_float)]),
     "gfx_debug_gridsync": (c_int, [c_void_p, c_int, c_int, c_int, c_int, POINTER(c_float)]),
     "gfx_debug_atomics": (c_int, [c_void_p, c_int, c_int, c_int, POINTER(c_double)]),
     "gfx_debug_chase": (c_int, [c_void_p, c_void_p, c_int, ctypes.c_uint32, POINTER(c_double)]),

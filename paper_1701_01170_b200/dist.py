@@ -736,3 +736,118 @@ def gather_sssp(engines, n: int):
         dist[e.r::P] = d
         preds[e.r::P] = p
     return dist, preds
+
+
+# ---------------------------------------------------------------------------
+# device-resident partitioned near/far SSSP (csrc/gfx_pdsssp.cu)
+# ---------------------------------------------------------------------------
+def _delta_arg(delta) -> float:
+    return float(delta) if delta is not None and delta > 0 else 0.0  # 0: one bucket
+
+
+class _PdSsspBase:
+    def close(self):
+        h = getattr(self, "handle", None)
+        if h:
+            self.handle = None
+            _native.call("gfx_pdsssp_destroy", h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown: the library may be gone
+            pass
+
+    def _run(self, source, delta, outs_d, outs_p, rec_cap):
+        recs = (_native.IterRec * rec_cap)()
+        st = _native.Stats()
+        dd = (ctypes.c_void_p * len(outs_d))(*[_native.ptr(t) for t in outs_d])
+        pp = (ctypes.c_void_p * len(outs_p))(*[_native.ptr(t) for t in outs_p])
+        _native.call("gfx_pdsssp_run", self.handle, int(source), _delta_arg(delta), dd, pp, recs,
+                     rec_cap, ctypes.byref(st))
+        return st
+
+    def batch_ms(self, source: int, count: int, delta=None) -> float:
+        ms = ctypes.c_float()
+        _native.call("gfx_pdsssp_batch", self.handle, int(source), int(count), _delta_arg(delta),
+                     ctypes.byref(ms))
+        return ms.value
+
+
+class VirtualRanksSssp(_PdSsspBase):
+    """P ranks of the device-resident partitioned SSSP in ONE launch on one GPU
+    (see VirtualRanksBfs).  ``run`` returns global int32 distances / preds."""
+
+    def __init__(self, dg, P: int):
+        import torch
+
+        self.P, self.n = int(P), dg.num_vertices
+        self.device = dg.row.device
+        parts = []
+        for r in range(self.P):
+            lrow, lcol = partition_graph(dg, self.P, r)
+            parts.append((lrow, lcol, partition_weights(dg, lrow, self.P, r)))
+        self._keep = parts
+        ctx = _native.Context.get(self.device.index)
+        torch.cuda.synchronize(self.device)
+        arr = lambda k: (ctypes.c_void_p * self.P)(*[_native.ptr(p[k]) for p in parts])  # noqa: E731
+        self.nl = [p[0].numel() - 1 for p in parts]
+        nl = (ctypes.c_int64 * self.P)(*self.nl)
+        ml = (ctypes.c_int64 * self.P)(*[p[1].numel() for p in parts])
+        h = ctypes.c_void_p()
+        _native.call("gfx_pdsssp_create_virtual", ctx.handle, self.n, self.P, arr(0), arr(1),
+                     arr(2), nl, ml, ctypes.byref(h))
+        self.handle = h
+        self.dist = [torch.empty(max(k, 1), dtype=torch.int32, device=self.device) for k in self.nl]
+        self.preds = [torch.empty_like(t) for t in self.dist]
+
+    def run(self, source: int, delta=None, rec_cap: int = 1 << 14):
+        import torch
+
+        st = self._run(source, delta, self.dist, self.preds, rec_cap)
+        dist = torch.empty(self.n, dtype=torch.int32, device=self.device)
+        preds = torch.empty(self.n, dtype=torch.int32, device=self.device)
+        for r in range(self.P):
+            dist[r::self.P] = self.dist[r][: self.nl[r]]
+            preds[r::self.P] = self.preds[r][: self.nl[r]]
+        return dist, preds, st
+
+
+class DeviceResidentSsspRank(_PdSsspBase):
+    """This process's rank of the device-resident partitioned SSSP (one
+    process per GPU; creation and runs are collective, see
+    DeviceResidentRank)."""
+
+    def __init__(self, dg, P: int, r: int, group=None):
+        import torch
+        import torch.distributed as tdist
+
+        self.P, self.r, self.n = int(P), int(r), dg.num_vertices
+        self.device = dg.row.device
+        self.lrow, self.lcol = partition_graph(dg, self.P, self.r)
+        self.lw = partition_weights(dg, self.lrow, self.P, self.r)
+        self.nl = self.lrow.numel() - 1
+        ctx = _native.Context.get(self.device.index)
+        torch.cuda.synchronize(self.device)
+        h = ctypes.c_void_p()
+        _native.call("gfx_pdsssp_create_rank", ctx.handle, self.n, self.P, self.r,
+                     _native.ptr(self.lrow), _native.ptr(self.lcol), _native.ptr(self.lw),
+                     self.nl, self.lcol.numel(), ctypes.byref(h))
+        self.handle = h
+        mine = ctypes.create_string_buffer(256)
+        _native.call("gfx_pdsssp_export", h, mine)
+        if self.P > 1:
+            gathered = [None] * self.P
+            tdist.all_gather_object(gathered, mine.raw, group=group)
+        else:
+            gathered = [mine.raw]
+        blob = ctypes.create_string_buffer(b"".join(gathered), 256 * self.P)
+        _native.call("gfx_pdsssp_import", h, blob)
+        self.dist = torch.empty(max(self.nl, 1), dtype=torch.int32, device=self.device)
+        self.preds = torch.empty_like(self.dist)
+
+    def run(self, source: int, delta=None, rec_cap: int = 1 << 14):
+        """One SSSP (collective): this rank's distances / global preds over its
+        local ids, and the stats."""
+        st = self._run(source, delta, [self.dist], [self.preds], rec_cap)
+        return self.dist[: self.nl], self.preds[: self.nl], st
