@@ -676,6 +676,42 @@ def _partitioned_sssp(args, dist, delta: int = 32, steps: int = 3):
     else:
         e_r = 0
     e_r = int(dist.sum(float(e_r)))
+    if not (args.host_loop or args.python_loop):
+        # the device-resident engine (csrc/gfx_pdsssp.cu): one cooperative
+        # launch per rank and run, offers / counters through peer memory
+        from paper_1701_01170_b200.dist import DeviceResidentSsspRank
+
+        eng = DeviceResidentSsspRank(dgw, P, r)
+        del dgw
+        dl, _, st = eng.run(args.source, delta)  # warm-up
+        dist.barrier()
+        torch.cuda.synchronize()
+        ms = dist.max(eng.batch_ms(args.source, steps, delta)) / steps
+        dl, _, st = eng.run(args.source, delta)
+        nl = eng.nl
+        nlmax = (n + P - 1) // P
+        buf = torch.full((nlmax,), -2, dtype=torch.int32, device=eng.device)
+        buf[:nl] = dl
+        parts = [buf]
+        if P > 1:
+            import torch.distributed as tdist
+
+            parts = [torch.empty_like(buf) for _ in range(P)]
+            tdist.all_gather(parts, buf)
+        ok = None
+        if r == 0:
+            ok = all(bool(torch.equal(parts[q][: len(range(q, n, P))], ref[q::P]))
+                     for q in range(P))
+        eng.close()
+        del eng
+        torch.cuda.empty_cache()
+        return {"gteps": round(e_r / (ms * 1e-3) / 1e9, 2), "ms": round(ms, 3), "delta": delta,
+                "n_gpus": P, "iterations": st.iterations,
+                "bucket_advances": st.direction_switches, "relaxed_slots": st.work_slots,
+                "dist_equal_single_gpu": ok,
+                "what": "device-resident partitioned near/far SSSP (gfx_pdsssp: one cooperative "
+                        "launch per rank, offers and counters through peer memory, flag "
+                        "barriers); batched launches, CUDA events, max over ranks"}
     lrow, lcol = partition_graph(dgw, P, r)
     lw = partition_weights(dgw, lrow, P, r)
     eng = SsspEngine(lrow, lcol, lw, n, P, r)

@@ -52,3 +52,19 @@ def test_rmat_virtual_ranks_sssp(scale, P, delta):
         assert valid_sssp_preds(g.row_offsets, g.column_indices, g.edge_weights, lab,
                                 preds_to_host(preds), 0)
     eng.close()
+
+
+@pytest.mark.parametrize("P,scale", [(2, 12), (3, 14)])
+def test_real_ranks_processes_share_one_gpu_sssp(P, scale):
+    """Real-rank mode of the partitioned SSSP: P processes on the one GPU,
+    CUDA-IPC-mapped inboxes / counter tables, flag barriers across processes;
+    distances equal the single-GPU SSSP."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    r = subprocess.run([sys.executable, str(root / "tools" / "pd_procs_one_gpu.py"), str(scale),
+                        str(P), "sssp"], capture_output=True, text=True, timeout=300, cwd=root)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "labels equal: True" in r.stdout, r.stdout[-2000:]
