@@ -308,23 +308,27 @@ class DeviceGraph:
         self.upload_packed_(packed)
         self.decode_packed_()
 
-    def upload_packed_(self, packed) -> None:
+    def upload_packed_(self, packed, slot: int = 0) -> None:
         """Copy the packed streams into the graph's device staging buffers
-        (asynchronous on the current stream)."""
+        ``slot`` (0 or 1: two sets, so the next upload can overlap the decode
+        of this one; asynchronous on the current stream)."""
         import torch
 
-        st = getattr(self, "_pack_stage", None)
+        stages = getattr(self, "_pack_stage", None)
+        if stages is None:
+            stages = self._pack_stage = [None, None]
+        st = stages[slot]
         parts = packed.row + packed.col
         if st is None or any(d.numel() < h.numel() for d, h in zip(st, parts)):
             dev = self.row.device
             st = tuple(torch.empty(h.numel(), dtype=h.dtype, device=dev) for h in parts)
-            self._pack_stage = st
+            stages[slot] = st
         for d, h in zip(st, parts):
             d[: h.numel()].copy_(h, non_blocking=True)
 
-    def decode_packed_(self) -> None:
-        """Decode the staged streams into row / col and refresh the graph."""
-        rc, rd, rb, cc, cd, cb = self._pack_stage
+    def decode_packed_(self, slot: int = 0) -> None:
+        """Decode the staged streams ``slot`` into row / col and refresh the graph."""
+        rc, rd, rb, cc, cd, cb = self._pack_stage[slot]
         _native.call("gfx_csr_unpack", self.ctx.handle, _native.ptr(rc), _native.ptr(rd),
                      _native.ptr(rb), self.num_vertices + 1, _native.ptr(self.row), 8, 0)
         _native.call("gfx_csr_unpack", self.ctx.handle, _native.ptr(cc), _native.ptr(cd),
