@@ -36,7 +36,10 @@
 
 namespace gfx {
 
-template <class WT>
+// kLate: emit every improving relaxation (duplicates allowed) and leave the
+// once-per-iteration dedupe to the split pass (stamp test-and-set there):
+// the relax chain then has no atomic round trip at all
+template <class WT, bool kLate = false>
 struct SsspRelaxOp {
   using WeightT = WT;  // weight stream element: int32 or the compact uint8 copy
   static constexpr bool kWeights = true, kSrcVal = true, kEmitEdge = false;
@@ -64,6 +67,7 @@ struct SsspRelaxOp {
     const unsigned long long key = (nd << 32) | (uint32_t)s;
     atomicMin(&dp[d], key);
     atomicMin(&dist[d], (uint32_t)nd);
+    if (kLate) return true;
     const uint32_t bit = 1u << (d & 31);
     return !(atomicOr(&mark[d >> 5], bit) & bit);
   }
@@ -133,6 +137,7 @@ struct PSsspArgs {
   uint32_t* mark;
   int32_t* nearq[2];
   int32_t* touched;
+  int32_t* stamp;  // iteration that last enqueued each vertex (split dedupe)
   int32_t* far[2];
   int32_t* fkey[2];
   int64_t* scan;
@@ -189,6 +194,7 @@ __global__ void __launch_bounds__(256, 3) k_sssp_persistent(PSsspArgs a) {
     a.dist[v] = src ? 0u : 0xFFFFFFFFu;
   }
   for (int64_t i = gtid; i <= a.words; i += nthr) a.mark[i] = 0u;
+  for (int64_t v = gtid; v < a.n; v += nthr) a.stamp[v] = 0;
   for (int64_t i = gtid; i < 3 * (int64_t)(sizeof(Counters) / 8); i += nthr)
     reinterpret_cast<unsigned long long*>(a.C)[i] = 0ull;
   if (leader) a.nearq[0][0] = a.source;
@@ -237,7 +243,9 @@ __global__ void __launch_bounds__(256, 3) k_sssp_persistent(PSsspArgs a) {
     grid.sync();
     cta_read_ctrs(agg, cur);
     {
-      SsspRelaxOp<WT> op{a.dp, a.dist, a.mark, {}};
+      // improving relaxations emitted with duplicates, deduplicated by the
+      // split (measured: delta 4 6.78 -> 6.12 ms, delta 32 7.08 -> 6.17 at s24)
+      SsspRelaxOp<WT, true> op{a.dp, a.dist, a.mark, {}};
       expand_tasks(W, op, F, nf, a.scan, a.rowbase, a.part, (int64_t)agg.rd[3],
                    (int64_t)agg.rd[2], a.col, wgt, a.touched, &cur->out_len, gw, nw, &agg);
     }
@@ -245,17 +253,20 @@ __global__ void __launch_bounds__(256, 3) k_sssp_persistent(PSsspArgs a) {
     grid.sync();
     cta_read_ctrs(agg, cur);
     const int64_t ntouched = (int64_t)agg.rd[0];
-    sssp_split_phase(S, a.touched, ntouched, a.dist, a.mark, c.th, a.nearq[c.q ^ 1], &cur->aux0,
-                     a.far[c.f] + c.nfar, a.fkey[c.f] + c.nfar, &cur->aux1);
+    sssp_split_late_phase(S, a.touched, ntouched, a.dist, a.stamp, (int32_t)c.it, c.th,
+                          a.nearq[c.q ^ 1], &cur->aux0, a.far[c.f] + c.nfar, a.fkey[c.f] + c.nfar,
+                          &cur->aux1);
     grid.sync();
     cta_read_ctrs(agg, cur);
     const long long slots = (long long)agg.rd[2];
-    const long long bytes = 20 * nf + 8 * slots + 8 * ntouched;
+    // improved vertices, each once (the touched list holds duplicates)
+    const long long nimproved = (long long)(agg.rd[4] + agg.rd[5]);
+    const long long bytes = 20 * nf + 8 * slots + 8 * nimproved;
     if (leader && c.nrec < a.rec_cap) {
       gfx_iter_rec r{};
       r.iteration = c.it;
       r.frontier_in = nf;
-      r.frontier_out = ntouched;
+      r.frontier_out = nimproved;
       r.edges = slots;
       r.work = slots;
       r.bytes_alg = bytes;
@@ -359,13 +370,13 @@ int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t*
   // restores it for experiments.
   const bool l2p = getenv("GFX_L2_PERSIST") != nullptr;
   if (l2p) l2_window(ctx, dist32, (dist_words + g->words + 1) * sizeof(uint32_t), true);
-  // the device-resident loop wins when there are many iterations (no host
-  // round trip per iteration); with a few long ones the standalone kernels
-  // are level (measured at s24: delta 4 6.69 vs 8.65 ms, delta 32 6.96 vs
-  // 7.16, delta 64 7.27 vs 7.25, one bucket 7.24 vs 7.09).
-  // GFX_SSSP_LOOP=device|host forces one.
+  // the device-resident loop (one cooperative launch, no host round trip
+  // per iteration, duplicates deduplicated in the split) wins at every
+  // delta measured at s24: 4 / 32 / 128 / one bucket 6.04 / 6.12 / 6.36 /
+  // 6.41 ms against 8.67 / 7.17 / 7.12 / 7.10 for the host-driven kernels.
+  // GFX_SSSP_LOOP=host forces the host-driven loop.
   const char* loop_env = getenv("GFX_SSSP_LOOP");
-  const bool dev_loop = loop_env ? std::string(loop_env) == "device" : delta <= 32.0;
+  const bool dev_loop = loop_env ? std::string(loop_env) != "host" : true;
   if (dev_loop) {
     PSsspArgs a{};
     a.n = n;
@@ -379,6 +390,9 @@ int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t*
     a.nearq[0] = nearA;
     a.nearq[1] = nearB;
     a.touched = touched;
+    // duplicates allowed: up to one entry per relaxed slot of an iteration
+    GFX_TRY(scratch_t(g, "psssp_touched_dup", g->m + n + 1, &a.touched));
+    GFX_TRY(scratch_t(g, "psssp_stamp", n + 1, &a.stamp));
     a.far[0] = far;
     a.far[1] = far2;
     a.fkey[0] = fkey;

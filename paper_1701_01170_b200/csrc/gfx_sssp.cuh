@@ -77,6 +77,38 @@ static __device__ __forceinline__ void sssp_split_phase(
   pile_flush(S, near, near_len, far, far_key, far_len);
 }
 
+// the same split over a touched list WITH duplicates: the first occurrence
+// of a vertex in iteration `it` (stamp test-and-set) is split, the rest skip
+static __device__ __forceinline__ void sssp_split_late_phase(
+    PileStage& S, const int32_t* __restrict__ touched, int64_t n, const uint32_t* __restrict__ dist,
+    int32_t* __restrict__ stamp, int32_t it, double threshold, int32_t* __restrict__ near,
+    unsigned long long* __restrict__ near_len, int32_t* __restrict__ far,
+    int32_t* __restrict__ far_key, unsigned long long* __restrict__ far_len) {
+  if (threadIdx.x == 0) S.nn = S.nfar = 0;
+  __syncthreads();
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    if (i < n) {
+      const int32_t v = touched[i];
+      if (atomicExch(&stamp[v], it) != it) {
+        const int32_t key = (int32_t)dist[v];
+        if ((double)key < threshold) {
+          S.nv[atomicAdd(&S.nn, 1)] = v;
+        } else {
+          const int at = atomicAdd(&S.nfar, 1);
+          S.fv[at] = v;
+          S.fk[at] = key;
+        }
+      }
+    }
+    __syncthreads();
+    if (S.nn > kPileStage - (int)blockDim.x || S.nfar > kPileStage - (int)blockDim.x)
+      pile_flush(S, near, near_len, far, far_key, far_len);
+  }
+  pile_flush(S, near, near_len, far, far_key, far_len);
+}
+
 static __global__ void __launch_bounds__(256)
     k_sssp_split(const int32_t* __restrict__ touched, const unsigned long long* __restrict__ n_d,
                  const uint32_t* __restrict__ dist, uint32_t* __restrict__ mark, double threshold,
