@@ -50,11 +50,11 @@ struct PsRank {
   const int32_t* w;
   unsigned long long* dp;     // local: dist << 32 | global pred
   uint32_t* dist;             // local: 32-bit distance mirror (probe array)
-  uint32_t* mark;             // local: enqueued this iteration
+  int32_t* stamp;             // local: iteration that last enqueued the vertex
   unsigned long long* sent_key;  // global ids: best offer sent this run
   uint32_t* sent;             // global ids: emitted this iteration
   int32_t* nearq[2];          // local ids
-  int32_t* touched;           // local ids improved this iteration
+  int32_t* touched;           // local ids improved this iteration (with duplicates)
   int32_t* emit;              // expansion output (global ids)
   int32_t* far[2];
   int32_t* fkey[2];
@@ -143,7 +143,6 @@ struct PsRelaxOp {
   static constexpr int kMinBlocks = 3;
   unsigned long long* dp;
   uint32_t* dist;
-  uint32_t* mark;
   unsigned long long* sent_key;
   uint32_t* sent;
   int P, r, sh;
@@ -164,11 +163,12 @@ struct PsRelaxOp {
     if (nd >= cur[u]) return false;
     const unsigned long long key = (nd << 32) | (uint32_t)(s * P + r);
     if (P == 1 || owner(d) == r) {
+      // every improving relaxation is emitted; the split keeps each vertex
+      // once per iteration (no atomic round trip on the relax chain)
       const int32_t l = P == 1 ? d : local(d);
       atomicMin(&dp[l], key);
       atomicMin(&dist[l], (uint32_t)nd);
-      const uint32_t bit = 1u << (l & 31);
-      return !(atomicOr(&mark[l >> 5], bit) & bit);
+      return true;
     }
     atomicMin(&sent_key[d], key);
     const uint32_t bit = 1u << (d & 31);
@@ -210,7 +210,7 @@ __device__ __forceinline__ void ps_flush(PsStage& S, int32_t* near, unsigned lon
 // pile (stale entries dropped, everything stays far)
 __device__ __forceinline__ void ps_pile(PsStage& S, int mode, const int32_t* src,
                                         const int32_t* skey, int64_t n, const uint32_t* dist,
-                                        uint32_t* mark, double th, int32_t* near,
+                                        int32_t* stamp, int32_t it, double th, int32_t* near,
                                         unsigned long long* near_len, int32_t* far, int32_t* fkey,
                                         unsigned long long* far_len, int64_t cta, int64_t ncta) {
   if (threadIdx.x == 0) S.nn = S.nfar = 0;
@@ -221,8 +221,8 @@ __device__ __forceinline__ void ps_pile(PsStage& S, int mode, const int32_t* src
       const int32_t v = src[i];
       const int32_t key = (int32_t)dist[v];
       bool keep = true;
-      if (mode == 0) atomicAnd(&mark[v >> 5], ~(1u << (v & 31)));  // re-arm
-      else keep = key == skey[i];                                   // fresh entries only
+      if (mode == 0) keep = atomicExch(&stamp[v], it) != it;  // first occurrence this iteration
+      else keep = key == skey[i];                              // fresh far entries only
       if (keep) {
         if (mode != 2 && (double)key < th) {
           S.nv[atomicAdd(&S.nn, 1)] = v;
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(256, 3) k_pdsssp(PsArgs a) {
     R.dp[l] = ~0ull;
     R.dist[l] = 0xFFFFFFFFu;
   }
-  for (int64_t w = gtid; w <= R.wl; w += nthr) R.mark[w] = 0u;
+  for (int64_t l = gtid; l < R.nl; l += nthr) R.stamp[l] = 0;
   if (kMulti) {
     for (int64_t i = gtid; i < a.n; i += nthr) R.sent_key[i] = ~0ull;
     for (int64_t w = gtid; w < (a.n + 31) / 32 + 1; w += nthr) R.sent[w] = 0u;
@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(256, 3) k_pdsssp(PsArgs a) {
       // advance_bucket (near_far.py:63-85): threshold += delta, stale far
       // entries dropped, the rest re-split
       const double th = c.th + a.delta;
-      ps_pile(S, 1, R.far[c.f], R.fkey[c.f], c.nfar_loc, R.dist, R.mark, th, R.nearq[c.q],
+      ps_pile(S, 1, R.far[c.f], R.fkey[c.f], c.nfar_loc, R.dist, R.stamp, 0, th, R.nearq[c.q],
               &cur->out_len, R.far[c.f ^ 1], R.fkey[c.f ^ 1], &cur->aux1, rcta, nrcta);
       sync.rank();
       cta_read_ctrs(agg, cur);
@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(256, 3) k_pdsssp(PsArgs a) {
       sync.rank();
       cta_read_ctrs(agg, cur);
       {
-        PsRelaxOp op{R.dp, R.dist, R.mark, R.sent_key, R.sent, P, me, a.sh, {}};
+        PsRelaxOp op{R.dp, R.dist, R.sent_key, R.sent, P, me, a.sh, {}};
         expand_tasks(W, op, F, nf, R.scan, R.rowbase, R.part, (int64_t)agg.rd[3],
                      (int64_t)agg.rd[2], R.col, R.w, kMulti ? R.emit : R.touched, &cur->out_len,
                      gw, nw, &agg);
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(256, 3) k_pdsssp(PsArgs a) {
         // owned improved -> touched (local ids); remote -> messages to owners
         tlen = &cur->aux2;
         const int64_t nemit = (int64_t)agg.rd[0];
-        PsRelaxOp op{R.dp, R.dist, R.mark, R.sent_key, R.sent, P, me, a.sh, {}};
+        PsRelaxOp op{R.dp, R.dist, R.sent_key, R.sent, P, me, a.sh, {}};
         for (int64_t base = gw * 32; base < nemit; base += nw * 32) {
           const int64_t i = base + lane;
           const bool ok = i < nemit;
@@ -407,8 +407,7 @@ __global__ void __launch_bounds__(256, 3) k_pdsssp(PsArgs a) {
               if (nd < R.dist[l]) {
                 atomicMin(&R.dp[l], key);
                 atomicMin(&R.dist[l], nd);
-                const uint32_t bit = 1u << (l & 31);
-                em = !(atomicOr(&R.mark[l >> 5], bit) & bit);
+                em = true;  // deduplicated in the split
               }
             }
             const unsigned wm = __ballot_sync(0xffffffffu, em);
@@ -424,13 +423,15 @@ __global__ void __launch_bounds__(256, 3) k_pdsssp(PsArgs a) {
       touched_loc = (long long)agg.rd[kMulti ? 6 : 0];
       // split the improved vertices at the (global) threshold; far appends
       // go behind the rank's far pile
-      ps_pile(S, 0, R.touched, nullptr, touched_loc, R.dist, R.mark, c.th, R.nearq[c.q ^ 1],
+      ps_pile(S, 0, R.touched, nullptr, touched_loc, R.dist, R.stamp, (int32_t)c.it, c.th,
+              R.nearq[c.q ^ 1],
               &cur->aux0, R.far[c.f] + c.nfar_loc, R.fkey[c.f] + c.nfar_loc, &cur->aux1, rcta,
               nrcta);
       sync.rank();
       cta_read_ctrs(agg, cur);
       near_loc = (long long)agg.rd[4];
       far_loc = c.nfar_loc + (long long)agg.rd[5];
+      touched_loc = (long long)(agg.rd[4] + agg.rd[5]);  // improved vertices, each once
       if (threadIdx.x == 0) c.q ^= 1;
     }
     // ---- global sums (near, far, slots, touched) over the ranks
@@ -496,7 +497,7 @@ __global__ void __launch_bounds__(256, 3) k_pdsssp(PsArgs a) {
       Counters* g2 = &R.C[c.ph % 3];
       if (rcta == 0 && threadIdx.x < (int)(sizeof(Counters) / 8))
         reinterpret_cast<unsigned long long*>(&R.C[(c.ph + 1) % 3])[threadIdx.x] = 0ull;
-      ps_pile(S, 2, R.far[c.f], R.fkey[c.f], c.nfar_loc, R.dist, R.mark, c.th, nullptr,
+      ps_pile(S, 2, R.far[c.f], R.fkey[c.f], c.nfar_loc, R.dist, R.stamp, 0, c.th, nullptr,
               &g2->aux2, R.far[c.f ^ 1], R.fkey[c.f ^ 1], &g2->aux1, rcta, nrcta);
       sync.rank();
       cta_read_ctrs(agg, g2);
@@ -565,18 +566,19 @@ int ps_setup_rank(gfx_pdsssp* e, const int64_t* lrow, const int32_t* lcol, const
   R.far_cap = 2 * nl + 2;
   GFX_TRY(ps_alloc(bufs, nl + 1, &R.dp));
   GFX_TRY(ps_alloc(bufs, nl + 1, &R.dist));
-  GFX_TRY(ps_alloc(bufs, R.wl + 2, &R.mark));
+  GFX_TRY(ps_alloc(bufs, nl + 1, &R.stamp));
   if (e->P > 1) {
     GFX_TRY(ps_alloc(bufs, (size_t)e->n + 1, &R.sent_key));
     GFX_TRY(ps_alloc(bufs, (size_t)(e->n + 31) / 32 + 2, &R.sent));
-    GFX_TRY(ps_alloc(bufs, (size_t)e->n + 1, &R.emit));
+    GFX_TRY(ps_alloc(bufs, (size_t)(ml + e->n) + 1, &R.emit));  // owned duplicates + remote firsts
   }
   for (int k = 0; k < 2; ++k) {
     GFX_TRY(ps_alloc(bufs, nl + 1, &R.nearq[k]));
     GFX_TRY(ps_alloc(bufs, R.far_cap + 1, &R.far[k]));
     GFX_TRY(ps_alloc(bufs, R.far_cap + 1, &R.fkey[k]));
   }
-  GFX_TRY(ps_alloc(bufs, nl + 1, &R.touched));
+  // duplicates allowed: every owned improving relaxation and every applied offer
+  GFX_TRY(ps_alloc(bufs, (size_t)(ml + nl + e->P * e->inbox_cap) + 1, &R.touched));
   GFX_TRY(ps_alloc(bufs, nl + 2, &R.scan));
   GFX_TRY(ps_alloc(bufs, nl + 1, &R.rowbase));
   GFX_TRY(ps_alloc(bufs, part_capacity(ml, nl), &R.part));
