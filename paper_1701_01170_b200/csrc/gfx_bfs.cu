@@ -76,6 +76,43 @@ struct BfsClaimOpT {
   }
 };
 
+// Push-only BFS, large levels: a claim without the atomic round trip.  A
+// lane whose prefetched visited word shows d unclaimed sets the visited and
+// next-frontier bits with fire-and-forget REDs and writes d's depth and
+// predecessor; two lanes racing for d both write (the same depth; either
+// predecessor is a frontier vertex one level up, a valid BFS parent).  The
+// next queue is then read off the frontier bitmap, so it holds each vertex
+// once.  Nothing is emitted by the expansion itself.
+template <int B>
+struct BfsLateClaimOpT {
+  static constexpr bool kWeights = false, kSrcVal = false, kEmitEdge = false;
+  static constexpr int kBatch = B;
+  static constexpr int kMinBlocks = 3;
+  static constexpr bool kPipeline = true;
+  uint32_t* visited;
+  int32_t* labels;
+  int32_t* preds;
+  int32_t depth;
+  uint32_t wv[kBatch];
+  uint8_t* lvl8;
+  uint32_t* fbits;  // the next frontier (pre-zeroed)
+  __device__ int32_t src_value(int32_t) const { return 0; }
+  __device__ void prefetch(const int32_t* d) {
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) wv[u] = d[u] >= 0 ? visited[d[u] >> 5] : 0xffffffffu;
+  }
+  __device__ bool visit(int u, int32_t d, int32_t s, int32_t, int32_t, int64_t) {
+    const uint32_t bit = 1u << (d & 31);
+    if (wv[u] & bit) return false;
+    atomicOr(&visited[d >> 5], bit);  // result unused: a RED
+    if (lvl8) lvl8[d] = (uint8_t)depth;
+    else labels[d] = depth;
+    preds[d] = s;
+    atomicOr(&fbits[d >> 5], bit);
+    return false;
+  }
+};
+
 using BfsClaimOp = BfsClaimOpT<kVisitBatch>;
 // the single-hub level (push_tiny): fewer visits per lane in flight, more
 // lanes issuing (measured: level 1 14 -> 12 us)
@@ -857,8 +894,7 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
       // the bitmap the NEXT level writes was last read one level ago: zero it
       // in passing (no barrier -- nothing reads it during this level)
       uint32_t* fclr = a.front[(c.fsel + 2) % 3];
-      if (kDO)
-        for (int64_t i = gtid; i < a.words; i += nthr) fclr[i] = 0u;
+      for (int64_t i = gtid; i < a.words; i += nthr) fclr[i] = 0u;
     }
     // a direction-optimising run keeps the frontier as a bitmap at every
     // level: push levels also set the new frontier's bits (fbits), so a pull
@@ -919,10 +955,22 @@ __global__ void __launch_bounds__(256, 3) k_bfs_persistent(PBfsArgs a) {
           scan_tile(t, stiles, F, nf, a.row, a.scan, a.rowbase, a.part, a.status, ep, cur, ss);
         GSYNC();
         cta_read_ctrs(agg, cur);
-        expand_tasks(W, op, F, nf, a.scan, a.rowbase, a.part, (int64_t)agg.rd[3],
-                     (int64_t)agg.rd[2], a.col, nullptr, a.order + c.q_end,
-                     &cur->out_len, gw, nw);
-        for (int64_t i = gtid; i < stiles; i += nthr) a.status[i] = 0ull;
+        if constexpr (!kDO) {
+          // push-only: late claims into the next frontier bitmap, queue from it
+          uint32_t* fnb = a.front[(c.fsel + 1) % 3];
+          BfsLateClaimOpT<kVisitBatch> lop{a.visited, a.labels, a.preds, depth, {}, lab.lvl8, fnb};
+          expand_tasks(W, lop, F, nf, a.scan, a.rowbase, a.part, (int64_t)agg.rd[3],
+                       (int64_t)agg.rd[2], a.col, nullptr, a.order + c.q_end, &cur->aux1, gw,
+                       nw);
+          for (int64_t i = gtid; i < stiles; i += nthr) a.status[i] = 0ull;
+          GSYNC();
+          bitmap_to_queue(a.words, fnb, a.order + c.q_end, &cur->out_len, gw, nw);
+        } else {
+          expand_tasks(W, op, F, nf, a.scan, a.rowbase, a.part, (int64_t)agg.rd[3],
+                       (int64_t)agg.rd[2], a.col, nullptr, a.order + c.q_end,
+                       &cur->out_len, gw, nw);
+          for (int64_t i = gtid; i < stiles; i += nthr) a.status[i] = 0ull;
+        }
       }
       GSTAMP();  // push body done
       GSYNC();
