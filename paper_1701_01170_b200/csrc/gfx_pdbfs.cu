@@ -664,7 +664,7 @@ int pd_alloc_t(PdOwned& o, size_t count, T** out) {
 }
 
 // rank-local buffers + the exchange block for local rank data (row, col)
-int pd_setup_rank(gfx_pdbfs* e, int q, const int64_t* lrow, const int32_t* lcol, int64_t nl,
+int pd_setup_rank(gfx_pdbfs* e, const int64_t* lrow, const int32_t* lcol, int64_t nl,
                   int64_t ml, PdOwned& o, PdRank& R) {
   gfx_ctx* ctx = e->ctx;
   GFX_TRY(gfx_graph_create(ctx, nl, ml, lrow, lcol, nullptr, GFX_GRAPH_UNDIRECTED, &o.lg));
@@ -711,7 +711,6 @@ int pd_setup_rank(gfx_pdbfs* e, int q, const int64_t* lrow, const int32_t* lcol,
   GFX_TRY(pd_alloc_t(o, kPdMaxRanks, &R.flags));
   GFX_CK(cudaMemsetAsync(R.flags, 0, kPdMaxRanks * 4, ctx->stream));
   GFX_CK(cudaMemsetAsync(R.ctab, 0, 2 * kPdMaxRanks * 4 * 8, ctx->stream));
-  (void)q;
   return GFX_OK;
 }
 
@@ -794,6 +793,9 @@ int gfx_pdbfs_create_virtual(gfx_ctx* ctx, int64_t n, int64_t m, int P,
   GFX_REQUIRE(ctx && lrow && lcol && n_local && m_local && out, "gfx_pdbfs_create_virtual: null argument");
   GFX_REQUIRE(P >= 1 && P <= kPdMaxRanks, "P=%d out of range 1..%d", P, kPdMaxRanks);
   GFX_REQUIRE(n > 0 && n < (int64_t)INT32_MAX, "n=%lld out of range", (long long)n);
+  for (int q = 0; q < P; ++q)
+    GFX_REQUIRE(n_local[q] == (n > q ? (n - q + P - 1) / P : 0),
+                "n_local[%d] does not match the partition", q);
   GFX_CK(cudaSetDevice(ctx->device));
   auto* e = new gfx_pdbfs();
   e->ctx = ctx;
@@ -807,8 +809,7 @@ int gfx_pdbfs_create_virtual(gfx_ctx* ctx, int64_t n, int64_t m, int P,
   e->own.resize(P);
   e->rk.resize(P);
   for (int q = 0; q < P; ++q) {
-    GFX_REQUIRE(n_local[q] == (n > q ? (n - q + P - 1) / P : 0), "n_local[%d] does not match the partition", q);
-    const int st = pd_setup_rank(e, q, lrow[q], lcol[q], n_local[q], m_local[q], e->own[q], e->rk[q]);
+    const int st = pd_setup_rank(e, lrow[q], lcol[q], n_local[q], m_local[q], e->own[q], e->rk[q]);
     if (st != GFX_OK) {
       gfx_pdbfs_destroy(e);
       return st;
@@ -854,7 +855,7 @@ int gfx_pdbfs_create_rank(gfx_ctx* ctx, int64_t n, int64_t m, int P, int r, cons
   e->inbox_cap = nmax + 1;
   e->own.resize(1);
   e->rk.assign(P, PdRank{});
-  int st = pd_setup_rank(e, r, lrow, lcol, n_local, m_local, e->own[0], e->rk[r]);
+  int st = pd_setup_rank(e, lrow, lcol, n_local, m_local, e->own[0], e->rk[r]);
   if (st == GFX_OK) {
     e->nnz = e->rk[r].nnz;  // the global count arrives with gfx_pdbfs_import
     st = pd_finish_create(e);

@@ -673,6 +673,8 @@ int gfx_pdsssp_create_virtual(gfx_ctx* ctx, int64_t n, int P, const int64_t* con
               "gfx_pdsssp_create_virtual: null argument");
   GFX_REQUIRE(P >= 1 && P <= kPsMaxRanks, "P=%d out of range 1..%d", P, kPsMaxRanks);
   GFX_REQUIRE(n > 0 && n < (int64_t)INT32_MAX, "n=%lld out of range", (long long)n);
+  for (int q = 0; q < P; ++q)
+    GFX_REQUIRE(n_local[q] == (n > q ? (n - q + P - 1) / P : 0), "n_local[%d] does not match", q);
   GFX_CK(cudaSetDevice(ctx->device));
   auto* e = new gfx_pdsssp();
   e->ctx = ctx;
@@ -683,7 +685,6 @@ int gfx_pdsssp_create_virtual(gfx_ctx* ctx, int64_t n, int P, const int64_t* con
   e->bufs.resize(P);
   e->rk.resize(P);
   for (int q = 0; q < P; ++q) {
-    GFX_REQUIRE(n_local[q] == (n > q ? (n - q + P - 1) / P : 0), "n_local[%d] does not match", q);
     const int st = ps_setup_rank(e, lrow[q], lcol[q], lw[q], n_local[q], m_local[q], e->bufs[q],
                                  e->rk[q]);
     if (st != GFX_OK) {
