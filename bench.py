@@ -571,7 +571,24 @@ def _partitioned_run_device(args, dist, scale: int, steps: int, warmup: int,
     one_gpu, ref_labels = None, None
     if with_1gpu and r == 0:
         one_gpu, ref_labels = _one_gpu_reference(args, dg)
-    eng = DeviceResidentRank(dg, P, r, group=None)
+    eng, err = None, None
+    try:
+        eng = DeviceResidentRank(dg, P, r, group=None)
+    except Exception as exc:  # noqa: BLE001 -- e.g. no CUDA IPC between these GPUs
+        err = repr(exc)
+    if dist.sum(0.0 if err is None else 1.0) > 0:
+        # every rank falls back together to the host-driven NCCL loop
+        if eng is not None:
+            eng.close()
+        del dg, ref_labels
+        torch.cuda.empty_cache()
+        import copy
+
+        args2 = copy.copy(args)
+        args2.host_loop = True
+        out = _partitioned_run(args2, dist, scale, steps, warmup, with_1gpu)
+        out["loop"] = f"{out['loop']} (device-resident engine unavailable: {err})"
+        return out
     del dg
     torch.cuda.empty_cache()
     torch.cuda.synchronize()
