@@ -693,12 +693,20 @@ def _partitioned_sssp(args, dist, delta: int = 32, steps: int = 3):
     else:
         e_r = 0
     e_r = int(dist.sum(float(e_r)))
+    eng, err = None, None
     if not (args.host_loop or args.python_loop):
-        # the device-resident engine (csrc/gfx_pdsssp.cu): one cooperative
-        # launch per rank and run, offers / counters through peer memory
         from paper_1701_01170_b200.dist import DeviceResidentSsspRank
 
-        eng = DeviceResidentSsspRank(dgw, P, r)
+        try:
+            eng = DeviceResidentSsspRank(dgw, P, r)
+        except Exception as exc:  # noqa: BLE001 -- e.g. no CUDA IPC between these GPUs
+            err = repr(exc)
+        if dist.sum(0.0 if err is None else 1.0) > 0 and eng is not None:
+            eng.close()
+            eng = None
+    if eng is not None:
+        # the device-resident engine (csrc/gfx_pdsssp.cu): one cooperative
+        # launch per rank and run, offers / counters through peer memory
         del dgw
         dl, _, st = eng.run(args.source, delta)  # warm-up
         dist.barrier()
@@ -762,7 +770,8 @@ def _partitioned_sssp(args, dist, delta: int = 32, steps: int = 3):
             "n_gpus": P, "iterations": st.iterations, "bucket_advances": st.bucket_advances,
             "relaxed_slots": st.relaxed_slots, "messages": st.messages,
             "dist_equal_single_gpu": ok,
-            "what": "host-driven level loop over torch.distributed (NCCL) collectives"}
+            "what": "host-driven level loop over torch.distributed (NCCL) collectives"
+                    + (f" (device-resident engine unavailable: {err})" if err else "")}
 
 
 def _labels_match(eng, ref_labels, P: int, r: int, n: int):
