@@ -35,6 +35,10 @@ def main():
         from paper_1701_01170_b200.primitives.sssp import sssp_device
 
         fn = lambda: sssp_device(dg, 0, delta=a.delta)
+    elif a.prim == "pagerank":
+        from paper_1701_01170_b200.primitives.pagerank import pagerank_device
+
+        fn = lambda: (None, None, pagerank_device(dg, 0.85, 0.0, 20)[1])
     else:
         raise SystemExit(f"unknown primitive {a.prim}")
     if a.timing:
@@ -47,7 +51,7 @@ def main():
         st = fn()[2]
     torch.cuda.synchronize()
     torch.cuda.cudart().cudaProfilerStop()
-    print("device_ms", st.device_ms, "E_r", st.edges_reached, "init_ms",
+    print("device_ms", st.device_ms, "E_r", getattr(st, "edges_reached", None), "init_ms",
           getattr(st, "init_ms", None), "loop_ms", getattr(st, "loop_ms", None))
     for lv in getattr(st, "device_levels", []):
         print("  ", lv)
