@@ -348,6 +348,15 @@ GFX_API int gfx_csr_pack(gfx_ctx* ctx, const void* vals_d, int elem_bytes, int64
 GFX_API int gfx_csr_unpack(gfx_ctx* ctx, const uint8_t* ctrl_d, const uint8_t* data_d,
                            const int64_t* boff_d, int64_t m, void* vals_d, int elem_bytes,
                            int sync);
+/* Rebuild an undirected graph's columns from its upper triangle (each
+ * edge once, as the reference's COO input holds it before coo_to_csr
+ * symmetrises it, graph.py:158-203): g->row must already hold the full row
+ * offsets; urow_d int64[n+1] / ucol_d int32[mu] are the upper triangle's CSR
+ * (entries > the row id), mu = m/2.  Writes the full sorted g->col (lower
+ * parts by a stable radix-sort transpose); enqueued on the ctx stream, call
+ * gfx_graph_refresh after it. */
+GFX_API int gfx_graph_rebuild_upper(gfx_graph* g, const int64_t* urow_d, const int32_t* ucol_d,
+                                    int64_t mu);
 
 /* ---- bit-exact R-MAT + canonical CSR builder ----------------------------
  * (reference generators.py:22-52, graph.py:158-203, graph.py:227-246)

@@ -135,6 +135,7 @@ _SIGS = {
     "gfx_csr_pack": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_void_p, c_void_p, c_void_p]),
     "gfx_csr_unpack": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int,
                                c_int]),
+    "gfx_graph_rebuild_upper": (c_int, [c_void_p, c_void_p, c_void_p, c_int64]),
     "gfx_rmat_keys": (c_int, [c_void_p, c_int, c_int, POINTER(c_double), c_uint64, c_uint64,
                               c_uint64, c_uint64, c_int, c_void_p, POINTER(c_int64)]),
     "gfx_keys_to_csr": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_void_p]),

@@ -10,6 +10,9 @@
 // bytes per slot instead of 4 (int32) or 8 (the reference's int64), so the
 // host->device copy of a graph -- the end-to-end bound -- moves about half
 // the bytes.  Decoding is two HBM-bandwidth passes on the device.
+#include <algorithm>
+
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
@@ -111,6 +114,54 @@ __global__ void k_unpack_deltas(const uint8_t* __restrict__ ctrl, const uint8_t*
   }
 }
 
+// ---- symmetric CSR from its upper triangle --------------------------------
+// An undirected CSR (reference coo_to_csr with make_undirected: no self
+// loops, no duplicates, rows sorted) is determined by its upper triangle U
+// (each row's entries > the row id, i.e. every edge once).  Row u of the full
+// CSR is [lower part: w < u with u in U(w), ascending] ++ [U(u)], so with the
+// full row offsets `row` and U's own offsets `urow`:
+//   upper slot j of row u  -> col[j + row[u+1] - urow[u+1]]
+//   lower entries          = U transposed: the pairs (v = U[j], u) sorted by
+//                            v, stable (u ascending within v) -> sorted index
+//                            i of a pair with key v goes to col[i + urow[v]]
+//                            (row[v] = lower entries before v + urow[v]).
+// The transpose is one stable radix sort of (v, u) pairs over log2(n) bits.
+
+// rowid[urow[u]] = u for every non-empty upper row (then a max-scan fills the rest)
+__global__ void k_upper_row_starts(const int64_t* __restrict__ urow, int64_t n,
+                                   int32_t* __restrict__ rowid) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = urow[u];
+    if (urow[u + 1] > b) rowid[b] = (int32_t)u;
+  }
+}
+
+__global__ void k_place_upper(const int64_t* __restrict__ row, const int64_t* __restrict__ urow,
+                              const int32_t* __restrict__ ucol, const int32_t* __restrict__ rowid,
+                              int64_t mu, int64_t m, int32_t* __restrict__ col) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < mu;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = rowid[j];
+    const int64_t dst = j + row[u + 1] - urow[u + 1];
+    if (dst >= 0 && dst < m) col[dst] = ucol[j];
+  }
+}
+
+__global__ void k_place_lower(const int64_t* __restrict__ urow, const uint32_t* __restrict__ key,
+                              const int32_t* __restrict__ val, int64_t mu, int64_t m,
+                              int32_t* __restrict__ col) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < mu;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t dst = i + urow[key[i]];
+    if (dst >= 0 && dst < m) col[dst] = val[i];
+  }
+}
+
+struct MaxI32 {
+  __device__ __forceinline__ int32_t operator()(int32_t a, int32_t b) const { return a > b ? a : b; }
+};
+
 }  // namespace gfx
 
 using namespace gfx;
@@ -204,6 +255,48 @@ int gfx_csr_unpack(gfx_ctx* ctx, const uint8_t* ctrl_d, const uint8_t* data_d,
   else GFX_TRY(unpack_t(ctx, ctrl_d, data_d, boff_d, m, static_cast<int64_t*>(vals_d)));
   GFX_CK(cudaGetLastError());
   if (sync) GFX_CK(cudaStreamSynchronize(ctx->stream));
+  return GFX_OK;
+}
+
+int gfx_graph_rebuild_upper(gfx_graph* g, const int64_t* urow_d, const int32_t* ucol_d,
+                            int64_t mu) {
+  GFX_NVTX("gfx_graph_rebuild_upper");
+  GFX_REQUIRE(g && (mu == 0 || (urow_d && ucol_d)), "gfx_graph_rebuild_upper: null argument");
+  GFX_REQUIRE(g->flags & GFX_GRAPH_UNDIRECTED, "gfx_graph_rebuild_upper: undirected graphs only");
+  GFX_REQUIRE(2 * mu == g->m, "gfx_graph_rebuild_upper: the upper triangle must hold m/2 slots");
+  gfx_ctx* ctx = g->ctx;
+  GFX_CK(cudaSetDevice(ctx->device));
+  if (mu == 0) return GFX_OK;
+  const int64_t n = g->n;
+  int32_t *rowid, *val_out;
+  uint32_t* key_out;
+  GFX_TRY(scratch_t(g, "up_rowid", mu, &rowid));
+  GFX_TRY(scratch_t(g, "up_key", mu, &key_out));
+  GFX_TRY(scratch_t(g, "up_val", mu, &val_out));
+  // row ids of the upper slots: row starts, then an inclusive max-scan
+  GFX_CK(cudaMemsetAsync(rowid, 0, mu * 4, ctx->stream));
+  GFX_LAUNCH(k_upper_row_starts, grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream, urow_d,
+             n, rowid);
+  size_t tb_scan = 0, tb_sort = 0;
+  GFX_CK(cub::DeviceScan::InclusiveScan(nullptr, tb_scan, rowid, rowid, MaxI32(), mu, ctx->stream));
+  int bits = 1;
+  while (bits < 31 && (int64_t(1) << bits) < n) ++bits;
+  const uint32_t* key_in = reinterpret_cast<const uint32_t*>(ucol_d);
+  GFX_CK(cub::DeviceRadixSort::SortPairs(nullptr, tb_sort, key_in, key_out, rowid, val_out, mu, 0,
+                                         bits, ctx->stream));
+  void* tmp;
+  GFX_TRY(scratch(g, "up_cub", std::max(tb_scan, tb_sort) + 16, &tmp));
+  GFX_CK(cub::DeviceScan::InclusiveScan(tmp, tb_scan, rowid, rowid, MaxI32(), mu, ctx->stream));
+  count_launch();
+  GFX_LAUNCH(k_place_upper, grid_for(mu, 256, ctx->sm_count * 16), 256, 0, ctx->stream, g->row,
+             urow_d, ucol_d, rowid, mu, g->m, const_cast<int32_t*>(g->col));
+  // the transpose: (v, u) pairs stably sorted by v
+  GFX_CK(cub::DeviceRadixSort::SortPairs(tmp, tb_sort, key_in, key_out, rowid, val_out, mu, 0, bits,
+                                         ctx->stream));
+  count_launch();
+  GFX_LAUNCH(k_place_lower, grid_for(mu, 256, ctx->sm_count * 16), 256, 0, ctx->stream, urow_d,
+             key_out, val_out, mu, g->m, const_cast<int32_t*>(g->col));
+  GFX_CK(cudaGetLastError());
   return GFX_OK;
 }
 

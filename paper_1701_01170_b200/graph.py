@@ -318,8 +318,9 @@ class DeviceGraph:
         if stages is None:
             stages = self._pack_stage = [None, None]
         st = stages[slot]
-        parts = packed.row + packed.col
-        if st is None or any(d.numel() < h.numel() for d, h in zip(st, parts)):
+        parts = packed.parts
+        self._pack_upper = packed.upper
+        if st is None or len(st) != len(parts) or any(d.numel() < h.numel() for d, h in zip(st, parts)):
             dev = self.row.device
             st = tuple(torch.empty(h.numel(), dtype=h.dtype, device=dev) for h in parts)
             stages[slot] = st
@@ -328,11 +329,32 @@ class DeviceGraph:
 
     def decode_packed_(self, slot: int = 0) -> None:
         """Decode the staged streams ``slot`` into row / col and refresh the graph."""
-        rc, rd, rb, cc, cd, cb = self._pack_stage[slot]
+        st = self._pack_stage[slot]
+        rc, rd, rb = st[:3]
+        cc, cd, cb = st[-3:]
         _native.call("gfx_csr_unpack", self.ctx.handle, _native.ptr(rc), _native.ptr(rd),
                      _native.ptr(rb), self.num_vertices + 1, _native.ptr(self.row), 8, 0)
-        _native.call("gfx_csr_unpack", self.ctx.handle, _native.ptr(cc), _native.ptr(cd),
-                     _native.ptr(cb), self.num_edges, _native.ptr(self.col), 4, 0)
+        if len(st) == 9:  # upper triangle: decode it, then rebuild the full columns
+            import torch
+
+            mu = self.num_edges // 2
+            tmp = getattr(self, "_upper_tmp", None)
+            if tmp is None:
+                dev = self.row.device
+                tmp = self._upper_tmp = (
+                    torch.empty(self.num_vertices + 1, dtype=torch.int64, device=dev),
+                    torch.empty(max(mu, 1), dtype=torch.int32, device=dev))
+            urow, ucol = tmp
+            uc, ud, ub = st[3:6]
+            _native.call("gfx_csr_unpack", self.ctx.handle, _native.ptr(uc), _native.ptr(ud),
+                         _native.ptr(ub), self.num_vertices + 1, _native.ptr(urow), 8, 0)
+            _native.call("gfx_csr_unpack", self.ctx.handle, _native.ptr(cc), _native.ptr(cd),
+                         _native.ptr(cb), mu, _native.ptr(ucol), 4, 0)
+            _native.call("gfx_graph_rebuild_upper", self.handle, _native.ptr(urow),
+                         _native.ptr(ucol), mu)
+        else:
+            _native.call("gfx_csr_unpack", self.ctx.handle, _native.ptr(cc), _native.ptr(cd),
+                         _native.ptr(cb), self.num_edges, _native.ptr(self.col), 4, 0)
         self._csc_dev = None
         _native.call("gfx_graph_refresh", self.handle)
 

@@ -243,15 +243,30 @@ class PackedCsr:
     int32 column ids (~1.9 bytes per slot on R-MAT ef16 instead of 4).  Each
     packed array is (ctrl, data, boff) uint8 / uint8 / int64 pinned tensors.
     ``DeviceGraph.reload_packed_`` uploads it into a resident graph and
-    decodes it on the device."""
+    decodes it on the device.
 
-    def __init__(self, n, m, row, col):
+    With ``urow`` set (``pack_csr_device(dg, upper=True)``) the image holds
+    only the upper triangle's columns (each undirected edge once, m/2 slots)
+    plus its row offsets; the device rebuilds the full sorted CSR
+    (gfx_graph_rebuild_upper: a stable radix-sort transpose), so about half
+    the bytes cross PCIe."""
+
+    def __init__(self, n, m, row, col, urow=None):
         self.num_vertices, self.num_edges = int(n), int(m)
         self.row, self.col = row, col  # (ctrl, data, boff) each
+        self.urow = urow  # upper-triangle row offsets (ctrl, data, boff), or None
+
+    @property
+    def upper(self) -> bool:
+        return self.urow is not None
+
+    @property
+    def parts(self):
+        return self.row + (self.urow or ()) + self.col
 
     @property
     def nbytes(self) -> int:
-        return sum(t.numel() * t.element_size() for part in (self.row, self.col) for t in part)
+        return sum(t.numel() * t.element_size() for t in self.parts)
 
 
 def _pack_device(ctx, vals, elem_bytes: int):
@@ -278,8 +293,26 @@ def _pack_device(ctx, vals, elem_bytes: int):
     return tuple(pinned(t) for t in (ctrl, data, boff))
 
 
-def pack_csr_device(dg: DeviceGraph) -> PackedCsr:
+def pack_csr_device(dg: DeviceGraph, upper: bool = False) -> PackedCsr:
     """Pack a device graph's row offsets and columns on the device and
-    download the packed streams into pinned host memory."""
-    return PackedCsr(dg.num_vertices, dg.num_edges, _pack_device(dg.ctx, dg.row, 8),
-                     _pack_device(dg.ctx, dg.col[: dg.num_edges], 4))
+    download the packed streams into pinned host memory.  ``upper``: pack
+    only the upper triangle of an undirected graph (see PackedCsr)."""
+    if not upper:
+        return PackedCsr(dg.num_vertices, dg.num_edges, _pack_device(dg.ctx, dg.row, 8),
+                         _pack_device(dg.ctx, dg.col[: dg.num_edges], 4))
+    import torch
+
+    if not dg.undirected:
+        raise ValueError("pack_csr_device(upper=True): undirected graphs only")
+    n, m = dg.num_vertices, dg.num_edges
+    deg = dg.row[1:] - dg.row[:-1]
+    rowid = torch.repeat_interleave(torch.arange(n, device=dg.row.device), deg)
+    keep = dg.col[:m].to(torch.int64) > rowid
+    ucol = dg.col[:m][keep].contiguous()
+    if 2 * ucol.numel() != m:
+        raise ValueError("pack_csr_device(upper=True): the CSR is not symmetric without self loops")
+    urow = torch.zeros(n + 1, dtype=torch.int64, device=dg.row.device)
+    urow[1:] = torch.cumsum(torch.bincount(rowid[keep], minlength=n), 0)
+    del rowid, keep
+    return PackedCsr(n, m, _pack_device(dg.ctx, dg.row, 8), _pack_device(dg.ctx, ucol, 4),
+                     urow=_pack_device(dg.ctx, urow, 8))

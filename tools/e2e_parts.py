@@ -34,7 +34,7 @@ def timed(name, fn, reps=3):
 
 
 timed("upload", lambda: dg.upload_packed_(packed))
-rc, rd, rb, cc, cd, cb = dg._pack_stage
+rc, rd, rb, cc, cd, cb = dg._pack_stage[0]
 timed("dec_rows", lambda: _native.call("gfx_csr_unpack", dg.ctx.handle, _native.ptr(rc),
                                        _native.ptr(rd), _native.ptr(rb), dg.num_vertices + 1,
                                        _native.ptr(dg.row), 8, 0))
@@ -45,3 +45,11 @@ timed("refresh", lambda: _native.call("gfx_graph_refresh", dg.handle))
 timed("bfs", lambda: bfs_device(dg, 0, direction="auto"))
 h = [t.numel() for t in packed.row + packed.col]
 print("stream sizes", h, [t.is_pinned() for t in packed.row + packed.col])
+
+up = pack_csr_device(dg, upper=True)
+print("upper packed bytes", up.nbytes)
+timed("upload_up", lambda: dg.upload_packed_(up))
+timed("decode_up", lambda: dg.decode_packed_())
+timed("rebuild", lambda: _native.call("gfx_graph_rebuild_upper", dg.handle,
+                                      _native.ptr(dg._upper_tmp[0]), _native.ptr(dg._upper_tmp[1]),
+                                      dg.num_edges // 2))
