@@ -268,26 +268,30 @@ int gfx_graph_rebuild_upper(gfx_graph* g, const int64_t* urow_d, const int32_t* 
   GFX_CK(cudaSetDevice(ctx->device));
   if (mu == 0) return GFX_OK;
   const int64_t n = g->n;
-  int32_t *rowid, *val_out;
-  uint32_t* key_out;
+  int32_t* rowid;
   GFX_TRY(scratch_t(g, "up_rowid", mu, &rowid));
-  GFX_TRY(scratch_t(g, "up_key", mu, &key_out));
-  GFX_TRY(scratch_t(g, "up_val", mu, &val_out));
   // row ids of the upper slots: row starts, then an inclusive max-scan
   GFX_CK(cudaMemsetAsync(rowid, 0, mu * 4, ctx->stream));
   GFX_LAUNCH(k_upper_row_starts, grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream, urow_d,
              n, rowid);
-  size_t tb_scan = 0, tb_sort = 0;
+  size_t tb_scan = 0;
   GFX_CK(cub::DeviceScan::InclusiveScan(nullptr, tb_scan, rowid, rowid, MaxI32(), mu, ctx->stream));
+  void* tmp;
+  GFX_TRY(scratch(g, "up_cub", tb_scan + 16, &tmp));
+  GFX_CK(cub::DeviceScan::InclusiveScan(tmp, tb_scan, rowid, rowid, MaxI32(), mu, ctx->stream));
+  count_launch();
+  // upper slots straight to their place; the lower parts by the transpose
+  int32_t* val_out;
+  uint32_t* key_out;
+  GFX_TRY(scratch_t(g, "up_key", mu, &key_out));
+  GFX_TRY(scratch_t(g, "up_val", mu, &val_out));
   int bits = 1;
   while (bits < 31 && (int64_t(1) << bits) < n) ++bits;
   const uint32_t* key_in = reinterpret_cast<const uint32_t*>(ucol_d);
+  size_t tb_sort = 0;
   GFX_CK(cub::DeviceRadixSort::SortPairs(nullptr, tb_sort, key_in, key_out, rowid, val_out, mu, 0,
                                          bits, ctx->stream));
-  void* tmp;
-  GFX_TRY(scratch(g, "up_cub", std::max(tb_scan, tb_sort) + 16, &tmp));
-  GFX_CK(cub::DeviceScan::InclusiveScan(tmp, tb_scan, rowid, rowid, MaxI32(), mu, ctx->stream));
-  count_launch();
+  GFX_TRY(scratch(g, "up_sorttmp", tb_sort + 16, &tmp));
   GFX_LAUNCH(k_place_upper, grid_for(mu, 256, ctx->sm_count * 16), 256, 0, ctx->stream, g->row,
              urow_d, ucol_d, rowid, mu, g->m, const_cast<int32_t*>(g->col));
   // the transpose: (v, u) pairs stably sorted by v

@@ -13,7 +13,7 @@ from paper_1701_01170_b200.io import pack_csr_device  # noqa: E402
 from paper_1701_01170_b200.primitives.bfs import bfs_device  # noqa: E402
 
 dg = rmat_device_graph(24, 16, 0)
-packed = pack_csr_device(dg)
+packed = pack_csr_device(dg, upper=len(sys.argv) > 1 and sys.argv[1] == "upper")
 n = dg.num_vertices
 comp = torch.cuda.current_stream()
 up, dn = torch.cuda.Stream(), torch.cuda.Stream()
