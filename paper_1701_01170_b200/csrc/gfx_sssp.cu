@@ -22,6 +22,8 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <limits>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -138,8 +140,11 @@ struct PSsspArgs {
   int32_t* nearq[2];
   int32_t* touched;
   int32_t* stamp;  // iteration that last enqueued each vertex (split dedupe)
-  int32_t* far[2];
+  int32_t* far[2];  // the soon pile (keys below the window bound)
   int32_t* fkey[2];
+  int32_t* later[2];  // the later pile (keys at or above it)
+  int32_t* lkey[2];
+  double win;         // window width (a multiple of delta)
   int64_t* scan;
   int64_t* rowbase;
   int32_t* part;
@@ -155,10 +160,12 @@ struct PSsspArgs {
   long long* summary;
 };
 
+constexpr double kSsspWindow = 2.0;  // the soon pile's window, in deltas (s24 sweep: 1-4 -> 2)
+
 struct PSCtl {
-  long long nnear, nfar, it, ph, slots, bytes, nrec, nadv;
-  int q, f;
-  double th;
+  long long nnear, nfar, nlater, it, ph, slots, bytes, nrec, nadv;
+  int q, f, l;
+  double th, fw;
   unsigned long long t0;
 };
 
@@ -177,7 +184,9 @@ __global__ void __launch_bounds__(256, 3) k_sssp_persistent(PSsspArgs a) {
   // slices (the phases are separated by grid barriers): 24 KB less shared
   // memory per CTA, i.e. that much more L1 for the distance probes
   static_assert(sizeof(PileStage) <= sizeof(WarpSmem) * kWarpsPerBlock, "pile stage must fit");
+  static_assert(sizeof(PileStage3) <= sizeof(WarpSmem) * kWarpsPerBlock, "pile stage must fit");
   PileStage& S = *reinterpret_cast<PileStage*>(smem_raw);
+  PileStage3& S3 = *reinterpret_cast<PileStage3*>(smem_raw);
   __shared__ ScanSmem ss;
   __shared__ PSCtl c;
   __shared__ CtaAgg agg;  // counters read back once per CTA (gfx_expand.cuh)
@@ -200,9 +209,10 @@ __global__ void __launch_bounds__(256, 3) k_sssp_persistent(PSsspArgs a) {
   if (leader) a.nearq[0][0] = a.source;
   if (threadIdx.x == 0) {
     c.nnear = 1;
-    c.nfar = c.it = c.ph = c.slots = c.bytes = c.nrec = c.nadv = 0;
-    c.q = c.f = 0;
+    c.nfar = c.nlater = c.it = c.ph = c.slots = c.bytes = c.nrec = c.nadv = 0;
+    c.q = c.f = c.l = 0;
     c.th = a.delta;
+    c.fw = a.delta + a.win;
   }
   grid.sync();
   for (;;) {
@@ -210,18 +220,47 @@ __global__ void __launch_bounds__(256, 3) k_sssp_persistent(PSsspArgs a) {
     if (blockIdx.x == 0 && threadIdx.x < (int)(sizeof(Counters) / 8))
       reinterpret_cast<unsigned long long*>(&a.C[(c.ph + 1) % 3])[threadIdx.x] = 0ull;
     if (c.nnear == 0) {
-      if (c.nfar == 0) break;
+      if (c.nfar == 0 && c.nlater == 0) break;
+      if (c.nlater + c.nfar > 3 * a.n) {
+        // later-pile capacity guard: drop its stale entries (then <= n remain)
+        sssp_refar_phase(S, a.later[c.l], a.lkey[c.l], c.nlater, a.dist, c.th, 0, a.nearq[c.q],
+                         &cur->aux2, a.later[c.l ^ 1], a.lkey[c.l ^ 1], &cur->aux3);
+        grid.sync();
+        if (threadIdx.x == 0) {
+          c.nlater = (long long)ld_volatile_u64(&cur->aux3);
+          c.l ^= 1;
+          c.ph += 1;
+        }
+        __syncthreads();
+        continue;
+      }
       // advance_bucket (near_far.py:63-85): threshold += delta, drop stale
-      // far entries, re-split the rest
+      // far entries, re-split the rest -- the soon pile while it lasts, then
+      // the later pile under the next window
       const double th = c.th + a.delta;
-      sssp_refar_phase(S, a.far[c.f], a.fkey[c.f], c.nfar, a.dist, th, 1, a.nearq[c.q],
-                       &cur->out_len, a.far[c.f ^ 1], a.fkey[c.f ^ 1], &cur->aux1);
+      const bool from_soon = c.nfar > 0;
+      const double fw = from_soon ? c.fw : th + a.win;
+      if (from_soon)
+        sssp_refar2_phase(S3, a.far[c.f], a.fkey[c.f], c.nfar, a.dist, th, fw, a.nearq[c.q],
+                          &cur->out_len, a.far[c.f ^ 1], a.fkey[c.f ^ 1], &cur->aux1,
+                          a.later[c.l] + c.nlater, a.lkey[c.l] + c.nlater, &cur->aux3);
+      else
+        sssp_refar2_phase(S3, a.later[c.l], a.lkey[c.l], c.nlater, a.dist, th, fw, a.nearq[c.q],
+                          &cur->out_len, a.far[c.f ^ 1], a.fkey[c.f ^ 1], &cur->aux1,
+                          a.later[c.l ^ 1], a.lkey[c.l ^ 1], &cur->aux3);
       grid.sync();
       if (threadIdx.x == 0) {
-        c.bytes += 8 * c.nfar;
+        c.bytes += 8 * (from_soon ? c.nfar : c.nlater);
         c.th = th;
+        c.fw = fw;
         c.nnear = (long long)ld_volatile_u64(&cur->out_len);
         c.nfar = (long long)ld_volatile_u64(&cur->aux1);
+        if (from_soon) {
+          c.nlater += (long long)ld_volatile_u64(&cur->aux3);
+        } else {
+          c.nlater = (long long)ld_volatile_u64(&cur->aux3);
+          c.l ^= 1;
+        }
         c.f ^= 1;
         c.ph += 1;
         c.nadv += 1;
@@ -397,6 +436,15 @@ int sssp_run(gfx_graph* g, int64_t source, double delta, int32_t* dist, int32_t*
     a.far[1] = far2;
     a.fkey[0] = fkey;
     a.fkey[1] = fkey2;
+    // the later pile: appended by soon-pile advances, compacted above 3n
+    GFX_TRY(scratch_t(g, "psssp_later0", 4 * n + 64, &a.later[0]));
+    GFX_TRY(scratch_t(g, "psssp_later1", 4 * n + 64, &a.later[1]));
+    GFX_TRY(scratch_t(g, "psssp_lkey0", 4 * n + 64, &a.lkey[0]));
+    GFX_TRY(scratch_t(g, "psssp_lkey1", 4 * n + 64, &a.lkey[1]));
+    // window = kSsspWindow deltas (GFX_SSSP_WIN=<k> for sweeps; 0 = one far pile)
+    double kwin = kSsspWindow;
+    if (const char* e = getenv("GFX_SSSP_WIN")) kwin = atof(e);
+    a.win = kwin > 0 ? kwin * delta : std::numeric_limits<double>::infinity();
     a.scan = scan;
     a.rowbase = rowbase;
     a.part = part;

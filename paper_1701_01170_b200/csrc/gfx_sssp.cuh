@@ -153,6 +153,89 @@ static __device__ __forceinline__ void sssp_refar_phase(
   pile_flush(S, near, near_len, far2, far2_key, far2_len);
 }
 
+// Two-level far pile (device-resident loop): `soon` holds far entries below
+// the window bound fw, `later` the rest.  An advance re-splits only the soon
+// pile; the later pile is re-split when the soon pile has run dry (with a new
+// window), so a far entry is scanned about window/delta times at most instead
+// of once per advance.  Same stale rule as near_far.py:68-85; every entry's
+// route depends only on (dist, key, threshold, fw), so distances are those of
+// the one-pile loop.
+constexpr int kPileStage3 = 1024;
+struct PileStage3 {
+  int32_t nv[kPileStage3];
+  int32_t fv[kPileStage3], fk[kPileStage3];
+  int32_t lv[kPileStage3], lk[kPileStage3];
+  int nn, nfar, nl;
+  unsigned long long base;
+};
+
+static __device__ __forceinline__ void pile_append(int32_t* __restrict__ sv,
+                                                   const int32_t* __restrict__ sk, int cnt,
+                                                   unsigned long long& base,
+                                                   int32_t* __restrict__ v,
+                                                   int32_t* __restrict__ k,
+                                                   unsigned long long* __restrict__ len) {
+  __syncthreads();
+  if (threadIdx.x == 0) base = cnt ? atomicAdd(len, (unsigned long long)cnt) : 0ull;
+  __syncthreads();
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    v[base + i] = sv[i];
+    if (k) k[base + i] = sk[i];
+  }
+}
+
+static __device__ __forceinline__ void pile_flush3(
+    PileStage3& S, int32_t* __restrict__ near, unsigned long long* __restrict__ near_len,
+    int32_t* __restrict__ soon, int32_t* __restrict__ soon_key,
+    unsigned long long* __restrict__ soon_len, int32_t* __restrict__ later,
+    int32_t* __restrict__ later_key, unsigned long long* __restrict__ later_len) {
+  pile_append(S.nv, nullptr, S.nn, S.base, near, nullptr, near_len);
+  pile_append(S.fv, S.fk, S.nfar, S.base, soon, soon_key, soon_len);
+  pile_append(S.lv, S.lk, S.nl, S.base, later, later_key, later_len);
+  __syncthreads();
+  if (threadIdx.x == 0) S.nn = S.nfar = S.nl = 0;
+  __syncthreads();
+}
+
+// fresh entries of in[0..n): key < threshold -> near, key < fw -> soon,
+// else -> later (stale ones dropped)
+static __device__ __forceinline__ void sssp_refar2_phase(
+    PileStage3& S, const int32_t* __restrict__ in, const int32_t* __restrict__ in_key, int64_t n,
+    const uint32_t* __restrict__ dist, double threshold, double fw, int32_t* __restrict__ near,
+    unsigned long long* __restrict__ near_len, int32_t* __restrict__ soon,
+    int32_t* __restrict__ soon_key, unsigned long long* __restrict__ soon_len,
+    int32_t* __restrict__ later, int32_t* __restrict__ later_key,
+    unsigned long long* __restrict__ later_len) {
+  if (threadIdx.x == 0) S.nn = S.nfar = S.nl = 0;
+  __syncthreads();
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    if (i < n) {
+      const int32_t v = in[i];
+      const int32_t key = in_key[i];
+      if ((int32_t)dist[v] == key) {  // fresh
+        if ((double)key < threshold) {
+          S.nv[atomicAdd(&S.nn, 1)] = v;
+        } else if ((double)key < fw) {
+          const int at = atomicAdd(&S.nfar, 1);
+          S.fv[at] = v;
+          S.fk[at] = key;
+        } else {
+          const int at = atomicAdd(&S.nl, 1);
+          S.lv[at] = v;
+          S.lk[at] = key;
+        }
+      }
+    }
+    __syncthreads();
+    const int lim = kPileStage3 - (int)blockDim.x;
+    if (S.nn > lim || S.nfar > lim || S.nl > lim)
+      pile_flush3(S, near, near_len, soon, soon_key, soon_len, later, later_key, later_len);
+  }
+  pile_flush3(S, near, near_len, soon, soon_key, soon_len, later, later_key, later_len);
+}
+
 static __global__ void __launch_bounds__(256)
     k_sssp_refar(const int32_t* __restrict__ far, const int32_t* __restrict__ far_key, int64_t n,
                  const uint32_t* __restrict__ dist, double threshold, int split,
