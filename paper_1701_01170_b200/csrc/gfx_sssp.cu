@@ -160,10 +160,10 @@ struct PSsspArgs {
   long long* summary;
 };
 
-constexpr double kSsspWindow = 2.0;  // the soon pile's window, in deltas (s24 sweep: 1-4 -> 2)
+constexpr double kSsspWindow = 4.0;  // the soon pile's window, in deltas (s24 sweep 2 / 4 / 8)
 
 struct PSCtl {
-  long long nnear, nfar, nlater, it, ph, slots, bytes, nrec, nadv;
+  long long nnear, nfar, nlater, lmin, it, ph, slots, bytes, nrec, nadv;
   int q, f, l;
   double th, fw;
   unsigned long long t0;
@@ -211,6 +211,7 @@ __global__ void __launch_bounds__(256, 3) k_sssp_persistent(PSsspArgs a) {
     c.nnear = 1;
     c.nfar = c.nlater = c.it = c.ph = c.slots = c.bytes = c.nrec = c.nadv = 0;
     c.q = c.f = c.l = 0;
+    c.lmin = 0xFFFFFFFFll;  // no later entry
     c.th = a.delta;
     c.fw = a.delta + a.win;
   }
@@ -238,27 +239,40 @@ __global__ void __launch_bounds__(256, 3) k_sssp_persistent(PSsspArgs a) {
       // far entries, re-split the rest -- the soon pile while it lasts, then
       // the later pile under the next window
       const double th = c.th + a.delta;
-      const bool from_soon = c.nfar > 0;
+      // while th does not pass the smallest later key, every key below th
+      // is in the soon pile, so only it is re-split (its entries at or above
+      // the window bound fw join the later pile); otherwise both piles are,
+      // under a new window -- the near set is exactly the one-pile loop's
+      const bool from_soon = c.nfar > 0 && th <= (double)c.lmin;
       const double fw = from_soon ? c.fw : th + a.win;
-      if (from_soon)
+      if (from_soon) {
         sssp_refar2_phase(S3, a.far[c.f], a.fkey[c.f], c.nfar, a.dist, th, fw, a.nearq[c.q],
                           &cur->out_len, a.far[c.f ^ 1], a.fkey[c.f ^ 1], &cur->aux1,
-                          a.later[c.l] + c.nlater, a.lkey[c.l] + c.nlater, &cur->aux3);
-      else
+                          a.later[c.l] + c.nlater, a.lkey[c.l] + c.nlater, &cur->aux3,
+                          &cur->aux2);
+      } else {
+        if (c.nfar > 0)
+          sssp_refar2_phase(S3, a.far[c.f], a.fkey[c.f], c.nfar, a.dist, th, fw, a.nearq[c.q],
+                            &cur->out_len, a.far[c.f ^ 1], a.fkey[c.f ^ 1], &cur->aux1,
+                            a.later[c.l ^ 1], a.lkey[c.l ^ 1], &cur->aux3, &cur->aux2);
         sssp_refar2_phase(S3, a.later[c.l], a.lkey[c.l], c.nlater, a.dist, th, fw, a.nearq[c.q],
                           &cur->out_len, a.far[c.f ^ 1], a.fkey[c.f ^ 1], &cur->aux1,
-                          a.later[c.l ^ 1], a.lkey[c.l ^ 1], &cur->aux3);
+                          a.later[c.l ^ 1], a.lkey[c.l ^ 1], &cur->aux3, &cur->aux2);
+      }
       grid.sync();
       if (threadIdx.x == 0) {
-        c.bytes += 8 * (from_soon ? c.nfar : c.nlater);
+        c.bytes += 8 * (from_soon ? c.nfar : c.nfar + c.nlater);
         c.th = th;
         c.fw = fw;
         c.nnear = (long long)ld_volatile_u64(&cur->out_len);
         c.nfar = (long long)ld_volatile_u64(&cur->aux1);
+        const long long lmin = 0xFFFFFFFFll - (long long)ld_volatile_u64(&cur->aux2);
         if (from_soon) {
           c.nlater += (long long)ld_volatile_u64(&cur->aux3);
+          c.lmin = c.lmin < lmin ? c.lmin : lmin;
         } else {
           c.nlater = (long long)ld_volatile_u64(&cur->aux3);
+          c.lmin = lmin;
           c.l ^= 1;
         }
         c.f ^= 1;

@@ -165,7 +165,7 @@ struct PileStage3 {
   int32_t nv[kPileStage3];
   int32_t fv[kPileStage3], fk[kPileStage3];
   int32_t lv[kPileStage3], lk[kPileStage3];
-  int nn, nfar, nl;
+  int nn, nfar, nl, lmin;
   unsigned long long base;
 };
 
@@ -198,15 +198,19 @@ static __device__ __forceinline__ void pile_flush3(
 }
 
 // fresh entries of in[0..n): key < threshold -> near, key < fw -> soon,
-// else -> later (stale ones dropped)
+// else -> later (stale ones dropped); *later_max_inv = max(0xFFFFFFFF - key)
+// over the entries sent to later (a running minimum of the later keys)
 static __device__ __forceinline__ void sssp_refar2_phase(
     PileStage3& S, const int32_t* __restrict__ in, const int32_t* __restrict__ in_key, int64_t n,
     const uint32_t* __restrict__ dist, double threshold, double fw, int32_t* __restrict__ near,
     unsigned long long* __restrict__ near_len, int32_t* __restrict__ soon,
     int32_t* __restrict__ soon_key, unsigned long long* __restrict__ soon_len,
     int32_t* __restrict__ later, int32_t* __restrict__ later_key,
-    unsigned long long* __restrict__ later_len) {
-  if (threadIdx.x == 0) S.nn = S.nfar = S.nl = 0;
+    unsigned long long* __restrict__ later_len, unsigned long long* __restrict__ later_max_inv) {
+  if (threadIdx.x == 0) {
+    S.nn = S.nfar = S.nl = 0;
+    S.lmin = 0x7fffffff;
+  }
   __syncthreads();
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n;
        base += (int64_t)gridDim.x * blockDim.x) {
@@ -225,6 +229,7 @@ static __device__ __forceinline__ void sssp_refar2_phase(
           const int at = atomicAdd(&S.nl, 1);
           S.lv[at] = v;
           S.lk[at] = key;
+          atomicMin(&S.lmin, key);
         }
       }
     }
@@ -234,6 +239,8 @@ static __device__ __forceinline__ void sssp_refar2_phase(
       pile_flush3(S, near, near_len, soon, soon_key, soon_len, later, later_key, later_len);
   }
   pile_flush3(S, near, near_len, soon, soon_key, soon_len, later, later_key, later_len);
+  if (threadIdx.x == 0 && S.lmin != 0x7fffffff)
+    atomicMax(later_max_inv, 0xFFFFFFFFull - (unsigned long long)(uint32_t)S.lmin);
 }
 
 static __global__ void __launch_bounds__(256)
