@@ -270,6 +270,10 @@ extern "C" int gfx_bc(gfx_graph* g, const int64_t* sources, int64_t num_sources,
   // forces the pull-gather on every level (diagnostic)
   const char* dp = std::getenv("GFX_BC_DELTA_PUSH");
   const bool delta_push = !(dp && dp[0] == '0');
+  // forward levels from the direction-optimising persistent BFS (no host
+  // round trip per level); GFX_BC_FWD=push restores the push-only level loop
+  const char* fw = std::getenv("GFX_BC_FWD");
+  const bool fwd_do = !(fw && fw[0] == 'p');
   unsigned long long* acc = nullptr;
   bool acc_fresh = false;
   GFX_TRY(scratch(g, "bc_fix128", (size_t)(n + 1) * 16, reinterpret_cast<void**>(&acc),
@@ -282,7 +286,8 @@ extern "C" int gfx_bc(gfx_graph* g, const int64_t* sources, int64_t num_sources,
     const int32_t src = (int32_t)sources[si];
     int32_t* order = nullptr;
     std::vector<int64_t> slots;
-    GFX_TRY(bfs_push_levels(g, src, labels, preds, &off, &order, &slots));
+    if (fwd_do) GFX_TRY(bfs_do_levels(g, src, labels, preds, &off, &order, &slots));
+    else GFX_TRY(bfs_push_levels(g, src, labels, preds, &off, &order, &slots));
     const bool undirected = (g->flags & GFX_GRAPH_UNDIRECTED) != 0;
     // push a level from its neighbour level when that is fewer slots
     auto push_from = [&](int64_t lvl, auto op) -> int {

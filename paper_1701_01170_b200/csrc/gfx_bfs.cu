@@ -22,6 +22,8 @@
 #include <cstdlib>
 #include <cuda_runtime.h>
 
+#include <cub/device/device_scan.cuh>
+
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -1301,6 +1303,122 @@ int bfs_device_batch(gfx_graph* g, const int64_t* sources, int64_t count, int di
   GFX_CK(cudaEventRecord(ctx->ev1, ctx->stream));
   GFX_CK(cudaEventSynchronize(ctx->ev1));
   GFX_CK(cudaEventElapsedTime(ms, ctx->ev0, ctx->ev1));
+  return GFX_OK;
+}
+
+// Level lists of a labelled BFS (BC's forward phase): pass A counts each
+// block's vertices per level (and the levels' out-degree sums), one exclusive
+// scan over the level-major (level, block) counts gives every block its
+// write base per level, pass B scatters the vertices.  Warp-aggregated: each
+// distinct level among a warp's 32 vertices is one shared-memory atomic.
+template <bool kScatter>
+__global__ void __launch_bounds__(256)
+    k_level_pass(const int32_t* __restrict__ labels, const int64_t* __restrict__ row, int64_t n,
+                 int L, int64_t chunk, uint32_t* __restrict__ blk,
+                 unsigned long long* __restrict__ gcnt, unsigned long long* __restrict__ gslots,
+                 int32_t* __restrict__ order) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned long long* s_slots = reinterpret_cast<unsigned long long*>(smem_raw);
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem_raw + (kScatter ? 0 : 8 * (size_t)L));
+  const int nb = gridDim.x;
+  for (int d = threadIdx.x; d < L; d += blockDim.x) {
+    s_cnt[d] = 0;
+    if (!kScatter) s_slots[d] = 0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t b0 = blockIdx.x * chunk, b1 = min(n, b0 + chunk);
+  for (int64_t vb = b0 + (threadIdx.x & ~31); vb < b1; vb += blockDim.x) {
+    const int64_t v = vb + lane;
+    int32_t d = v < b1 ? labels[v] : -1;
+    if (d == GFX_UNVISITED || d >= L) d = -1;
+    const unsigned long long deg = (!kScatter && d >= 0) ? (unsigned long long)(row[v + 1] - row[v]) : 0ull;
+    unsigned rem = __ballot_sync(0xffffffffu, d >= 0);
+    while (rem) {
+      const int leader = __ffs(rem) - 1;
+      const int32_t dl = __shfl_sync(0xffffffffu, d, leader);
+      const unsigned mask = __ballot_sync(0xffffffffu, d == dl);
+      if (!kScatter) {
+        const unsigned long long sdeg = warp_sum_u64(d == dl ? deg : 0ull);
+        if (lane == leader) {
+          atomicAdd(&s_cnt[dl], (uint32_t)__popc(mask));
+          atomicAdd(&s_slots[dl], sdeg);
+        }
+      } else {
+        uint32_t gb = 0;
+        if (lane == leader) gb = atomicAdd(&s_cnt[dl], (uint32_t)__popc(mask));
+        gb = __shfl_sync(0xffffffffu, gb, leader);
+        if (d == dl)
+          order[blk[(int64_t)dl * nb + blockIdx.x] + gb + __popc(mask & ((1u << lane) - 1))] =
+              (int32_t)v;
+      }
+      rem &= ~mask;
+    }
+  }
+  if (!kScatter) {
+    __syncthreads();
+    for (int d = threadIdx.x; d < L; d += blockDim.x) {
+      blk[(int64_t)d * nb + blockIdx.x] = s_cnt[d];
+      if (s_cnt[d]) {
+        atomicAdd(&gcnt[d], (unsigned long long)s_cnt[d]);
+        atomicAdd(&gslots[d], s_slots[d]);
+      }
+    }
+  }
+}
+
+// BC's forward phase on the direction-optimising persistent BFS: labels and
+// preds as gfx_bfs writes them, then level d's vertices in
+// order[off[d], off[d+1]) and slots[d] = sum of their out-degrees (the same
+// contract as bfs_push_levels, whose push-only level loop needs a host
+// round trip per level; the order within a level differs, which BC's
+// per-vertex gathers and exact pushes do not see).  Falls back to
+// bfs_push_levels for BFS trees deeper than 1024 levels.
+int bfs_do_levels(gfx_graph* g, int64_t source, int32_t* labels, int32_t* preds,
+                  std::vector<int64_t>* off, int32_t** order_out, std::vector<int64_t>* slots) {
+  gfx_ctx* ctx = g->ctx;
+  const int64_t n = g->n;
+  PBfsArgs a{};
+  int blocks = 0, smem = 0;
+  GFX_TRY(pbfs_setup(g, source, GFX_DIR_AUTO, 0.001, 0.2, 0, labels, preds, &a, &blocks, &smem));
+  const int64_t stiles_max = std::max<int64_t>(1, (n + kScanTileItems - 1) / kScanTileItems);
+  GFX_CK(cudaMemsetAsync(a.status, 0, (stiles_max + 1) * 8, ctx->stream));
+  void* kargs[] = {&a};
+  GFX_CK(cudaLaunchCooperativeKernel((const void*)k_bfs_persistent<true>, dim3(blocks), dim3(256),
+                                     kargs, smem, ctx->stream));
+  count_launch();
+  long long summary[10];
+  GFX_CK(cudaMemcpyAsync(summary, a.summary, sizeof(summary), cudaMemcpyDeviceToHost, ctx->stream));
+  GFX_CK(cudaStreamSynchronize(ctx->stream));
+  const int64_t L = summary[0];  // levels 0 .. L-1 hold vertices
+  if (L > 1024) return bfs_push_levels(g, source, labels, preds, off, order_out, slots);
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->sm_count * 8, (n + 1023) / 1024));
+  const int64_t chunk = (n + nb - 1) / nb;
+  uint32_t* blk;
+  unsigned long long* lv;
+  GFX_TRY(scratch_t(g, "lvl_blk", (size_t)L * nb + 1, &blk));
+  GFX_TRY(scratch_t(g, "lvl_cnt", 2 * (size_t)L + 2, &lv));
+  GFX_CK(cudaMemsetAsync(lv, 0, (2 * L + 2) * 8, ctx->stream));
+  GFX_LAUNCH(k_level_pass<false>, nb, 256, (size_t)L * 12 + 16, ctx->stream, labels, g->row, n,
+             (int)L, chunk, blk, lv, lv + L, nullptr);
+  size_t tb = 0;
+  GFX_CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, blk, blk, (int64_t)L * nb, ctx->stream));
+  void* tmp;
+  GFX_TRY(scratch(g, "lvl_cub", tb + 16, &tmp));
+  GFX_CK(cub::DeviceScan::ExclusiveSum(tmp, tb, blk, blk, (int64_t)L * nb, ctx->stream));
+  count_launch();
+  GFX_LAUNCH(k_level_pass<true>, nb, 256, (size_t)L * 4 + 16, ctx->stream, labels, g->row, n,
+             (int)L, chunk, blk, nullptr, nullptr, a.order);
+  std::vector<unsigned long long> h(2 * L);
+  GFX_CK(cudaMemcpyAsync(h.data(), lv, 2 * L * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  GFX_CK(cudaStreamSynchronize(ctx->stream));
+  off->assign(1, 0);
+  if (slots) slots->clear();
+  for (int64_t d = 0; d < L; ++d) {
+    off->push_back(off->back() + (int64_t)h[d]);
+    if (slots) slots->push_back((int64_t)h[L + d]);
+  }
+  *order_out = a.order;
   return GFX_OK;
 }
 

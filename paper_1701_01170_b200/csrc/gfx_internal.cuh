@@ -179,6 +179,10 @@ int reached_stats(gfx_graph* g, const int32_t* labels, int64_t* reached, int64_t
 int bfs_push_levels(gfx_graph* g, int64_t source, int32_t* labels, int32_t* preds,
                     std::vector<int64_t>* off, int32_t** order_out,
                     std::vector<int64_t>* slots = nullptr);
+// the same level lists from the direction-optimising persistent BFS
+int bfs_do_levels(gfx_graph* g, int64_t source, int32_t* labels, int32_t* preds,
+                  std::vector<int64_t>* off, int32_t** order_out,
+                  std::vector<int64_t>* slots = nullptr);
 // identity frontier 0..n-1 (graph-constant scratch)
 int iota_frontier(gfx_graph* g, int32_t** out);
 
