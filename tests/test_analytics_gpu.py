@@ -180,3 +180,25 @@ def test_s24_sssp_cc_pagerank_golden():
     rank = rank.cpu().numpy()
     assert abs(rank.sum() - rec["pr20_sum"]) < 1e-9
     assert np.allclose(rank[arrays["pr_idx"]], arrays["pr_vals"], rtol=1e-9, atol=1e-15)
+
+
+@pytest.mark.parametrize("n", [300, 700, 1500])
+def test_bc_deep_levels(n):
+    """BC's forward levels from the DO-BFS (bfs_do_levels: level lists by
+    two passes over the labels) on graphs with hundreds of levels -- past
+    the depth-byte limit (255) of the persistent BFS, and past 1024 levels
+    (the push-level fallback) -- plus a dense head: a path with a clique at
+    one end; values equal the numpy port of bc.py:32-116"""
+    import paper_1701_01170_b200 as gfx
+    from oracle import graphfx_port as port
+
+    k = 24
+    a, b = np.triu_indices(k, 1)
+    src = np.concatenate([a, np.arange(k - 1, n - 1)]).astype(np.int64)
+    dst = np.concatenate([b, np.arange(k, n)]).astype(np.int64)
+    g = gfx.coo_to_csr(gfx.CooGraph(n, src, dst), make_undirected=True)
+    row, col = g.row_offsets, g.column_indices
+    for s in (0, n - 1, n // 2):
+        want = port.bc(row, col, [s])
+        got = gfx.bc(g, [s]).bc_values
+        assert np.allclose(got, want, rtol=1e-9, atol=1e-9), s

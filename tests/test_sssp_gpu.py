@@ -105,3 +105,24 @@ def test_device_loop_equals_host_loop(delta, monkeypatch):
                             out["device"][1], 0)
     st = out["device"][2]
     assert st.iterations > 0 and st.edges_traversed >= st.edges_reached
+
+
+@pytest.mark.parametrize("delta,window", [(1, "4"), (3, "1"), (2, "0"), (50, "4")])
+def test_two_level_far_pile_wide_weights(delta, window, monkeypatch):
+    """the device loop's two-level far pile (soon / later piles, re-split
+    when the threshold passes the later pile's smallest key) on a graph whose
+    keys span far more than the window: weights 1..1000 at small delta, so
+    the later pile is appended, re-split and rebuilt many times; distances
+    equal the numpy port of sssp.py:41-121 (GFX_SSSP_WIN: window in deltas,
+    0 = one far pile)"""
+    import paper_1701_01170_b200 as gfx
+    from oracle import graphfx_port as port
+
+    monkeypatch.setenv("GFX_SSSP_WIN", window)
+    row, col = port.rmat_csr(12, 8, 3)
+    w = port.assign_random_weights(row, col, 1, 1000, 5)
+    g = gfx.CsrGraph(len(row) - 1, row, col, w, undirected=True)
+    want = port.sssp(row, col, w, 0, delta=delta)[0]
+    r = gfx.sssp(g, 0, delta=delta)
+    assert np.array_equal(r.labels, want)
+    assert valid_sssp_preds(g.row_offsets, g.column_indices, g.edge_weights, r.labels, r.preds, 0)
