@@ -110,7 +110,9 @@ __global__ void __launch_bounds__(kPrBlock)
                 double* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const double base = *base_p;
-  const unsigned long long pol = l2_evict_first_policy();  // column ids stream past contrib
+  // a lane reads its row's column ids kPrBatch at a time: through L1, so the
+  // row's sector is fetched from L2 once, not once per load (s24 20 rounds
+  // 43.4 -> 42.9 ms against L1::no_allocate streaming)
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t grp = gw; grp * 32 < n; grp += nw) {
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(kPrBlock)
         int32_t u[kPrBatch];
         double c[kPrBatch];
 #pragma unroll
-        for (int k = 0; k < kPrBatch; ++k) u[k] = p + k < e ? ld_stream_i32(rcol + p + k, pol) : -1;
+        for (int k = 0; k < kPrBatch; ++k) u[k] = p + k < e ? __ldg(rcol + p + k) : -1;
 #pragma unroll
         for (int k = 0; k < kPrBatch; ++k) c[k] = u[k] >= 0 ? contrib[u[k]] : 0.0;
 #pragma unroll
