@@ -128,12 +128,14 @@ __global__ void k_unpack_deltas(const uint8_t* __restrict__ ctrl, const uint8_t*
 // The transpose is one stable radix sort of (v, u) pairs over log2(n) bits.
 
 // rowid[urow[u]] = u for every non-empty upper row (then a max-scan fills the rest)
-__global__ void k_upper_row_starts(const int64_t* __restrict__ urow, int64_t n,
+// (every index derived from the host image is range-checked: a malformed
+// image leaves wrong columns, never an out-of-bounds access)
+__global__ void k_upper_row_starts(const int64_t* __restrict__ urow, int64_t n, int64_t mu,
                                    int32_t* __restrict__ rowid) {
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
        u += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = urow[u];
-    if (urow[u + 1] > b) rowid[b] = (int32_t)u;
+    if (urow[u + 1] > b && b >= 0 && b < mu) rowid[b] = (int32_t)u;
   }
 }
 
@@ -149,11 +151,13 @@ __global__ void k_place_upper(const int64_t* __restrict__ row, const int64_t* __
 }
 
 __global__ void k_place_lower(const int64_t* __restrict__ urow, const uint32_t* __restrict__ key,
-                              const int32_t* __restrict__ val, int64_t mu, int64_t m,
+                              const int32_t* __restrict__ val, int64_t n, int64_t mu, int64_t m,
                               int32_t* __restrict__ col) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < mu;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t dst = i + urow[key[i]];
+    const uint32_t v = key[i];
+    if ((int64_t)v >= n) continue;
+    const int64_t dst = i + urow[v];
     if (dst >= 0 && dst < m) col[dst] = val[i];
   }
 }
@@ -273,7 +277,7 @@ int gfx_graph_rebuild_upper(gfx_graph* g, const int64_t* urow_d, const int32_t* 
   // row ids of the upper slots: row starts, then an inclusive max-scan
   GFX_CK(cudaMemsetAsync(rowid, 0, mu * 4, ctx->stream));
   GFX_LAUNCH(k_upper_row_starts, grid_for(n, 256, ctx->sm_count * 8), 256, 0, ctx->stream, urow_d,
-             n, rowid);
+             n, mu, rowid);
   size_t tb_scan = 0;
   GFX_CK(cub::DeviceScan::InclusiveScan(nullptr, tb_scan, rowid, rowid, MaxI32(), mu, ctx->stream));
   void* tmp;
@@ -299,7 +303,7 @@ int gfx_graph_rebuild_upper(gfx_graph* g, const int64_t* urow_d, const int32_t* 
                                          ctx->stream));
   count_launch();
   GFX_LAUNCH(k_place_lower, grid_for(mu, 256, ctx->sm_count * 16), 256, 0, ctx->stream, urow_d,
-             key_out, val_out, mu, g->m, const_cast<int32_t*>(g->col));
+             key_out, val_out, n, mu, g->m, const_cast<int32_t*>(g->col));
   GFX_CK(cudaGetLastError());
   return GFX_OK;
 }
